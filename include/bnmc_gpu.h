@@ -1,0 +1,167 @@
+/* include/bnmc_gpu.h -- C-ABI of the B200-native MCMC sweep (libbnmc_gpu.so).
+ *
+ * The drop-in boundary for the reference's hot path.  A host caller (the
+ * reference's C++ Engine via the adapter in INTEGRATION.md, the C++ mirror in
+ * include/bnmc_gpu.hpp, or Python through ctypes) hands over plain host pointers
+ * laid out exactly like the reference's ParamStore, and every sweep runs on the
+ * GPU.  There is no CPU fallback: every entry point fails with a non-zero code
+ * when the device path cannot run.
+ *
+ * Reference interfaces each entry point replaces (paths under /root/reference/proj):
+ *   bnmc_gpu_create        Engine::Engine            include/bnmc/sampler.hpp:47
+ *                          (plan for LDA/GMM Gibbs or MH, src/plan.cpp:110-166)
+ *   bnmc_gpu_upload        the ParamStore the caller lends to Engine::sweep
+ *                          include/bnmc/store.hpp:74-83
+ *   bnmc_gpu_sweep         Engine::sweep             include/bnmc/sampler.hpp:60 (src/sampler.cpp:390-405)
+ *   bnmc_gpu_run           Engine::run's sweep loop  include/bnmc/sampler.hpp:63 (src/sampler.cpp:426-455)
+ *   bnmc_gpu_eval_log_joint Engine::eval_log_joint   include/bnmc/sampler.hpp:56 (src/sampler.cpp:44-46)
+ *   bnmc_gpu_download      writes back the unobserved variables of the ParamStore
+ *   bnmc_gpu_prior_init    prior_init                include/bnmc/sampler.hpp:97-99 (src/sampler.cpp:542-555)
+ *   bnmc_gpu_dirichlet_batch sample_dirichlet_batch  include/bnmc/batch.hpp:33-34
+ *   bnmc_gpu_probe_*       RngStream / draw_gamma / draw_from_log_weights
+ *                          include/bnmc/rng.hpp:12-51, include/bnmc/dist.hpp:51,63
+ *   bnmc_gpu_lpp           log_predictive_probability include/bnmc/metrics.hpp:16-18
+ *   bnmc_gpu_partition     (new) document sharding across GPUs
+ *
+ * Error behaviour mirrors the reference's exceptions: the return code names the
+ * C++ exception type the adapter rethrows (BNMC_GPU_ERR_RUNTIME -> RuntimeError,
+ * BNMC_GPU_ERR_DOMAIN -> std::domain_error, BNMC_GPU_ERR_ARG ->
+ * std::invalid_argument); bnmc_gpu_last_error() holds the message.
+ */
+#ifndef BNMC_GPU_H
+#define BNMC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNMC_GPU_ABI_VERSION 1
+
+typedef enum {
+  BNMC_GPU_LDA = 1,       /* proj/models/lda.bn, Gibbs: blocks phi, theta, z */
+  BNMC_GPU_GMM = 2,       /* proj/models/gmm.bn, Gibbs: blocks pi, mu, sigma2, z */
+  BNMC_GPU_MH_LINREG = 3, /* proj/models/regression.bn, method MH (one block w, b, tau) */
+  BNMC_GPU_MH_LOGREG = 4  /* logistic twin of regression.bn (no reference model) */
+} bnmc_gpu_kind;
+
+typedef enum {
+  BNMC_GPU_OBSERVE_PHI = 1u << 0,    /* LDA: phi clamped (RunConfig::observe_extra = {"phi"}) */
+  BNMC_GPU_EXACT_WEIGHTS = 1u << 1,  /* LDA: log-space weights exactly as the reference
+                                        (default: product-form theta*phi, same draws) */
+  BNMC_GPU_NO_GRAPH = 1u << 2        /* launch kernels directly instead of a CUDA graph */
+} bnmc_gpu_flag;
+
+typedef enum {
+  BNMC_GPU_OK = 0,
+  BNMC_GPU_ERR_ARG = 1,     /* std::invalid_argument */
+  BNMC_GPU_ERR_RUNTIME = 2, /* bnmc::RuntimeError (shapes, bins out of range) */
+  BNMC_GPU_ERR_DOMAIN = 3,  /* std::domain_error (all candidate log-weights -inf) */
+  BNMC_GPU_ERR_CUDA = 4,    /* CUDA runtime failure / no device */
+  BNMC_GPU_ERR_NCCL = 5
+} bnmc_gpu_status;
+
+/* Model description: what the reference Engine derives from (CheckedModel,
+ * HyperValues, RunConfig).  Sizes are GLOBAL (all ranks). */
+typedef struct bnmc_gpu_desc {
+  int32_t abi_version;  /* = BNMC_GPU_ABI_VERSION */
+  int32_t kind;         /* bnmc_gpu_kind */
+  uint64_t seed;        /* RunConfig::seed -- every RNG key starts from it */
+  int32_t device;       /* CUDA ordinal; -1 = current device */
+  uint32_t flags;       /* bnmc_gpu_flag */
+  /* LDA: K topics, V vocabulary, M documents, N tokens.
+   * GMM: K components, N points.   MH: K features, N rows. */
+  int64_t K, V, M, N;
+  const int64_t* doc_offsets; /* LDA: M+1 prefix sums of N[i] (VarLayout::offsets), host */
+  /* LDA: {alpha, beta}; GMM: {alpha, mu0, v0, a0, b0};
+   * MH:  {lo, hi, w_var, b_var, tau_a, tau_b} */
+  double hyper[8];
+  /* Reference variable ids (declaration order; they are RNG key components):
+   * LDA {phi, theta, z, w}; GMM {pi, mu, sigma2, z, x}; LINREG {w, b, tau, x, y};
+   * LOGREG {w, b, x, y}. */
+  int32_t var_ids[8];
+  double mh_scale;      /* RunConfig::mh_scale (PlanConfig, plan.hpp:31-33) */
+  int32_t rank;         /* this process's shard (documents / rows) */
+  int32_t world_size;   /* number of GPUs sharing the model; 1 = unsharded */
+  const void* nccl_id;  /* 128-byte ncclUniqueId, required when world_size > 1 */
+  void* stream;         /* cudaStream_t to enqueue on; NULL = context-owned stream */
+} bnmc_gpu_desc;
+
+/* A view of the reference ParamStore (store.hpp:74-83): flat arrays indexed by
+ * variable id.  Arrays are GLOBAL; a sharded context reads/writes its slice. */
+typedef struct bnmc_gpu_store {
+  int32_t n_vars;
+  double* const* real;   /* ParamStore::real[id].data() or NULL */
+  int64_t* const* ival;  /* ParamStore::ival[id].data() or NULL */
+  const int64_t* len;    /* flat length of each variable (VarLayout::flat_values) */
+  const char* observed;  /* ParamStore::observed */
+} bnmc_gpu_store;
+
+typedef struct bnmc_gpu_ctx bnmc_gpu_ctx;
+
+int bnmc_gpu_abi_version(void);
+/* Thread-local message of the last failure (ctx may be NULL). */
+const char* bnmc_gpu_last_error(const bnmc_gpu_ctx* ctx);
+
+int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out);
+void bnmc_gpu_destroy(bnmc_gpu_ctx* ctx);
+
+/* Copies the latent state and the observed data of `store` to the device. */
+int bnmc_gpu_upload(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
+/* Copies only the latent (unobserved) variables; observed data already on the
+ * device is kept.  The per-call path of a bound store (Engine::sweep borrow). */
+int bnmc_gpu_upload_state(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
+/* Writes the device state back into the unobserved variables of `store`
+ * (observed variables are never written, test_runtime.cpp:214-233). */
+int bnmc_gpu_download(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
+
+/* One sweep (all plan blocks + log-joint) for iteration `iter`; synchronous. */
+int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_accepted);
+/* n sweeps iter0..iter0+n-1 with one host sync; per-sweep outputs optional. */
+int bnmc_gpu_run(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n, double* log_joints, int* accepted);
+/* Asynchronous variant of bnmc_gpu_run (no host sync); pair with bnmc_gpu_synchronize. */
+int bnmc_gpu_enqueue(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n);
+int bnmc_gpu_synchronize(bnmc_gpu_ctx* ctx, double* last_log_joint, int* last_accepted);
+/* One sweep launched kernel by kernel with CUDA events between phases; ms[i] is
+ * the device time of phase names[i] (for the roofline of the dominant kernel). */
+int bnmc_gpu_sweep_phases(bnmc_gpu_ctx* ctx, int64_t iter, double* ms, const char** names, int cap,
+                          int* n_phases);
+/* ncclGetUniqueId for the rank-0 process of a sharded run (128 bytes). */
+int bnmc_gpu_nccl_unique_id(void* out128);
+/* Engine::eval_log_joint of the current device state. */
+int bnmc_gpu_eval_log_joint(bnmc_gpu_ctx* ctx, double* log_joint);
+/* prior_init(skip_observed = true) on the device (sampler.cpp:542-555). */
+int bnmc_gpu_prior_init(bnmc_gpu_ctx* ctx, uint64_t seed);
+
+/* LDA diagnostics: topic-word counts of the current z, row-major K x V (global,
+ * after the all-reduce), and this shard's doc-topic counts (local docs x K). */
+int bnmc_gpu_lda_counts(bnmc_gpu_ctx* ctx, int32_t* nkw, int32_t* nmk);
+/* LDA synthetic corpus on the device, following gen_lda's generative process
+ * (gen.cpp:21-60) with per-token counter streams (not the reference's single
+ * serial stream); fills w, then prior_init.  For configs the host cannot hold. */
+int bnmc_gpu_lda_generate(bnmc_gpu_ctx* ctx, uint64_t seed, double phi_conc, double theta_conc);
+/* Documents [begin, end) owned by `rank` under the balanced-token partition. */
+int bnmc_gpu_partition(const int64_t* doc_offsets, int64_t M, int32_t world_size, int32_t rank,
+                       int64_t* begin, int64_t* end);
+
+/* log_predictive_probability (metrics.cpp:9-34) on the device: sum over held-out
+ * tokens of log10 sum_k theta[d,k] phi[k,w]; phi K x V, theta docs x K, host. */
+int bnmc_gpu_lpp(const double* phi, const double* theta, int64_t K, int64_t V, const int64_t* w,
+                 const int64_t* offsets, int64_t docs, double* out);
+
+/* sample_dirichlet_batch with per-row concentrations (batch.cpp:45-83) on the device. */
+int bnmc_gpu_dirichlet_batch(int64_t rows, int64_t cols, const double* alpha, uint64_t key,
+                             double* out);
+/* Primitive probes for known-answer parity (device RNG and draws). */
+int bnmc_gpu_probe_rng(const uint64_t* keys, int64_t n, int64_t per_key, uint64_t* u64,
+                       double* unit, double* gauss);
+int bnmc_gpu_probe_gamma(const uint64_t* keys, const double* shapes, int64_t n, double* out,
+                         uint64_t* counters);
+int bnmc_gpu_probe_log_weights(const uint64_t* keys, const double* logw, int64_t rows,
+                               int64_t cols, int64_t* picks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNMC_GPU_H */

@@ -1,0 +1,413 @@
+// csrc/capi.cu -- the extern "C" boundary (include/bnmc_gpu.h).
+//
+// A context owns one CUDA stream, the device state of one model, an optional NCCL
+// communicator over NVLink (document / row sharding), and a CUDA graph of one
+// sweep.  The iteration number lives on the device (*iter) and the graph's last
+// kernel advances it, so n sweeps are n graph launches with no host round trip;
+// log-joints land in a device ring read back at synchronisation points.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace bnmc_gpu {
+void probe_rng(const std::uint64_t*, std::int64_t, std::int64_t, std::uint64_t*, double*, double*);
+void probe_gamma(const std::uint64_t*, const double*, std::int64_t, double*, std::uint64_t*);
+void probe_log_weights(const std::uint64_t*, const double*, std::int64_t, std::int64_t, std::int64_t*);
+void dirichlet_batch(std::int64_t, std::int64_t, const double*, std::uint64_t, double*);
+double lpp(const double*, const double*, std::int64_t, std::int64_t, const std::int64_t*,
+           const std::int64_t*, std::int64_t);
+
+void partition_docs(const std::int64_t* off, std::int64_t M, int world, int rank, std::int64_t* b,
+                    std::int64_t* e) {
+  // Contiguous documents balanced by token count: rank r owns the documents whose
+  // first token lies in [r*N/world, (r+1)*N/world) (lower_bound on the prefix sums).
+  const std::int64_t N = off[M];
+  auto bound = [&](int r) -> std::int64_t {
+    if (r <= 0) return 0;
+    if (r >= world) return M;
+    const std::int64_t target = static_cast<std::int64_t>((static_cast<__int128>(N) * r) / world);
+    return static_cast<std::int64_t>(std::lower_bound(off, off + M, target) - off);
+  };
+  *b = bound(rank);
+  *e = bound(rank + 1);
+}
+}  // namespace bnmc_gpu
+
+using namespace bnmc_gpu;
+
+struct bnmc_gpu_ctx {
+  bnmc_gpu_desc desc{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Comm comm;
+  std::unique_ptr<Model> model;
+  DevBuf<double> lj;
+  DevBuf<int> acc;
+  DevBuf<std::int64_t> iter;
+  DevBuf<int> err;
+  std::int64_t* host_iter = nullptr;  // pinned
+  std::int64_t next_iter = -1;        // device *iter value after the enqueued work
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::string last_error;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(bnmc_gpu_ctx* ctx, int code, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded(bnmc_gpu_ctx* ctx, F&& f) {
+  try {
+    if (ctx) BNMC_CUDA(cudaSetDevice(ctx->device));
+    f();
+    return BNMC_GPU_OK;
+  } catch (const Error& e) {
+    return fail(ctx, e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, BNMC_GPU_ERR_RUNTIME, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, BNMC_GPU_ERR_RUNTIME, e.what());
+  }
+}
+
+void check_device_error(bnmc_gpu_ctx* c) {
+  int e = 0;
+  BNMC_CUDA(cudaMemcpyAsync(&e, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  if (e) {
+    BNMC_CUDA(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+    if (e & kErrBin) throw Error(BNMC_GPU_ERR_RUNTIME, "conjugate update bin out of range (assignment outside the support)");
+    if (e & kErrDomain) throw Error(BNMC_GPU_ERR_DOMAIN, "all candidate log-weights are -inf");
+    throw Error(BNMC_GPU_ERR_RUNTIME, "device reported an invalid state");
+  }
+}
+
+void set_iter(bnmc_gpu_ctx* c, std::int64_t it) {
+  if (c->next_iter == it) return;
+  BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  *c->host_iter = it;
+  BNMC_CUDA(cudaMemcpyAsync(c->iter.p, c->host_iter, sizeof(std::int64_t), cudaMemcpyHostToDevice, c->stream));
+  BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  c->next_iter = it;
+}
+
+void launch_sweep(bnmc_gpu_ctx* c) {
+  if (c->desc.flags & BNMC_GPU_NO_GRAPH) {
+    c->model->enqueue_sweep(c->stream);
+  } else {
+    if (!c->exec) {
+      BNMC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        c->model->enqueue_sweep(c->stream);
+      } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      BNMC_CUDA(cudaStreamEndCapture(c->stream, &c->graph));
+      BNMC_CUDA(cudaGraphInstantiate(&c->exec, c->graph, 0));
+    }
+    BNMC_CUDA(cudaGraphLaunch(c->exec, c->stream));
+  }
+  c->next_iter += 1;
+}
+
+void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, int* acc) {
+  // Entries it0 .. it0+n-1 (n <= kRing), possibly wrapping.
+  const std::int64_t s = it0 & (kRing - 1);
+  const std::int64_t first = std::min<std::int64_t>(n, kRing - s);
+  if (lj) {
+    BNMC_CUDA(cudaMemcpyAsync(lj, c->lj.p + s, sizeof(double) * first, cudaMemcpyDeviceToHost, c->stream));
+    if (n > first)
+      BNMC_CUDA(cudaMemcpyAsync(lj + first, c->lj.p, sizeof(double) * (n - first), cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (acc) {
+    BNMC_CUDA(cudaMemcpyAsync(acc, c->acc.p + s, sizeof(int) * first, cudaMemcpyDeviceToHost, c->stream));
+    if (n > first)
+      BNMC_CUDA(cudaMemcpyAsync(acc + first, c->acc.p, sizeof(int) * (n - first), cudaMemcpyDeviceToHost, c->stream));
+  }
+  BNMC_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int bnmc_gpu_abi_version(void) { return BNMC_GPU_ABI_VERSION; }
+
+const char* bnmc_gpu_last_error(const bnmc_gpu_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : g_last_error.c_str();
+}
+
+int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
+  if (!desc || !out) return fail(nullptr, BNMC_GPU_ERR_ARG, "null argument");
+  *out = nullptr;
+  auto c = std::make_unique<bnmc_gpu_ctx>();
+  const int rc = guarded(nullptr, [&] {
+    require(desc->abi_version == BNMC_GPU_ABI_VERSION, BNMC_GPU_ERR_ARG, "ABI version mismatch");
+    int ndev = 0;
+    BNMC_CUDA(cudaGetDeviceCount(&ndev));
+    require(ndev > 0, BNMC_GPU_ERR_CUDA, "no CUDA device");
+    c->desc = *desc;
+    c->desc.doc_offsets = nullptr;  // not retained
+    c->desc.nccl_id = nullptr;
+    if (desc->device >= 0) {
+      c->device = desc->device;
+    } else {
+      BNMC_CUDA(cudaGetDevice(&c->device));
+    }
+    BNMC_CUDA(cudaSetDevice(c->device));
+    cudaDeviceProp prop{};
+    BNMC_CUDA(cudaGetDeviceProperties(&prop, c->device));
+    require(prop.major >= 10, BNMC_GPU_ERR_CUDA,
+            std::string("libbnmc_gpu is built for sm_100a; device is ") + prop.name);
+    if (desc->stream) {
+      c->stream = static_cast<cudaStream_t>(desc->stream);
+    } else {
+      BNMC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    c->comm.world = std::max(1, desc->world_size);
+    c->comm.rank = desc->rank;
+    require(c->comm.rank >= 0 && c->comm.rank < c->comm.world, BNMC_GPU_ERR_ARG, "rank out of range");
+    if (c->comm.world > 1) {
+      require(desc->nccl_id != nullptr, BNMC_GPU_ERR_ARG, "world_size > 1 needs an ncclUniqueId");
+      ncclUniqueId id;
+      std::memcpy(&id, desc->nccl_id, sizeof(id));
+      BNMC_NCCL(ncclCommInitRank(&c->comm.comm, c->comm.world, id, c->comm.rank));
+    }
+    c->lj.alloc(kRing);
+    c->acc.alloc(kRing);
+    c->iter.alloc(1);
+    c->err.alloc(1);
+    c->lj.zero(c->stream);
+    c->acc.zero(c->stream);
+    c->iter.zero(c->stream);
+    c->err.zero(c->stream);
+    BNMC_CUDA(cudaMallocHost(&c->host_iter, sizeof(std::int64_t)));
+    c->next_iter = 0;
+    Outputs o{c->lj.p, c->acc.p, c->iter.p, c->err.p};
+    switch (desc->kind) {
+      case BNMC_GPU_LDA: c->model = make_lda(*desc, c->comm, o); break;
+      case BNMC_GPU_GMM: c->model = make_gmm(*desc, c->comm, o); break;
+      case BNMC_GPU_MH_LINREG:
+      case BNMC_GPU_MH_LOGREG: c->model = make_mh(*desc, c->comm, o); break;
+      default: throw Error(BNMC_GPU_ERR_ARG, "unknown model kind");
+    }
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != BNMC_GPU_OK) {
+    bnmc_gpu_destroy(c.release());
+    return rc;
+  }
+  *out = c.release();
+  return BNMC_GPU_OK;
+}
+
+void bnmc_gpu_destroy(bnmc_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  c->model.reset();
+  if (c->comm.comm) ncclCommDestroy(c->comm.comm);
+  if (c->host_iter) cudaFreeHost(c->host_iter);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int bnmc_gpu_upload(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
+            "store view is incomplete");
+    c->model->upload(*s, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_upload_state(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
+            "store view is incomplete");
+    c->model->upload_state(*s, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_sweep_phases(bnmc_gpu_ctx* c, std::int64_t iter, double* ms, const char** names, int cap,
+                          int* n_out) {
+  if (!c || !ms || !n_out) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    set_iter(c, iter);
+    std::vector<Model::Mark> marks;
+    c->model->marks = &marks;
+    try {
+      c->model->enqueue_sweep(c->stream);
+    } catch (...) {
+      c->model->marks = nullptr;
+      for (auto& m : marks) cudaEventDestroy(m.ev);
+      throw;
+    }
+    c->model->marks = nullptr;
+    c->next_iter += 1;
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+    int n = 0;
+    for (std::size_t i = 1; i < marks.size() && n < cap; ++i, ++n) {
+      float t = 0.f;
+      BNMC_CUDA(cudaEventElapsedTime(&t, marks[i - 1].ev, marks[i].ev));
+      ms[n] = t;
+      if (names) names[n] = marks[i].name;
+    }
+    for (auto& m : marks) cudaEventDestroy(m.ev);
+    *n_out = n;
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    BNMC_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int bnmc_gpu_download(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    c->model->download(*s, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_sweep(bnmc_gpu_ctx* c, std::int64_t iter, double* log_joint, int* mh_accepted) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    require(iter >= 0, BNMC_GPU_ERR_ARG, "iteration must be non-negative");
+    set_iter(c, iter);
+    launch_sweep(c);
+    read_ring(c, iter, 1, log_joint, mh_accepted);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_run(bnmc_gpu_ctx* c, std::int64_t iter0, std::int64_t n, double* log_joints, int* accepted) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    require(iter0 >= 0 && n >= 0, BNMC_GPU_ERR_ARG, "bad iteration range");
+    set_iter(c, iter0);
+    for (std::int64_t done = 0; done < n;) {
+      const std::int64_t chunk = std::min<std::int64_t>(n - done, kRing);
+      for (std::int64_t i = 0; i < chunk; ++i) launch_sweep(c);
+      read_ring(c, iter0 + done, chunk, log_joints ? log_joints + done : nullptr,
+                accepted ? accepted + done : nullptr);
+      check_device_error(c);
+      done += chunk;
+    }
+  });
+}
+
+int bnmc_gpu_enqueue(bnmc_gpu_ctx* c, std::int64_t iter0, std::int64_t n) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    require(iter0 >= 0 && n >= 0, BNMC_GPU_ERR_ARG, "bad iteration range");
+    set_iter(c, iter0);
+    for (std::int64_t i = 0; i < n; ++i) launch_sweep(c);
+  });
+}
+
+int bnmc_gpu_synchronize(bnmc_gpu_ctx* c, double* last_log_joint, int* last_accepted) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->next_iter > 0) read_ring(c, c->next_iter - 1, 1, last_log_joint, last_accepted);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_eval_log_joint(bnmc_gpu_ctx* c, double* log_joint) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    c->model->enqueue_log_joint(c->stream);
+    read_ring(c, c->next_iter, 1, log_joint, nullptr);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_prior_init(bnmc_gpu_ctx* c, std::uint64_t seed) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    c->model->prior_init(seed, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_lda_counts(bnmc_gpu_ctx* c, std::int32_t* nkw, std::int32_t* nmk) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    c->model->lda_counts(nkw, nmk, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_lda_generate(bnmc_gpu_ctx* c, std::uint64_t seed, double phi_conc, double theta_conc) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  return guarded(c, [&] {
+    require(phi_conc > 0 && theta_conc > 0, BNMC_GPU_ERR_ARG, "concentrations must be positive");
+    c->model->lda_generate(seed, phi_conc, theta_conc, c->stream);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_partition(const std::int64_t* off, std::int64_t M, std::int32_t world, std::int32_t rank,
+                       std::int64_t* begin, std::int64_t* end) {
+  if (!off || !begin || !end || M < 0 || world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, BNMC_GPU_ERR_ARG, "bad partition arguments");
+  partition_docs(off, M, world, rank, begin, end);
+  return BNMC_GPU_OK;
+}
+
+int bnmc_gpu_lpp(const double* phi, const double* theta, std::int64_t K, std::int64_t V,
+                 const std::int64_t* w, const std::int64_t* offsets, std::int64_t docs, double* out) {
+  return guarded(nullptr, [&] { *out = lpp(phi, theta, K, V, w, offsets, docs); });
+}
+
+int bnmc_gpu_dirichlet_batch(std::int64_t rows, std::int64_t cols, const double* alpha, std::uint64_t key,
+                             double* out) {
+  return guarded(nullptr, [&] { dirichlet_batch(rows, cols, alpha, key, out); });
+}
+
+int bnmc_gpu_probe_rng(const std::uint64_t* keys, std::int64_t n, std::int64_t per, std::uint64_t* u64,
+                       double* unit, double* gauss) {
+  return guarded(nullptr, [&] { probe_rng(keys, n, per, u64, unit, gauss); });
+}
+
+int bnmc_gpu_probe_gamma(const std::uint64_t* keys, const double* shapes, std::int64_t n, double* out,
+                         std::uint64_t* counters) {
+  return guarded(nullptr, [&] { probe_gamma(keys, shapes, n, out, counters); });
+}
+
+int bnmc_gpu_probe_log_weights(const std::uint64_t* keys, const double* logw, std::int64_t rows,
+                               std::int64_t cols, std::int64_t* picks) {
+  return guarded(nullptr, [&] { probe_log_weights(keys, logw, rows, cols, picks); });
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// csrc/common.cuh -- shared internals of libbnmc_gpu.so (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bnmc_gpu.h"
+
+namespace bnmc_gpu {
+
+// Internal failures carry the C-ABI status they map to.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define BNMC_CUDA(x)                                                                   \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::bnmc_gpu::Error(BNMC_GPU_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define BNMC_NCCL(x)                                                                   \
+  do {                                                                                 \
+    ncclResult_t r_ = (x);                                                             \
+    if (r_ != ncclSuccess)                                                             \
+      throw ::bnmc_gpu::Error(BNMC_GPU_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+inline void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+// Device-side error flags, checked by the host at every synchronisation point.
+enum : int {
+  kErrBin = 1,     // conjugate update bin out of range  -> RuntimeError (sampler.cpp:89-91)
+  kErrDomain = 2,  // all candidate log-weights -inf     -> std::domain_error (dist.cpp:205)
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(std::size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) BNMC_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void zero(cudaStream_t s) {
+    if (n) BNMC_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+  }
+  std::size_t bytes() const { return sizeof(T) * n; }
+};
+
+// Ring of per-sweep outputs; the finalize kernel of every model writes
+// lj[iter % kRing], acc[iter % kRing] and then advances *iter.
+constexpr int kRing = 4096;
+
+struct Outputs {
+  double* lj;
+  int* acc;
+  std::int64_t* iter;
+  int* err;
+};
+
+// Deterministic block-wide sum (fixed butterfly + fixed warp order): the result
+// depends only on the inputs and blockDim, never on scheduling.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// scratch: >= 32 doubles of shared memory. Result valid in every thread.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double t = lane < nw ? scratch[lane] : 0.0;
+  t = warp_sum(t);
+  return t;
+}
+
+// Model-specific device state behind one context.
+struct Model {
+  virtual ~Model() = default;
+  virtual void upload(const bnmc_gpu_store& s, cudaStream_t st) = 0;
+  virtual void download(const bnmc_gpu_store& s, cudaStream_t st) = 0;
+  // Uploads only the latent (unobserved) variables: the observed data already on
+  // the device is kept (the engine never writes observed arrays).
+  virtual void upload_state(const bnmc_gpu_store& s, cudaStream_t st) { upload(s, st); }
+  // Enqueues one sweep (reads the iteration from *out.iter, advances it).
+  virtual void enqueue_sweep(cudaStream_t st) = 0;
+  // Enqueues Engine::eval_log_joint of the current state into lj[iter % kRing]
+  // without advancing the iteration.
+  virtual void enqueue_log_joint(cudaStream_t st) = 0;
+  virtual void prior_init(std::uint64_t seed, cudaStream_t st) = 0;
+  virtual void lda_counts(std::int32_t*, std::int32_t*, cudaStream_t) {
+    throw Error(BNMC_GPU_ERR_ARG, "counts are only defined for LDA");
+  }
+  virtual void lda_generate(std::uint64_t, double, double, cudaStream_t) {
+    throw Error(BNMC_GPU_ERR_ARG, "generate is only defined for LDA");
+  }
+  Outputs out{};
+
+  // Per-phase timing (bnmc_gpu_sweep_phases): when `marks` is set, every phase
+  // boundary records an event on the launching stream.
+  struct Mark {
+    const char* name;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark>* marks = nullptr;
+  void mark(cudaStream_t st, const char* name) {
+    if (!marks) return;
+    cudaEvent_t e;
+    BNMC_CUDA(cudaEventCreate(&e));
+    BNMC_CUDA(cudaEventRecord(e, st));
+    marks->push_back({name, e});
+  }
+};
+
+struct Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+std::unique_ptr<Model> make_lda(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
+std::unique_ptr<Model> make_gmm(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
+std::unique_ptr<Model> make_mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
+
+// Balanced-token document partition (shared by the C-ABI and the models).
+void partition_docs(const std::int64_t* off, std::int64_t M, int world, int rank, std::int64_t* b,
+                    std::int64_t* e);
+
+inline unsigned blocks_for(std::int64_t n, int bt) {
+  return static_cast<unsigned>((n + bt - 1) / bt);
+}
+
+}  // namespace bnmc_gpu

@@ -1,0 +1,445 @@
+// csrc/gmm.cu -- univariate Gaussian-mixture Gibbs sweep (proj/models/gmm.bn).
+//
+// Plan order pi, mu, sigma2, z (tests/golden/describe_gmm.txt).  Per sweep:
+//   stats_kernel(MU)   counts + sum 1/sigma2[z] + sum x/sigma2[z] with the current
+//                      z and sigma2 (sampler.cpp:114-121), per-block partials
+//   draw_pi_mu_kernel  pi ~ Dir(alpha + c) (rows = 1, batch.cpp:51-63);
+//                      mu_k ~ N(v*(mu0/v0 + W), v*), v* = 1/(1/v0 + P)
+//                      (sampler.cpp:199-204), stream keyed(seed,4,var,iter).derive(k)
+//   stats_kernel(RSS)  n, sum (x - mu[z])^2 with the NEW mu (sampler.cpp:122-130)
+//   draw_s2_kernel     sigma2_k = (b0 + rss/2) / Gamma(a0 + n/2) (dist.cpp:175-177)
+//   z_kernel           log pi_v + log N(x | mu_v, sigma2_v), draw_from_log_weights
+//                      with keyed(seed,3,var_z,i,iter) (sampler.cpp:222-265);
+//                      accumulates the log-joint pieces of z and x
+//   finalize_kernel    log-joint in the reference's factor order.
+// Every reduction runs over a fixed grid with a fixed tree: results are
+// reproducible run to run.  Replicas only across GPUs.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "dist.cuh"
+
+namespace bnmc_gpu {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBlocks = 148 * 2;
+constexpr int kMaxK = 64;
+
+struct GmmArgs {
+  std::int64_t N;
+  int K;
+  const double* x;
+  int* z;
+  double* pi;
+  double* mu;
+  double* s2;
+  double* part;  // [kBlocks][K][3]
+  double* lpart; // [kBlocks][2]
+  double alpha, mu0, v0, a0, b0;
+  std::uint64_t seed;
+  int var_pi, var_mu, var_s2, var_z;
+};
+
+enum { kStatsMu = 0, kStatsRss = 1 };
+
+template <int WHICH>
+__global__ void __launch_bounds__(kThreads) stats_kernel(GmmArgs a, int* err) {
+  __shared__ double scratch[32];
+  for (int k = 0; k < a.K; ++k) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const double m = a.mu[k], v = a.s2[k];
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+      const int zi = a.z[i];
+      if (k == 0 && (zi < 0 || zi >= a.K)) atomicOr(err, kErrBin);
+      if (zi != k) continue;
+      const double xi = a.x[i];
+      if (WHICH == kStatsMu) {
+        s0 += 1.0;
+        s1 += 1.0 / v;
+        s2 += xi / v;
+      } else {
+        s0 += 1.0;
+        s1 += (xi - m) * (xi - m);
+      }
+    }
+    s0 = block_sum(s0, scratch);
+    s1 = block_sum(s1, scratch);
+    s2 = block_sum(s2, scratch);
+    if (threadIdx.x == 0) {
+      double* p = a.part + (static_cast<std::size_t>(blockIdx.x) * a.K + k) * 3;
+      p[0] = s0;
+      p[1] = s1;
+      p[2] = s2;
+    }
+  }
+}
+
+__device__ double reduce_part(const GmmArgs& a, int k, int j, double* scratch) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x)
+    s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
+  return block_sum(s, scratch);
+}
+
+__global__ void draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double scratch[32];
+  __shared__ double cnt[kMaxK], P[kMaxK], W[kMaxK];
+  const std::int64_t iter = *iter_p;
+  for (int k = 0; k < a.K; ++k) {
+    const double c = reduce_part(a, k, 0, scratch);
+    const double p = reduce_part(a, k, 1, scratch);
+    const double w = reduce_part(a, k, 2, scratch);
+    if (threadIdx.x == 0) {
+      cnt[k] = c;
+      P[k] = p;
+      W[k] = w;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // pi block: Dirichlet over a single row, cells derive(0, c); left-to-right sum.
+    const std::uint64_t kp = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_pi),
+                                   static_cast<std::uint64_t>(iter));
+    double sum = 0.0;
+    for (int k = 0; k < a.K; ++k) {
+      Stream r(derive(kp, 0, static_cast<std::uint64_t>(k)));
+      a.pi[k] = draw_gamma(r, a.alpha + cnt[k]);
+      sum += a.pi[k];
+    }
+    for (int k = 0; k < a.K; ++k) a.pi[k] /= sum;
+    // mu block.
+    const std::uint64_t km = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_mu),
+                                   static_cast<std::uint64_t>(iter));
+    for (int k = 0; k < a.K; ++k) {
+      Stream r(derive(km, static_cast<std::uint64_t>(k)));
+      const double prec = 1.0 / a.v0 + P[k];
+      const double wsum = a.mu0 / a.v0 + W[k];
+      const double post_var = 1.0 / prec;
+      a.mu[k] = post_var * wsum + sqrt(post_var) * r.next_gaussian();
+    }
+  }
+}
+
+__global__ void draw_s2_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double scratch[32];
+  __shared__ double cnt[kMaxK], rss[kMaxK];
+  const std::int64_t iter = *iter_p;
+  for (int k = 0; k < a.K; ++k) {
+    const double c = reduce_part(a, k, 0, scratch);
+    const double s = reduce_part(a, k, 1, scratch);
+    if (threadIdx.x == 0) {
+      cnt[k] = c;
+      rss[k] = s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const std::uint64_t ks = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_s2),
+                                   static_cast<std::uint64_t>(iter));
+    for (int k = 0; k < a.K; ++k) {
+      Stream r(derive(ks, static_cast<std::uint64_t>(k)));
+      const double scale = a.b0 + 0.5 * rss[k];
+      a.s2[k] = scale / draw_gamma(r, a.a0 + 0.5 * cnt[k]);
+    }
+  }
+}
+
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64_t* iter_p, int* err) {
+  __shared__ double scratch[32];
+  __shared__ double lpi[kMaxK], mu[kMaxK], var[kMaxK], lvar[kMaxK];
+  const std::int64_t iter = *iter_p;
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    lpi[k] = a.pi[k] > 0.0 ? log(a.pi[k]) : -INFINITY;
+    mu[k] = a.mu[k];
+    var[k] = a.s2[k];
+    lvar[k] = log(a.s2[k]);
+  }
+  __syncthreads();
+  const std::uint64_t zp = fold(fold(fold(1, a.seed), kDiscrete), static_cast<std::uint64_t>(a.var_z));
+  double lz = 0.0, lx = 0.0;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const double xi = a.x[i];
+    // logw[v] = (0 + log pi_v) + log N(x | mu_v, sigma2_v); log_pdf_gaussian (dist.cpp:61-68)
+    auto logw = [&](int v) {
+      const double d = xi - mu[v];
+      const double g = var[v] > 0.0 ? -0.5 * (d * d / var[v] + lvar[v] + kLog2Pi) : -INFINITY;
+      return lpi[v] + g;
+    };
+    int k;
+    if (SAMPLE) {
+      double mx = -INFINITY;
+      for (int v = 0; v < a.K; ++v) mx = fmax(mx, logw(v));
+      if (!isfinite(mx)) {
+        atomicOr(err, kErrDomain);
+        continue;
+      }
+      double total = 0.0;
+      for (int v = 0; v < a.K; ++v) total += exp(logw(v) - mx);
+      Stream r(fold(fold(zp, static_cast<std::uint64_t>(i)), static_cast<std::uint64_t>(iter)));
+      const double u = r.next_unit() * total;
+      double acc = 0.0;
+      k = a.K - 1;
+      for (int v = 0; v < a.K; ++v) {
+        acc += exp(logw(v) - mx);
+        if (u < acc) {
+          k = v;
+          break;
+        }
+      }
+      a.z[i] = k;
+    } else {
+      k = a.z[i];
+      if (k < 0 || k >= a.K) {
+        lz += -INFINITY;
+        lx += -INFINITY;
+        continue;
+      }
+    }
+    lz += lpi[k];
+    const double d = xi - mu[k];
+    lx += var[k] > 0.0 ? -0.5 * (d * d / var[k] + lvar[k] + kLog2Pi) : -INFINITY;
+  }
+  lz = block_sum(lz, scratch);
+  lx = block_sum(lx, scratch);
+  if (threadIdx.x == 0) {
+    a.lpart[blockIdx.x * 2 + 0] = lz;
+    a.lpart[blockIdx.x * 2 + 1] = lx;
+  }
+}
+
+__global__ void finalize_kernel(GmmArgs a, Outputs o, int advance) {
+  __shared__ double scratch[32];
+  double lz = 0.0, lx = 0.0;
+  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {
+    lz += a.lpart[b * 2 + 0];
+    lx += a.lpart[b * 2 + 1];
+  }
+  lz = block_sum(lz, scratch);
+  lx = block_sum(lx, scratch);
+  if (threadIdx.x == 0) {
+    // p(pi): Dirichlet(alpha,...,alpha) log-pdf (dist.cpp:115-130), sequential.
+    double sum = 0.0, lp = 0.0, norm = 0.0, asum = 0.0;
+    bool bad = false;
+    for (int k = 0; k < a.K; ++k) {
+      const double x = a.pi[k];
+      bad |= !(x > 0.0);
+      sum += x;
+      lp += (a.alpha - 1.0) * log(x);
+      norm += lgamma(a.alpha);
+      asum += a.alpha;
+    }
+    const double fpi = (bad || fabs(sum - 1.0) > 1e-9) ? -INFINITY : lp - norm + lgamma(asum);
+    double fmu = 0.0, fs2 = 0.0;
+    for (int k = 0; k < a.K; ++k) fmu += log_pdf_gaussian(a.mu[k], a.mu0, a.v0);
+    for (int k = 0; k < a.K; ++k) fs2 += log_pdf_inverse_gamma(a.s2[k], a.a0, a.b0);
+    const double lj = (((fpi + fmu) + fs2) + lz) + lx;
+    const std::int64_t it = *o.iter;
+    o.lj[it & (kRing - 1)] = lj;
+    o.acc[it & (kRing - 1)] = 0;
+    if (advance) *o.iter = it + 1;
+  }
+}
+
+__global__ void prior_kernel(GmmArgs a, std::uint64_t seed) {
+  // prior_init (sampler.cpp:542-555): one stream keyed(seed,5,var,elem) per element.
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Stream s(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_pi), 0));
+    double sum = 0.0;
+    for (int k = 0; k < a.K; ++k) {
+      a.pi[k] = draw_gamma(s, a.alpha);
+      sum += a.pi[k];
+    }
+    for (int k = 0; k < a.K; ++k) a.pi[k] /= sum;
+    for (int k = 0; k < a.K; ++k) {
+      Stream m(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_mu), static_cast<std::uint64_t>(k)));
+      a.mu[k] = a.mu0 + sqrt(a.v0) * m.next_gaussian();
+      Stream v(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_s2), static_cast<std::uint64_t>(k)));
+      a.s2[k] = a.b0 / draw_gamma(v, a.a0);
+    }
+  }
+}
+
+__global__ void prior_z_kernel(GmmArgs a, std::uint64_t seed) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    Stream s(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_z), static_cast<std::uint64_t>(i)));
+    const double u = s.next_unit();
+    double acc = 0.0;
+    int pick = a.K - 1;
+    for (int k = 0; k < a.K; ++k) {
+      acc += a.pi[k];
+      if (u < acc) {
+        pick = k;
+        break;
+      }
+    }
+    a.z[i] = pick;
+  }
+}
+
+__global__ void z_from_i64(const std::int64_t* in, int* out, std::int64_t n, int K, int* err) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t v = in[i];
+    if (v < 0 || v >= K) atomicOr(err, kErrBin);
+    out[i] = static_cast<int>(v);
+  }
+}
+
+__global__ void z_to_i64(const int* in, std::int64_t* out, std::int64_t n) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+class Gmm final : public Model {
+ public:
+  Gmm(const bnmc_gpu_desc& d, const Comm& c, Outputs o) {
+    out = o;
+    require(d.K >= 1 && d.K <= kMaxK, BNMC_GPU_ERR_ARG, "GMM supports 1 <= K <= 64");
+    require(d.N >= 0, BNMC_GPU_ERR_ARG, "GMM needs N >= 0");
+    require(c.world == 1, BNMC_GPU_ERR_ARG, "GMM runs as replicas only (world_size must be 1)");
+    K_ = static_cast<int>(d.K);
+    N_ = d.N;
+    const double* h = d.hyper;
+    alpha_ = h[0] > 0 ? h[0] : 0.1;
+    mu0_ = h[1];
+    v0_ = h[2] > 0 ? h[2] : 10.0;
+    a0_ = h[3] > 0 ? h[3] : 1.0;
+    b0_ = h[4] > 0 ? h[4] : 1.0;
+    seed_ = d.seed;
+    for (int i = 0; i < 5; ++i) var_[i] = d.var_ids[i];
+    x_.alloc(std::max<std::int64_t>(N_, 1));
+    z_.alloc(std::max<std::int64_t>(N_, 1));
+    pi_.alloc(K_);
+    mu_.alloc(K_);
+    s2_.alloc(K_);
+    part_.alloc(static_cast<std::size_t>(kBlocks) * K_ * 3);
+    lpart_.alloc(kBlocks * 2);
+    part_.zero(nullptr);
+    lpart_.zero(nullptr);
+    z_.zero(nullptr);
+    BNMC_CUDA(cudaDeviceSynchronize());
+  }
+
+  void upload(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, true); }
+  void upload_state(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, !data_); }
+
+  void upload_impl(const bnmc_gpu_store& s, cudaStream_t st, bool with_data) {
+    require(s.n_vars > 4, BNMC_GPU_ERR_RUNTIME, "store has the wrong number of variables");
+    const int vpi = var_[0], vmu = var_[1], vs2 = var_[2], vz = var_[3], vx = var_[4];
+    require(s.len[vpi] == K_ && s.len[vmu] == K_ && s.len[vs2] == K_ && s.len[vz] == N_ &&
+                s.len[vx] == N_,
+            BNMC_GPU_ERR_RUNTIME, "GMM store arrays have the wrong flat lengths");
+    if (with_data) BNMC_CUDA(cudaMemcpyAsync(x_.p, s.real[vx], sizeof(double) * N_, cudaMemcpyHostToDevice, st));
+    data_ = true;
+    BNMC_CUDA(cudaMemcpyAsync(pi_.p, s.real[vpi], sizeof(double) * K_, cudaMemcpyHostToDevice, st));
+    BNMC_CUDA(cudaMemcpyAsync(mu_.p, s.real[vmu], sizeof(double) * K_, cudaMemcpyHostToDevice, st));
+    BNMC_CUDA(cudaMemcpyAsync(s2_.p, s.real[vs2], sizeof(double) * K_, cudaMemcpyHostToDevice, st));
+    if (N_ > 0) {
+      DevBuf<std::int64_t> tmp;
+      tmp.alloc(N_);
+      BNMC_CUDA(cudaMemcpyAsync(tmp.p, s.ival[vz], sizeof(std::int64_t) * N_, cudaMemcpyHostToDevice, st));
+      z_from_i64<<<kBlocks, kThreads, 0, st>>>(tmp.p, z_.p, N_, K_, out.err);
+      BNMC_CUDA(cudaStreamSynchronize(st));
+    }
+    BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  void download(const bnmc_gpu_store& s, cudaStream_t st) override {
+    const int vpi = var_[0], vmu = var_[1], vs2 = var_[2], vz = var_[3];
+    const char* obs = s.observed;
+    auto want = [&](int v) { return !(obs && obs[v]); };
+    if (want(vpi)) BNMC_CUDA(cudaMemcpyAsync(s.real[vpi], pi_.p, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
+    if (want(vmu)) BNMC_CUDA(cudaMemcpyAsync(s.real[vmu], mu_.p, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
+    if (want(vs2)) BNMC_CUDA(cudaMemcpyAsync(s.real[vs2], s2_.p, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
+    if (want(vz) && N_ > 0) {
+      DevBuf<std::int64_t> tmp;
+      tmp.alloc(N_);
+      z_to_i64<<<kBlocks, kThreads, 0, st>>>(z_.p, tmp.p, N_);
+      BNMC_CUDA(cudaMemcpyAsync(s.ival[vz], tmp.p, sizeof(std::int64_t) * N_, cudaMemcpyDeviceToHost, st));
+      BNMC_CUDA(cudaStreamSynchronize(st));
+    }
+    BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  void enqueue_sweep(cudaStream_t st) override {
+    GmmArgs a = args();
+    mark(st, "begin");
+    stats_kernel<kStatsMu><<<kBlocks, kThreads, 0, st>>>(a, out.err);
+    mark(st, "stats_mu");
+    draw_pi_mu_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
+    mark(st, "draw_pi_mu");
+    stats_kernel<kStatsRss><<<kBlocks, kThreads, 0, st>>>(a, out.err);
+    mark(st, "stats_rss");
+    draw_s2_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
+    mark(st, "draw_sigma2");
+    z_kernel<true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    mark(st, "z");
+    finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 1);
+    mark(st, "finalize");
+    BNMC_CUDA(cudaGetLastError());
+  }
+
+  void enqueue_log_joint(cudaStream_t st) override {
+    GmmArgs a = args();
+    z_kernel<false><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 0);
+    BNMC_CUDA(cudaGetLastError());
+  }
+
+  void prior_init(std::uint64_t seed, cudaStream_t st) override {
+    GmmArgs a = args();
+    prior_kernel<<<1, 32, 0, st>>>(a, seed);
+    prior_z_kernel<<<kBlocks, kThreads, 0, st>>>(a, seed);
+    BNMC_CUDA(cudaGetLastError());
+    BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+ private:
+  GmmArgs args() const {
+    GmmArgs a{};
+    a.N = N_;
+    a.K = K_;
+    a.x = x_.p;
+    a.z = z_.p;
+    a.pi = pi_.p;
+    a.mu = mu_.p;
+    a.s2 = s2_.p;
+    a.part = part_.p;
+    a.lpart = lpart_.p;
+    a.alpha = alpha_;
+    a.mu0 = mu0_;
+    a.v0 = v0_;
+    a.a0 = a0_;
+    a.b0 = b0_;
+    a.seed = seed_;
+    a.var_pi = var_[0];
+    a.var_mu = var_[1];
+    a.var_s2 = var_[2];
+    a.var_z = var_[3];
+    return a;
+  }
+
+  bool data_ = false;
+  int K_ = 0;
+  std::int64_t N_ = 0;
+  double alpha_, mu0_, v0_, a0_, b0_;
+  std::uint64_t seed_ = 0;
+  int var_[5] = {0, 1, 2, 3, 4};
+  DevBuf<double> x_, pi_, mu_, s2_, part_, lpart_;
+  DevBuf<int> z_;
+};
+
+}  // namespace
+
+std::unique_ptr<Model> make_gmm(const bnmc_gpu_desc& d, const Comm& c, Outputs o) {
+  return std::make_unique<Gmm>(d, c, o);
+}
+
+}  // namespace bnmc_gpu

@@ -1,0 +1,379 @@
+// csrc/mh.cu -- random-walk Metropolis-Hastings over i.i.d. rows
+// (Engine::run_mh_block, proj/src/sampler.cpp:284-340).
+//
+// Models: proj/models/regression.bn (y ~ N(w.x + b, tau), method MH) and its
+// logistic twin (y ~ Bernoulli(sigmoid(w.x + b)); no reference model exists, the
+// MH machinery is shared).  The reference evaluates the blanket before, the
+// blanket after, and the full log-joint: three passes over the N x K data.  Here
+// the current state's blanket is cached on the device, so one step is ONE pass:
+//
+//   propose_kernel   w' = w + s*N(0,1) from keyed(seed,1,var,t,iter) (:311-318)
+//   lik_kernel       per-row log-likelihood of the proposal, warp per row,
+//                    fixed-grid partial sums (the data-parallel reduction)
+//   [allreduce]      NCCL double sum of the partial (row-sharded, world > 1)
+//   accept_kernel    after = priors(w') + lik; accept iff isfinite(after) &&
+//                    log(u) < after - before, u from keyed(seed,2,vars[0],iter)
+//                    (:321-328); commit or keep; log-joint
+//                    = Fw + Fb + Ftau + Fx + Fy in the reference's order.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "dist.cuh"
+
+namespace bnmc_gpu {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBlocks = 148 * 8;
+
+struct MhArgs {
+  std::int64_t N;  // local rows
+  int K;
+  const double* x;
+  const double* y;
+  double* w;      // [K+2]: w..., b, tau (current)
+  double* wp;     // [K+2]: proposal
+  double* part;   // [kBlocks]
+  double* state;  // [8]: cur_lik, cur_fw, cur_fb, cur_ftau, fx, lik_prop, -, -
+  double lo, hi, w_var, b_var, tau_a, tau_b, mh_scale;
+  std::uint64_t seed;
+  int var_w, var_b, var_tau;
+  int logistic;
+};
+
+__device__ __forceinline__ double softplus(double s) {
+  return s > 0.0 ? s + log1p(exp(-s)) : log1p(exp(s));
+}
+
+__global__ void propose_kernel(MhArgs a, const std::int64_t* iter_p) {
+  const std::int64_t iter = *iter_p;
+  for (int t = threadIdx.x; t < a.K + 2; t += blockDim.x) {
+    double v = a.w[t];
+    if (t < a.K) {
+      Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(a.var_w), static_cast<std::uint64_t>(t),
+                     static_cast<std::uint64_t>(iter)));
+      v += a.mh_scale * r.next_gaussian();
+    } else if (t == a.K) {
+      Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(a.var_b), 0, static_cast<std::uint64_t>(iter)));
+      v += a.mh_scale * r.next_gaussian();
+    } else if (!a.logistic) {
+      Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(a.var_tau), 0, static_cast<std::uint64_t>(iter)));
+      v += a.mh_scale * r.next_gaussian();
+    }
+    a.wp[t] = v;
+  }
+}
+
+// Sum over local rows of the row log-likelihood at parameters p (K + 2 values).
+// Warp per row: lanes stride the K features (coalesced 256 B per load), the dot
+// product is a fixed butterfly.
+__global__ void __launch_bounds__(kThreads) lik_kernel(MhArgs a, const double* p, double* part) {
+  extern __shared__ double wsh[];
+  __shared__ double scratch[32];
+  for (int j = threadIdx.x; j < a.K + 2; j += blockDim.x) wsh[j] = p[j];
+  __syncthreads();
+  const double b = wsh[a.K], tau = wsh[a.K + 1];
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (std::int64_t i = warp; i < a.N; i += nwarps) {
+    const double* xi = a.x + i * a.K;
+    double s = 0.0;
+    for (int j = lane; j < a.K; j += 32) s += wsh[j] * __ldg(xi + j);
+    s = warp_sum(s) + b;
+    if (lane == 0) {
+      const double yi = __ldg(a.y + i);
+      acc += a.logistic ? yi * s - softplus(s) : log_pdf_gaussian(yi, s, tau);
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// log prod_{i,j} Uniform(x_ij | lo, hi): -log(hi - lo) each, -inf outside [lo, hi].
+__global__ void fx_kernel(MhArgs a, double* part) {
+  __shared__ double scratch[32];
+  double acc = 0.0;
+  const double c = -log(a.hi - a.lo);
+  const std::int64_t n = a.N * a.K;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const double v = a.x[i];
+    acc += (!(a.hi > a.lo) || v < a.lo || v > a.hi) ? -INFINITY : c;
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__device__ double priors(const MhArgs& a, const double* p, double* fw, double* fb, double* ftau) {
+  double s = 0.0;
+  for (int j = 0; j < a.K; ++j) s += log_pdf_gaussian(p[j], 0.0, a.w_var);
+  *fw = s;
+  *fb = log_pdf_gaussian(p[a.K], 0.0, a.b_var);
+  *ftau = a.logistic ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
+  return a.logistic ? (*fw + *fb) : ((*fw + *fb) + *ftau);
+}
+
+__device__ double sum_parts(const double* part, int n, double* scratch) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) s += part[b];
+  return block_sum(s, scratch);
+}
+
+// mode 0: initialise the cache from the current state (no step);
+// mode 1: MH step; mode 2: log-joint of the current state only.
+__global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_total) {
+  __shared__ double scratch[32];
+  __shared__ int take_s;
+  const double lik = sum_parts(a.part, kBlocks, scratch);
+  const double fx = a.state[4];
+  if (threadIdx.x == 0) {
+    const std::int64_t it = *o.iter;
+    const double lik_all = lik_total ? *lik_total : lik;
+    int take = 0;
+    if (mode == 0) {
+      double fw, fb, ft;
+      priors(a, a.w, &fw, &fb, &ft);
+      a.state[0] = lik_all;
+      a.state[1] = fw;
+      a.state[2] = fb;
+      a.state[3] = ft;
+    } else if (mode == 1) {
+      double fw, fb, ft;
+      const double pr = priors(a, a.wp, &fw, &fb, &ft);
+      const double after = pr + lik_all;
+      const double before = a.logistic ? ((a.state[1] + a.state[2]) + a.state[0])
+                                       : (((a.state[1] + a.state[2]) + a.state[3]) + a.state[0]);
+      const double delta = after - before;
+      Stream acc(keyed(a.seed, kAccept, static_cast<std::uint64_t>(a.var_w), static_cast<std::uint64_t>(it)));
+      take = isfinite(after) && log(acc.next_unit()) < delta;
+      if (take) {
+        a.state[0] = lik_all;
+        a.state[1] = fw;
+        a.state[2] = fb;
+        a.state[3] = ft;
+      }
+    }
+    take_s = take;
+    const double lj = a.logistic ? (((a.state[1] + a.state[2]) + fx) + a.state[0])
+                                 : ((((a.state[1] + a.state[2]) + a.state[3]) + fx) + a.state[0]);
+    o.lj[it & (kRing - 1)] = lj;
+    o.acc[it & (kRing - 1)] = take;
+    if (mode == 1) *o.iter = it + 1;
+  }
+  __syncthreads();
+  if (mode == 1 && take_s)
+    for (int t = threadIdx.x; t < a.K + 2; t += blockDim.x) a.w[t] = a.wp[t];
+}
+
+__global__ void fx_finalize_kernel(MhArgs a, const double* fx_total) {
+  __shared__ double scratch[32];
+  const double s = sum_parts(a.part, kBlocks, scratch);
+  if (threadIdx.x == 0) a.state[4] = fx_total ? *fx_total : s;
+}
+
+// prior_init: w_t ~ N(0, w_var), b ~ N(0, b_var), tau ~ IG(tau_a, tau_b), one stream
+// keyed(seed,5,var,t) per element (sampler.cpp:542-555, draw_gaussian dist.cpp:161-163).
+__global__ void prior_kernel(MhArgs a, std::uint64_t seed) {
+  for (int t = threadIdx.x; t < a.K + 2; t += blockDim.x) {
+    if (t < a.K) {
+      Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_w), static_cast<std::uint64_t>(t)));
+      a.w[t] = 0.0 + sqrt(a.w_var) * r.next_gaussian();
+    } else if (t == a.K) {
+      Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_b), 0));
+      a.w[t] = 0.0 + sqrt(a.b_var) * r.next_gaussian();
+    } else {
+      if (a.logistic) {
+        a.w[t] = 0.0;
+      } else {
+        Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_tau), 0));
+        a.w[t] = a.tau_b / draw_gamma(r, a.tau_a);
+      }
+    }
+  }
+}
+
+__global__ void sum_to_kernel(const double* part, int n, double* out) {
+  __shared__ double scratch[32];
+  const double s = sum_parts(part, n, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+class Mh final : public Model {
+ public:
+  Mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o) : comm_(c) {
+    out = o;
+    logistic_ = d.kind == BNMC_GPU_MH_LOGREG;
+    require(d.K >= 1 && d.N >= 0, BNMC_GPU_ERR_ARG, "MH needs K >= 1 features");
+    K_ = static_cast<int>(d.K);
+    N_ = d.N;
+    r0_ = N_ * c.rank / c.world;
+    r1_ = N_ * (c.rank + 1) / c.world;
+    Nl_ = r1_ - r0_;
+    const double* h = d.hyper;
+    lo_ = h[0];
+    hi_ = h[1];
+    w_var_ = h[2] > 0 ? h[2] : 10.0;
+    b_var_ = h[3] > 0 ? h[3] : 10.0;
+    tau_a_ = h[4] > 0 ? h[4] : 3.0;
+    tau_b_ = h[5] > 0 ? h[5] : 1.0;
+    mh_scale_ = d.mh_scale;
+    seed_ = d.seed;
+    for (int i = 0; i < 5; ++i) var_[i] = d.var_ids[i];
+    x_.alloc(std::max<std::int64_t>(Nl_ * K_, 1));
+    y_.alloc(std::max<std::int64_t>(Nl_, 1));
+    w_.alloc(K_ + 2);
+    wp_.alloc(K_ + 2);
+    part_.alloc(kBlocks);
+    state_.alloc(8);
+    tot_.alloc(2);
+    w_.zero(nullptr);
+    wp_.zero(nullptr);
+    part_.zero(nullptr);
+    state_.zero(nullptr);
+    tot_.zero(nullptr);
+    BNMC_CUDA(cudaDeviceSynchronize());
+  }
+
+  void upload(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, true); }
+  void upload_state(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, !data_); }
+
+  void upload_impl(const bnmc_gpu_store& s, cudaStream_t st, bool with_data) {
+    const int vw = var_[0], vb = var_[1];
+    const int vtau = logistic_ ? -1 : var_[2];
+    const int vx = logistic_ ? var_[2] : var_[3], vy = logistic_ ? var_[3] : var_[4];
+    require(s.len[vw] == K_ && s.len[vb] == 1 && s.len[vx] == N_ * K_ && s.len[vy] == N_ &&
+                (vtau < 0 || s.len[vtau] == 1),
+            BNMC_GPU_ERR_RUNTIME, "MH store arrays have the wrong flat lengths");
+    std::vector<double> p(K_ + 2, 0.0);
+    for (int j = 0; j < K_; ++j) p[j] = s.real[vw][j];
+    p[K_] = s.real[vb][0];
+    p[K_ + 1] = vtau >= 0 ? s.real[vtau][0] : 0.0;
+    BNMC_CUDA(cudaMemcpyAsync(w_.p, p.data(), sizeof(double) * (K_ + 2), cudaMemcpyHostToDevice, st));
+    if (Nl_ > 0 && with_data) {
+      BNMC_CUDA(cudaMemcpyAsync(x_.p, s.real[vx] + r0_ * K_, sizeof(double) * Nl_ * K_, cudaMemcpyHostToDevice, st));
+      BNMC_CUDA(cudaMemcpyAsync(y_.p, s.real[vy] + r0_, sizeof(double) * Nl_, cudaMemcpyHostToDevice, st));
+    }
+    data_ = true;
+    BNMC_CUDA(cudaStreamSynchronize(st));
+    refresh(st);
+  }
+
+  void download(const bnmc_gpu_store& s, cudaStream_t st) override {
+    std::vector<double> p(K_ + 2);
+    BNMC_CUDA(cudaMemcpyAsync(p.data(), w_.p, sizeof(double) * (K_ + 2), cudaMemcpyDeviceToHost, st));
+    BNMC_CUDA(cudaStreamSynchronize(st));
+    const char* obs = s.observed;
+    const int vw = var_[0], vb = var_[1];
+    if (!(obs && obs[vw]))
+      for (int j = 0; j < K_; ++j) s.real[vw][j] = p[j];
+    if (!(obs && obs[vb])) s.real[vb][0] = p[K_];
+    if (!logistic_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
+  }
+
+  void enqueue_sweep(cudaStream_t st) override {
+    MhArgs a = args();
+    mark(st, "begin");
+    propose_kernel<<<1, 128, 0, st>>>(a, out.iter);
+    mark(st, "propose");
+    lik_kernel<<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, wp_.p, part_.p);
+    mark(st, "lik");
+    const double* tot = nullptr;
+    if (comm_.world > 1) {
+      sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
+      BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      tot = tot_.p;
+      mark(st, "allreduce_lik");
+    }
+    accept_kernel<<<1, 256, 0, st>>>(a, out, 1, tot);
+    mark(st, "accept");
+    BNMC_CUDA(cudaGetLastError());
+  }
+
+  void enqueue_log_joint(cudaStream_t st) override {
+    MhArgs a = args();
+    // The cached state already holds the current blanket; report it.
+    accept_kernel_cached(a, st);
+  }
+
+  void prior_init(std::uint64_t seed, cudaStream_t st) override {
+    prior_kernel<<<1, 128, 0, st>>>(args(), seed);
+    BNMC_CUDA(cudaGetLastError());
+    BNMC_CUDA(cudaStreamSynchronize(st));
+    refresh(st);
+  }
+
+ private:
+
+  void accept_kernel_cached(const MhArgs& a, cudaStream_t st) {
+    lik_kernel<<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, w_.p, part_.p);
+    const double* tot = nullptr;
+    if (comm_.world > 1) {
+      sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
+      BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      tot = tot_.p;
+    }
+    accept_kernel<<<1, 256, 0, st>>>(a, out, 0, tot);
+    BNMC_CUDA(cudaGetLastError());
+  }
+
+  // Recompute the constant data factor and the cached blanket of the current state.
+  void refresh(cudaStream_t st) {
+    MhArgs a = args();
+    fx_kernel<<<kBlocks, kThreads, 0, st>>>(a, part_.p);
+    const double* tot = nullptr;
+    if (comm_.world > 1) {
+      sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p + 1);
+      BNMC_NCCL(ncclAllReduce(tot_.p + 1, tot_.p + 1, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      tot = tot_.p + 1;
+    }
+    fx_finalize_kernel<<<1, 256, 0, st>>>(a, tot);
+    accept_kernel_cached(a, st);
+    BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  MhArgs args() const {
+    MhArgs a{};
+    a.N = Nl_;
+    a.K = K_;
+    a.x = x_.p;
+    a.y = y_.p;
+    a.w = w_.p;
+    a.wp = wp_.p;
+    a.part = part_.p;
+    a.state = state_.p;
+    a.lo = lo_;
+    a.hi = hi_;
+    a.w_var = w_var_;
+    a.b_var = b_var_;
+    a.tau_a = tau_a_;
+    a.tau_b = tau_b_;
+    a.mh_scale = mh_scale_;
+    a.seed = seed_;
+    a.var_w = var_[0];
+    a.var_b = var_[1];
+    a.var_tau = logistic_ ? -1 : var_[2];
+    a.logistic = logistic_ ? 1 : 0;
+    return a;
+  }
+
+  Comm comm_;
+  bool data_ = false;
+  bool logistic_ = false;
+  int K_ = 0;
+  std::int64_t N_ = 0, r0_ = 0, r1_ = 0, Nl_ = 0;
+  double lo_, hi_, w_var_, b_var_, tau_a_, tau_b_, mh_scale_;
+  std::uint64_t seed_ = 0;
+  int var_[5] = {0, 1, 2, 3, 4};
+  DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_;
+};
+
+}  // namespace
+
+std::unique_ptr<Model> make_mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o) {
+  return std::make_unique<Mh>(d, c, o);
+}
+
+}  // namespace bnmc_gpu

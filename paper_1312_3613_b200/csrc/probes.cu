@@ -1,0 +1,219 @@
+// csrc/probes.cu -- standalone device operators behind the C-ABI:
+// the reference's primitive operators (RngStream, draw_gamma,
+// draw_from_log_weights, sample_dirichlet_batch) and log_predictive_probability,
+// each run on the GPU for known-answer parity and for callers that use them
+// directly.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "dist.cuh"
+
+namespace bnmc_gpu {
+namespace {
+
+__global__ void rng_probe_kernel(const std::uint64_t* keys, std::int64_t n, std::int64_t per,
+                                 std::uint64_t* u64, double* unit, double* gauss) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  Stream a(keys[i]), b(keys[i]), c(keys[i]);
+  for (std::int64_t j = 0; j < per; ++j) {
+    if (u64) u64[i * per + j] = a.next_u64();
+    if (unit) unit[i * per + j] = b.next_unit();
+    if (gauss) gauss[i * per + j] = c.next_gaussian();
+  }
+}
+
+__global__ void gamma_probe_kernel(const std::uint64_t* keys, const double* shapes, std::int64_t n,
+                                   double* out, std::uint64_t* counters) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  Stream r(keys[i]);
+  out[i] = draw_gamma(r, shapes[i]);
+  if (counters) counters[i] = r.counter;
+}
+
+// draw_from_log_weights (dist.cpp:202-215), one row per thread, reference order.
+__global__ void logw_probe_kernel(const std::uint64_t* keys, const double* logw, std::int64_t rows,
+                                  std::int64_t cols, std::int64_t* picks) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  const double* lw = logw + i * cols;
+  double mx = -INFINITY;
+  for (std::int64_t j = 0; j < cols; ++j)
+    if (mx < lw[j]) mx = lw[j];
+  if (!isfinite(mx)) {
+    picks[i] = -1;
+    return;
+  }
+  double total = 0.0;
+  for (std::int64_t j = 0; j < cols; ++j) total += exp(lw[j] - mx);
+  Stream r(keys[i]);
+  const double u = r.next_unit() * total;
+  double acc = 0.0;
+  std::int64_t pick = cols - 1;
+  for (std::int64_t j = 0; j < cols; ++j) {
+    acc += exp(lw[j] - mx);
+    if (u < acc) {
+      pick = j;
+      break;
+    }
+  }
+  picks[i] = pick;
+}
+
+// sample_dirichlet_batch: one thread per cell (stream derive(key, r, c)), then a
+// fixed-order row sum and normalisation (batch.cpp:38-63).
+__global__ void dir_cells_kernel(std::int64_t rows, std::int64_t cols, const double* alpha,
+                                 std::uint64_t key, double* out, int* err) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows * cols) return;
+  const double a = alpha[i];
+  if (!(a > 0.0)) {
+    atomicOr(err, 4);
+    return;
+  }
+  Stream s(derive(key, static_cast<std::uint64_t>(i / cols), static_cast<std::uint64_t>(i % cols)));
+  out[i] = draw_gamma(s, a);
+}
+
+__global__ void dir_norm_kernel(std::int64_t cols, double* out) {
+  __shared__ double scratch[32];
+  double* row = out + blockIdx.x * cols;
+  double s = 0.0;
+  for (std::int64_t c = threadIdx.x; c < cols; c += blockDim.x) s += row[c];
+  s = block_sum(s, scratch);
+  for (std::int64_t c = threadIdx.x; c < cols; c += blockDim.x) row[c] /= s;
+}
+
+// log_predictive_probability (metrics.cpp:9-34): warp per held-out token.
+__global__ void lpp_kernel(const double* phi, const double* theta, int K, std::int64_t V,
+                           const std::int64_t* w, const std::int64_t* off, std::int64_t docs,
+                           double* part, int* err) {
+  __shared__ double scratch[32];
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (std::int64_t d = blockIdx.x; d < docs; d += gridDim.x) {
+    const double* th = theta + d * K;
+    for (std::int64_t t = off[d] + (threadIdx.x >> 5); t < off[d + 1]; t += blockDim.x >> 5) {
+      const std::int64_t wv = w[t];
+      if (wv < 0 || wv >= V) {
+        if (lane == 0) atomicOr(err, 4);
+        continue;
+      }
+      double p = 0.0;
+      for (int k = lane; k < K; k += 32) p += th[k] * phi[static_cast<std::size_t>(k) * V + wv];
+      p = warp_sum(p);
+      if (lane == 0) acc += log10(p);
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+template <class T>
+void h2d(DevBuf<T>& b, const T* h, std::size_t n) {
+  b.alloc(n);
+  if (n) BNMC_CUDA(cudaMemcpy(b.p, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+}
+
+template <class T>
+void d2h(T* h, const DevBuf<T>& b) {
+  if (b.n) BNMC_CUDA(cudaMemcpy(h, b.p, b.bytes(), cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+
+void probe_rng(const std::uint64_t* keys, std::int64_t n, std::int64_t per, std::uint64_t* u64,
+               double* unit, double* gauss) {
+  DevBuf<std::uint64_t> k, du;
+  DevBuf<double> dn, dg;
+  h2d(k, keys, n);
+  du.alloc(u64 ? n * per : 0);
+  dn.alloc(unit ? n * per : 0);
+  dg.alloc(gauss ? n * per : 0);
+  rng_probe_kernel<<<blocks_for(n, 128), 128>>>(k.p, n, per, du.p, dn.p, dg.p);
+  BNMC_CUDA(cudaGetLastError());
+  BNMC_CUDA(cudaDeviceSynchronize());
+  if (u64) d2h(u64, du);
+  if (unit) d2h(unit, dn);
+  if (gauss) d2h(gauss, dg);
+}
+
+void probe_gamma(const std::uint64_t* keys, const double* shapes, std::int64_t n, double* out,
+                 std::uint64_t* counters) {
+  DevBuf<std::uint64_t> k, c;
+  DevBuf<double> s, o;
+  h2d(k, keys, n);
+  h2d(s, shapes, n);
+  o.alloc(n);
+  c.alloc(counters ? n : 0);
+  gamma_probe_kernel<<<blocks_for(n, 128), 128>>>(k.p, s.p, n, o.p, c.p);
+  BNMC_CUDA(cudaGetLastError());
+  BNMC_CUDA(cudaDeviceSynchronize());
+  d2h(out, o);
+  if (counters) d2h(counters, c);
+}
+
+void probe_log_weights(const std::uint64_t* keys, const double* logw, std::int64_t rows,
+                       std::int64_t cols, std::int64_t* picks) {
+  DevBuf<std::uint64_t> k;
+  DevBuf<double> l;
+  DevBuf<std::int64_t> p;
+  h2d(k, keys, rows);
+  h2d(l, logw, rows * cols);
+  p.alloc(rows);
+  logw_probe_kernel<<<blocks_for(rows, 128), 128>>>(k.p, l.p, rows, cols, p.p);
+  BNMC_CUDA(cudaGetLastError());
+  BNMC_CUDA(cudaDeviceSynchronize());
+  d2h(picks, p);
+}
+
+void dirichlet_batch(std::int64_t rows, std::int64_t cols, const double* alpha, std::uint64_t key,
+                     double* out) {
+  require(rows >= 1 && cols >= 1, BNMC_GPU_ERR_ARG, "batch needs rows, cols >= 1");
+  DevBuf<double> a, o;
+  DevBuf<int> err;
+  h2d(a, alpha, rows * cols);
+  o.alloc(rows * cols);
+  err.alloc(1);
+  err.zero(nullptr);
+  dir_cells_kernel<<<blocks_for(rows * cols, 128), 128>>>(rows, cols, a.p, key, o.p, err.p);
+  dir_norm_kernel<<<static_cast<unsigned>(rows), 256>>>(cols, o.p);
+  BNMC_CUDA(cudaGetLastError());
+  BNMC_CUDA(cudaDeviceSynchronize());
+  int e = 0;
+  BNMC_CUDA(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  require(e == 0, BNMC_GPU_ERR_ARG, "Dirichlet concentrations must be positive");
+  d2h(out, o);
+}
+
+double lpp(const double* phi, const double* theta, std::int64_t K, std::int64_t V,
+           const std::int64_t* w, const std::int64_t* off, std::int64_t docs) {
+  require(K >= 1 && V >= 1 && docs >= 0, BNMC_GPU_ERR_ARG, "lpp needs topics, vocab >= 1");
+  DevBuf<double> p, t, part;
+  DevBuf<std::int64_t> wd, od;
+  DevBuf<int> err;
+  const std::int64_t n = off[docs];
+  h2d(p, phi, K * V);
+  h2d(t, theta, docs * K);
+  h2d(wd, w, n);
+  h2d(od, off, docs + 1);
+  const unsigned nb = static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(docs, 148 * 8)));
+  part.alloc(nb);
+  err.alloc(1);
+  err.zero(nullptr);
+  lpp_kernel<<<nb, 256>>>(p.p, t.p, static_cast<int>(K), V, wd.p, od.p, docs, part.p, err.p);
+  BNMC_CUDA(cudaGetLastError());
+  std::vector<double> h(nb);
+  BNMC_CUDA(cudaDeviceSynchronize());
+  int e = 0;
+  BNMC_CUDA(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  require(e == 0, BNMC_GPU_ERR_ARG, "token id outside the vocabulary");
+  d2h(h.data(), part);
+  double total = 0.0;  // final fold of <= 1184 block partials, fixed order
+  for (double v : h) total += v;
+  return total;
+}
+
+}  // namespace bnmc_gpu

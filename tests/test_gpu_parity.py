@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's outputs.
+
+Contract: integer state (z, counts, MH accept decisions) bit-exact;
+phi/theta <= 1e-12 relative per element; GMM mu/sigma2 <= 1e-10; log-joint <= 1e-10
+relative.  The float tolerances exist because device log/exp/cos/pow may differ from
+glibc's by an ulp (the RNG integer stream itself is bit-exact).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+RTOL_PARAM = 1e-12
+RTOL_MU = 1e-10
+RTOL_LJ = 1e-10
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_1312_3613_b200 as g
+
+    g.lib()
+    return g
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if a.size else 0.0
+
+
+# ----------------------------------------------------------------------------------------
+# primitives
+# ----------------------------------------------------------------------------------------
+def test_rng_bit_exact(g):
+    r = golden("rng_dist")
+    u, un, ga = g.probe_rng(r["keys"], 16)
+    assert np.array_equal(u, r["u64"])            # integer stream: bit-exact
+    assert np.array_equal(un, r["unit"])          # (u >> 11 + 0.5) * 2^-53: exact
+    assert rel(ga, r["gauss"]) < 1e-14            # Box-Muller through device log/cos
+
+
+def test_gamma_draws(g):
+    r = golden("rng_dist")
+    shapes = np.repeat(r["gamma_shapes"], len(r["gamma_keys"]))
+    keys = np.tile(r["gamma_keys"], len(r["gamma_shapes"]))
+    out, cnt = g.probe_gamma(keys, shapes)
+    assert np.array_equal(cnt, r["gamma_counters"].ravel())  # same rejection path everywhere
+    assert rel(out, r["gamma"].ravel()) < RTOL_PARAM
+
+
+def test_draw_from_log_weights(g):
+    r = golden("rng_dist")
+    picks = g.probe_log_weights(r["logw_keys"], r["logw"])
+    assert np.array_equal(picks[picks >= 0], r["logw_picks"][picks >= 0])
+
+
+def test_dirichlet_batch(g):
+    r = golden("rng_dist")
+    out = g.dirichlet_batch(r["dir_alpha"], int(r["dir_key"]))
+    assert rel(out, r["dir_out"]) < RTOL_PARAM
+    with pytest.raises(ValueError):
+        g.dirichlet_batch(np.array([[1.0, 0.0]]), 1)
+
+
+# ----------------------------------------------------------------------------------------
+# LDA
+# ----------------------------------------------------------------------------------------
+def lda_engine(g, fx, exact=False, graph=True, observe=()):
+    K, V, M = int(fx["K"]), int(fx["V"]), int(fx["M"])
+    lengths = np.diff(fx["offsets"])
+    hyper = {"K": K, "V": V, "M": M, "N": lengths.tolist()}
+    cfg = g.RunConfig(seed=int(fx["seed"]), exact_weights=exact, use_graph=graph, observe_extra=list(observe))
+    e = g.Engine("lda", hyper, cfg)
+    s = e.allocate()
+    s["w"] = fx["w"]
+    s["z"] = fx["z0"]
+    s["phi"] = fx["phi0"]
+    s["theta"] = fx["theta0"]
+    return e, s
+
+
+@pytest.mark.parametrize("name", ["lda_desk", "lda_ragged", "lda_k1"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_lda_sweeps_vs_reference(g, name, exact):
+    fx = golden(name)
+    e, s = lda_engine(g, fx, exact=exact)
+    assert abs(e.eval_log_joint(s) - fx["lj0"]) <= RTOL_LJ * abs(fx["lj0"])
+    for it in range(len(fx["lj"])):
+        lj = e.sweep(s, it)
+        assert np.array_equal(s["z"], fx["z"][it]), f"z mismatch at sweep {it}: {(s['z'] != fx['z'][it]).sum()}"
+        assert rel(s["phi"], fx["phi"][it]) < RTOL_PARAM
+        assert rel(s["theta"], fx["theta"][it]) < RTOL_PARAM
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
+    e.close()
+
+
+def test_lda_counts_bit_exact(g):
+    fx = golden("lda_desk")
+    e, s = lda_engine(g, fx)
+    e.upload(s)
+    K, V = int(fx["K"]), int(fx["V"])
+    nkw, nmk = e.lda_counts()
+    z, w, off = fx["z0"], fx["w"], fx["offsets"]
+    want = np.zeros((K, V), dtype=np.int64)
+    np.add.at(want, (z, w), 1)
+    assert np.array_equal(nkw, want)
+    docs = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    wm = np.zeros((len(off) - 1, K), dtype=np.int64)
+    np.add.at(wm, (docs, z), 1)
+    assert np.array_equal(nmk, wm)
+    assert nkw.sum() == len(z)
+
+
+def test_lda_graph_equals_direct_launch(g):
+    fx = golden("lda_desk")
+    e1, s1 = lda_engine(g, fx, graph=True)
+    e2, s2 = lda_engine(g, fx, graph=False)
+    for it in range(3):
+        assert e1.sweep(s1, it) == e2.sweep(s2, it)
+        assert np.array_equal(s1["z"], s2["z"]) and np.array_equal(s1["phi"], s2["phi"])
+
+
+def test_lda_run_matches_stepwise(g):
+    """run_device (one host sync for n sweeps) == n single sweeps, bitwise."""
+    fx = golden("lda_desk")
+    e1, s1 = lda_engine(g, fx)
+    e2, s2 = lda_engine(g, fx)
+    e1.upload(s1)
+    lj, _ = e1.run_device(0, 4)
+    e1.download(s1)
+    ljs = [e2.sweep(s2, it) for it in range(4)]
+    assert np.array_equal(lj, ljs)
+    assert np.array_equal(s1["z"], s2["z"]) and np.array_equal(s1["theta"], s2["theta"])
+
+
+def test_lda_observed_phi_never_written(g, restatement):
+    """Clamped phi (bench.cpp:30-77 protocol): no phi block, phi untouched, z exact."""
+    fx = golden("lda_desk")
+    e, s = lda_engine(g, fx, observe=("phi",))
+    phi0 = s["phi"].copy()
+    K, V = int(fx["K"]), int(fx["V"])
+    off, w = fx["offsets"], fx["w"]
+    z, phi, theta = fx["z0"].copy(), fx["phi0"].copy(), fx["theta0"].copy()
+    for it in range(3):
+        lj = e.sweep(s, it)
+        lj2 = restatement.lda_sweep(K, V, off, w, z, phi, theta, int(fx["seed"]), it, observe_phi=True)
+        assert np.array_equal(s["phi"], phi0)
+        assert np.array_equal(s["z"], z)
+        assert abs(lj - lj2) <= RTOL_LJ * abs(lj2)
+
+
+def test_lda_bad_assignment_raises(g):
+    fx = golden("lda_desk")
+    e, s = lda_engine(g, fx)
+    z = s["z"].copy()
+    z[3] = int(fx["K"])  # outside the support
+    s["z"] = z
+    with pytest.raises(g.BnmcError):
+        e.upload(s)
+
+
+def _gen_lda(restatement, reference, M, V, K, L, seed):
+    w, _, _ = reference.gen_lda(M, V, K, L, seed)
+    off = np.arange(M + 1, dtype=np.int64) * L
+    phi, theta, z = restatement.lda_prior_init(K, V, off, w, seed)
+    return w, off, phi, theta, z
+
+
+@pytest.mark.parametrize("cfg", [("kos", 3430, 6906, 50, 136), ("nips", 1500, 12419, 100, 1267)])
+def test_lda_full_size_one_sweep(g, restatement, reference, cfg):
+    """KOS / NIPS-shaped corpora: one sweep from the reference's prior_init
+    state; z and the counts must be bit-exact (0 mismatches), floats within tolerance."""
+    name, M, V, K, L = cfg
+    seed = 42
+    w, off, phi, theta, z = _gen_lda(restatement, reference, M, V, K, L, seed)
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+    e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["w"], s["z"], s["phi"], s["theta"] = w, z, phi, theta
+    lj = e.sweep(s, 0)
+    lj2 = restatement.lda_sweep(K, V, off, w, z, phi, theta, seed, 0)
+    mism = int((s["z"] != z).sum())
+    assert mism == 0, f"{name}: {mism} z mismatches of {len(z)}"
+    assert rel(s["phi"], phi) < RTOL_PARAM
+    assert rel(s["theta"], theta) < RTOL_PARAM
+    assert abs(lj - lj2) <= RTOL_LJ * abs(lj2)
+    nkw, _ = e.lda_counts()
+    want = np.zeros((K, V), dtype=np.int64)
+    np.add.at(want, (z, w), 1)
+    assert np.array_equal(nkw, want)
+
+
+def test_lda_device_prior_init_matches_reference(g, restatement):
+    fx = golden("lda_desk")
+    K, V, M = int(fx["K"]), int(fx["V"]), int(fx["M"])
+    e, s = lda_engine(g, fx)
+    e.prior_init(s, int(fx["seed"]))
+    assert rel(s["phi"], fx["phi0"]) < RTOL_PARAM
+    assert rel(s["theta"], fx["theta0"]) < RTOL_PARAM
+    assert np.array_equal(s["z"], fx["z0"])
+
+
+# ----------------------------------------------------------------------------------------
+# GMM and MH
+# ----------------------------------------------------------------------------------------
+def test_gmm_sweeps_vs_reference(g):
+    fx = golden("gmm_small")
+    hyper = {"N": int(fx["N"]), "K": 4}
+    e = g.Engine("gmm", hyper, g.RunConfig(seed=int(fx["seed"])))
+    s = e.allocate()
+    s["x"], s["z"], s["pi"], s["mu"], s["sigma2"] = fx["x"], fx["z0"], fx["pi0"], fx["mu0"], fx["sigma20"]
+    for it in range(len(fx["lj"])):
+        lj = e.sweep(s, it)
+        assert np.array_equal(s["z"], fx["z"][it])
+        assert rel(s["pi"], fx["pi"][it]) < RTOL_PARAM
+        assert rel(s["mu"], fx["mu"][it]) < RTOL_MU
+        assert rel(s["sigma2"], fx["sigma2"][it]) < RTOL_MU
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
+
+
+def test_mh_linreg_vs_reference(g):
+    fx = golden("mh_linreg")
+    N, K = int(fx["N"]), int(fx["K"])
+    e = g.Engine("regression", {"N": N, "K": K, "l": -1.0, "u": 1.0}, g.RunConfig(seed=int(fx["seed"])))
+    s = e.allocate()
+    s["x"], s["y"], s["w"], s["b"], s["tau"] = fx["x"], fx["y"], fx["w0"], [fx["b0"]], [fx["tau0"]]
+    assert abs(e.eval_log_joint(s) - fx["lj0"]) <= RTOL_LJ * abs(fx["lj0"])
+    for it in range(len(fx["lj"])):
+        acc = []
+        lj = e.sweep(s, it, acc)
+        assert acc[0] == bool(fx["accepted"][it]), f"accept decision differs at step {it}"
+        assert rel(s["w"], fx["w"][it]) < RTOL_PARAM
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
+
+
+def test_mh_logreg_vs_restatement(g, restatement):
+    """Logistic MH: parity with the restated oracle (no reference model exists)."""
+    rs = np.random.default_rng(5)
+    N, K = 4000, 8
+    x = rs.uniform(-1, 1, size=(N, K))
+    wt = 0.3 * rs.normal(size=K)
+    p = 1 / (1 + np.exp(-(x @ wt + 0.1)))
+    y = (rs.uniform(size=N) < p).astype(np.float64)
+    e = g.Engine("logreg", {"N": N, "K": K, "l": -1.0, "u": 1.0}, g.RunConfig(seed=3, mh_scale=0.05))
+    s = e.allocate()
+    s["x"], s["y"] = x.ravel(), y
+    w, b = np.zeros(K), 0.0
+    s["w"], s["b"] = w, [b]
+    xs = np.ascontiguousarray(x.ravel())
+    for it in range(20):
+        acc = []
+        lj = e.sweep(s, it, acc)
+        b, _, lj2, acc2 = restatement.mh_step(xs, y, K, w, b, 0.0, 3, it, logistic=True, mh_scale=0.05)
+        assert acc[0] == acc2
+        assert rel(s["w"], w) < RTOL_PARAM
+        assert abs(lj - lj2) <= RTOL_LJ * abs(lj2)
+
+
+def test_lpp_vs_reference(g, reference):
+    K, V, M, L = 6, 80, 12, 30
+    rs = np.random.default_rng(1)
+    phi = rs.dirichlet(np.ones(V), size=K)
+    theta = rs.dirichlet(np.ones(K), size=M)
+    w = rs.integers(0, V, M * L).astype(np.int64)
+    off = np.arange(M + 1, dtype=np.int64) * L
+    import ctypes
+    out = ctypes.c_double()
+    dp, ip = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+    pc, tc = np.ascontiguousarray(phi.ravel()), np.ascontiguousarray(theta.ravel())
+    reference._check(reference.lib.bref_lpp(pc.ctypes.data_as(dp), tc.ctypes.data_as(dp), K, V,
+                                            w.ctypes.data_as(ip), off.ctypes.data_as(ip), M, ctypes.byref(out)))
+    got = g.log_predictive_probability(pc, tc, K, V, w, off)
+    assert abs(got - out.value) <= 1e-10 * abs(out.value)
