@@ -24,8 +24,27 @@ LIB = os.path.join(HERE, "libbnmc_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """The NCCL that torch loads (the pip nvidia-nccl wheel): linking against the same
+    libnccl.so.2 keeps one NCCL in the process whichever library loads first."""
+    try:
+        import nvidia.nccl as n
+
+        d = os.path.join(list(n.__path__)[0])
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    except Exception:
+        pass
+    return None
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+if NCCL:
+    FLAGS += ["-I", os.path.join(NCCL, "include")]
 
 
 def _deps():
@@ -63,7 +82,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if log:
             sys.stderr.write(log)
     if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lcudart"]
+        nccl = (["-Xlinker", os.path.join(NCCL, "lib", "libnccl.so.2"), "-Xlinker", "-rpath",
+                 "-Xlinker", os.path.join(NCCL, "lib")] if NCCL else ["-lnccl"])
+        # static CUDA runtime: no second libcudart.so.12 next to torch's
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, *nccl]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

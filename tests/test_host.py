@@ -1,0 +1,110 @@
+"""CPU: the C-ABI library, the host mirror and the sharding logic (no GPU compute)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "bnmc_gpu.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|void|const char\*)\s+(bnmc_gpu_\w+)\s*\(", text, re.M)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    import paper_1312_3613_b200 as g
+
+    L = g.lib()  # loads libbnmc_gpu.so (built for sm_100a) without touching a device
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), f"{s} declared in include/bnmc_gpu.h but not exported"
+    assert L.bnmc_gpu_abi_version() == 1
+    out = subprocess.run(["nm", "-D", "--defined-only", g.engine.LIB_PATH], capture_output=True, text=True).stdout
+    for s in syms:
+        assert re.search(rf"\bT {s}$", out, re.M), s
+
+
+def test_library_is_sm100a_code():
+    import paper_1312_3613_b200 as g
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", g.engine.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_device_fails_loudly():
+    import torch
+
+    import paper_1312_3613_b200 as g
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(g.BnmcError):
+        g.Engine("lda", {"K": 2, "V": 3, "M": 1, "N": [2]})
+
+
+def test_unsupported_model_rejected():
+    import paper_1312_3613_b200 as g
+
+    with pytest.raises(ValueError):
+        g.Engine("hmm", {})
+    with pytest.raises(ValueError):
+        g.Engine("lda", {"K": 2, "V": 3, "M": 1, "N": [2]}, g.RunConfig(method="mh"))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition_contiguous_balanced(world):
+    import paper_1312_3613_b200 as g
+
+    rs = np.random.default_rng(world)
+    lengths = rs.integers(0, 50, 97)
+    off = np.concatenate([[0], np.cumsum(lengths)])
+    bounds = [g.partition(off, world, r) for r in range(world)]
+    assert bounds[0][0] == 0 and bounds[-1][1] == len(lengths)
+    for (b0, e0), (b1, e1) in zip(bounds, bounds[1:]):
+        assert e0 == b1 and b0 <= e0
+    toks = [off[e] - off[b] for b, e in bounds]
+    assert sum(toks) == off[-1]
+    assert max(toks) - min(toks) <= 2 * lengths.max() + 1
+
+
+def test_store_layout_mirrors_reference():
+    import paper_1312_3613_b200 as g
+
+    s = g.ParamStore("lda", {"K": 3, "V": 5, "M": 2, "N": [4, 1]})
+    assert s.names == ["phi", "theta", "z", "w"]  # declaration order = reference var ids
+    assert s["phi"].size == 15 and s["theta"].size == 6 and s["z"].size == 5
+    assert s["z"].dtype == np.int64 and s["phi"].dtype == np.float64
+    assert s.observed == {"phi": False, "theta": False, "z": False, "w": True}
+    a = np.arange(5)
+    s["z"] = a
+    a[0] = 99
+    assert s["z"][0] == 0  # the store owns its arrays
+    with pytest.raises(g.BnmcError):
+        s["z"] = np.arange(4)
+
+
+def test_cpp_mirror_compiles():
+    lib = os.path.join(ROOT, "paper_1312_3613_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "lda_sweep.cpp"), "-L", lib, "-lbnmc_gpu",
+                        "-o", "/tmp/bnmc_lda_sweep_test"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-x", "c", HEADER],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_bench_corpus_generator_shape():
+    import bench
+
+    w = bench.gen_lda_corpus(20, 300, 5, 17, 3)
+    assert w.shape == (340,) and w.min() >= 0 and w.max() < 300
+    assert np.array_equal(w, bench.gen_lda_corpus(20, 300, 5, 17, 3))
