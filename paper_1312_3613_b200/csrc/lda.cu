@@ -6,23 +6,27 @@
 //   [allreduce nkw]      NCCL int32 sum of the topic-word counts (world > 1 only)
 //   phi_gamma_kernel     phi block draw: per cell Gamma(beta + n[k,v]) from stream
 //                        keyed(seed,4,var_phi,iter).derive(k,v) (batch.cpp:38-41);
-//                        consumes the counts and zeroes them for this sweep's z-step
+//                        consumes the counts (zeroes them for this sweep's z-step)
 //   colsum_kernel        row sums of the gamma matrix (fixed-order, deterministic)
 //   phi_norm_kernel      phi = g / sum (batch.cpp:58-61) + Dirichlet log-pdf pieces
 //   phi_terms_kernel     per-topic Dirichlet log-pdf (dist.cpp:115-130)
-//   doc_kernel           per document: theta-block counts + Dirichlet draw
-//                        (sampler.cpp:61-181), then the z block for every token
-//                        (sampler.cpp:222-265, draw_from_log_weights dist.cpp:202-215),
-//                        next sweep's topic-word counts (atomics) and the document's
-//                        log-joint pieces
-//   reduce_docs_kernel   fixed-order sum of the per-document log-joint pieces
+//   theta_kernel         theta block: per document Dirichlet(alpha + n[d,.]) from the
+//                        doc-topic counts the previous z-step left (sampler.cpp:61-181),
+//                        stream keyed(seed,4,var_theta,iter).derive(d,k); theta log-pdf
+//   zstep_kernel         z block (sampler.cpp:222-265, draw_from_log_weights
+//                        dist.cpp:202-215) over token chunks: new z, the NEXT sweep's
+//                        topic-word and doc-topic counts (integer atomics), and the
+//                        z-factor of the log-joint (sum log theta[d, z])
+//   wterm_kernel         w-factor of the log-joint from the counts:
+//                        sum_t log phi[z_t, w_t] = sum_{k,v} n[k,v] log phi[k,v]
+//   reduce_kernel        fixed-order sums of the theta / z / w pieces
 //   [allreduce 3 doubles]
 //   finalize_kernel      log-joint = ((F_phi + F_theta) + F_z) + F_w (eval.cpp:393-422)
 //
 // Device layout (HBM): w, z int32 [N_local]; phiT fp64 [V][Kp] (word-major, so
 // the K weights of a token are one contiguous row; Kp = K rounded up to the
-// z-step tile, padding is zero); nkw int32 [V][Kp]; theta fp64 [M_local][K]
-// (the reference's row-major layout); per-sweep scratch is O(K * blocks + M).
+// z-step tile, padding is zero); nkw int32 [V][Kp]; nmk int32 [M_local][K];
+// theta fp64 [M_local][K] (the reference's row-major layout).
 #include <cmath>
 #include <algorithm>
 #include <cstring>
@@ -33,56 +37,67 @@
 namespace bnmc_gpu {
 namespace {
 
-constexpr int kDocThreads = 256;
-constexpr int kPhiThreadsMax = 256;
+constexpr int kZThreads = 256;
+constexpr int kChunk = 512;  // tokens per z-step work unit
 
 struct LdaArgs {
   int K, Kp, V;
   std::int64_t Ml, Nl;
   const int* w;
   int* z;
-  const std::int64_t* off;  // local offsets, off[0] = 0
+  const std::int64_t* off;   // local offsets, off[0] = 0
+  const std::int64_t* units; // z-step work units: [n_units][3] = doc, t0, t1
+  std::int64_t n_units;
   std::int64_t tok_base, doc_base;
   double* phiT;
-  double* logphiT;  // exact mode only
+  double* logphiT;   // exact mode only
   double* theta;
-  int* nkw;
+  int* nkw;          // [V][Kp]
+  int* nmk;          // [Ml][K]
   double* colpart;   // [nb_phi][K]
   double* colpart2;  // [nb_phi][K][2]
   double* S;         // [K]
   double* phi_term;  // [K]
-  double* doc_part;  // [Ml][3]
-  double* red;       // [4]: F_theta, F_z, F_w (local) ; F_phi
+  double* tpart;     // [Ml] theta-factor pieces
+  double* zpart;     // [n_units] z-factor pieces
+  double* wpart;     // [nb_phi] w-factor pieces
+  double* doc_part;  // [Ml][3] (eval path)
+  double* red;       // [4]
   double alpha, beta;
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
   int var_phi, var_theta, var_z;
   int rows_per_block, nb_phi;
-  int count_next;  // accumulate next sweep's topic-word counts (phi block active)
+  int consume_nkw;  // wterm zeroes the counts (phi clamped: no phi block consumes them)
 };
 
 // ---------------------------------------------------------------------------------
 // phi block
 // ---------------------------------------------------------------------------------
-__global__ void phi_gamma_kernel(LdaArgs a, const std::int64_t* iter_p) {
+// Block b owns vocabulary rows [b*R, b*R + R); its threads sweep the R x K cells
+// (k fastest: coalesced phiT rows), then threads k < K sum their column over the
+// block's rows in fixed order -> colpart[b][k].
+__global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::int64_t* iter_p) {
   const std::int64_t iter = *iter_p;
   const std::uint64_t key = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
                                   static_cast<std::uint64_t>(iter));
   const int b = blockIdx.x;
   const int v0 = b * a.rows_per_block;
   const int v1 = min(a.V, v0 + a.rows_per_block);
+  const int cells = (v1 - v0) * a.K;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    const int v = v0 + c / a.K, k = c % a.K;
+    const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
+    const int n = a.nkw[i];
+    a.nkw[i] = 0;
+    Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
+    a.phiT[i] = draw_gamma(r, a.beta + static_cast<double>(n));
+  }
+  __syncthreads();
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
     double s = 0.0;
-    for (int v = v0; v < v1; ++v) {
-      const std::size_t c = static_cast<std::size_t>(v) * a.Kp + k;
-      const int n = a.nkw[c];
-      a.nkw[c] = 0;
-      Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
-      const double g = draw_gamma(r, a.beta + static_cast<double>(n));
-      a.phiT[c] = g;
-      s += g;
-    }
+    for (int v = v0; v < v1; ++v) s += a.phiT[static_cast<std::size_t>(v) * a.Kp + k];
     a.colpart[static_cast<std::size_t>(b) * a.K + k] = s;
   }
 }
@@ -146,15 +161,54 @@ __global__ void phi_terms_kernel(LdaArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+// theta block: one CTA per document row
+// ---------------------------------------------------------------------------------
+__global__ void theta_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* g = reinterpret_cast<double*>(smem_raw);  // [K]
+  __shared__ double scratch[32];
+  const std::int64_t iter = *iter_p;
+  const std::uint64_t tkey = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
+                                   static_cast<std::uint64_t>(iter));
+  for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
+    const std::uint64_t mg = static_cast<std::uint64_t>(a.doc_base + m);
+    int* cnt = a.nmk + m * a.K;
+    double part = 0.0;
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+      const int n = cnt[k];
+      cnt[k] = 0;  // consumed: the z-step accumulates the next sweep's counts here
+      Stream r(derive(tkey, mg, static_cast<std::uint64_t>(k)));
+      const double x = draw_gamma(r, a.alpha + static_cast<double>(n));
+      g[k] = x;
+      part += x;
+    }
+    const double S = block_sum(part, scratch);
+    double lp = 0.0, sx = 0.0;
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+      const double x = g[k] / S;
+      a.theta[m * a.K + k] = x;
+      lp += (a.alpha - 1.0) * (x > 0.0 ? log(x) : -INFINITY);
+      sx += x;
+    }
+    lp = block_sum(lp, scratch);
+    sx = block_sum(sx, scratch);
+    if (threadIdx.x == 0)
+      a.tpart[m] = fabs(sx - 1.0) > 1e-9 ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // z block: grouped inverse-CDF categorical draw
 // ---------------------------------------------------------------------------------
-// A token's K candidate weights are handled by a group of G lanes; lane gl owns
-// candidates 4*(r*G + gl) .. +3 for rounds r < R = Kp/(4G), so each round is one
-// coalesced 32*G-byte segment of the token's phiT row.  Weights are either the
-// product theta*phi (default) or exp(log theta + log phi - max) exactly as the
-// reference (EXACT).  The inverse CDF keeps the reference's candidate order:
-// cstart[r] = running sum of every earlier candidate, and the draw is the first k
-// with u < acc_k, u = next_unit * total (dist.cpp:209-214).
+// A token's candidate weights are handled by a group of G lanes; lane gl owns
+// candidates 4*(r*G + gl) .. +3 for rounds r < Rr = Kp/(4G), so every round is one
+// coalesced 32*G-byte segment of the token's phiT row.  All rounds' loads are
+// issued before any cross-lane work (memory-level parallelism), then the R
+// per-round group scans run interleaved.  Weights are the product theta*phi
+// (default) or exp(log theta + log phi - max) exactly as the reference (EXACT).
+// The inverse CDF keeps the reference's candidate order: the draw is the first k
+// whose running sum exceeds u = next_unit * total (dist.cpp:209-214).
 template <int G>
 __device__ __forceinline__ unsigned group_mask() {
   if constexpr (G == 32) {
@@ -187,7 +241,7 @@ template <bool EXACT>
 __device__ __forceinline__ Quad weights(const double* th, const double* lth, const double* row,
                                         const double* lrow, int k, double mx) {
   Quad q;
-  if (!EXACT) {
+  if constexpr (!EXACT) {
     const double2 a0 = __ldg(reinterpret_cast<const double2*>(row + k));
     const double2 a1 = __ldg(reinterpret_cast<const double2*>(row + k + 2));
     const double2 t0 = *reinterpret_cast<const double2*>(th + k);
@@ -209,19 +263,20 @@ __device__ __forceinline__ Quad weights(const double* th, const double* lth, con
   return q;
 }
 
-// Returns the drawn topic in every lane of the group, or -1 when every weight
-// is zero/-inf (the reference throws std::domain_error).
-template <int G, int RMAX, bool EXACT>
-__device__ int draw_topic(const double* th, const double* lth, const double* row,
-                          const double* lrow, int K, int R, double u01) {
+// Returns the drawn topic in every lane of the group, or -1 when every weight is
+// zero/-inf (the reference throws std::domain_error; the product form retries in
+// log space).
+template <int G, int R, bool EXACT>
+__device__ __forceinline__ int draw_topic(const double* th, const double* lth, const double* row,
+                                          const double* lrow, int K, int Rr, double u01) {
   const unsigned m = group_mask<G>();
   const int gl = threadIdx.x & (G - 1);
   double mx = 0.0;
-  if (EXACT) {
+  if constexpr (EXACT) {
     double lm = -INFINITY;
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      if (r < R) {
+    for (int r = 0; r < R; ++r) {
+      if (r < Rr) {
         const int k = 4 * (r * G + gl);
         const double2 a0 = __ldg(reinterpret_cast<const double2*>(lrow + k));
         const double2 a1 = __ldg(reinterpret_cast<const double2*>(lrow + k + 2));
@@ -233,43 +288,50 @@ __device__ int draw_topic(const double* th, const double* lth, const double* row
     mx = g_max<G>(lm, m);
     if (!isfinite(mx)) return -1;
   }
-  double cstart[RMAX];
-  double B = 0.0;
+  // phase A: every round's weights and lane sums (independent loads)
+  double s[R];
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    cstart[r] = 0.0;
-    if (r < R) {
+  for (int r = 0; r < R; ++r) {
+    s[r] = 0.0;
+    if (r < Rr) {
       const Quad q = weights<EXACT>(th, lth, row, lrow, 4 * (r * G + gl), mx);
-      const double s = ((q.v0 + q.v1) + q.v2) + q.v3;
-      double inc = s;
-#pragma unroll
-      for (int d = 1; d < G; d <<= 1) {
-        const double t = __shfl_up_sync(m, inc, d, G);
-        if (gl >= d) inc += t;
-      }
-      double ex = __shfl_up_sync(m, inc, 1, G);
-      if (gl == 0) ex = 0.0;
-      const double tot = __shfl_sync(m, inc, G - 1, G);
-      cstart[r] = B + ex;
-      B = B + tot;
+      s[r] = ((q.v0 + q.v1) + q.v2) + q.v3;
     }
   }
+  // phase B: R independent inclusive group scans, interleaved
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double t = __shfl_up_sync(m, s[r], d, G);
+      if (gl >= d) s[r] += t;
+    }
+  }
+  // running start of every lane-chunk in candidate order
+  double B = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double ex = __shfl_up_sync(m, s[r], 1, G);
+    if (gl == 0) ex = 0.0;
+    const double tot = __shfl_sync(m, s[r], G - 1, G);
+    s[r] = B + ex;  // s[] now holds cstart
+    B = B + tot;
+  }
   const double total = B;
-  if (!(total > 0.0) || !isfinite(total)) return -1;
+  if (!(total > 0x1p-1000) || !isfinite(total)) return -1;
   const double u = u01 * total;
-  // Last chunk (k-order) whose running start is <= u.
   int q_l = -1;
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r)
-    if (r < R && cstart[r] <= u) q_l = r * G + gl;
+  for (int r = 0; r < R; ++r)
+    if (r < Rr && s[r] <= u) q_l = r * G + gl;
   const int qs = g_max_i<G>(q_l, m);
   int kk = 0;
   if (qs >= 0 && (qs & (G - 1)) == gl) {
     const int rs = qs / G;
     double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r)
-      if (r == rs) acc = cstart[r];
+    for (int r = 0; r < R; ++r)
+      if (r == rs) acc = s[r];
     const int k0 = 4 * qs;
     const Quad q = weights<EXACT>(th, lth, row, lrow, k0, mx);
     kk = k0 + 3;
@@ -290,145 +352,112 @@ __device__ int draw_topic(const double* th, const double* lth, const double* row
   return __shfl_sync(m, kk, qs < 0 ? 0 : (qs & (G - 1)), G);
 }
 
-// ---------------------------------------------------------------------------------
-// theta block + z block, one CTA per document
-// ---------------------------------------------------------------------------------
-template <int G, int RMAX, bool EXACT>
-__global__ void __launch_bounds__(kDocThreads) doc_kernel(LdaArgs a, const std::int64_t* iter_p,
-                                                          int* err) {
+// Sequential log-space draw exactly as draw_from_log_weights, for the rare token
+// whose product weights underflow (lane 0 of the group; result broadcast).
+template <int G>
+__device__ int draw_topic_logspace(const double* lth, const double* row, int K, double u01) {
+  const unsigned m = group_mask<G>();
+  const int gl = threadIdx.x & (G - 1);
+  int pick = -1;
+  if (gl == 0) {
+    double mx = -INFINITY;
+    for (int k = 0; k < K; ++k) mx = fmax(mx, lth[k] + (row[k] > 0.0 ? log(row[k]) : -INFINITY));
+    if (isfinite(mx)) {
+      double total = 0.0;
+      for (int k = 0; k < K; ++k) total += exp((lth[k] + (row[k] > 0.0 ? log(row[k]) : -INFINITY)) - mx);
+      const double u = u01 * total;
+      double acc = 0.0;
+      pick = K - 1;
+      for (int k = 0; k < K; ++k) {
+        acc += exp((lth[k] + (row[k] > 0.0 ? log(row[k]) : -INFINITY)) - mx);
+        if (u < acc) {
+          pick = k;
+          break;
+        }
+      }
+    }
+  }
+  return __shfl_sync(m, pick, 0, G);
+}
+
+// One CTA per work unit (a chunk of <= kChunk tokens of one document).
+template <int G, int R, bool EXACT>
+__global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* th = reinterpret_cast<double*>(smem_raw);  // [Kp]
   double* lth = th + a.Kp;                            // [Kp]
-  int* cnt = reinterpret_cast<int*>(lth + a.Kp);      // [Kp]
   __shared__ double scratch[32];
-
   const std::int64_t iter = *iter_p;
-  const std::uint64_t tkey = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
-                                   static_cast<std::uint64_t>(iter));
-  const int R = a.Kp / (4 * G);
-  const int gid = threadIdx.x / G;
-  constexpr int kGroups = kDocThreads / G;
+  const int Rr = a.Kp / (4 * G);
+  const int gid = threadIdx.x / G, gl = threadIdx.x & (G - 1);
+  constexpr int kGroups = kZThreads / G;
 
-  for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
-    const std::int64_t t0 = a.off[m], t1 = a.off[m + 1];
-    for (int k = threadIdx.x; k < a.Kp; k += blockDim.x) cnt[k] = 0;
-    __syncthreads();
-    // theta-block counting phase: c[val] += [z[i,j] == val] (sampler.cpp:61-136).
-    for (std::int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-      const int k = a.z[t];
-      if (k < 0 || k >= a.K)
-        atomicOr(err, kErrBin);
-      else
-        atomicAdd(&cnt[k], 1);
-    }
-    __syncthreads();
-    // Dirichlet(alpha + c) draw, cell stream keyed(seed,4,var_theta,iter).derive(m,k).
-    const std::uint64_t mg = static_cast<std::uint64_t>(a.doc_base + m);
-    double part = 0.0;
+  for (std::int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+    const std::int64_t m = a.units[u * 3], t0 = a.units[u * 3 + 1], t1 = a.units[u * 3 + 2];
+    const double* thg = a.theta + m * a.K;
     for (int k = threadIdx.x; k < a.Kp; k += blockDim.x) {
-      double g = 0.0;
-      if (k < a.K) {
-        Stream r(derive(tkey, mg, static_cast<std::uint64_t>(k)));
-        g = draw_gamma(r, a.alpha + static_cast<double>(cnt[k]));
-      }
-      th[k] = g;
-      part += g;
+      const double x = k < a.K ? thg[k] : 0.0;
+      th[k] = x;
+      lth[k] = x > 0.0 ? log(x) : -INFINITY;
     }
-    const double S = block_sum(part, scratch);
-    double lp = 0.0, sx = 0.0;
-    for (int k = threadIdx.x; k < a.Kp; k += blockDim.x) {
-      if (k < a.K) {
-        const double x = th[k] / S;
-        const double lx = x > 0.0 ? log(x) : -INFINITY;
-        th[k] = x;
-        lth[k] = lx;
-        a.theta[m * a.K + k] = x;
-        lp += (a.alpha - 1.0) * lx;
-        sx += x;
-      } else {
-        th[k] = 0.0;
-        lth[k] = -INFINITY;
-      }
-    }
-    lp = block_sum(lp, scratch);
-    sx = block_sum(sx, scratch);
-    const double theta_term =
-        fabs(sx - 1.0) > 1e-9 ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
     __syncthreads();
-
-    // z block: every token of the document, G lanes per token.
-    double zs = 0.0, ws = 0.0;
+    int* cnt = a.nmk + m * a.K;
+    double zs = 0.0;
+    int wv_next = t0 + gid < t1 ? __ldg(a.w + t0 + gid) : 0;
     for (std::int64_t base = t0; base < t1; base += kGroups) {
       const std::int64_t t = base + gid;
       const bool valid = t < t1;
-      const int wv = valid ? a.w[t] : 0;
+      const int wv = wv_next;
+      wv_next = t + kGroups < t1 ? __ldg(a.w + t + kGroups) : 0;
       const double* row = a.phiT + static_cast<std::size_t>(wv) * a.Kp;
       const double* lrow = EXACT ? a.logphiT + static_cast<std::size_t>(wv) * a.Kp : nullptr;
       // keyed(seed, 3, var_z, t, iter) with the first three folds hoisted.
       Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                       static_cast<std::uint64_t>(iter)));
       const double u01 = rng.next_unit();
-      int k = draw_topic<G, RMAX, EXACT>(th, lth, row, lrow, a.K, R, u01);
-      if (!EXACT && k < 0) {
-        // Product weights underflowed: redo this token in log space (needs no table:
-        // log phi is taken on the fly from the row).
-        k = -2;
-      }
-      if (k == -2) {
-        // log-space fallback without a log table: the group recomputes weights.
-        const unsigned msk = group_mask<G>();
-        const int gl = threadIdx.x & (G - 1);
-        double lm = -INFINITY;
-        for (int kk = gl; kk < a.K; kk += G) lm = fmax(lm, lth[kk] + (row[kk] > 0.0 ? log(row[kk]) : -INFINITY));
-        lm = g_max<G>(lm, msk);
-        int pick = -1;
-        if (isfinite(lm)) {
-          // sequential scan by lane 0, reference order and arithmetic
-          if (gl == 0) {
-            double total = 0.0;
-            for (int kk = 0; kk < a.K; ++kk)
-              total += exp((lth[kk] + (row[kk] > 0.0 ? log(row[kk]) : -INFINITY)) - lm);
-            const double u = u01 * total;
-            double acc = 0.0;
-            pick = a.K - 1;
-            for (int kk = 0; kk < a.K; ++kk) {
-              acc += exp((lth[kk] + (row[kk] > 0.0 ? log(row[kk]) : -INFINITY)) - lm);
-              if (u < acc) {
-                pick = kk;
-                break;
-              }
-            }
-          }
-          pick = __shfl_sync(msk, pick, 0, G);
-        }
-        k = pick;
-      }
-      if (valid) {
-        const int gl = threadIdx.x & (G - 1);
+      int k = draw_topic<G, R, EXACT>(th, lth, row, lrow, a.K, Rr, u01);
+      if (!EXACT && k < 0) k = draw_topic_logspace<G>(lth, row, a.K, u01);
+      if (valid && gl == 0) {
         if (k < 0) {
-          if (gl == 0) atomicOr(err, kErrDomain);
-        } else if (gl == 0) {
+          atomicOr(err, kErrDomain);
+        } else {
           a.z[t] = k;
-          if (a.count_next) atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
+          atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
+          atomicAdd(&cnt[k], 1);
           zs += lth[k];
-          const double p = row[k];
-          ws += p > 0.0 ? log(p) : -INFINITY;
         }
       }
     }
     zs = block_sum(zs, scratch);
-    ws = block_sum(ws, scratch);
-    if (threadIdx.x == 0) {
-      a.doc_part[m * 3 + 0] = theta_term;
-      a.doc_part[m * 3 + 1] = zs;
-      a.doc_part[m * 3 + 2] = ws;
-    }
+    if (threadIdx.x == 0) a.zpart[u] = zs;
     __syncthreads();
   }
 }
 
+// w-factor from the counts: sum_{v,k} n[v,k] * log phi[k,v] over this rank's tokens.
+__global__ void wterm_kernel(LdaArgs a) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.x;
+  const int v0 = b * a.rows_per_block;
+  const int v1 = min(a.V, v0 + a.rows_per_block);
+  const int cells = (v1 - v0) * a.K;
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    const int v = v0 + c / a.K, k = c % a.K;
+    const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
+    const int n = a.nkw[i];
+    if (n) {
+      const double p = a.phiT[i];
+      acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
+      if (a.consume_nkw) a.nkw[i] = 0;
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) a.wpart[b] = acc;
+}
+
 // Log-joint pieces of the current state without sampling (Engine::eval_log_joint).
-__global__ void __launch_bounds__(kDocThreads) doc_eval_kernel(LdaArgs a, int* err) {
+__global__ void __launch_bounds__(256) doc_eval_kernel(LdaArgs a, int* err) {
   __shared__ double scratch[32];
   for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
     const double* th = a.theta + m * a.K;
@@ -467,14 +496,21 @@ __global__ void __launch_bounds__(kDocThreads) doc_eval_kernel(LdaArgs a, int* e
   }
 }
 
-// red[0..2] = sum over local documents of the three pieces (fixed order).
-__global__ void reduce_docs_kernel(LdaArgs a) {
+// red[0..2] = F_theta, F_z, F_w of this rank (fixed order).
+template <bool EVAL>
+__global__ void reduce_kernel(LdaArgs a) {
   __shared__ double scratch[32];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) {
-    s0 += a.doc_part[m * 3 + 0];
-    s1 += a.doc_part[m * 3 + 1];
-    s2 += a.doc_part[m * 3 + 2];
+  if (EVAL) {
+    for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) {
+      s0 += a.doc_part[m * 3 + 0];
+      s1 += a.doc_part[m * 3 + 1];
+      s2 += a.doc_part[m * 3 + 2];
+    }
+  } else {
+    for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += a.tpart[m];
+    for (std::int64_t u = threadIdx.x; u < a.n_units; u += blockDim.x) s1 += a.zpart[u];
+    for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) s2 += a.wpart[b];
   }
   s0 = block_sum(s0, scratch);
   s1 = block_sum(s1, scratch);
@@ -517,6 +553,7 @@ __global__ void count_kernel(LdaArgs a, int* err) {
   }
 }
 
+// Doc-topic counts of the current z (the theta block's sufficient statistics).
 __global__ void doc_counts_kernel(LdaArgs a, int* nmk) {
   for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x)
     for (std::int64_t t = a.off[m] + threadIdx.x; t < a.off[m + 1]; t += blockDim.x) {
@@ -669,8 +706,17 @@ class Lda final : public Model {
             "doc_offsets must run from 0 to N");
     exact_ = (d.flags & BNMC_GPU_EXACT_WEIGHTS) != 0;
     observe_phi_ = (d.flags & BNMC_GPU_OBSERVE_PHI) != 0;
-    G_ = K_ <= 256 ? 4 : (K_ <= 512 ? 8 : 32);
-    Kp_ = static_cast<int>((d.K + 4 * G_ - 1) / (4 * G_) * (4 * G_));
+    // z-step tile: the smallest group width G whose rounds fit R <= 8 registers.
+    G_ = 32;
+    for (int g : {4, 8, 16, 32}) {
+      if ((K_ + 4 * g - 1) / (4 * g) <= 8) {
+        G_ = g;
+        break;
+      }
+    }
+    Kp_ = (K_ + 4 * G_ - 1) / (4 * G_) * (4 * G_);
+    const int rounds = Kp_ / (4 * G_);
+    R_ = rounds <= 2 ? 2 : (rounds <= 4 ? 4 : (rounds <= 8 ? 8 : 16));
     partition_docs(d.doc_offsets, M_, c.world, c.rank, &d0_, &d1_);
     Ml_ = d1_ - d0_;
     tok0_ = d.doc_offsets[d0_];
@@ -686,11 +732,21 @@ class Lda final : public Model {
     var_z_ = d.var_ids[2];
     var_w_ = d.var_ids[3];
 
-    const int pt = std::min(kPhiThreadsMax, ((K_ + 31) / 32) * 32);
-    phi_threads_ = pt;
-    const std::int64_t target_blocks = 148 * 8;
+    phi_threads_ = std::min(256, ((K_ + 31) / 32) * 32);
+    // ~16 resident blocks' worth of gamma cells per SM: rows per phi block.
+    const std::int64_t target_blocks = 148 * 16;
     rows_per_block_ = static_cast<int>(std::max<std::int64_t>(1, (V_ + target_blocks - 1) / target_blocks));
     nb_phi_ = (V_ + rows_per_block_ - 1) / rows_per_block_;
+    theta_threads_ = std::min(256, ((K_ + 31) / 32) * 32);
+
+    // z-step work units: chunks of <= kChunk tokens of one document.
+    for (std::int64_t m = 0; m < Ml_; ++m)
+      for (std::int64_t t = off_host_[m]; t < off_host_[m + 1]; t += kChunk) {
+        units_host_.push_back(m);
+        units_host_.push_back(t);
+        units_host_.push_back(std::min(t + kChunk, off_host_[m + 1]));
+      }
+    n_units_ = static_cast<std::int64_t>(units_host_.size() / 3);
 
     w_.alloc(std::max<std::int64_t>(Nl_, 1));
     z_.alloc(std::max<std::int64_t>(Nl_, 1));
@@ -699,6 +755,11 @@ class Lda final : public Model {
     if (exact_) logphiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
+    units_.alloc(std::max<std::size_t>(units_host_.size(), 3));
+    tpart_.alloc(std::max<std::int64_t>(Ml_, 1));
+    zpart_.alloc(std::max<std::int64_t>(n_units_, 1));
+    wpart_.alloc(nb_phi_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
@@ -707,6 +768,13 @@ class Lda final : public Model {
     red_.alloc(4);
     cudaStream_t s0 = nullptr;
     BNMC_CUDA(cudaMemcpy(off_.p, off_host_.data(), sizeof(std::int64_t) * (Ml_ + 1), cudaMemcpyHostToDevice));
+    if (!units_host_.empty())
+      BNMC_CUDA(cudaMemcpy(units_.p, units_host_.data(), sizeof(std::int64_t) * units_host_.size(),
+                           cudaMemcpyHostToDevice));
+    nmk_.zero(s0);
+    tpart_.zero(s0);
+    zpart_.zero(s0);
+    wpart_.zero(s0);
     phiT_.zero(s0);
     nkw_.zero(s0);
     w_.zero(s0);
@@ -727,7 +795,7 @@ class Lda final : public Model {
     theta_norm_ = seq_sum_const(std::lgamma(alpha_), K_);
     theta_lgasum_ = std::lgamma(seq_sum_const(alpha_, K_));
 
-    configure_doc_kernel();
+    configure_kernels();
   }
 
   void upload(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, true); }
@@ -797,7 +865,7 @@ class Lda final : public Model {
         BNMC_NCCL(ncclAllReduce(nkw_.p, nkw_.p, nkw_.n, ncclInt32, ncclSum, comm_.comm, st));
         mark(st, "allreduce_counts");
       }
-      phi_gamma_kernel<<<nb_phi_, phi_threads_, 0, st>>>(a, out.iter);
+      phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
       mark(st, "phi_gamma");
       colsum_kernel<<<K_, 128, 0, st>>>(colpart_.p, nb_phi_, K_, 1, 0, S_.p);
       mark(st, "phi_colsum");
@@ -806,10 +874,16 @@ class Lda final : public Model {
       phi_terms_kernel<<<K_, 128, 0, st>>>(a);
       mark(st, "phi_terms");
     }
-    launch_doc(a, st);
-    mark(st, "doc_theta_z");
-    reduce_docs_kernel<<<1, 1024, 0, st>>>(a);
-    mark(st, "reduce_docs");
+    if (Ml_ > 0) {
+      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
+      mark(st, "theta");
+      launch_zstep(a, st);
+      mark(st, "zstep");
+    }
+    wterm_kernel<<<nb_phi_, 256, 0, st>>>(a);
+    mark(st, "wterm");
+    reduce_kernel<false><<<1, 1024, 0, st>>>(a);
+    mark(st, "reduce");
     if (comm_.world > 1) {
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
       mark(st, "allreduce_lj");
@@ -823,8 +897,8 @@ class Lda final : public Model {
     LdaArgs a = args();
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
-    doc_eval_kernel<<<grid_docs(), kDocThreads, 0, st>>>(a, out.err);
-    reduce_docs_kernel<<<1, 1024, 0, st>>>(a);
+    doc_eval_kernel<<<grid_docs(), 256, 0, st>>>(a, out.err);
+    reduce_kernel<true><<<1, 1024, 0, st>>>(a);
     if (comm_.world > 1)
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
     finalize_kernel<<<1, 256, 0, st>>>(a, out, 0);
@@ -903,7 +977,11 @@ class Lda final : public Model {
   void after_state_change(cudaStream_t st) {
     LdaArgs a = args();
     nkw_.zero(st);
-    if (Nl_ > 0) count_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(a, out.err);
+    nmk_.zero(st);
+    if (Nl_ > 0) {
+      count_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(a, out.err);
+      doc_counts_kernel<<<grid_docs(), 256, 0, st>>>(a, nmk_.p);
+    }
     // phi terms (and the exact-mode log table) of the uploaded phi: used as-is by
     // clamped-phi runs, recomputed by the phi block otherwise.
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
@@ -914,34 +992,47 @@ class Lda final : public Model {
 
   unsigned grid_docs() const { return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(Ml_, 1 << 20))); }
 
-  std::size_t doc_smem() const { return sizeof(double) * 2 * Kp_ + sizeof(int) * Kp_; }
+  std::size_t zstep_smem() const { return sizeof(double) * 2 * Kp_; }
 
-  template <int G, int RMAX, bool E>
-  void set_attr() {
-    BNMC_CUDA(cudaFuncSetAttribute(doc_kernel<G, RMAX, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(doc_smem())));
+  template <int G, int R, bool E>
+  void zstep_attr() {
+    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(zstep_smem())));
   }
 
-  void configure_doc_kernel() {
-    if (doc_smem() <= 48 * 1024) return;
-    if (G_ == 4) exact_ ? set_attr<4, 16, true>() : set_attr<4, 16, false>();
-    if (G_ == 8) exact_ ? set_attr<8, 16, true>() : set_attr<8, 16, false>();
-    if (G_ == 32) exact_ ? set_attr<32, 16, true>() : set_attr<32, 16, false>();
+  void configure_kernels() {
+    if (sizeof(double) * K_ > 48 * 1024)
+      BNMC_CUDA(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sizeof(double) * K_)));
+    if (zstep_smem() <= 48 * 1024) return;
+    dispatch_zstep([&](auto g, auto r, auto e) { zstep_attr<decltype(g)::value, decltype(r)::value, decltype(e)::value>(); });
   }
 
-  void launch_doc(const LdaArgs& a, cudaStream_t st) {
-    if (Ml_ == 0) return;
-    const unsigned g = grid_docs();
-    const std::size_t sm = doc_smem();
-#define BNMC_DOC(GG, E) doc_kernel<GG, 16, E><<<g, kDocThreads, sm, st>>>(a, out.iter, out.err)
-    if (G_ == 4) {
-      if (exact_) BNMC_DOC(4, true); else BNMC_DOC(4, false);
-    } else if (G_ == 8) {
-      if (exact_) BNMC_DOC(8, true); else BNMC_DOC(8, false);
-    } else {
-      if (exact_) BNMC_DOC(32, true); else BNMC_DOC(32, false);
-    }
-#undef BNMC_DOC
+  template <class F>
+  void dispatch_zstep(F&& f) {
+    using std::integral_constant;
+    auto with_e = [&](auto g, auto r) {
+      if (exact_) f(g, r, integral_constant<bool, true>{});
+      else f(g, r, integral_constant<bool, false>{});
+    };
+    if (G_ == 4 && R_ == 2) with_e(integral_constant<int, 4>{}, integral_constant<int, 2>{});
+    else if (G_ == 4 && R_ == 4) with_e(integral_constant<int, 4>{}, integral_constant<int, 4>{});
+    else if (G_ == 4) with_e(integral_constant<int, 4>{}, integral_constant<int, 8>{});
+    else if (G_ == 8) with_e(integral_constant<int, 8>{}, integral_constant<int, 8>{});
+    else if (G_ == 16) with_e(integral_constant<int, 16>{}, integral_constant<int, 8>{});
+    else if (R_ <= 8) with_e(integral_constant<int, 32>{}, integral_constant<int, 8>{});
+    else with_e(integral_constant<int, 32>{}, integral_constant<int, 16>{});
+  }
+
+  void launch_zstep(const LdaArgs& a, cudaStream_t st) {
+    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
+    const std::size_t sm = zstep_smem();
+    const int* err = out.err;
+    const std::int64_t* it = out.iter;
+    dispatch_zstep([&](auto gg, auto r, auto e) {
+      zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value>
+          <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+    });
   }
 
   LdaArgs args() const {
@@ -966,6 +1057,12 @@ class Lda final : public Model {
     a.phi_term = phi_term_.p;
     a.doc_part = doc_part_.p;
     a.red = red_.p;
+    a.nmk = nmk_.p;
+    a.units = units_.p;
+    a.n_units = n_units_;
+    a.tpart = tpart_.p;
+    a.zpart = zpart_.p;
+    a.wpart = wpart_.p;
     a.alpha = alpha_;
     a.beta = beta_;
     a.phi_norm = phi_norm_;
@@ -979,25 +1076,29 @@ class Lda final : public Model {
     a.var_z = var_z_;
     a.rows_per_block = rows_per_block_;
     a.nb_phi = nb_phi_;
-    a.count_next = observe_phi_ ? 0 : 1;
+    a.consume_nkw = observe_phi_ ? 1 : 0;
     return a;
   }
 
   Comm comm_;
-  int K_ = 0, Kp_ = 0, V_ = 0, G_ = 4;
+  int K_ = 0, Kp_ = 0, V_ = 0, G_ = 4, R_ = 8;
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
-  int phi_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
+  int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
+  std::vector<std::int64_t> units_host_;
+  std::int64_t n_units_ = 0;
   bool data_on_device_ = false;
   DevBuf<std::int64_t> stage64_;  // int64 <-> int32 staging for z / w
   DevBuf<double> stage_phi_;      // K x V staging for the phi transpose
-  DevBuf<int> w_, z_, nkw_;
+  DevBuf<int> w_, z_, nkw_, nmk_;
+  DevBuf<std::int64_t> units_;
   DevBuf<std::int64_t> off_;
-  DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_;
+  DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
+      zpart_, wpart_;
 };
 
 }  // namespace
