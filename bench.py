@@ -10,9 +10,10 @@ north_star's per-GPU target is stated on.  A "step" is one full sweep (phi block
 theta block, z block, log-joint), exactly Engine::sweep (sampler.cpp:390-405).
 
 Prints ONE JSON line (rank 0).  Fields beyond the base contract:
-  roofline     the dominant kernel (doc_theta_z: theta draw + z-step) against the
-               measured HBM copy bandwidth; achieved = algorithmic bytes per launch
-               (8K + 16 + 16K/L per token) / its CUDA-event duration
+  roofline     the dominant kernel (zstep: the z block) against the measured HBM copy
+               bandwidth; achieved = algorithmic bytes per launch (phi row
+               8K + 16 B of token state per site + the theta row per 512-token unit) /
+               its CUDA-event duration
   cpu_baseline the compiled reference (oracle/_ref) timed on this host's cores on a
                bounded sample of the same workload
   e2e          the same metric through the public API with HOST buffers: every step
@@ -211,9 +212,11 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             store = None
         b, e = g.partition(np.arange(docs + 1, dtype=np.int64) * L, world, rank)
         sites_local = (e - b) * L
-        per_sweep_kernels = 7
-        dominant = "doc_theta_z"
-        bytes_per_site_dom = 8 * K + 16 + 16 * K / L
+        per_sweep_kernels = 9
+        dominant = "zstep"
+        # per token: phi row 8K + w 4 + z 4 + topic-word count 4 + doc-topic count 4,
+        # theta row 8K per work unit (<= 512 tokens of one document)
+        bytes_per_site_dom = 8 * K + 16 + 8 * K / min(L, 512)
         bytes_per_site_sweep = 8 * K + 16 * K / L + 16 + 20 * K * V / (docs * L)
         config = {"workload": f"lda-{args.workload}", "model": "lda (proj/models/lda.bn)", "docs": docs,
                   "vocab": V, "topics": K, "doc_len": L, "tokens": sites_total, "seed": args.seed,

@@ -17,7 +17,7 @@ constexpr double kLog2Pi = 1.8378770664093454835606594728112;
 // at shape+1 and applies the u^(1/shape) boost (the recursion is one level deep,
 // so it is unrolled here).  Returns NaN for a non-positive shape.
 __device__ __forceinline__ double draw_gamma(Stream& rng, double shape) {
-  if (!(shape > 0.0)) return nan("");
+  if (!(shape > 0.0)) return __longlong_as_double(0x7ff8000000000000ll);  // NaN
   const bool boost = shape < 1.0;
   const double a = boost ? shape + 1.0 : shape;
   const double d = a - 1.0 / 3.0;

@@ -69,7 +69,6 @@ struct LdaArgs {
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
   int var_phi, var_theta, var_z;
   int rows_per_block, nb_phi;
-  int consume_nkw;  // wterm zeroes the counts (phi clamped: no phi block consumes them)
 };
 
 // ---------------------------------------------------------------------------------
@@ -86,13 +85,35 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
   const int v0 = b * a.rows_per_block;
   const int v1 = min(a.V, v0 + a.rows_per_block);
   const int cells = (v1 - v0) * a.K;
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+  // The counts come from HBM at the start of a sweep: issue the thread's count loads
+  // up front (<= 4 cells per thread at the configured rows per block) before the
+  // latency-bound gamma draws.
+  int n[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = threadIdx.x + j * blockDim.x;
+    n[j] = 0;
+    if (c < cells) {
+      const std::size_t i = static_cast<std::size_t>(v0 + c / a.K) * a.Kp + c % a.K;
+      n[j] = a.nkw[i];
+      a.nkw[i] = 0;
+    }
+  }
+  for (int c = threadIdx.x, j = 0; c < cells; c += blockDim.x, ++j) {
     const int v = v0 + c / a.K, k = c % a.K;
     const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
-    const int n = a.nkw[i];
-    a.nkw[i] = 0;
+    int cnt;
+    if (j < 4) {
+      cnt = n[0];
+      if (j == 1) cnt = n[1];
+      if (j == 2) cnt = n[2];
+      if (j == 3) cnt = n[3];
+    } else {
+      cnt = a.nkw[i];
+      a.nkw[i] = 0;
+    }
     Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
-    a.phiT[i] = draw_gamma(r, a.beta + static_cast<double>(n));
+    a.phiT[i] = draw_gamma(r, a.beta + static_cast<double>(cnt));
   }
   __syncthreads();
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
@@ -237,28 +258,36 @@ struct Quad {
   double v0, v1, v2, v3;
 };
 
+// 256-bit read-only global load (LDG.E.ENL2.256 on sm_100a): a lane's 4 candidates
+// in one request, so a G=4 group reads one full 128-byte line per round.
+__device__ __forceinline__ Quad ldg256(const double* p) {
+  Quad q;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(q.v0), "=d"(q.v1), "=d"(q.v2), "=d"(q.v3)
+      : "l"(p));
+  return q;
+}
+
 template <bool EXACT>
 __device__ __forceinline__ Quad weights(const double* th, const double* lth, const double* row,
                                         const double* lrow, int k, double mx) {
   Quad q;
   if constexpr (!EXACT) {
-    const double2 a0 = __ldg(reinterpret_cast<const double2*>(row + k));
-    const double2 a1 = __ldg(reinterpret_cast<const double2*>(row + k + 2));
+    const Quad a = ldg256(row + k);
     const double2 t0 = *reinterpret_cast<const double2*>(th + k);
     const double2 t1 = *reinterpret_cast<const double2*>(th + k + 2);
-    q.v0 = t0.x * a0.x;
-    q.v1 = t0.y * a0.y;
-    q.v2 = t1.x * a1.x;
-    q.v3 = t1.y * a1.y;
+    q.v0 = t0.x * a.v0;
+    q.v1 = t0.y * a.v1;
+    q.v2 = t1.x * a.v2;
+    q.v3 = t1.y * a.v3;
   } else {
-    const double2 a0 = __ldg(reinterpret_cast<const double2*>(lrow + k));
-    const double2 a1 = __ldg(reinterpret_cast<const double2*>(lrow + k + 2));
+    const Quad a = ldg256(lrow + k);
     const double2 t0 = *reinterpret_cast<const double2*>(lth + k);
     const double2 t1 = *reinterpret_cast<const double2*>(lth + k + 2);
-    q.v0 = exp((t0.x + a0.x) - mx);
-    q.v1 = exp((t0.y + a0.y) - mx);
-    q.v2 = exp((t1.x + a1.x) - mx);
-    q.v3 = exp((t1.y + a1.y) - mx);
+    q.v0 = exp((t0.x + a.v0) - mx);
+    q.v1 = exp((t0.y + a.v1) - mx);
+    q.v2 = exp((t1.x + a.v2) - mx);
+    q.v3 = exp((t1.y + a.v3) - mx);
   }
   return q;
 }
@@ -278,11 +307,10 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
     for (int r = 0; r < R; ++r) {
       if (r < Rr) {
         const int k = 4 * (r * G + gl);
-        const double2 a0 = __ldg(reinterpret_cast<const double2*>(lrow + k));
-        const double2 a1 = __ldg(reinterpret_cast<const double2*>(lrow + k + 2));
+        const Quad a = ldg256(lrow + k);
         const double2 t0 = *reinterpret_cast<const double2*>(lth + k);
         const double2 t1 = *reinterpret_cast<const double2*>(lth + k + 2);
-        lm = fmax(lm, fmax(fmax(t0.x + a0.x, t0.y + a0.y), fmax(t1.x + a1.x, t1.y + a1.y)));
+        lm = fmax(lm, fmax(fmax(t0.x + a.v0, t0.y + a.v1), fmax(t1.x + a.v2, t1.y + a.v3)));
       }
     }
     mx = g_max<G>(lm, m);
@@ -449,7 +477,6 @@ __global__ void wterm_kernel(LdaArgs a) {
     if (n) {
       const double p = a.phiT[i];
       acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
-      if (a.consume_nkw) a.nkw[i] = 0;
     }
   }
   acc = block_sum(acc, scratch);
@@ -873,6 +900,10 @@ class Lda final : public Model {
       mark(st, "phi_norm");
       phi_terms_kernel<<<K_, 128, 0, st>>>(a);
       mark(st, "phi_terms");
+    } else {
+      // phi clamped: no phi block consumes the counts; the z-step's counts of this
+      // sweep feed only the w-factor.
+      nkw_.zero(st);
     }
     if (Ml_ > 0) {
       theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
@@ -1076,7 +1107,6 @@ class Lda final : public Model {
     a.var_z = var_z_;
     a.rows_per_block = rows_per_block_;
     a.nb_phi = nb_phi_;
-    a.consume_nkw = observe_phi_ ? 1 : 0;
     return a;
   }
 
