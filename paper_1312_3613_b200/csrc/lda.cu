@@ -248,6 +248,13 @@ __device__ __forceinline__ double g_max(double v, unsigned m) {
 }
 
 template <int G>
+__device__ __forceinline__ double g_sum(double v, unsigned m) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o, G);
+  return v;
+}
+
+template <int G>
 __device__ __forceinline__ int g_max_i(int v, unsigned m) {
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(m, v, o, G));
@@ -316,8 +323,10 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
     mx = g_max<G>(lm, m);
     if (!isfinite(mx)) return -1;
   }
-  // phase A: every round's weights and lane sums (independent loads)
-  double s[R];
+  // phase A: every round's weights (independent loads), lane-chunk sums s[r] and the
+  // lane's running prefix over rounds Q[r] (registers only, no cross-lane traffic)
+  double s[R], Q[R];
+  double run = 0.0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     s[r] = 0.0;
@@ -325,43 +334,51 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
       const Quad q = weights<EXACT>(th, lth, row, lrow, 4 * (r * G + gl), mx);
       s[r] = ((q.v0 + q.v1) + q.v2) + q.v3;
     }
+    run += s[r];
+    Q[r] = run;
   }
-  // phase B: R independent inclusive group scans, interleaved
-#pragma unroll
-  for (int d = 1; d < G; d <<= 1) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double t = __shfl_up_sync(m, s[r], d, G);
-      if (gl >= d) s[r] += t;
-    }
-  }
-  // running start of every lane-chunk in candidate order
-  double B = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    double ex = __shfl_up_sync(m, s[r], 1, G);
-    if (gl == 0) ex = 0.0;
-    const double tot = __shfl_sync(m, s[r], G - 1, G);
-    s[r] = B + ex;  // s[] now holds cstart
-    B = B + tot;
-  }
-  const double total = B;
+  // Candidate order is round-major, so the running sum at the end of round r is
+  // f(r) = sum over the group of Q[r].  total = f(R-1); the crossing round is found
+  // by a branch-free binary search over r (log2 R group sums instead of R scans).
+  const double total = g_sum<G>(Q[R - 1], m);
   if (!(total > 0x1p-1000) || !isfinite(total)) return -1;
   const double u = u01 * total;
-  int q_l = -1;
+  int pos = 0;
+  double base = 0.0;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (r < Rr && s[r] <= u) q_l = r * G + gl;
-  const int qs = g_max_i<G>(q_l, m);
-  int kk = 0;
-  if (qs >= 0 && (qs & (G - 1)) == gl) {
-    const int rs = qs / G;
-    double acc = 0.0;
+  for (int step = R / 2; step >= 1; step >>= 1) {
+    const int c = pos + step - 1;
+    double qc = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (r == rs) acc = s[r];
-    const int k0 = 4 * qs;
+      if (r == c) qc = Q[r];
+    const double f = g_sum<G>(qc, m);
+    if (c < Rr && !(u < f)) {
+      pos += step;
+      base = f;
+    }
+  }
+  if (R == 1 || pos >= Rr) pos = Rr - 1;  // u >= total by rounding: last round
+  // Within round `pos`: exclusive scan of the lane-chunk sums -> each chunk's start.
+  double sc = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r == pos) sc = s[r];
+  double inc = sc;
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    const double t = __shfl_up_sync(m, inc, d, G);
+    if (gl >= d) inc += t;
+  }
+  double ex = __shfl_up_sync(m, inc, 1, G);
+  if (gl == 0) ex = 0.0;
+  const double start = base + ex;
+  const int owner = g_max_i<G>(start <= u ? gl : 0, m);
+  int kk = 0;
+  if (gl == owner) {
+    const int k0 = 4 * (pos * G + gl);
     const Quad q = weights<EXACT>(th, lth, row, lrow, k0, mx);
+    double acc = start;
     kk = k0 + 3;
     acc += q.v0;
     if (u < acc) {
@@ -377,7 +394,7 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
     }
     kk = min(kk, K - 1);  // past-the-end fallback (dist.cpp:214)
   }
-  return __shfl_sync(m, kk, qs < 0 ? 0 : (qs & (G - 1)), G);
+  return __shfl_sync(m, kk, owner, G);
 }
 
 // Sequential log-space draw exactly as draw_from_log_weights, for the rare token
