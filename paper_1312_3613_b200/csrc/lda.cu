@@ -29,7 +29,9 @@
 // theta fp64 [M_local][K] (the reference's row-major layout).
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "common.cuh"
 #include "dist.cuh"
@@ -275,26 +277,54 @@ __device__ __forceinline__ Quad ldg256(const double* p) {
   return q;
 }
 
+// Where a lane's theta values come from: registers loaded once per work unit (TR)
+// or the CTA's shared-memory row (fewer registers, more LSU traffic).
+template <int R, bool TR>
+struct ThetaSrc;
+
+template <int R>
+struct ThetaSrc<R, true> {
+  Quad q[R];
+  __device__ __forceinline__ Quad at(int r, int) const { return q[r]; }
+  __device__ __forceinline__ Quad dyn(int rr, int) const {
+    Quad t = q[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r)
+      if (r == rr) t = q[r];
+    return t;
+  }
+};
+
+template <int R>
+struct ThetaSrc<R, false> {
+  const double* p;
+  __device__ __forceinline__ Quad at(int, int k) const {
+    const double2 t0 = *reinterpret_cast<const double2*>(p + k);
+    const double2 t1 = *reinterpret_cast<const double2*>(p + k + 2);
+    return Quad{t0.x, t0.y, t1.x, t1.y};
+  }
+  __device__ __forceinline__ Quad dyn(int, int k) const { return at(0, k); }
+};
+
+// The lane's 4 candidate weights at column k: theta*phi (tq = the lane's theta
+// values, kept in registers for the whole work unit) or, EXACT, exp(log theta +
+// log phi - max) with tq = log theta.
 template <bool EXACT>
-__device__ __forceinline__ Quad weights(const double* th, const double* lth, const double* row,
-                                        const double* lrow, int k, double mx) {
+__device__ __forceinline__ Quad weights(const Quad& tq, const double* row, const double* lrow, int k,
+                                        double mx) {
   Quad q;
   if constexpr (!EXACT) {
     const Quad a = ldg256(row + k);
-    const double2 t0 = *reinterpret_cast<const double2*>(th + k);
-    const double2 t1 = *reinterpret_cast<const double2*>(th + k + 2);
-    q.v0 = t0.x * a.v0;
-    q.v1 = t0.y * a.v1;
-    q.v2 = t1.x * a.v2;
-    q.v3 = t1.y * a.v3;
+    q.v0 = tq.v0 * a.v0;
+    q.v1 = tq.v1 * a.v1;
+    q.v2 = tq.v2 * a.v2;
+    q.v3 = tq.v3 * a.v3;
   } else {
     const Quad a = ldg256(lrow + k);
-    const double2 t0 = *reinterpret_cast<const double2*>(lth + k);
-    const double2 t1 = *reinterpret_cast<const double2*>(lth + k + 2);
-    q.v0 = exp((t0.x + a.v0) - mx);
-    q.v1 = exp((t0.y + a.v1) - mx);
-    q.v2 = exp((t1.x + a.v2) - mx);
-    q.v3 = exp((t1.y + a.v3) - mx);
+    q.v0 = exp((tq.v0 + a.v0) - mx);
+    q.v1 = exp((tq.v1 + a.v1) - mx);
+    q.v2 = exp((tq.v2 + a.v2) - mx);
+    q.v3 = exp((tq.v3 + a.v3) - mx);
   }
   return q;
 }
@@ -302,9 +332,9 @@ __device__ __forceinline__ Quad weights(const double* th, const double* lth, con
 // Returns the drawn topic in every lane of the group, or -1 when every weight is
 // zero/-inf (the reference throws std::domain_error; the product form retries in
 // log space).
-template <int G, int R, bool EXACT>
-__device__ __forceinline__ int draw_topic(const double* th, const double* lth, const double* row,
-                                          const double* lrow, int K, int Rr, double u01) {
+template <int G, int R, bool EXACT, class TS>
+__device__ __forceinline__ int draw_topic(const TS& tq, const double* row, const double* lrow, int K,
+                                          int Rr, double u01) {
   const unsigned m = group_mask<G>();
   const int gl = threadIdx.x & (G - 1);
   double mx = 0.0;
@@ -313,11 +343,9 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r < Rr) {
-        const int k = 4 * (r * G + gl);
-        const Quad a = ldg256(lrow + k);
-        const double2 t0 = *reinterpret_cast<const double2*>(lth + k);
-        const double2 t1 = *reinterpret_cast<const double2*>(lth + k + 2);
-        lm = fmax(lm, fmax(fmax(t0.x + a.v0, t0.y + a.v1), fmax(t1.x + a.v2, t1.y + a.v3)));
+        const Quad a = ldg256(lrow + 4 * (r * G + gl));
+        const Quad t = tq.at(r, 4 * (r * G + gl));
+        lm = fmax(lm, fmax(fmax(t.v0 + a.v0, t.v1 + a.v1), fmax(t.v2 + a.v2, t.v3 + a.v3)));
       }
     }
     mx = g_max<G>(lm, m);
@@ -331,7 +359,7 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
   for (int r = 0; r < R; ++r) {
     s[r] = 0.0;
     if (r < Rr) {
-      const Quad q = weights<EXACT>(th, lth, row, lrow, 4 * (r * G + gl), mx);
+      const Quad q = weights<EXACT>(tq.at(r, 4 * (r * G + gl)), row, lrow, 4 * (r * G + gl), mx);
       s[r] = ((q.v0 + q.v1) + q.v2) + q.v3;
     }
     run += s[r];
@@ -345,8 +373,9 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
   const double u = u01 * total;
   int pos = 0;
   double base = 0.0;
+  constexpr int P = R <= 1 ? 1 : (R <= 2 ? 2 : (R <= 4 ? 4 : (R <= 8 ? 8 : 16)));  // pow2 >= R
 #pragma unroll
-  for (int step = R / 2; step >= 1; step >>= 1) {
+  for (int step = P / 2; step >= 1; step >>= 1) {
     const int c = pos + step - 1;
     double qc = 0.0;
 #pragma unroll
@@ -377,7 +406,7 @@ __device__ __forceinline__ int draw_topic(const double* th, const double* lth, c
   int kk = 0;
   if (gl == owner) {
     const int k0 = 4 * (pos * G + gl);
-    const Quad q = weights<EXACT>(th, lth, row, lrow, k0, mx);
+    const Quad q = weights<EXACT>(tq.dyn(pos, k0), row, lrow, k0, mx);
     double acc = start;
     kk = k0 + 3;
     acc += q.v0;
@@ -426,7 +455,7 @@ __device__ int draw_topic_logspace(const double* lth, const double* row, int K, 
 }
 
 // One CTA per work unit (a chunk of <= kChunk tokens of one document).
-template <int G, int R, bool EXACT>
+template <int G, int R, bool EXACT, bool TR>
 __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* th = reinterpret_cast<double*>(smem_raw);  // [Kp]
@@ -446,6 +475,25 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
       lth[k] = x > 0.0 ? log(x) : -INFINITY;
     }
     __syncthreads();
+    // The lane's theta (log theta when EXACT) for its candidates, held in registers
+    // across the unit's tokens.
+    ThetaSrc<R, TR> tq;
+    if constexpr (TR) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = 4 * (r * G + gl);
+        const double* src = EXACT ? lth : th;
+        if (r < Rr) {
+          const double2 t0 = *reinterpret_cast<const double2*>(src + k);
+          const double2 t1 = *reinterpret_cast<const double2*>(src + k + 2);
+          tq.q[r] = Quad{t0.x, t0.y, t1.x, t1.y};
+        } else {
+          tq.q[r] = Quad{0.0, 0.0, 0.0, 0.0};
+        }
+      }
+    } else {
+      tq.p = EXACT ? lth : th;
+    }
     int* cnt = a.nmk + m * a.K;
     double zs = 0.0;
     int wv_next = t0 + gid < t1 ? __ldg(a.w + t0 + gid) : 0;
@@ -460,7 +508,7 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
       Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                       static_cast<std::uint64_t>(iter)));
       const double u01 = rng.next_unit();
-      int k = draw_topic<G, R, EXACT>(th, lth, row, lrow, a.K, Rr, u01);
+      int k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
       if (!EXACT && k < 0) k = draw_topic_logspace<G>(lth, row, a.K, u01);
       if (valid && gl == 0) {
         if (k < 0) {
@@ -760,7 +808,9 @@ class Lda final : public Model {
     }
     Kp_ = (K_ + 4 * G_ - 1) / (4 * G_) * (4 * G_);
     const int rounds = Kp_ / (4 * G_);
-    R_ = rounds <= 2 ? 2 : (rounds <= 4 ? 4 : (rounds <= 8 ? 8 : 16));
+    // G = 4 kernels are instantiated for every round count 1..8 (no dead rounds held
+    // in registers); wider groups use 8 or 16.
+    R_ = G_ == 4 ? rounds : (rounds <= 8 ? 8 : 16);
     partition_docs(d.doc_offsets, M_, c.world, c.rank, &d0_, &d1_);
     Ml_ = d1_ - d0_;
     tok0_ = d.doc_offsets[d0_];
@@ -839,6 +889,9 @@ class Lda final : public Model {
     theta_norm_ = seq_sum_const(std::lgamma(alpha_), K_);
     theta_lgasum_ = std::lgamma(seq_sum_const(alpha_, K_));
 
+    // theta operands of the z-step: registers (default) or shared memory.
+    const char* tr = std::getenv("BNMC_ZSTEP_THETA");
+    theta_regs_ = !(tr && std::string(tr) == "smem");
     configure_kernels();
   }
 
@@ -1044,7 +1097,9 @@ class Lda final : public Model {
 
   template <int G, int R, bool E>
   void zstep_attr() {
-    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(zstep_smem())));
+    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(zstep_smem())));
   }
 
@@ -1063,9 +1118,18 @@ class Lda final : public Model {
       if (exact_) f(g, r, integral_constant<bool, true>{});
       else f(g, r, integral_constant<bool, false>{});
     };
-    if (G_ == 4 && R_ == 2) with_e(integral_constant<int, 4>{}, integral_constant<int, 2>{});
-    else if (G_ == 4 && R_ == 4) with_e(integral_constant<int, 4>{}, integral_constant<int, 4>{});
-    else if (G_ == 4) with_e(integral_constant<int, 4>{}, integral_constant<int, 8>{});
+    if (G_ == 4) {
+      switch (R_) {
+        case 1: with_e(integral_constant<int, 4>{}, integral_constant<int, 1>{}); break;
+        case 2: with_e(integral_constant<int, 4>{}, integral_constant<int, 2>{}); break;
+        case 3: with_e(integral_constant<int, 4>{}, integral_constant<int, 3>{}); break;
+        case 4: with_e(integral_constant<int, 4>{}, integral_constant<int, 4>{}); break;
+        case 5: with_e(integral_constant<int, 4>{}, integral_constant<int, 5>{}); break;
+        case 6: with_e(integral_constant<int, 4>{}, integral_constant<int, 6>{}); break;
+        case 7: with_e(integral_constant<int, 4>{}, integral_constant<int, 7>{}); break;
+        default: with_e(integral_constant<int, 4>{}, integral_constant<int, 8>{}); break;
+      }
+    }
     else if (G_ == 8) with_e(integral_constant<int, 8>{}, integral_constant<int, 8>{});
     else if (G_ == 16) with_e(integral_constant<int, 16>{}, integral_constant<int, 8>{});
     else if (R_ <= 8) with_e(integral_constant<int, 32>{}, integral_constant<int, 8>{});
@@ -1078,8 +1142,12 @@ class Lda final : public Model {
     const int* err = out.err;
     const std::int64_t* it = out.iter;
     dispatch_zstep([&](auto gg, auto r, auto e) {
-      zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value>
-          <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+      if (theta_regs_)
+        zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value, true>
+            <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+      else
+        zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value, false>
+            <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
     });
   }
 
@@ -1131,7 +1199,7 @@ class Lda final : public Model {
   int K_ = 0, Kp_ = 0, V_ = 0, G_ = 4, R_ = 8;
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
-  bool exact_ = false, observe_phi_ = false;
+  bool exact_ = false, observe_phi_ = false, theta_regs_ = true;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
