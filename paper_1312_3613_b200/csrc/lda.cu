@@ -889,9 +889,10 @@ class Lda final : public Model {
     theta_norm_ = seq_sum_const(std::lgamma(alpha_), K_);
     theta_lgasum_ = std::lgamma(seq_sum_const(alpha_, K_));
 
-    // theta operands of the z-step: registers (default) or shared memory.
+    // theta operands of the z-step: shared memory (default: 60 registers, 4 CTAs/SM)
+    // or registers (BNMC_ZSTEP_THETA=regs: 128 registers; measured 20 % slower on NIPS).
     const char* tr = std::getenv("BNMC_ZSTEP_THETA");
-    theta_regs_ = !(tr && std::string(tr) == "smem");
+    theta_regs_ = tr && std::string(tr) == "regs";
     configure_kernels();
   }
 
@@ -1199,7 +1200,7 @@ class Lda final : public Model {
   int K_ = 0, Kp_ = 0, V_ = 0, G_ = 4, R_ = 8;
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
-  bool exact_ = false, observe_phi_ = false, theta_regs_ = true;
+  bool exact_ = false, observe_phi_ = false, theta_regs_ = false;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
