@@ -118,11 +118,43 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
     a.phiT[i] = draw_gamma(r, a.beta + static_cast<double>(cnt));
   }
   __syncthreads();
+  // Column partials of the block's rows, fixed order: sum g (the Dirichlet row sum,
+  // batch.cpp:55-58) and sum log g (the phi factor of the log-joint without a
+  // normalisation pass: sum log(g/S) = sum log g - V log S).
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-    double s = 0.0;
-    for (int v = v0; v < v1; ++v) s += a.phiT[static_cast<std::size_t>(v) * a.Kp + k];
-    a.colpart[static_cast<std::size_t>(b) * a.K + k] = s;
+    double sg = 0.0, sl = 0.0;
+    for (int v = v0; v < v1; ++v) {
+      const double g = a.phiT[static_cast<std::size_t>(v) * a.Kp + k];
+      sg += g;
+      sl += g > 0.0 ? log(g) : -INFINITY;
+    }
+    a.colpart[static_cast<std::size_t>(b) * a.K + k] = sg;
+    a.colpart2[(static_cast<std::size_t>(b) * a.K + k) * 2] = sl;
   }
+}
+
+// Per topic: S[k] = sum_b colpart (the gamma row sum) and the phi factor
+// lp - sum lgamma(beta) + lgamma(sum beta) with lp = (beta-1) (sum log g - V log S)
+// (dist.cpp:115-130; sum phi = sum g / S = 1 by construction).
+__global__ void phi_colsum_terms_kernel(LdaArgs a) {
+  __shared__ double scratch[32];
+  const int k = blockIdx.x;
+  double sg = 0.0, sl = 0.0;
+  for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) {
+    sg += a.colpart[static_cast<std::size_t>(b) * a.K + k];
+    sl += a.colpart2[(static_cast<std::size_t>(b) * a.K + k) * 2];
+  }
+  sg = block_sum(sg, scratch);
+  sl = block_sum(sl, scratch);
+  if (threadIdx.x == 0) {
+    a.S[k] = sg;
+    const double lp = (a.beta - 1.0) * (sl - static_cast<double>(a.V) * log(sg));
+    a.phi_term[k] = (!(sg > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
+  }
+}
+
+__global__ void fill_kernel(double* p, int n, double v) {
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x) p[i] = v;
 }
 
 // out[k] = sum_b part[b*stride + k*width + which], fixed order.
@@ -144,15 +176,12 @@ __global__ void phi_norm_kernel(LdaArgs a) {
   const int v0 = b * a.rows_per_block;
   const int v1 = min(a.V, v0 + a.rows_per_block);
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-    const double S = NORMALISE ? a.S[k] : 1.0;
+    const double S = a.S[k];
     double lp = 0.0, sx = 0.0;
     for (int v = v0; v < v1; ++v) {
       const std::size_t c = static_cast<std::size_t>(v) * a.Kp + k;
-      double x = a.phiT[c];
-      if (NORMALISE) {
-        x = x / S;
-        a.phiT[c] = x;
-      }
+      const double x = a.phiT[c] / S;
+      if (NORMALISE) a.phiT[c] = x;
       const double lx = x > 0.0 ? log(x) : -INFINITY;
       if (a.logphiT) a.logphiT[c] = lx;
       lp += (a.beta - 1.0) * lx;
@@ -471,7 +500,9 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
     const double* thg = a.theta + m * a.K;
     for (int k = threadIdx.x; k < a.Kp; k += blockDim.x) {
       const double x = k < a.K ? thg[k] : 0.0;
-      th[k] = x;
+      // phiT holds the unnormalised gamma row g (phi = g / S[k]); fold 1/S into the
+      // theta operand: weight = (theta / S) * g.
+      th[k] = k < a.K ? x / a.S[k] : 0.0;
       lth[k] = x > 0.0 ? log(x) : -INFINITY;
     }
     __syncthreads();
@@ -540,7 +571,7 @@ __global__ void wterm_kernel(LdaArgs a) {
     const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
     const int n = a.nkw[i];
     if (n) {
-      const double p = a.phiT[i];
+      const double p = a.phiT[i] / a.S[k];  // phi = g / S (S = 1 once normalised)
       acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
     }
   }
@@ -574,7 +605,7 @@ __global__ void __launch_bounds__(256) doc_eval_kernel(LdaArgs a, int* err) {
       }
       const double pt = th[k];
       zs += pt > 0.0 ? log(pt) : -INFINITY;
-      const double pp = a.phiT[static_cast<std::size_t>(a.w[t]) * a.Kp + k];
+      const double pp = a.phiT[static_cast<std::size_t>(a.w[t]) * a.Kp + k] / a.S[k];
       ws += pp > 0.0 ? log(pp) : -INFINITY;
     }
     zs = block_sum(zs, scratch);
@@ -588,9 +619,10 @@ __global__ void __launch_bounds__(256) doc_eval_kernel(LdaArgs a, int* err) {
   }
 }
 
-// red[0..2] = F_theta, F_z, F_w of this rank (fixed order).
-template <bool EVAL>
-__global__ void reduce_kernel(LdaArgs a) {
+// red[0..2] = F_theta, F_z, F_w of this rank (fixed order).  FINAL (single GPU):
+// also the log-joint, as finalize_kernel.
+template <bool EVAL, bool FINAL = false>
+__global__ void reduce_kernel(LdaArgs a, Outputs o = Outputs{}, int advance = 0) {
   __shared__ double scratch[32];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   if (EVAL) {
@@ -611,6 +643,18 @@ __global__ void reduce_kernel(LdaArgs a) {
     a.red[0] = s0;
     a.red[1] = s1;
     a.red[2] = s2;
+  }
+  if constexpr (FINAL) {
+    double f = 0.0;
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) f += a.phi_term[k];
+    f = block_sum(f, scratch);
+    if (threadIdx.x == 0) {
+      const double lj = ((f + s0) + s1) + s2;
+      const std::int64_t it = *o.iter;
+      o.lj[it & (kRing - 1)] = lj;
+      o.acc[it & (kRing - 1)] = 0;
+      if (advance) *o.iter = it + 1;
+    }
   }
 }
 
@@ -672,14 +716,17 @@ __global__ void i32_to_i64_kernel(const int* in, std::int64_t* out, std::int64_t
     out[i] = in[i];
 }
 
-// phiT [V][Kp] <-> phi [K][V] (reference layout), tiled through shared memory.
+// phiT [V][Kp] <-> phi [K][V] (reference layout), tiled through shared memory;
+// with `colscale` (download), out = in / colscale[column of in] = g / S.
 __global__ void transpose_kernel(const double* in, double* out, int rows, int cols, int ld_in,
-                                 int ld_out) {
+                                 int ld_out, const double* colscale = nullptr) {
   __shared__ double tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[i][threadIdx.x] = in[static_cast<std::size_t>(r) * ld_in + c];
+    if (r < rows && c < cols)
+      tile[i][threadIdx.x] = colscale ? in[static_cast<std::size_t>(r) * ld_in + c] / colscale[c]
+                                      : in[static_cast<std::size_t>(r) * ld_in + c];
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -894,6 +941,15 @@ class Lda final : public Model {
     const char* tr = std::getenv("BNMC_ZSTEP_THETA");
     theta_regs_ = tr && std::string(tr) == "regs";
     configure_kernels();
+    BNMC_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  }
+
+  ~Lda() override {
+    if (side_) cudaStreamDestroy(side_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
   }
 
   void upload(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, true); }
@@ -948,7 +1004,7 @@ class Lda final : public Model {
                                 cudaMemcpyDeviceToHost, st));
     if (!(obs && obs[var_phi_]) && !observe_phi_ && s.real[var_phi_]) {
       if (stage_phi_.n == 0) stage_phi_.alloc(static_cast<std::size_t>(K_) * V_);
-      transpose_kernel<<<dim3((K_ + 31) / 32, (V_ + 31) / 32), dim3(32, 8), 0, st>>>(phiT_.p, stage_phi_.p, V_, K_, Kp_, V_);
+      transpose_kernel<<<dim3((K_ + 31) / 32, (V_ + 31) / 32), dim3(32, 8), 0, st>>>(phiT_.p, stage_phi_.p, V_, K_, Kp_, V_, S_.p);
       BNMC_CUDA(cudaMemcpyAsync(s.real[var_phi_], stage_phi_.p, stage_phi_.bytes(), cudaMemcpyDeviceToHost, st));
     }
     BNMC_CUDA(cudaGetLastError());
@@ -957,7 +1013,16 @@ class Lda final : public Model {
 
   void enqueue_sweep(cudaStream_t st) override {
     LdaArgs a = args();
+    const bool timed = marks != nullptr;  // phase timing: everything on one stream
     mark(st, "begin");
+    // The theta block depends only on the doc-topic counts: it runs on a side stream
+    // concurrently with the phi block (fork/join events; captured into the graph).
+    if (Ml_ > 0 && !timed) {
+      BNMC_CUDA(cudaEventRecord(ev_fork_, st));
+      BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, side_>>>(a, out.iter);
+      BNMC_CUDA(cudaEventRecord(ev_join_, side_));
+    }
     if (!observe_phi_) {
       if (comm_.world > 1) {
         BNMC_NCCL(ncclAllReduce(nkw_.p, nkw_.p, nkw_.n, ncclInt32, ncclSum, comm_.comm, st));
@@ -965,33 +1030,39 @@ class Lda final : public Model {
       }
       phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
       mark(st, "phi_gamma");
-      colsum_kernel<<<K_, 128, 0, st>>>(colpart_.p, nb_phi_, K_, 1, 0, S_.p);
+      phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
       mark(st, "phi_colsum");
-      phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
-      mark(st, "phi_norm");
-      phi_terms_kernel<<<K_, 128, 0, st>>>(a);
-      mark(st, "phi_terms");
+      if (exact_) {
+        // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
+        phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
+        fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
+        mark(st, "phi_norm");
+      }
     } else {
       // phi clamped: no phi block consumes the counts; the z-step's counts of this
       // sweep feed only the w-factor.
       nkw_.zero(st);
     }
     if (Ml_ > 0) {
-      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
-      mark(st, "theta");
+      if (timed) {
+        theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
+        mark(st, "theta");
+      } else {
+        BNMC_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+      }
       launch_zstep(a, st);
       mark(st, "zstep");
     }
     wterm_kernel<<<nb_phi_, 256, 0, st>>>(a);
     mark(st, "wterm");
-    reduce_kernel<false><<<1, 1024, 0, st>>>(a);
-    mark(st, "reduce");
     if (comm_.world > 1) {
+      reduce_kernel<false><<<1, 1024, 0, st>>>(a);
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
-      mark(st, "allreduce_lj");
+      finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
+    } else {
+      reduce_kernel<false, true><<<1, 1024, 0, st>>>(a, out, 1);
     }
-    finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
-    mark(st, "finalize");
+    mark(st, "reduce_finalize");
     BNMC_CUDA(cudaGetLastError());
   }
 
@@ -999,7 +1070,7 @@ class Lda final : public Model {
     LdaArgs a = args();
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
-    doc_eval_kernel<<<grid_docs(), 256, 0, st>>>(a, out.err);
+    if (Ml_ > 0) doc_eval_kernel<<<grid_docs(), 256, 0, st>>>(a, out.err);
     reduce_kernel<true><<<1, 1024, 0, st>>>(a);
     if (comm_.world > 1)
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
@@ -1077,6 +1148,7 @@ class Lda final : public Model {
 
   // After an upload / prior_init: counts of the current z for the next phi block.
   void after_state_change(cudaStream_t st) {
+    fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);  // phiT holds phi itself
     LdaArgs a = args();
     nkw_.zero(st);
     nmk_.zero(st);
@@ -1201,6 +1273,8 @@ class Lda final : public Model {
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
