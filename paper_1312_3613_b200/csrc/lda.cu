@@ -52,6 +52,8 @@ struct LdaArgs {
   std::int64_t n_units;
   std::int64_t tok_base, doc_base;
   double* phiT;
+  float* phiT32;     // fp32 copy of phiT [V][Kp32] for the screened z-step (else null)
+  int Kp32;
   double* logphiT;   // exact mode only
   double* theta;
   int* nkw;          // [V][Kp]
@@ -115,7 +117,9 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
       a.nkw[i] = 0;
     }
     Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
-    a.phiT[i] = draw_gamma(r, a.beta + static_cast<double>(cnt));
+    const double g = draw_gamma(r, a.beta + static_cast<double>(cnt));
+    a.phiT[i] = g;
+    if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + k] = static_cast<float>(g);
   }
   __syncthreads();
   // Column partials of the block's rows, fixed order: sum g (the Dirichlet row sum,
@@ -150,6 +154,16 @@ __global__ void phi_colsum_terms_kernel(LdaArgs a) {
     a.S[k] = sg;
     const double lp = (a.beta - 1.0) * (sl - static_cast<double>(a.V) * log(sg));
     a.phi_term[k] = (!(sg > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
+  }
+}
+
+// fp32 screen copy of phi's numerator: phiT32 = (float)(phiT / S) (S = 1 outside a sweep).
+__global__ void phi_f32_kernel(LdaArgs a) {
+  const std::int64_t n = static_cast<std::int64_t>(a.V) * a.K;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t v = i / a.K, k = i % a.K;
+    a.phiT32[v * a.Kp32 + k] = static_cast<float>(a.phiT[v * a.Kp + k] / a.S[k]);
   }
 }
 
@@ -455,6 +469,123 @@ __device__ __forceinline__ int draw_topic(const TS& tq, const double* row, const
   return __shfl_sync(m, kk, owner, G);
 }
 
+
+// ---------------------------------------------------------------------------------
+// z block, fp32 screen + fp64 verification
+// ---------------------------------------------------------------------------------
+// The same inverse-CDF draw is first evaluated on fp32 copies of theta/S and g (half
+// the bytes: one 256-bit load carries 8 candidates, a G-lane group reads a full
+// 128-byte line per round).  fp32 running sums differ from the fp64 ones by at most
+// ~23 * 2^-24 * total (products: 3 roundings; sums: depth <= 8 + log2 G + R + 1), and
+// the draw is decided by the two running sums adjacent to u.  When u is farther than
+// kScreenMargin * total from both (and the total is far from fp32 underflow), the fp64
+// draw must pick the same candidate; otherwise the token is redrawn with the fp64
+// path.  The margin (2^-16, ~5x the bound) makes ~2 * K * 2^-16 of the tokens take the
+// fp64 path (0.3 % at K = 100); the result is the fp64 product-form draw either way.
+constexpr float kScreenMargin = 1.52587890625e-05f;  // 2^-16
+constexpr int kAmbiguous = -3;
+
+struct Oct {
+  float v[8];
+};
+
+__device__ __forceinline__ Oct ldg256f(const float* p) {
+  Oct o;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(o.v[0]), "=f"(o.v[1]), "=f"(o.v[2]), "=f"(o.v[3]), "=f"(o.v[4]), "=f"(o.v[5]), "=f"(o.v[6]),
+        "=f"(o.v[7])
+      : "l"(p));
+  return o;
+}
+
+template <int G>
+__device__ __forceinline__ float g_sumf(float v, unsigned m) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o, G);
+  return v;
+}
+
+// Returns the candidate (all lanes) or kAmbiguous.  tf: the lane's theta/S in fp32,
+// candidates 8*(r*G + gl) .. +7 of round r.
+template <int G, int R32>
+__device__ __forceinline__ int draw_topic_f32(const Oct (&tf)[R32], const float* row, int K, double u01) {
+  const unsigned m = group_mask<G>();
+  const int gl = threadIdx.x & (G - 1);
+  float s[R32], Q[R32];
+  float run = 0.0f;
+#pragma unroll
+  for (int r = 0; r < R32; ++r) {
+    const Oct a = ldg256f(row + 8 * (r * G + gl));
+    float t = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += tf[r].v[j] * a.v[j];
+    s[r] = t;
+    run += t;
+    Q[r] = run;
+  }
+  const float total = g_sumf<G>(Q[R32 - 1], m);
+  if (!(total > 0x1p-90f) || !isfinite(total)) return kAmbiguous;
+  const double u = u01 * static_cast<double>(total);
+  int pos = 0;
+  float base = 0.0f;
+  constexpr int P = R32 <= 1 ? 1 : (R32 <= 2 ? 2 : (R32 <= 4 ? 4 : (R32 <= 8 ? 8 : 16)));
+#pragma unroll
+  for (int step = P / 2; step >= 1; step >>= 1) {
+    const int c = pos + step - 1;
+    float qc = 0.0f;
+#pragma unroll
+    for (int r = 0; r < R32; ++r)
+      if (r == c) qc = Q[r];
+    const float f = g_sumf<G>(qc, m);
+    if (c < R32 && !(u < static_cast<double>(f))) {
+      pos += step;
+      base = f;
+    }
+  }
+  if (pos >= R32) return kAmbiguous;
+  float sc = 0.0f;
+#pragma unroll
+  for (int r = 0; r < R32; ++r)
+    if (r == pos) sc = s[r];
+  float inc = sc;
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    const float t = __shfl_up_sync(m, inc, d, G);
+    if (gl >= d) inc += t;
+  }
+  float ex = __shfl_up_sync(m, inc, 1, G);
+  if (gl == 0) ex = 0.0f;
+  const float start = base + ex;
+  const int owner = g_max_i<G>(static_cast<double>(start) <= u ? gl : 0, m);
+  int kk = kAmbiguous;
+  if (gl == owner) {
+    Oct tp = tf[0];
+#pragma unroll
+    for (int r = 1; r < R32; ++r)
+      if (r == pos) tp = tf[r];
+    const int k0 = 8 * (pos * G + gl);
+    const Oct a = ldg256f(row + k0);
+    float acc = start, lo = start;
+    int found = -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float nx = acc + tp.v[j] * a.v[j];
+      if (found < 0 && u < static_cast<double>(nx)) {
+        found = j;
+        lo = acc;
+        acc = nx;
+        break;
+      }
+      acc = nx;
+    }
+    if (found >= 0 && k0 + found < K) {
+      const double margin = static_cast<double>(kScreenMargin) * static_cast<double>(total);
+      if (u - static_cast<double>(lo) >= margin && static_cast<double>(acc) - u >= margin) kk = k0 + found;
+    }
+  }
+  return __shfl_sync(m, kk, owner, G);
+}
+
 // Sequential log-space draw exactly as draw_from_log_weights, for the rare token
 // whose product weights underflow (lane 0 of the group; result broadcast).
 template <int G>
@@ -484,7 +615,7 @@ __device__ int draw_topic_logspace(const double* lth, const double* row, int K, 
 }
 
 // One CTA per work unit (a chunk of <= kChunk tokens of one document).
-template <int G, int R, bool EXACT, bool TR>
+template <int G, int R, bool EXACT, bool TR, int R32 = 0>
 __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* th = reinterpret_cast<double*>(smem_raw);  // [Kp]
@@ -525,6 +656,16 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
     } else {
       tq.p = EXACT ? lth : th;
     }
+    // fp32 screen operands: the lane's theta/S for its 8 candidates of each round.
+    Oct tf[R32 > 0 ? R32 : 1];
+    if constexpr (R32 > 0) {
+#pragma unroll
+      for (int r = 0; r < R32; ++r) {
+        const int k0 = 8 * (r * G + gl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tf[r].v[j] = k0 + j < a.Kp ? static_cast<float>(th[k0 + j]) : 0.0f;
+      }
+    }
     int* cnt = a.nmk + m * a.K;
     double zs = 0.0;
     int wv_next = t0 + gid < t1 ? __ldg(a.w + t0 + gid) : 0;
@@ -539,7 +680,13 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
       Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                       static_cast<std::uint64_t>(iter)));
       const double u01 = rng.next_unit();
-      int k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
+      int k;
+      if constexpr (R32 > 0) {
+        k = draw_topic_f32<G, R32>(tf, a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32, a.K, u01);
+        if (k == kAmbiguous) k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
+      } else {
+        k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
+      }
       if (!EXACT && k < 0) k = draw_topic_logspace<G>(lth, row, a.K, u01);
       if (valid && gl == 0) {
         if (k < 0) {
@@ -894,6 +1041,11 @@ class Lda final : public Model {
     off_.alloc(Ml_ + 1);
     phiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
     if (exact_) logphiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    // fp32-screened z-step (product weights only); BNMC_ZSTEP_SCREEN=0 disables it.
+    const char* sc = std::getenv("BNMC_ZSTEP_SCREEN");
+    screen_ = !exact_ && !(sc && std::string(sc) == "0");
+    Kp32_ = (K_ + 8 * G_ - 1) / (8 * G_) * (8 * G_);
+    if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
@@ -917,6 +1069,7 @@ class Lda final : public Model {
     zpart_.zero(s0);
     wpart_.zero(s0);
     phiT_.zero(s0);
+    phiT32_.zero(s0);
     nkw_.zero(s0);
     w_.zero(s0);
     z_.zero(s0);
@@ -1160,6 +1313,7 @@ class Lda final : public Model {
     // clamped-phi runs, recomputed by the phi block otherwise.
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
+    if (screen_) phi_f32_kernel<<<148 * 8, 256, 0, st>>>(a);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
@@ -1170,10 +1324,12 @@ class Lda final : public Model {
 
   template <int G, int R, bool E>
   void zstep_attr() {
-    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(zstep_smem())));
-    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(zstep_smem())));
+    const int sm = static_cast<int>(zstep_smem());
+    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    if constexpr (!E)
+      BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, false, false, (R + 1) / 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   }
 
   void configure_kernels() {
@@ -1215,12 +1371,18 @@ class Lda final : public Model {
     const int* err = out.err;
     const std::int64_t* it = out.iter;
     dispatch_zstep([&](auto gg, auto r, auto e) {
+      constexpr int GG = decltype(gg)::value, RR = decltype(r)::value;
+      constexpr bool EE = decltype(e)::value;
+      if constexpr (!EE) {
+        if (screen_) {
+          zstep_kernel<GG, RR, false, false, (RR + 1) / 2><<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+          return;
+        }
+      }
       if (theta_regs_)
-        zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value, true>
-            <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+        zstep_kernel<GG, RR, EE, true><<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
       else
-        zstep_kernel<decltype(gg)::value, decltype(r)::value, decltype(e)::value, false>
-            <<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+        zstep_kernel<GG, RR, EE, false><<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
     });
   }
 
@@ -1237,6 +1399,8 @@ class Lda final : public Model {
     a.tok_base = tok0_;
     a.doc_base = d0_;
     a.phiT = phiT_.p;
+    a.phiT32 = screen_ ? phiT32_.p : nullptr;
+    a.Kp32 = Kp32_;
     a.logphiT = exact_ ? logphiT_.p : nullptr;
     a.theta = theta_.p;
     a.nkw = nkw_.p;
@@ -1272,7 +1436,9 @@ class Lda final : public Model {
   int K_ = 0, Kp_ = 0, V_ = 0, G_ = 4, R_ = 8;
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
-  bool exact_ = false, observe_phi_ = false, theta_regs_ = false;
+  bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
+  int Kp32_ = 0;
+  DevBuf<float> phiT32_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;

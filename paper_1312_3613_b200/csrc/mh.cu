@@ -66,26 +66,72 @@ __global__ void propose_kernel(MhArgs a, const std::int64_t* iter_p) {
 }
 
 // Sum over local rows of the row log-likelihood at parameters p (K + 2 values).
-// Warp per row: lanes stride the K features (coalesced 256 B per load), the dot
-// product is a fixed butterfly.
+// A group of 8 lanes per row: lane gl reads the row's 4-feature chunks gl, gl+8, ...
+// with one 256-bit load each (8 lanes = 256 contiguous bytes per request, 4 rows per
+// warp), keeps its slice of w in registers, and the dot product is a fixed 3-step
+// butterfly; lane 0 of the group evaluates the row's log-likelihood.
+constexpr int kRowGroup = 8;
+constexpr int kMaxChunks = 8;  // K <= 4 * 8 * kMaxChunks = 256 on the vector path
+
+__device__ __forceinline__ void ldg256(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+__device__ __forceinline__ double row_loglik(const MhArgs& a, double s, double yi, double tau) {
+  return a.logistic ? yi * s - softplus(s) : log_pdf_gaussian(yi, s, tau);
+}
+
+template <bool VEC, int CPL = 1>  // CPL: 4-feature chunks per lane (vector path)
 __global__ void __launch_bounds__(kThreads) lik_kernel(MhArgs a, const double* p, double* part) {
   extern __shared__ double wsh[];
   __shared__ double scratch[32];
   for (int j = threadIdx.x; j < a.K + 2; j += blockDim.x) wsh[j] = p[j];
   __syncthreads();
   const double b = wsh[a.K], tau = wsh[a.K + 1];
-  const int lane = threadIdx.x & 31;
-  const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
   double acc = 0.0;
-  for (std::int64_t i = warp; i < a.N; i += nwarps) {
-    const double* xi = a.x + i * a.K;
-    double s = 0.0;
-    for (int j = lane; j < a.K; j += 32) s += wsh[j] * __ldg(xi + j);
-    s = warp_sum(s) + b;
-    if (lane == 0) {
-      const double yi = __ldg(a.y + i);
-      acc += a.logistic ? yi * s - softplus(s) : log_pdf_gaussian(yi, s, tau);
+  if constexpr (VEC) {
+    const int gl = threadIdx.x & (kRowGroup - 1);
+    const unsigned gm = 0xffu << ((threadIdx.x & 31) & ~(kRowGroup - 1));
+    const int chunks = a.K / 4;
+    double wr[CPL][4];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int j = 4 * (gl + kRowGroup * c);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) wr[c][e] = j < a.K ? wsh[j + e] : 0.0;
+    }
+    const std::int64_t g = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / kRowGroup;
+    const std::int64_t ng = static_cast<std::int64_t>(gridDim.x) * blockDim.x / kRowGroup;
+    for (std::int64_t i = g; i < a.N; i += ng) {
+      const double* xi = a.x + i * a.K;
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = gl + kRowGroup * c;
+        if (ch < chunks) {
+          double x0, x1, x2, x3;
+          ldg256(xi + 4 * ch, x0, x1, x2, x3);
+          s += wr[c][0] * x0;
+          s += wr[c][1] * x1;
+          s += wr[c][2] * x2;
+          s += wr[c][3] * x3;
+        }
+      }
+#pragma unroll
+      for (int o = kRowGroup / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gm, s, o, kRowGroup);
+      if (gl == 0) acc += row_loglik(a, s + b, __ldg(a.y + i), tau);
+    }
+  } else {
+    // any K: warp per row, lanes stride the features
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t i = warp; i < a.N; i += nwarps) {
+      const double* xi = a.x + i * a.K;
+      double s = 0.0;
+      for (int j = lane; j < a.K; j += 32) s += wsh[j] * __ldg(xi + j);
+      s = warp_sum(s) + b;
+      if (lane == 0) acc += row_loglik(a, s, __ldg(a.y + i), tau);
     }
   }
   acc = block_sum(acc, scratch);
@@ -278,7 +324,7 @@ class Mh final : public Model {
     mark(st, "begin");
     propose_kernel<<<1, 128, 0, st>>>(a, out.iter);
     mark(st, "propose");
-    lik_kernel<<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, wp_.p, part_.p);
+    launch_lik(a, wp_.p, st);
     mark(st, "lik");
     const double* tot = nullptr;
     if (comm_.world > 1) {
@@ -307,8 +353,23 @@ class Mh final : public Model {
 
  private:
 
+  void launch_lik(const MhArgs& a, const double* p, cudaStream_t st) {
+    const std::size_t sm = sizeof(double) * (K_ + 2);
+    const int cpl = (K_ / 4 + kRowGroup - 1) / kRowGroup;
+    if (K_ % 4 == 0 && cpl <= 1)
+      lik_kernel<true, 1><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+    else if (K_ % 4 == 0 && cpl <= 2)
+      lik_kernel<true, 2><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+    else if (K_ % 4 == 0 && cpl <= 4)
+      lik_kernel<true, 4><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+    else if (K_ % 4 == 0 && cpl <= kMaxChunks)
+      lik_kernel<true, 8><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+    else
+      lik_kernel<false><<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, p, part_.p);
+  }
+
   void accept_kernel_cached(const MhArgs& a, cudaStream_t st) {
-    lik_kernel<<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, w_.p, part_.p);
+    launch_lik(a, w_.p, st);
     const double* tot = nullptr;
     if (comm_.world > 1) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
