@@ -60,53 +60,95 @@ def env_int(k, d):
 # measurement helpers
 # ----------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """SM clocks + throttle reasons sampled while the timed region runs.
+
+    NVML (libnvidia-ml, the library nvidia-smi reads) polled from a background thread
+    every ~0.5 ms, so even a timed region of a few tens of ms gets dozens of samples;
+    only samples taken between __enter__ and __exit__ are kept.  Falls back to
+    `nvidia-smi -lms 20` when NVML cannot be loaded."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.rows = []  # (sm_mhz, sm_max_mhz, [flag names active])
+        self.source = None
+
+    def _nvml_loop(self, nv, h, bits):
+        import time as _t
+
+        while not self._stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), [n for n, b in zip(self.NAMES, bits) if r & b]))
+            except Exception:
+                break
+            _t.sleep(0.0005)
 
     def __enter__(self):
+        self._stop = False
+        self.thread = None
+        try:
+            import threading
+
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h, bits), daemon=True)
+            self.source = "nvml"
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self._stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+        out = ""
         if self.proc:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                out, _ = self.proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                self.out, _ = self.proc.communicate()
-
-    def summary(self):
-        rows = []
-        for line in (self.out or "").strip().splitlines():
+                out, _ = self.proc.communicate()
+        for line in (out or "").strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) != len(self.FIELDS):
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+                flags = [n for n, f in zip(self.NAMES, parts[3:]) if f.lower() == "active"]
+                self.rows.append((float(parts[0]), float(parts[1]), flags))
             except ValueError:
                 continue
+
+    def summary(self):
+        rows = self.rows
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for _, _, flags in rows for n, f in zip(names, flags) if f.lower() == "active"})
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
+        reasons = sorted({n for _, _, flags in rows for n in flags})
         loaded = [r[0] for r in rows if r[0] > 500] or [r[0] for r in rows]
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": self.source}
 
 
 def measured_peak_hbm():
