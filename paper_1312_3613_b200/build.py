@@ -19,8 +19,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libbnmc_gpu.so")
+# BNMC_BUILD_VARIANT=name builds an experiment copy (extra nvcc flags from
+# BNMC_NVCC_EXTRA) into _build_<name>/ and libbnmc_gpu_<name>.so; load it with
+# BNMC_GPU_LIB=<path>.  The default build is the product library.
+_VAR = os.environ.get("BNMC_BUILD_VARIANT", "")
+OBJ = os.path.join(HERE, "_build" + (f"_{_VAR}" if _VAR else ""))
+LIB = os.path.join(HERE, "libbnmc_gpu" + (f"_{_VAR}" if _VAR else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +46,8 @@ def _nccl_dir():
 
 NCCL = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+         "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
+         *os.environ.get("BNMC_NVCC_EXTRA", "").split()]
 if NCCL:
     FLAGS += ["-I", os.path.join(NCCL, "include")]
 

@@ -29,6 +29,7 @@
 // theta fp64 [M_local][K] (the reference's row-major layout).
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -42,6 +43,14 @@ namespace {
 constexpr int kZThreads = 256;
 constexpr int kChunk = 512;  // tokens per z-step work unit
 
+// Column of logical candidate k in a phiT32 row (see zscreen_kernel): lane gl of a
+// G-lane group owns candidates [CW*R*gl, CW*R*(gl+1)); its round-r chunk of CW is
+// stored at CW*(r*G + gl), so each round of a group is one contiguous G*CW*4 bytes.
+__host__ __device__ __forceinline__ int phys32(int k, int R, int G, int CW) {
+  const int c = k / CW, j = k - c * CW, gl = c / R, r = c - gl * R;
+  return (r * G + gl) * CW + j;
+}
+
 struct LdaArgs {
   int K, Kp, V;
   std::int64_t Ml, Nl;
@@ -52,8 +61,8 @@ struct LdaArgs {
   std::int64_t n_units;
   std::int64_t tok_base, doc_base;
   double* phiT;
-  float* phiT32;     // fp32 copy of phiT [V][Kp32] for the screened z-step (else null)
-  int Kp32;
+  float* phiT32;     // fp32 copy of phiT [V][Kp32], columns permuted by phys32 (screen only)
+  int Kp32, G32, R32, CW32; // screen layout: Kp32 = CW32 * G32 * R32
   double* logphiT;   // exact mode only
   double* theta;
   int* nkw;          // [V][Kp]
@@ -63,7 +72,9 @@ struct LdaArgs {
   double* S;         // [K]
   double* phi_term;  // [K]
   double* tpart;     // [Ml] theta-factor pieces
-  double* zpart;     // [n_units] z-factor pieces
+  double* zpart;     // [nb_doc] z-factor pieces (sum_k n[d,k] log theta[d,k])
+  int* fq;           // screen fallback queue: local token indices [Nl]
+  int* fq_len;
   double* wpart;     // [nb_phi] w-factor pieces
   double* doc_part;  // [Ml][3] (eval path)
   double* red;       // [4]
@@ -73,6 +84,7 @@ struct LdaArgs {
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
   int var_phi, var_theta, var_z;
   int rows_per_block, nb_phi;
+  std::int64_t docs_per_block, nb_doc;
 };
 
 // ---------------------------------------------------------------------------------
@@ -119,7 +131,7 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
     Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
     const double g = draw_gamma(r, a.beta + static_cast<double>(cnt));
     a.phiT[i] = g;
-    if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + k] = static_cast<float>(g);
+    if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(g);
   }
   __syncthreads();
   // Column partials of the block's rows, fixed order: sum g (the Dirichlet row sum,
@@ -163,24 +175,12 @@ __global__ void phi_f32_kernel(LdaArgs a) {
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const std::int64_t v = i / a.K, k = i % a.K;
-    a.phiT32[v * a.Kp32 + k] = static_cast<float>(a.phiT[v * a.Kp + k] / a.S[k]);
+    a.phiT32[v * a.Kp32 + phys32(static_cast<int>(k), a.R32, a.G32, a.CW32)] = static_cast<float>(a.phiT[v * a.Kp + k] / a.S[k]);
   }
 }
 
 __global__ void fill_kernel(double* p, int n, double v) {
   for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x) p[i] = v;
-}
-
-// out[k] = sum_b part[b*stride + k*width + which], fixed order.
-__global__ void colsum_kernel(const double* part, int nb, int stride, int width, int which,
-                              double* out) {
-  __shared__ double scratch[32];
-  const int k = blockIdx.x;
-  double s = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x)
-    s += part[static_cast<std::size_t>(b) * stride + static_cast<std::size_t>(k) * width + which];
-  s = block_sum(s, scratch);
-  if (threadIdx.x == 0) out[k] = s;
 }
 
 // phi = g / S[k]; accumulates (beta-1)*log(phi) and phi per topic for the log-joint.
@@ -473,17 +473,16 @@ __device__ __forceinline__ int draw_topic(const TS& tq, const double* row, const
 // ---------------------------------------------------------------------------------
 // z block, fp32 screen + fp64 verification
 // ---------------------------------------------------------------------------------
-// The same inverse-CDF draw is first evaluated on fp32 copies of theta/S and g (half
-// the bytes: one 256-bit load carries 8 candidates, a G-lane group reads a full
-// 128-byte line per round).  fp32 running sums differ from the fp64 ones by at most
-// ~23 * 2^-24 * total (products: 3 roundings; sums: depth <= 8 + log2 G + R + 1), and
-// the draw is decided by the two running sums adjacent to u.  When u is farther than
-// kScreenMargin * total from both (and the total is far from fp32 underflow), the fp64
-// draw must pick the same candidate; otherwise the token is redrawn with the fp64
-// path.  The margin (2^-16, ~5x the bound) makes ~2 * K * 2^-16 of the tokens take the
-// fp64 path (0.3 % at K = 100); the result is the fp64 product-form draw either way.
+// The inverse-CDF draw is first evaluated on fp32 copies of theta/S and g (half the
+// bytes: one 256-bit load carries 8 candidates).  The fp32 running sums differ from
+// the exact cumulative weights by a small multiple of 2^-24 * total (bound below, at
+// zscreen_kernel), and the draw is decided by the two running sums adjacent to u.
+// When u is farther than kScreenMargin * total from both (and the total is far from
+// fp32 underflow), the fp64 draw must pick the same candidate; otherwise the token is
+// redrawn with the fp64 path.  The margin (2^-16) makes ~2 * K * 2^-16 of the tokens
+// take the fp64 path (0.3 % at K = 100); the result is the fp64 product-form draw
+// either way.
 constexpr float kScreenMargin = 1.52587890625e-05f;  // 2^-16
-constexpr int kAmbiguous = -3;
 
 struct Oct {
   float v[8];
@@ -491,99 +490,15 @@ struct Oct {
 
 __device__ __forceinline__ Oct ldg256f(const float* p) {
   Oct o;
+#ifdef BNMC_LDG_NOALLOC
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#else
   asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#endif
       : "=f"(o.v[0]), "=f"(o.v[1]), "=f"(o.v[2]), "=f"(o.v[3]), "=f"(o.v[4]), "=f"(o.v[5]), "=f"(o.v[6]),
         "=f"(o.v[7])
       : "l"(p));
   return o;
-}
-
-template <int G>
-__device__ __forceinline__ float g_sumf(float v, unsigned m) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o, G);
-  return v;
-}
-
-// Returns the candidate (all lanes) or kAmbiguous.  tf: the lane's theta/S in fp32,
-// candidates 8*(r*G + gl) .. +7 of round r.
-template <int G, int R32>
-__device__ __forceinline__ int draw_topic_f32(const Oct (&tf)[R32], const float* row, int K, double u01) {
-  const unsigned m = group_mask<G>();
-  const int gl = threadIdx.x & (G - 1);
-  float s[R32], Q[R32];
-  float run = 0.0f;
-#pragma unroll
-  for (int r = 0; r < R32; ++r) {
-    const Oct a = ldg256f(row + 8 * (r * G + gl));
-    float t = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t += tf[r].v[j] * a.v[j];
-    s[r] = t;
-    run += t;
-    Q[r] = run;
-  }
-  const float total = g_sumf<G>(Q[R32 - 1], m);
-  if (!(total > 0x1p-90f) || !isfinite(total)) return kAmbiguous;
-  const double u = u01 * static_cast<double>(total);
-  int pos = 0;
-  float base = 0.0f;
-  constexpr int P = R32 <= 1 ? 1 : (R32 <= 2 ? 2 : (R32 <= 4 ? 4 : (R32 <= 8 ? 8 : 16)));
-#pragma unroll
-  for (int step = P / 2; step >= 1; step >>= 1) {
-    const int c = pos + step - 1;
-    float qc = 0.0f;
-#pragma unroll
-    for (int r = 0; r < R32; ++r)
-      if (r == c) qc = Q[r];
-    const float f = g_sumf<G>(qc, m);
-    if (c < R32 && !(u < static_cast<double>(f))) {
-      pos += step;
-      base = f;
-    }
-  }
-  if (pos >= R32) return kAmbiguous;
-  float sc = 0.0f;
-#pragma unroll
-  for (int r = 0; r < R32; ++r)
-    if (r == pos) sc = s[r];
-  float inc = sc;
-#pragma unroll
-  for (int d = 1; d < G; d <<= 1) {
-    const float t = __shfl_up_sync(m, inc, d, G);
-    if (gl >= d) inc += t;
-  }
-  float ex = __shfl_up_sync(m, inc, 1, G);
-  if (gl == 0) ex = 0.0f;
-  const float start = base + ex;
-  const int owner = g_max_i<G>(static_cast<double>(start) <= u ? gl : 0, m);
-  int kk = kAmbiguous;
-  if (gl == owner) {
-    Oct tp = tf[0];
-#pragma unroll
-    for (int r = 1; r < R32; ++r)
-      if (r == pos) tp = tf[r];
-    const int k0 = 8 * (pos * G + gl);
-    const Oct a = ldg256f(row + k0);
-    float acc = start, lo = start;
-    int found = -1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float nx = acc + tp.v[j] * a.v[j];
-      if (found < 0 && u < static_cast<double>(nx)) {
-        found = j;
-        lo = acc;
-        acc = nx;
-        break;
-      }
-      acc = nx;
-    }
-    if (found >= 0 && k0 + found < K) {
-      const double margin = static_cast<double>(kScreenMargin) * static_cast<double>(total);
-      if (u - static_cast<double>(lo) >= margin && static_cast<double>(acc) - u >= margin) kk = k0 + found;
-    }
-  }
-  return __shfl_sync(m, kk, owner, G);
 }
 
 // Sequential log-space draw exactly as draw_from_log_weights, for the rare token
@@ -614,13 +529,448 @@ __device__ int draw_topic_logspace(const double* lth, const double* row, int K, 
   return __shfl_sync(m, pick, 0, G);
 }
 
+// ---------------------------------------------------------------------------------
+// z block, lean fp32 screen (default): lane-contiguous candidates
+// ---------------------------------------------------------------------------------
+// The screened draw, structured to keep the per-token instruction count low
+// (vs. a round-major grouped screen; ncu r01 v6: that kernel issued ~60 warp
+// instructions per token, 22 % of them IMAD from RNG evaluated by every lane):
+//  * lane gl of a G-lane group owns the CONTIGUOUS candidates [8R*gl, 8R*(gl+1)).
+//    phiT32 rows are stored permuted (phys32) so that round r of the group is still
+//    one contiguous 32G-byte segment (G = 4: one 128-byte line per round);
+//  * the lane's own running prefix over its rounds stays in registers; one group
+//    scan of the lane totals gives every lane its [start, end) interval, the owner
+//    of u is found with one ballot, and only the owner searches (no per-round
+//    group sums, no binary search over rounds);
+//  * the RNG (3 splitmix finalizers) and the w load run once per token: lane j of a
+//    warp handles token j of the warp's 32-token batch, then the values are
+//    shuffled to the group that draws that token;
+//  * FMA in the screen (explicit __fmaf_rn: --fmad=false only governs contraction).
+// Error budget: every screen partial sum is within (8 + R + log2 G + 4) * 2^-24 *
+// total of the exact cumulative weight (non-negative terms, fma chains); with
+// G <= 32, R <= 8 that is < 2^-19 * total, 8x below the 2^-16 margin.
+
+template <int CW>
+struct FChunk {
+  float v[CW];
+};
+
+template <int CW>
+__device__ __forceinline__ FChunk<CW> ldg_chunk(const float* p) {
+  FChunk<CW> c;
+  if constexpr (CW == 8) {
+    const Oct o = ldg256f(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c.v[j] = o.v[j];
+  } else {
+    static_assert(CW == 4, "chunk width 4 or 8");
+    asm("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(c.v[0]), "=f"(c.v[1]), "=f"(c.v[2]), "=f"(c.v[3])
+        : "l"(p));
+  }
+  return c;
+}
+
+// G lanes per token, CW candidates per lane per round (G * CW = 32: one 128-byte
+// line per round), R rounds; TFR keeps the lane's theta operands in registers
+// across the work unit (else they are re-read from shared memory every token).
+template <int G, int CW, int R, bool TFR>
+__global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // theta/S in fp32: lane gl's KL candidates at thf[gl * KLP ..], the +4 pad keeps the
+  // G lanes' 16-byte reads of one round in distinct banks
+  float* thf = reinterpret_cast<float*>(smem_raw);
+  const std::int64_t iter = *iter_p;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kZThreads / 32;
+  constexpr int KL = CW * R;  // candidates per lane
+  constexpr int KLP = KL + 4;
+  const unsigned gmask = group_mask<G>();
+  const unsigned gshift = static_cast<unsigned>(lane & ~(G - 1));
+  constexpr unsigned gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  // rounds of this lane that hold real candidates (the rest is padding, not fetched)
+  const int rl = min(R, max(0, (a.K - gl * KL + CW - 1) / CW));
+
+  for (std::int64_t unit = blockIdx.x; unit < a.n_units; unit += gridDim.x) {
+    const std::int64_t m = a.units[unit * 3], t0 = a.units[unit * 3 + 1], t1 = a.units[unit * 3 + 2];
+    const double* thg = a.theta + m * a.K;
+    for (int k = threadIdx.x; k < G * KL; k += blockDim.x)
+      thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+    __syncthreads();
+    float tf[TFR ? KL : 1];
+    if constexpr (TFR) {
+#pragma unroll
+      for (int i = 0; i < KL; i += 4) {
+        const float4 t = *reinterpret_cast<const float4*>(thf + gl * KLP + i);
+        tf[i] = t.x;
+        tf[i + 1] = t.y;
+        tf[i + 2] = t.z;
+        tf[i + 3] = t.w;
+      }
+    }
+    int* cnt = a.nmk + m * a.K;
+    for (std::int64_t b0 = t0 + warp * 32; b0 < t1; b0 += kWarps * 32) {
+      // token b0 + lane: its word and its uniform, keyed(seed, 3, var_z, t, iter)
+      const std::int64_t tl = b0 + lane;
+      const bool lvalid = tl < t1;
+      const int wl = lvalid ? __ldg(a.w + tl) : 0;
+      float ul = 0.5f;
+      if (lvalid) {
+        Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + tl)),
+                        static_cast<std::uint64_t>(iter)));
+        ul = static_cast<float>(rng.next_unit());
+      }
+#pragma unroll 1
+      for (int s = 0; s < G; ++s) {
+        if (b0 + s * (32 / G) >= t1) break;  // warp-uniform: no token left in this sub-batch
+        const int src = s * (32 / G) + gid;  // lane holding this group's token
+        const std::int64_t t = b0 + src;
+        const bool valid = t < t1;
+        const int wv = __shfl_sync(0xffffffffu, wl, src);
+        const float u01 = __shfl_sync(0xffffffffu, ul, src);
+        const float* row = a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
+        // all rounds' loads first (memory-level parallelism), then the fma chains
+        FChunk<CW> ph[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < rl) ph[r] = ldg_chunk<CW>(row + CW * (r * G + gl));
+          else ph[r] = FChunk<CW>{};
+        }
+        float Q[R];
+        float run = 0.0f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float x[CW];
+          if constexpr (TFR) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) x[j] = tf[CW * r + j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; j += 4) {
+              const float4 y = *reinterpret_cast<const float4*>(thf + gl * KLP + CW * r + j);
+              x[j] = y.x, x[j + 1] = y.y, x[j + 2] = y.z, x[j + 3] = y.w;
+            }
+          }
+          float sr = x[0] * ph[r].v[0];
+#pragma unroll
+          for (int j = 1; j < CW; ++j) sr = __fmaf_rn(x[j], ph[r].v[j], sr);
+          run += sr;
+          Q[r] = run;
+        }
+        // group inclusive scan of the lane totals -> [start, end) per lane
+        float inc = run;
+#pragma unroll
+        for (int d = 1; d < G; d <<= 1) {
+          const float y = __shfl_up_sync(gmask, inc, d, G);
+          if (gl >= d) inc += y;
+        }
+        float start = __shfl_up_sync(gmask, inc, 1, G);
+        if (gl == 0) start = 0.0f;
+        const float total = __shfl_sync(gmask, inc, G - 1, G);
+        const float uf = u01 * total;
+        const float mg = kScreenMargin * total;
+        int k = -1;
+        if (start <= uf && uf < inc && total > 0x1p-90f && total < 0x1p100f) {
+          // owner lane: the crossing round (registers), then the crossing candidate
+          float lo = start;
+          int rr = R - 1;
+#pragma unroll
+          for (int r = R - 1; r >= 0; --r)
+            if (uf < start + Q[r]) rr = r;
+#pragma unroll
+          for (int r = 0; r < R - 1; ++r)
+            if (r < rr) lo = start + Q[r];
+          const int kl0 = gl * KL + CW * rr;  // logical index of the chunk's first candidate
+          const FChunk<CW> p = ldg_chunk<CW>(row + CW * (rr * G + gl));
+          float tv[CW];
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 y = *reinterpret_cast<const float4*>(thf + gl * KLP + CW * rr + j);
+            tv[j] = y.x, tv[j + 1] = y.y, tv[j + 2] = y.z, tv[j + 3] = y.w;
+          }
+          float acc = lo, prev = lo;
+          int j = -1;
+#pragma unroll
+          for (int jj = 0; jj < CW; ++jj) {
+            const float nx = __fmaf_rn(tv[jj], p.v[jj], acc);
+            if (j < 0) {
+              if (uf < nx) {
+                j = jj;
+                prev = acc;
+              }
+              acc = nx;
+            }
+          }
+          if (j >= 0 && kl0 + j < a.K && uf - prev >= mg && acc - uf >= mg) k = kl0 + j;
+        }
+        const bool decided = ((__ballot_sync(0xffffffffu, k >= 0) >> gshift) & gbits) != 0;
+        if (valid) {
+          if (k >= 0) {
+            a.z[t] = k;
+            atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
+            atomicAdd(&cnt[k], 1);
+          } else if (!decided && gl == 0) {
+            // ambiguous for the screen: queued for the fp64 draw (zfallback_kernel)
+            const int slot = atomicAdd(a.fq_len, 1);
+            a.fq[slot] = static_cast<int>(t);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Transposed-search screen for K <= 128 (default there).  Two phases per warp batch
+// of 32 tokens:
+//  (1) products: G = 4 lanes per token (CW = 8, R rounds, lane-contiguous chunks as
+//      in zscreen_kernel, coalesced 128-byte lines); each lane writes its R chunk
+//      sums (8 candidates each) to the warp's shared-memory table csum[token][chunk];
+//  (2) search: lane j takes token j -- prefix over the C = 4R chunk sums in
+//      registers, u * total, the crossing chunk, one reload of that chunk and the
+//      in-chunk scan, the margin check, z and the count atomics.
+// Every lane does useful work in (2), instead of 1 lane in 4 for the in-group
+// search, and no cross-lane scans are needed (ncu r01 v10: the grouped search was
+// ~2/3 of the z-step's ~31 warp instructions per token).
+template <int R, bool TFR>
+__global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  constexpr int G = 4, CW = 8, KL = CW * R, KLP = KL + 4, C = G * R, CSP = C + 4;
+  constexpr int kWarps = kZThreads / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* thf = reinterpret_cast<float*>(smem_raw);  // [G][KLP] theta/S, fp32
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
+  const int warp = threadIdx.x >> 5;
+  float* csum = thf + G * KLP + warp * 32 * CSP;     // [32][CSP] chunk sums of the batch
+  const std::int64_t iter = *iter_p;
+  const int rl = min(R, max(0, (a.K - gl * KL + CW - 1) / CW));
+
+  for (std::int64_t unit = blockIdx.x; unit < a.n_units; unit += gridDim.x) {
+    const std::int64_t m = a.units[unit * 3], t0 = a.units[unit * 3 + 1], t1 = a.units[unit * 3 + 2];
+    const double* thg = a.theta + m * a.K;
+    for (int k = threadIdx.x; k < G * KL; k += blockDim.x)
+      thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+    __syncthreads();
+    float tf[TFR ? KL : 1];
+    if constexpr (TFR) {
+#pragma unroll
+      for (int i = 0; i < KL; i += 4) {
+        const float4 t = *reinterpret_cast<const float4*>(thf + gl * KLP + i);
+        tf[i] = t.x, tf[i + 1] = t.y, tf[i + 2] = t.z, tf[i + 3] = t.w;
+      }
+    }
+    int* cnt = a.nmk + m * a.K;
+    for (std::int64_t b0 = t0 + warp * 32; b0 < t1; b0 += kWarps * 32) {
+      const std::int64_t t = b0 + lane;
+      const bool valid = t < t1;
+      const int wl = valid ? __ldg(a.w + t) : 0;
+      // (1) products
+#pragma unroll 1
+      for (int s = 0; s < 32 / (32 / G); ++s) {
+        if (b0 + s * (32 / G) >= t1) break;  // warp-uniform
+        const int src = s * (32 / G) + gid;
+        const int wv = __shfl_sync(0xffffffffu, wl, src);
+        const float* row = a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
+        Oct ph[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < rl) ph[r] = ldg256f(row + CW * (r * G + gl));
+          else ph[r] = Oct{};
+        }
+        float cs[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float x[CW];
+          if constexpr (TFR) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) x[j] = tf[CW * r + j];
+          } else {
+            const float4 y0 = *reinterpret_cast<const float4*>(thf + gl * KLP + CW * r);
+            const float4 y1 = *reinterpret_cast<const float4*>(thf + gl * KLP + CW * r + 4);
+            x[0] = y0.x, x[1] = y0.y, x[2] = y0.z, x[3] = y0.w, x[4] = y1.x, x[5] = y1.y, x[6] = y1.z, x[7] = y1.w;
+          }
+          float sr = x[0] * ph[r].v[0];
+#pragma unroll
+          for (int j = 1; j < CW; ++j) sr = __fmaf_rn(x[j], ph[r].v[j], sr);
+          cs[r] = sr;
+        }
+        float* dst = csum + src * CSP + gl * R;
+        if constexpr (R == 4) {
+          *reinterpret_cast<float4*>(dst) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) dst[r] = cs[r];
+        }
+      }
+      __syncwarp();
+      // (2) search: lane = token
+      if (valid) {
+        Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
+                        static_cast<std::uint64_t>(iter)));
+        const float u01 = static_cast<float>(rng.next_unit());
+        float P[C];
+        float run = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; c += 4) {
+          const float4 y = *reinterpret_cast<const float4*>(csum + lane * CSP + c);
+          run += y.x;
+          P[c] = run;
+          run += y.y;
+          P[c + 1] = run;
+          run += y.z;
+          P[c + 2] = run;
+          run += y.w;
+          P[c + 3] = run;
+        }
+        const float total = run;
+        const float uf = u01 * total;
+        const float mg = kScreenMargin * total;
+        int k = -1;
+        if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
+          int cs = C - 1;
+          float lo = 0.0f;
+#pragma unroll
+          for (int c = C - 1; c >= 0; --c)
+            if (uf < P[c]) cs = c;
+#pragma unroll
+          for (int c = 0; c < C - 1; ++c)
+            if (c < cs) lo = P[c];
+          // chunk cs = lane cs / R's round cs % R (phys32 layout)
+          const int og = cs / R, orr = cs - og * R;
+          const Oct p = ldg256f(a.phiT32 + static_cast<std::size_t>(wl) * a.Kp32 + CW * (orr * G + og));
+          const float4 y0 = *reinterpret_cast<const float4*>(thf + og * KLP + CW * orr);
+          const float4 y1 = *reinterpret_cast<const float4*>(thf + og * KLP + CW * orr + 4);
+          const float tv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+          float acc = lo, prev = lo;
+          int j = -1;
+#pragma unroll
+          for (int jj = 0; jj < CW; ++jj) {
+            const float nx = __fmaf_rn(tv[jj], p.v[jj], acc);
+            if (j < 0) {
+              if (uf < nx) {
+                j = jj;
+                prev = acc;
+              }
+              acc = nx;
+            }
+          }
+          const int kk = CW * cs + j;
+          if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
+        }
+        if (k >= 0) {
+          a.z[t] = k;
+          atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
+          atomicAdd(&cnt[k], 1);
+        } else {
+          const int slot = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
+          a.fq[slot] = static_cast<int>(t);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// fp64 product-form draw for the tokens the screen could not decide (~2K * 2^-16
+// of them): one warp per queued token.  Lane l owns the contiguous candidates
+// [l*c, (l+1)*c), c = ceil(K/32); warp scan of the lane sums, the owner rescans
+// its chunk (the reference's candidate order and u = next_unit * total rule,
+// dist.cpp:202-215).  Tokens whose product weights underflow take the sequential
+// log-space draw.
+__global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
+  const std::int64_t iter = *iter_p;
+  const int lane = threadIdx.x & 31;
+  const int n = *a.fq_len;
+  const int c = (a.K + 31) / 32;
+  const int k0 = min(a.K, lane * c), k1 = min(a.K, k0 + c);
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const std::int64_t t = a.fq[i];
+    // document of t: the last m with off[m] <= t
+    std::int64_t lo = 0, hi = a.Ml - 1;
+    while (lo < hi) {
+      const std::int64_t mid = (lo + hi + 1) >> 1;
+      if (a.off[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const std::int64_t m = lo;
+    const int wv = a.w[t];
+    const double* thg = a.theta + m * a.K;
+    const double* row = a.phiT + static_cast<std::size_t>(wv) * a.Kp;
+    Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
+                    static_cast<std::uint64_t>(iter)));
+    const double u01 = rng.next_unit();
+    double own = 0.0;
+    for (int k = k0; k < k1; ++k) own += (thg[k] / a.S[k]) * row[k];
+    double inc = own;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    double start = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) start = 0.0;
+    const double total = __shfl_sync(0xffffffffu, inc, 31);
+    int pick = -1;
+    if (total > 0x1p-1000 && isfinite(total)) {
+      const double u = u01 * total;
+      int cand = (lane == 31 && !(u < inc)) ? a.K - 1 : -1;  // past-the-end: K - 1
+      if (start <= u && u < inc && k0 < k1) {
+        double acc = start;
+        cand = k1 - 1;
+        for (int k = k0; k < k1; ++k) {
+          acc += (thg[k] / a.S[k]) * row[k];
+          if (u < acc) {
+            cand = k;
+            break;
+          }
+        }
+      }
+      pick = __reduce_max_sync(0xffffffffu, cand);
+    } else if (lane == 0) {
+      // log-space, sequential (draw_from_log_weights)
+      double mx = -INFINITY;
+      for (int k = 0; k < a.K; ++k) {
+        const double x = thg[k], g = row[k] / a.S[k];
+        mx = fmax(mx, (x > 0.0 ? log(x) : -INFINITY) + (g > 0.0 ? log(g) : -INFINITY));
+      }
+      if (isfinite(mx)) {
+        double tot = 0.0;
+        for (int k = 0; k < a.K; ++k) {
+          const double x = thg[k], g = row[k] / a.S[k];
+          tot += exp(((x > 0.0 ? log(x) : -INFINITY) + (g > 0.0 ? log(g) : -INFINITY)) - mx);
+        }
+        const double u = u01 * tot;
+        double acc = 0.0;
+        pick = a.K - 1;
+        for (int k = 0; k < a.K; ++k) {
+          const double x = thg[k], g = row[k] / a.S[k];
+          acc += exp(((x > 0.0 ? log(x) : -INFINITY) + (g > 0.0 ? log(g) : -INFINITY)) - mx);
+          if (u < acc) {
+            pick = k;
+            break;
+          }
+        }
+      }
+    }
+    pick = __shfl_sync(0xffffffffu, pick, 0);
+    if (lane == 0) {
+      if (pick < 0) {
+        atomicOr(err, kErrDomain);
+      } else {
+        a.z[t] = pick;
+        atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + pick], 1);
+        atomicAdd(&a.nmk[m * a.K + pick], 1);
+      }
+    }
+  }
+}
+
 // One CTA per work unit (a chunk of <= kChunk tokens of one document).
-template <int G, int R, bool EXACT, bool TR, int R32 = 0>
+template <int G, int R, bool EXACT, bool TR>
 __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* th = reinterpret_cast<double*>(smem_raw);  // [Kp]
   double* lth = th + a.Kp;                            // [Kp]
-  __shared__ double scratch[32];
   const std::int64_t iter = *iter_p;
   const int Rr = a.Kp / (4 * G);
   const int gid = threadIdx.x / G, gl = threadIdx.x & (G - 1);
@@ -656,18 +1006,7 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
     } else {
       tq.p = EXACT ? lth : th;
     }
-    // fp32 screen operands: the lane's theta/S for its 8 candidates of each round.
-    Oct tf[R32 > 0 ? R32 : 1];
-    if constexpr (R32 > 0) {
-#pragma unroll
-      for (int r = 0; r < R32; ++r) {
-        const int k0 = 8 * (r * G + gl);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) tf[r].v[j] = k0 + j < a.Kp ? static_cast<float>(th[k0 + j]) : 0.0f;
-      }
-    }
     int* cnt = a.nmk + m * a.K;
-    double zs = 0.0;
     int wv_next = t0 + gid < t1 ? __ldg(a.w + t0 + gid) : 0;
     for (std::int64_t base = t0; base < t1; base += kGroups) {
       const std::int64_t t = base + gid;
@@ -680,13 +1019,7 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
       Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                       static_cast<std::uint64_t>(iter)));
       const double u01 = rng.next_unit();
-      int k;
-      if constexpr (R32 > 0) {
-        k = draw_topic_f32<G, R32>(tf, a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32, a.K, u01);
-        if (k == kAmbiguous) k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
-      } else {
-        k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
-      }
+      int k = draw_topic<G, R, EXACT>(tq, row, lrow, a.K, Rr, u01);
       if (!EXACT && k < 0) k = draw_topic_logspace<G>(lth, row, a.K, u01);
       if (valid && gl == 0) {
         if (k < 0) {
@@ -695,20 +1028,36 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
           a.z[t] = k;
           atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
           atomicAdd(&cnt[k], 1);
-          zs += lth[k];
         }
       }
     }
-    zs = block_sum(zs, scratch);
-    if (threadIdx.x == 0) a.zpart[u] = zs;
     __syncthreads();
   }
 }
 
-// w-factor from the counts: sum_{v,k} n[v,k] * log phi[k,v] over this rank's tokens.
+// w- and z-factors of the log-joint from the counts the z-step just produced:
+// sum_t log phi[z_t, w_t] = sum_{v,k} n[v,k] log phi[k,v]  (blocks < nb_phi) and
+// sum_t log theta[d_t, z_t] = sum_{d,k} n[d,k] log theta[d,k]  (the other blocks),
+// over this rank's tokens; fixed-order partials.
 __global__ void wterm_kernel(LdaArgs a) {
   __shared__ double scratch[32];
   const int b = blockIdx.x;
+  if (b >= a.nb_phi) {
+    const std::int64_t d0 = static_cast<std::int64_t>(b - a.nb_phi) * a.docs_per_block;
+    const std::int64_t d1 = min(a.Ml, d0 + a.docs_per_block);
+    const std::int64_t c0 = d0 * a.K, c1 = d1 * a.K;
+    double acc = 0.0;
+    for (std::int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+      const int n = a.nmk[c];
+      if (n) {
+        const double x = a.theta[c];
+        acc += static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY);
+      }
+    }
+    acc = block_sum(acc, scratch);
+    if (threadIdx.x == 0) a.zpart[b - a.nb_phi] = acc;
+    return;
+  }
   const int v0 = b * a.rows_per_block;
   const int v1 = min(a.V, v0 + a.rows_per_block);
   const int cells = (v1 - v0) * a.K;
@@ -780,7 +1129,7 @@ __global__ void reduce_kernel(LdaArgs a, Outputs o = Outputs{}, int advance = 0)
     }
   } else {
     for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += a.tpart[m];
-    for (std::int64_t u = threadIdx.x; u < a.n_units; u += blockDim.x) s1 += a.zpart[u];
+    for (std::int64_t u = threadIdx.x; u < a.nb_doc; u += blockDim.x) s1 += a.zpart[u];
     for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) s2 += a.wpart[b];
   }
   s0 = block_sum(s0, scratch);
@@ -1044,14 +1393,19 @@ class Lda final : public Model {
     // fp32-screened z-step (product weights only); BNMC_ZSTEP_SCREEN=0 disables it.
     const char* sc = std::getenv("BNMC_ZSTEP_SCREEN");
     screen_ = !exact_ && !(sc && std::string(sc) == "0");
-    Kp32_ = (K_ + 8 * G_ - 1) / (8 * G_) * (8 * G_);
+    choose_screen();
+    Kp32_ = CW32_ * G32_ * RS_;
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     units_.alloc(std::max<std::size_t>(units_host_.size(), 3));
     tpart_.alloc(std::max<std::int64_t>(Ml_, 1));
-    zpart_.alloc(std::max<std::int64_t>(n_units_, 1));
+    docs_per_block_ = std::max<std::int64_t>(1, 4096 / K_);
+    nb_doc_ = (Ml_ + docs_per_block_ - 1) / docs_per_block_;
+    zpart_.alloc(std::max<std::int64_t>(nb_doc_, 1));
+    fq_.alloc(std::max<std::int64_t>(Nl_, 1));
+    fq_len_.alloc(1);
     wpart_.alloc(nb_phi_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
@@ -1206,7 +1560,7 @@ class Lda final : public Model {
       launch_zstep(a, st);
       mark(st, "zstep");
     }
-    wterm_kernel<<<nb_phi_, 256, 0, st>>>(a);
+    wterm_kernel<<<static_cast<unsigned>(nb_phi_ + nb_doc_), 256, 0, st>>>(a);
     mark(st, "wterm");
     if (comm_.world > 1) {
       reduce_kernel<false><<<1, 1024, 0, st>>>(a);
@@ -1327,9 +1681,7 @@ class Lda final : public Model {
     const int sm = static_cast<int>(zstep_smem());
     BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, E, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    if constexpr (!E)
-      BNMC_CUDA(cudaFuncSetAttribute(zstep_kernel<G, R, false, false, (R + 1) / 2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+
   }
 
   void configure_kernels() {
@@ -1365,6 +1717,115 @@ class Lda final : public Model {
     else with_e(integral_constant<int, 32>{}, integral_constant<int, 16>{});
   }
 
+  // Screen layout: G lanes x CW candidates per round (G*CW = 32 floats, one 128-byte
+  // line), R rounds.  Default: CW = 4 and the smallest G with R <= 4, theta operands
+  // in registers (ncu r01 v8: with G = 4 x CW = 8 the per-token theta re-reads from
+  // shared memory doubled the L1 register-writeback traffic, the limiter); K > 512:
+  // G = 32 x CW = 8, theta in shared memory.  BNMC_ZSCREEN=g<G>w<CW>[s|r] overrides.
+  void choose_screen() {
+    transposed_ = K_ <= 128;
+    G32_ = 32;
+    CW32_ = 8;
+    tfr_ = false;
+    for (int g : {8, 16, 32}) {
+      if ((K_ + 4 * g - 1) / (4 * g) <= 4) {
+        G32_ = g;
+        CW32_ = 4;
+        tfr_ = true;
+        break;
+      }
+    }
+    if (const char* e = std::getenv("BNMC_ZSCREEN")) {
+      int g = 0, w = 0;
+      char mode = 'r';
+      if (std::sscanf(e, "g%dw%d%c", &g, &w, &mode) >= 2 && g * w >= 32 && (w == 4 || w == 8) &&
+          (g == 4 || g == 8 || g == 16 || g == 32)) {
+        G32_ = g;
+        CW32_ = w;
+        tfr_ = mode != 's';
+        transposed_ = false;
+      }
+    }
+    if (const char* e = std::getenv("BNMC_ZSCREEN_T")) transposed_ = std::string(e) != "0" && K_ <= 128;
+    if (transposed_) {
+      G32_ = 4;
+      CW32_ = 8;
+      // theta operands in registers (ncu r01 v11: 108 us vs 131 us from shared memory)
+      tfr_ = true;
+      if (const char* e = std::getenv("BNMC_ZSTEP_THETA")) tfr_ = std::string(e) != "smem";
+    }
+    RS_ = (K_ + CW32_ * G32_ - 1) / (CW32_ * G32_);
+    if (G32_ < 32 || CW32_ == 4) RS_ = RS_ <= 4 ? RS_ : -1;
+    require(RS_ >= 1 && RS_ <= 8, BNMC_GPU_ERR_ARG, "z-step screen layout does not fit K");
+    if (G32_ == 32 && CW32_ == 8) RS_ = RS_ <= 4 ? 4 : 8;
+    else if (G32_ != 8 && G32_ != 4) RS_ = 4;
+  }
+
+  template <int G, int CW, int R, bool TFR>
+  void zscreen_launch(const LdaArgs& a, cudaStream_t st) {
+    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
+    const std::size_t sm = sizeof(float) * G * (CW * R + 4);
+    zscreen_kernel<G, CW, R, TFR><<<g, kZThreads, sm, st>>>(a, out.iter);
+  }
+
+  template <int G, int CW, bool TFR>
+  void zscreen_rounds(const LdaArgs& a, cudaStream_t st) {
+    if constexpr (G <= 8) {
+      switch (RS_) {
+        case 1: zscreen_launch<G, CW, 1, TFR>(a, st); return;
+        case 2: zscreen_launch<G, CW, 2, TFR>(a, st); return;
+        case 3: zscreen_launch<G, CW, 3, TFR>(a, st); return;
+        default: zscreen_launch<G, CW, 4, TFR>(a, st); return;
+      }
+    } else if constexpr (G == 32 && CW == 8 && !TFR) {
+      if (RS_ > 4) zscreen_launch<G, CW, 8, TFR>(a, st);
+      else zscreen_launch<G, CW, 4, TFR>(a, st);
+    } else {
+      zscreen_launch<G, CW, 4, TFR>(a, st);
+    }
+  }
+
+  template <int R, bool TFR>
+  void zscreen_t_launch(const LdaArgs& a, cudaStream_t st) {
+    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
+    const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + (kZThreads / 32) * 32 * (4 * R + 4));
+    zscreen_t_kernel<R, TFR><<<g, kZThreads, sm, st>>>(a, out.iter);
+  }
+
+  template <bool TFR>
+  void zscreen_t_rounds(const LdaArgs& a, cudaStream_t st) {
+    switch (RS_) {
+      case 1: zscreen_t_launch<1, TFR>(a, st); break;
+      case 2: zscreen_t_launch<2, TFR>(a, st); break;
+      case 3: zscreen_t_launch<3, TFR>(a, st); break;
+      default: zscreen_t_launch<4, TFR>(a, st); break;
+    }
+  }
+
+  void launch_zscreen(const LdaArgs& a, cudaStream_t st) {
+    BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+    if (transposed_) {
+      if (tfr_) zscreen_t_rounds<true>(a, st);
+      else zscreen_t_rounds<false>(a, st);
+      zfallback_kernel<<<148 * 2, 256, 0, st>>>(a, out.iter, out.err);
+      return;
+    }
+    const int key = G32_ * 100 + CW32_ * 10 + (tfr_ ? 1 : 0);
+    switch (key) {
+      case 441: zscreen_rounds<4, 4, true>(a, st); break;   // (G*CW < 32: experiments only)
+      case 481: zscreen_rounds<4, 8, true>(a, st); break;
+      case 480: zscreen_rounds<4, 8, false>(a, st); break;
+      case 841: zscreen_rounds<8, 4, true>(a, st); break;
+      case 840: zscreen_rounds<8, 4, false>(a, st); break;
+      case 1641: zscreen_rounds<16, 4, true>(a, st); break;
+      case 1640: zscreen_rounds<16, 4, false>(a, st); break;
+      case 3241: zscreen_rounds<32, 4, true>(a, st); break;
+      case 3240: zscreen_rounds<32, 4, false>(a, st); break;
+      default: zscreen_rounds<32, 8, false>(a, st); break;
+    }
+    zfallback_kernel<<<148 * 2, 256, 0, st>>>(a, out.iter, out.err);
+  }
+
   void launch_zstep(const LdaArgs& a, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
     const std::size_t sm = zstep_smem();
@@ -1375,7 +1836,7 @@ class Lda final : public Model {
       constexpr bool EE = decltype(e)::value;
       if constexpr (!EE) {
         if (screen_) {
-          zstep_kernel<GG, RR, false, false, (RR + 1) / 2><<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));
+          launch_zscreen(a, st);
           return;
         }
       }
@@ -1401,6 +1862,9 @@ class Lda final : public Model {
     a.phiT = phiT_.p;
     a.phiT32 = screen_ ? phiT32_.p : nullptr;
     a.Kp32 = Kp32_;
+    a.G32 = G32_;
+    a.R32 = RS_;
+    a.CW32 = CW32_;
     a.logphiT = exact_ ? logphiT_.p : nullptr;
     a.theta = theta_.p;
     a.nkw = nkw_.p;
@@ -1429,6 +1893,10 @@ class Lda final : public Model {
     a.var_z = var_z_;
     a.rows_per_block = rows_per_block_;
     a.nb_phi = nb_phi_;
+    a.docs_per_block = docs_per_block_;
+    a.nb_doc = nb_doc_;
+    a.fq = fq_.p;
+    a.fq_len = fq_len_.p;
     return a;
   }
 
@@ -1437,7 +1905,8 @@ class Lda final : public Model {
   std::int64_t M_ = 0, N_ = 0, d0_ = 0, d1_ = 0, Ml_ = 0, Nl_ = 0, tok0_ = 0;
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
-  int Kp32_ = 0;
+  int Kp32_ = 0, RS_ = 1, G32_ = 8, CW32_ = 4;
+  bool tfr_ = true, transposed_ = false;
   DevBuf<float> phiT32_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
@@ -1446,7 +1915,8 @@ class Lda final : public Model {
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
   int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
   std::vector<std::int64_t> units_host_;
-  std::int64_t n_units_ = 0;
+  std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0;
+  DevBuf<int> fq_, fq_len_;
   bool data_on_device_ = false;
   DevBuf<std::int64_t> stage64_;  // int64 <-> int32 staging for z / w
   DevBuf<double> stage_phi_;      // K x V staging for the phi transpose

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbnmc_gpu.so")
+LIB_PATH = os.environ.get("BNMC_GPU_LIB") or os.path.join(HERE, "libbnmc_gpu.so")
 ABI_VERSION = 1
 
 LDA, GMM, MH_LINREG, MH_LOGREG = 1, 2, 3, 4
