@@ -84,6 +84,12 @@ struct LdaArgs {
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
   int var_phi, var_theta, var_z;
   int rows_per_block, nb_phi;
+  double* gpart;     // [nvb][K] phi block v2 partials: sum g, sum log g
+  double* lpart;
+  std::int64_t nvb;
+  double* spart;     // [kColStripes][K][2]
+  int* ticket;       // [ceil(K/32)] last-block tickets of phi_colsum2
+  int* ticket2;      // last-block ticket of wterm_kernel<true>
   std::int64_t docs_per_block, nb_doc;
 };
 
@@ -147,6 +153,162 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
     a.colpart[static_cast<std::size_t>(b) * a.K + k] = sg;
     a.colpart2[(static_cast<std::size_t>(b) * a.K + k) * 2] = sl;
   }
+}
+
+// phi block, v2: thread (k, vb) draws the cells (v, k), v in [vb*L, vb*L + L), of one
+// topic column in order and keeps fixed-order partials of sum g and sum log g.
+// * Rejection sampling without warp-level waste: the Marsaglia-Tsang loop runs one
+//   attempt per iteration and a thread whose attempt is accepted moves straight on
+//   to its next cell, so a warp iterates ~(1 + reject rate) * L times instead of
+//   L * (max attempts over the warp) (ncu r01 v6: the per-cell loop executed
+//   ~1290 thread instructions per cell, ~2.5x the straight-line count).
+// * Per-count constants d = a - 1/3, c = 1/sqrt(9d), 1/shape for counts < 64 come
+//   from a shared table computed with the reference's expressions (dist.cpp:136-155;
+//   bit-identical), saving a sqrt and two divisions per cell.
+// * sum log g as log of a renormalised running product (frexp): one log per thread
+//   instead of one per cell.
+// The stream of every cell is keyed(seed, 4, var_phi, iter).derive(k, v) and is
+// consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
+// uniform]), so the draws are the reference's.
+constexpr int kGammaTab = 64;
+constexpr int kPhiRows = 8;  // L: cells per thread
+
+__global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  __shared__ double tab_d[kGammaTab], tab_c[kGammaTab], tab_inv[kGammaTab];
+  __shared__ int cnt_s[kPhiRows][256];  // the thread's counts, loaded up front
+  const std::int64_t iter = *iter_p;
+  for (int i = threadIdx.x; i < kGammaTab; i += blockDim.x) {
+    const double shape = a.beta + static_cast<double>(i);
+    const bool boost = shape < 1.0;
+    const double aa = boost ? shape + 1.0 : shape;
+    const double d = aa - 1.0 / 3.0;
+    tab_d[i] = d;
+    tab_c[i] = 1.0 / sqrt(9.0 * d);
+    tab_inv[i] = boost ? 1.0 / shape : 0.0;
+  }
+  __syncthreads();
+  const std::int64_t idx = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int k = static_cast<int>(idx % a.K);
+  const std::int64_t vb = idx / a.K;
+  if (vb >= a.nvb) return;
+  const int v0 = static_cast<int>(vb * kPhiRows), v1 = min(a.V, v0 + kPhiRows);
+#pragma unroll
+  for (int j = 0; j < kPhiRows; ++j) {
+    if (v0 + j < v1) {
+      const std::size_t i = static_cast<std::size_t>(v0 + j) * a.Kp + k;
+      cnt_s[j][threadIdx.x] = a.nkw[i];
+      a.nkw[i] = 0;  // consumed: the z-step accumulates the next sweep's counts here
+    }
+  }
+  const int col32 = a.phiT32 ? phys32(k, a.R32, a.G32, a.CW32) : 0;
+  const std::uint64_t kkey = fold(keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
+                                        static_cast<std::uint64_t>(iter)),
+                                  static_cast<std::uint64_t>(k));
+  double sg = 0.0, mant = 1.0;
+  int ex = 0;
+  bool zero = false;
+  int v = v0;
+  bool fresh = true;
+  Stream r(0);
+  double d = 1.0, c = 1.0, inv = 0.0;
+  while (v < v1) {
+    if (fresh) {
+      const int n = cnt_s[v - v0][threadIdx.x];
+      r = Stream(fold(kkey, static_cast<std::uint64_t>(v)));
+      if (n < kGammaTab) {
+        d = tab_d[n];
+        c = tab_c[n];
+        inv = tab_inv[n];
+      } else {
+        const double shape = a.beta + static_cast<double>(n);  // >= 64: no boost
+        d = shape - 1.0 / 3.0;
+        c = 1.0 / sqrt(9.0 * d);
+        inv = 0.0;
+      }
+      fresh = false;
+    }
+    const double x = r.next_gaussian();
+    double vv = 1.0 + c * x;
+    if (vv > 0.0) {
+      vv = vv * vv * vv;
+      const double u = r.next_unit();
+      bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
+      if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
+      if (acc) {
+        double g = d * vv;
+        if (inv != 0.0) g = g * pow(r.next_unit(), inv);
+        const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
+        a.phiT[i] = g;
+        if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + col32] = static_cast<float>(g);
+        sg += g;
+        if (g > 0.0) {
+          int e1, e2;
+          mant = frexp(mant * frexp(g, &e1), &e2);
+          ex += e1 + e2;
+        } else {
+          zero = true;
+        }
+        ++v;
+        fresh = true;
+      }
+    }
+  }
+  a.gpart[vb * a.K + k] = sg;
+  a.lpart[vb * a.K + k] = zero ? -INFINITY : log(mant) + static_cast<double>(ex) * 0.69314718055994530942;
+}
+
+// Per topic: S[k] = sum over vb of gpart and the phi factor
+// (beta-1) (sum log g - V log S) - sum lgamma(beta) + lgamma(sum beta)
+// (dist.cpp:115-130).  Grid (ceil(K/32), kColStripes): block (kb, s) sums stripe s of
+// the row blocks for 32 topics (threads 32 x 8, fixed-order smem reduction) into
+// spart[s][k]; the last stripe block of kb to finish (atomic ticket) adds the
+// stripes in stripe order.  The ticket decides who adds, never the order, so the
+// result is deterministic.
+constexpr int kColStripes = 16;
+
+__global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
+  __shared__ double sg_s[8][33], sl_s[8][33];
+  __shared__ bool last;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + tx;
+  const std::int64_t chunk = (a.nvb + kColStripes - 1) / kColStripes;
+  const std::int64_t b0 = blockIdx.y * chunk, b1 = min(a.nvb, b0 + chunk);
+  double sg = 0.0, sl = 0.0;
+  if (k < a.K)
+    for (std::int64_t b = b0 + ty; b < b1; b += 8) {
+      sg += a.gpart[b * a.K + k];
+      sl += a.lpart[b * a.K + k];
+    }
+  sg_s[ty][tx] = sg;
+  sl_s[ty][tx] = sl;
+  __syncthreads();
+  if (ty == 0 && k < a.K) {
+    double g = 0.0, l = 0.0;
+    for (int j = 0; j < 8; ++j) {
+      g += sg_s[j][tx];
+      l += sl_s[j][tx];
+    }
+    a.spart[(static_cast<std::size_t>(blockIdx.y) * a.K + k) * 2] = g;
+    a.spart[(static_cast<std::size_t>(blockIdx.y) * a.K + k) * 2 + 1] = l;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(&a.ticket[blockIdx.x], 1);
+    last = t == kColStripes - 1;
+    if (last) a.ticket[blockIdx.x] = 0;  // every stripe has arrived: reset for the next sweep
+  }
+  __syncthreads();
+  if (!last || ty != 0 || k >= a.K) return;
+  __threadfence();
+  double g = 0.0, l = 0.0;
+  for (int s = 0; s < kColStripes; ++s) {
+    g += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2]);
+    l += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2 + 1]);
+  }
+  a.S[k] = g;
+  const double lp = (a.beta - 1.0) * (l - static_cast<double>(a.V) * log(g));
+  a.phi_term[k] = (!(g > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
 }
 
 // Per topic: S[k] = sum_b colpart (the gamma row sum) and the phi factor
@@ -1038,8 +1200,44 @@ __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::
 // w- and z-factors of the log-joint from the counts the z-step just produced:
 // sum_t log phi[z_t, w_t] = sum_{v,k} n[v,k] log phi[k,v]  (blocks < nb_phi) and
 // sum_t log theta[d_t, z_t] = sum_{d,k} n[d,k] log theta[d,k]  (the other blocks),
-// over this rank's tokens; fixed-order partials.
-__global__ void wterm_kernel(LdaArgs a) {
+// over this rank's tokens; fixed-order partials.  FINAL (single GPU): the last
+// block to finish (atomic ticket) also forms the log-joint from all partials in
+// fixed order, as reduce_kernel<false, true> does -- one launch less per sweep.
+template <bool FINAL>
+__device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o, int advance, double* scratch) {
+  if constexpr (FINAL) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t = atomicAdd(a.ticket2, 1);
+      last = t == static_cast<int>(gridDim.x) - 1;
+      if (last) *a.ticket2 = 0;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, f = 0.0;
+    for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += __ldcg(&a.tpart[m]);
+    for (std::int64_t u = threadIdx.x; u < a.nb_doc; u += blockDim.x) s1 += __ldcg(&a.zpart[u]);
+    for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) s2 += __ldcg(&a.wpart[b]);
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) f += __ldcg(&a.phi_term[k]);
+    s0 = block_sum(s0, scratch);
+    s1 = block_sum(s1, scratch);
+    s2 = block_sum(s2, scratch);
+    f = block_sum(f, scratch);
+    if (threadIdx.x == 0) {
+      const double lj = ((f + s0) + s1) + s2;
+      const std::int64_t it = *o.iter;
+      o.lj[it & (kRing - 1)] = lj;
+      o.acc[it & (kRing - 1)] = 0;
+      if (advance) *o.iter = it + 1;
+    }
+  }
+}
+
+template <bool FINAL>
+__global__ void wterm_kernel(LdaArgs a, Outputs o, int advance) {
   __shared__ double scratch[32];
   const int b = blockIdx.x;
   if (b >= a.nb_phi) {
@@ -1056,6 +1254,7 @@ __global__ void wterm_kernel(LdaArgs a) {
     }
     acc = block_sum(acc, scratch);
     if (threadIdx.x == 0) a.zpart[b - a.nb_phi] = acc;
+    loglik_finish<FINAL>(a, o, advance, scratch);
     return;
   }
   const int v0 = b * a.rows_per_block;
@@ -1073,6 +1272,7 @@ __global__ void wterm_kernel(LdaArgs a) {
   }
   acc = block_sum(acc, scratch);
   if (threadIdx.x == 0) a.wpart[b] = acc;
+  loglik_finish<FINAL>(a, o, advance, scratch);
 }
 
 // Log-joint pieces of the current state without sampling (Engine::eval_log_joint).
@@ -1408,6 +1608,12 @@ class Lda final : public Model {
     fq_len_.alloc(1);
     wpart_.alloc(nb_phi_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
+    nvb_ = (V_ + kPhiRows - 1) / kPhiRows;
+    spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
+    ticket_.alloc((K_ + 31) / 32 + 1);
+    ticket_.zero(nullptr);
+    gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
+    lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
     phi_term_.alloc(K_);
@@ -1447,6 +1653,8 @@ class Lda final : public Model {
     // or registers (BNMC_ZSTEP_THETA=regs: 128 registers; measured 20 % slower on NIPS).
     const char* tr = std::getenv("BNMC_ZSTEP_THETA");
     theta_regs_ = tr && std::string(tr) == "regs";
+    const char* pv = std::getenv("BNMC_PHI_V1");
+    phi_v1_ = pv && std::string(pv) == "1";
     configure_kernels();
     BNMC_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
@@ -1535,9 +1743,15 @@ class Lda final : public Model {
         BNMC_NCCL(ncclAllReduce(nkw_.p, nkw_.p, nkw_.n, ncclInt32, ncclSum, comm_.comm, st));
         mark(st, "allreduce_counts");
       }
-      phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
-      mark(st, "phi_gamma");
-      phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
+      if (phi_v1_) {
+        phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
+        mark(st, "phi_gamma");
+        phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
+      } else {
+        phi_gamma2_kernel<<<blocks_for(nvb_ * K_, 256), 256, 0, st>>>(a, out.iter);
+        mark(st, "phi_gamma");
+        phi_colsum2_kernel<<<dim3((K_ + 31) / 32, kColStripes), 256, 0, st>>>(a);
+      }
       mark(st, "phi_colsum");
       if (exact_) {
         // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
@@ -1560,16 +1774,18 @@ class Lda final : public Model {
       launch_zstep(a, st);
       mark(st, "zstep");
     }
-    wterm_kernel<<<static_cast<unsigned>(nb_phi_ + nb_doc_), 256, 0, st>>>(a);
-    mark(st, "wterm");
+    const unsigned nbw = static_cast<unsigned>(nb_phi_ + nb_doc_);
     if (comm_.world > 1) {
+      wterm_kernel<false><<<nbw, 256, 0, st>>>(a, out, 0);
+      mark(st, "wterm");
       reduce_kernel<false><<<1, 1024, 0, st>>>(a);
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
       finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
+      mark(st, "reduce_finalize");
     } else {
-      reduce_kernel<false, true><<<1, 1024, 0, st>>>(a, out, 1);
+      wterm_kernel<true><<<nbw, 256, 0, st>>>(a, out, 1);
+      mark(st, "wterm_finalize");
     }
-    mark(st, "reduce_finalize");
     BNMC_CUDA(cudaGetLastError());
   }
 
@@ -1892,6 +2108,12 @@ class Lda final : public Model {
     a.var_theta = var_theta_;
     a.var_z = var_z_;
     a.rows_per_block = rows_per_block_;
+    a.gpart = gpart_.p;
+    a.lpart = lpart_.p;
+    a.nvb = nvb_;
+    a.spart = spart_.p;
+    a.ticket = ticket_.p;
+    a.ticket2 = ticket_.p + (K_ + 31) / 32;
     a.nb_phi = nb_phi_;
     a.docs_per_block = docs_per_block_;
     a.nb_doc = nb_doc_;
@@ -1906,7 +2128,7 @@ class Lda final : public Model {
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
   int Kp32_ = 0, RS_ = 1, G32_ = 8, CW32_ = 4;
-  bool tfr_ = true, transposed_ = false;
+  bool tfr_ = true, transposed_ = false, phi_v1_ = false;
   DevBuf<float> phiT32_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
@@ -1923,6 +2145,9 @@ class Lda final : public Model {
   DevBuf<int> w_, z_, nkw_, nmk_;
   DevBuf<std::int64_t> units_;
   DevBuf<std::int64_t> off_;
+  std::int64_t nvb_ = 1;
+  DevBuf<double> gpart_, lpart_, spart_;
+  DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
       zpart_, wpart_;
 };
