@@ -73,7 +73,11 @@ struct LdaArgs {
   double* phi_term;  // [K]
   double* tpart;     // [Ml] theta-factor pieces
   double* zpart;     // [nb_doc] z-factor pieces (sum_k n[d,k] log theta[d,k])
-  int* fq;           // screen fallback queue: local token indices [Nl]
+  double* logg;      // [V][Kp] log of this sweep's gamma draws (phi block v2)
+  double* logS;      // [K] log of the gamma row sums
+  int logg_valid;    // logg/logS belong to the current phi (set inside a v2 sweep)
+  float screen_margin;  // kScreenMargin (BNMC_SCREEN_MARGIN overrides: tests force the fallback)
+  int2* fq;          // screen fallback queue: (local token, local document) [Nl]
   int* fq_len;
   double* wpart;     // [nb_phi] w-factor pieces
   double* doc_part;  // [Ml][3] (eval path)
@@ -165,8 +169,8 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
 // * Per-count constants d = a - 1/3, c = 1/sqrt(9d), 1/shape for counts < 64 come
 //   from a shared table computed with the reference's expressions (dist.cpp:136-155;
 //   bit-identical), saving a sqrt and two divisions per cell.
-// * sum log g as log of a renormalised running product (frexp): one log per thread
-//   instead of one per cell.
+// * log g is stored per cell (logg): the w-factor of the log-joint then needs no
+//   transcendental after the z-step.
 // The stream of every cell is keyed(seed, 4, var_phi, iter).derive(k, v) and is
 // consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
 // uniform]), so the draws are the reference's.
@@ -204,9 +208,7 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
   const std::uint64_t kkey = fold(keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
                                         static_cast<std::uint64_t>(iter)),
                                   static_cast<std::uint64_t>(k));
-  double sg = 0.0, mant = 1.0;
-  int ex = 0;
-  bool zero = false;
+  double sg = 0.0, sl = 0.0;
   int v = v0;
   bool fresh = true;
   Stream r(0);
@@ -241,20 +243,17 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
         a.phiT[i] = g;
         if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + col32] = static_cast<float>(g);
         sg += g;
-        if (g > 0.0) {
-          int e1, e2;
-          mant = frexp(mant * frexp(g, &e1), &e2);
-          ex += e1 + e2;
-        } else {
-          zero = true;
-        }
+        // log g: the phi prior term here, the w-factor after the z-step (wterm_kernel)
+        const double lg = g > 0.0 ? log(g) : -INFINITY;
+        a.logg[i] = lg;
+        sl += lg;
         ++v;
         fresh = true;
       }
     }
   }
   a.gpart[vb * a.K + k] = sg;
-  a.lpart[vb * a.K + k] = zero ? -INFINITY : log(mant) + static_cast<double>(ex) * 0.69314718055994530942;
+  a.lpart[vb * a.K + k] = sl;
 }
 
 // Per topic: S[k] = sum over vb of gpart and the phi factor
@@ -307,7 +306,9 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
     l += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2 + 1]);
   }
   a.S[k] = g;
-  const double lp = (a.beta - 1.0) * (l - static_cast<double>(a.V) * log(g));
+  const double lS = log(g);
+  a.logS[k] = lS;
+  const double lp = (a.beta - 1.0) * (l - static_cast<double>(a.V) * lS);
   a.phi_term[k] = (!(g > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
 }
 
@@ -423,6 +424,114 @@ __global__ void theta_kernel(LdaArgs a, const std::int64_t* iter_p) {
     if (threadIdx.x == 0)
       a.tpart[m] = fabs(sx - 1.0) > 1e-9 ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
     __syncthreads();
+  }
+}
+
+// theta block, v2: the phi_gamma2 scheme on document rows.  A block holds `dpb`
+// documents; each document row is split into runs of TL consecutive topics, one
+// run per thread (persistent rejection loop, counts prefetched to shared memory,
+// shared per-count constants).  Per document: S = sum g (fixed order: thread runs
+// in order), theta = g / S, and the Dirichlet log-pdf via
+// sum log theta = sum log g - K log S with sum log g from renormalised products.
+// Streams keyed(seed, 4, var_theta, iter).derive(d, k) as the reference (batch.cpp:38-41).
+constexpr int kThetaRun = 4;
+
+__global__ void __launch_bounds__(256) theta2_kernel(LdaArgs a, const std::int64_t* iter_p, int tpd, int dpb) {
+  __shared__ double tab_d[kGammaTab], tab_c[kGammaTab], tab_inv[kGammaTab];
+  __shared__ int cnt_s[kThetaRun][256];
+  __shared__ double g_s[kThetaRun][256];
+  __shared__ double ps[256], pl[256], dS[256];
+  const std::int64_t iter = *iter_p;
+  for (int i = threadIdx.x; i < kGammaTab; i += blockDim.x) {
+    const double shape = a.alpha + static_cast<double>(i);
+    const bool boost = shape < 1.0;
+    const double aa = boost ? shape + 1.0 : shape;
+    const double d = aa - 1.0 / 3.0;
+    tab_d[i] = d;
+    tab_c[i] = 1.0 / sqrt(9.0 * d);
+    tab_inv[i] = boost ? 1.0 / shape : 0.0;
+  }
+  const std::uint64_t tkey = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
+                                   static_cast<std::uint64_t>(iter));
+  const int j = threadIdx.x / tpd, t = threadIdx.x - (threadIdx.x / tpd) * tpd;
+  const std::int64_t m = static_cast<std::int64_t>(blockIdx.x) * dpb + j;
+  const bool active = j < dpb && m < a.Ml;
+  const int k0 = t * kThetaRun, k1 = active ? min(a.K, k0 + kThetaRun) : k0;
+#pragma unroll
+  for (int i = 0; i < kThetaRun; ++i) {
+    if (k0 + i < k1) {
+      int* c = a.nmk + m * a.K + k0 + i;
+      cnt_s[i][threadIdx.x] = *c;
+      *c = 0;  // consumed: the z-step accumulates the next sweep's counts here
+    }
+  }
+  __syncthreads();
+  const std::uint64_t mkey = fold(tkey, static_cast<std::uint64_t>(a.doc_base + m));
+  double sg = 0.0, mant = 1.0;
+  int ex = 0;
+  bool zero = false;
+  int k = k0;
+  bool fresh = true;
+  Stream r(0);
+  double d = 1.0, c = 1.0, inv = 0.0;
+  while (k < k1) {
+    if (fresh) {
+      const int n = cnt_s[k - k0][threadIdx.x];
+      r = Stream(fold(mkey, static_cast<std::uint64_t>(k)));
+      if (n < kGammaTab) {
+        d = tab_d[n];
+        c = tab_c[n];
+        inv = tab_inv[n];
+      } else {
+        const double shape = a.alpha + static_cast<double>(n);
+        d = shape - 1.0 / 3.0;
+        c = 1.0 / sqrt(9.0 * d);
+        inv = 0.0;
+      }
+      fresh = false;
+    }
+    const double x = r.next_gaussian();
+    double vv = 1.0 + c * x;
+    if (vv > 0.0) {
+      vv = vv * vv * vv;
+      const double u = r.next_unit();
+      bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
+      if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
+      if (acc) {
+        double g = d * vv;
+        if (inv != 0.0) g = g * pow(r.next_unit(), inv);
+        g_s[k - k0][threadIdx.x] = g;
+        sg += g;
+        if (g > 0.0) {
+          int e1, e2;
+          mant = frexp(mant * frexp(g, &e1), &e2);
+          ex += e1 + e2;
+        } else {
+          zero = true;
+        }
+        ++k;
+        fresh = true;
+      }
+    }
+  }
+  ps[threadIdx.x] = sg;
+  pl[threadIdx.x] = zero ? -INFINITY : log(mant) + static_cast<double>(ex) * 0.69314718055994530942;
+  __syncthreads();
+  if (active && t == 0) {  // document row sums, runs in topic order
+    double S = 0.0, L = 0.0;
+    for (int q = 0; q < tpd; ++q) {
+      S += ps[threadIdx.x + q];
+      L += pl[threadIdx.x + q];
+    }
+    dS[j] = S;
+    // sum log theta = sum log g - K log S;  sum theta = 1 by construction
+    const double lp = (a.alpha - 1.0) * (L - static_cast<double>(a.K) * log(S));
+    a.tpart[m] = (!(S > 0.0) || !isfinite(S)) ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
+  }
+  __syncthreads();
+  if (active) {
+    const double S = dS[j];
+    for (int kk = k0; kk < k1; ++kk) a.theta[m * a.K + kk] = g_s[kk - k0][threadIdx.x] / S;
   }
 }
 
@@ -831,7 +940,7 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
         if (gl == 0) start = 0.0f;
         const float total = __shfl_sync(gmask, inc, G - 1, G);
         const float uf = u01 * total;
-        const float mg = kScreenMargin * total;
+        const float mg = a.screen_margin * total;
         int k = -1;
         if (start <= uf && uf < inc && total > 0x1p-90f && total < 0x1p100f) {
           // owner lane: the crossing round (registers), then the crossing candidate
@@ -875,7 +984,7 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
           } else if (!decided && gl == 0) {
             // ambiguous for the screen: queued for the fp64 draw (zfallback_kernel)
             const int slot = atomicAdd(a.fq_len, 1);
-            a.fq[slot] = static_cast<int>(t);
+            a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
           }
         }
       }
@@ -986,7 +1095,7 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
         }
         const float total = run;
         const float uf = u01 * total;
-        const float mg = kScreenMargin * total;
+        const float mg = a.screen_margin * total;
         int k = -1;
         if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
           int cs = C - 1;
@@ -1025,7 +1134,7 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
           atomicAdd(&cnt[k], 1);
         } else {
           const int slot = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
-          a.fq[slot] = static_cast<int>(t);
+          a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
         }
       }
       __syncwarp();
@@ -1047,14 +1156,8 @@ __global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::in
   const int c = (a.K + 31) / 32;
   const int k0 = min(a.K, lane * c), k1 = min(a.K, k0 + c);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
-    const std::int64_t t = a.fq[i];
-    // document of t: the last m with off[m] <= t
-    std::int64_t lo = 0, hi = a.Ml - 1;
-    while (lo < hi) {
-      const std::int64_t mid = (lo + hi + 1) >> 1;
-      if (a.off[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    const std::int64_t m = lo;
+    const int2 q = a.fq[i];
+    const std::int64_t t = q.x, m = q.y;
     const int wv = a.w[t];
     const double* thg = a.theta + m * a.K;
     const double* row = a.phiT + static_cast<std::size_t>(wv) * a.Kp;
@@ -1266,8 +1369,12 @@ __global__ void wterm_kernel(LdaArgs a, Outputs o, int advance) {
     const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
     const int n = a.nkw[i];
     if (n) {
-      const double p = a.phiT[i] / a.S[k];  // phi = g / S (S = 1 once normalised)
-      acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
+      if (a.logg_valid) {
+        acc += static_cast<double>(n) * (a.logg[i] - a.logS[k]);  // log phi = log g - log S
+      } else {
+        const double p = a.phiT[i] / a.S[k];  // phi = g / S (S = 1 once normalised)
+        acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
+      }
     }
   }
   acc = block_sum(acc, scratch);
@@ -1613,6 +1720,8 @@ class Lda final : public Model {
     ticket_.alloc((K_ + 31) / 32 + 1);
     ticket_.zero(nullptr);
     gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
+    logg_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    logS_.alloc(K_);
     lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
@@ -1655,6 +1764,9 @@ class Lda final : public Model {
     theta_regs_ = tr && std::string(tr) == "regs";
     const char* pv = std::getenv("BNMC_PHI_V1");
     phi_v1_ = pv && std::string(pv) == "1";
+    if (const char* e = std::getenv("BNMC_SCREEN_MARGIN")) screen_margin_ = static_cast<float>(std::atof(e));
+    const char* tv = std::getenv("BNMC_THETA_V1");
+    theta_v1_ = tv && std::string(tv) == "1";
     configure_kernels();
     BNMC_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
@@ -1728,6 +1840,7 @@ class Lda final : public Model {
 
   void enqueue_sweep(cudaStream_t st) override {
     LdaArgs a = args();
+    a.logg_valid = (!observe_phi_ && !phi_v1_) ? 1 : 0;  // this sweep's phi block writes logg/logS
     const bool timed = marks != nullptr;  // phase timing: everything on one stream
     mark(st, "begin");
     // The theta block depends only on the doc-topic counts: it runs on a side stream
@@ -1735,7 +1848,7 @@ class Lda final : public Model {
     if (Ml_ > 0 && !timed) {
       BNMC_CUDA(cudaEventRecord(ev_fork_, st));
       BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, side_>>>(a, out.iter);
+      launch_theta(a, side_);
       BNMC_CUDA(cudaEventRecord(ev_join_, side_));
     }
     if (!observe_phi_) {
@@ -1766,7 +1879,7 @@ class Lda final : public Model {
     }
     if (Ml_ > 0) {
       if (timed) {
-        theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
+        launch_theta(a, st);
         mark(st, "theta");
       } else {
         BNMC_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
@@ -1886,6 +1999,16 @@ class Lda final : public Model {
     if (screen_) phi_f32_kernel<<<148 * 8, 256, 0, st>>>(a);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  void launch_theta(const LdaArgs& a, cudaStream_t st) {
+    if (theta_v1_ || K_ > 256 * kThetaRun) {
+      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
+      return;
+    }
+    const int tpd = (K_ + kThetaRun - 1) / kThetaRun;
+    const int dpb = std::max(1, 256 / tpd);
+    theta2_kernel<<<static_cast<unsigned>((Ml_ + dpb - 1) / dpb), 256, 0, st>>>(a, out.iter, tpd, dpb);
   }
 
   unsigned grid_docs() const { return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(Ml_, 1 << 20))); }
@@ -2023,7 +2146,7 @@ class Lda final : public Model {
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
-      zfallback_kernel<<<148 * 2, 256, 0, st>>>(a, out.iter, out.err);
+      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
       return;
     }
     const int key = G32_ * 100 + CW32_ * 10 + (tfr_ ? 1 : 0);
@@ -2039,7 +2162,7 @@ class Lda final : public Model {
       case 3240: zscreen_rounds<32, 4, false>(a, st); break;
       default: zscreen_rounds<32, 8, false>(a, st); break;
     }
-    zfallback_kernel<<<148 * 2, 256, 0, st>>>(a, out.iter, out.err);
+    zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
   }
 
   void launch_zstep(const LdaArgs& a, cudaStream_t st) {
@@ -2111,12 +2234,16 @@ class Lda final : public Model {
     a.gpart = gpart_.p;
     a.lpart = lpart_.p;
     a.nvb = nvb_;
+    a.logg = logg_.p;
+    a.logS = logS_.p;
+    a.logg_valid = 0;
     a.spart = spart_.p;
     a.ticket = ticket_.p;
     a.ticket2 = ticket_.p + (K_ + 31) / 32;
     a.nb_phi = nb_phi_;
     a.docs_per_block = docs_per_block_;
     a.nb_doc = nb_doc_;
+    a.screen_margin = screen_margin_;
     a.fq = fq_.p;
     a.fq_len = fq_len_.p;
     return a;
@@ -2128,7 +2255,7 @@ class Lda final : public Model {
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
   int Kp32_ = 0, RS_ = 1, G32_ = 8, CW32_ = 4;
-  bool tfr_ = true, transposed_ = false, phi_v1_ = false;
+  bool tfr_ = true, transposed_ = false, phi_v1_ = false, theta_v1_ = false;
   DevBuf<float> phiT32_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
@@ -2138,7 +2265,9 @@ class Lda final : public Model {
   int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
   std::vector<std::int64_t> units_host_;
   std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0;
-  DevBuf<int> fq_, fq_len_;
+  float screen_margin_ = kScreenMargin;
+  DevBuf<int2> fq_;
+  DevBuf<int> fq_len_;
   bool data_on_device_ = false;
   DevBuf<std::int64_t> stage64_;  // int64 <-> int32 staging for z / w
   DevBuf<double> stage_phi_;      // K x V staging for the phi transpose
@@ -2146,7 +2275,7 @@ class Lda final : public Model {
   DevBuf<std::int64_t> units_;
   DevBuf<std::int64_t> off_;
   std::int64_t nvb_ = 1;
-  DevBuf<double> gpart_, lpart_, spart_;
+  DevBuf<double> gpart_, lpart_, spart_, logg_, logS_;
   DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
       zpart_, wpart_;

@@ -273,3 +273,61 @@ def test_lpp_vs_reference(g, reference):
                                             w.ctypes.data_as(ip), off.ctypes.data_as(ip), M, ctypes.byref(out)))
     got = g.log_predictive_probability(pc, tc, K, V, w, off)
     assert abs(got - out.value) <= 1e-10 * abs(out.value)
+
+
+# ----------------------------------------------------------------------------------------
+# z-step layouts: every screen / fallback instantiation against the restatement
+# ----------------------------------------------------------------------------------------
+def _ragged_corpus(restatement, K, V, M, seed):
+    rs = np.random.default_rng(seed)
+    lengths = rs.integers(0, 90, M)
+    lengths[0] = 0          # an empty document
+    lengths[1] = 700        # one document spanning several 512-token work units
+    off = np.zeros(M + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lengths)
+    # Zipf-like word frequencies (some words frequent: count-table contention)
+    pw = 1.0 / np.arange(1, V + 1) ** 1.1
+    w = rs.choice(V, size=int(off[-1]), p=pw / pw.sum()).astype(np.int64)
+    phi, theta, z = restatement.lda_prior_init(K, V, off, w, seed)
+    return off, w, phi, theta, z
+
+
+LAYOUTS = [
+    # (K, env): transposed screen (K <= 128, every round count), grouped screens, big K
+    (1, {}), (5, {}), (32, {}), (33, {}), (64, {}), (100, {}), (128, {}),
+    (129, {}), (200, {}), (256, {}), (300, {}), (512, {}), (513, {}), (1000, {}),
+    (100, {"BNMC_ZSCREEN": "g4w8s"}), (100, {"BNMC_ZSCREEN": "g8w4r"}),
+    (100, {"BNMC_ZSCREEN": "g16w4s"}), (100, {"BNMC_ZSCREEN": "g32w4r"}),
+    (100, {"BNMC_ZSTEP_THETA": "smem"}),
+    # every token through the fp64 fallback queue
+    (100, {"BNMC_SCREEN_MARGIN": "1.0"}), (1000, {"BNMC_SCREEN_MARGIN": "1.0"}),
+    # screen off: the grouped fp64 kernel
+    (100, {"BNMC_ZSTEP_SCREEN": "0"}), (1000, {"BNMC_ZSTEP_SCREEN": "0"}),
+    # phi / theta block v1 kernels
+    (100, {"BNMC_PHI_V1": "1", "BNMC_THETA_V1": "1"}),
+]
+
+
+@pytest.mark.parametrize("K,env", LAYOUTS, ids=[f"K{k}-" + "-".join(f"{a}={b}" for a, b in e.items()) for k, e in LAYOUTS])
+def test_lda_layouts_vs_restatement(g, restatement, monkeypatch, K, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    V, M, seed = 400, 40, 11 + K
+    off, w, phi, theta, z = _ragged_corpus(restatement, K, V, M, seed)
+    hyper = {"K": K, "V": V, "M": M, "N": np.diff(off).tolist()}
+    e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["w"], s["z"], s["phi"], s["theta"] = w, z, phi, theta
+    for it in range(3):
+        lj = e.sweep(s, it)
+        lj2 = restatement.lda_sweep(K, V, off, w, z, phi, theta, seed, it)
+        mism = int((s["z"] != z).sum())
+        assert mism == 0, f"sweep {it}: {mism} z mismatches of {len(z)}"
+        assert rel(s["phi"], phi) < RTOL_PARAM
+        assert rel(s["theta"], theta) < RTOL_PARAM
+        assert abs(lj - lj2) <= RTOL_LJ * abs(lj2)
+    nkw, nmk = e.lda_counts()
+    want = np.zeros((K, V), dtype=np.int64)
+    np.add.at(want, (z, w), 1)
+    assert np.array_equal(nkw, want)
+    e.close()
