@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "dist.cuh"
@@ -1143,6 +1144,182 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
   }
 }
 
+// ---------------------------------------------------------------------------------
+// z block, TMA-staged screen (experimental, BNMC_ZSTAGE=1; slower, see choose_screen)
+// ---------------------------------------------------------------------------------
+// ncu r01 v15 (zscreen_t): every warp serialised ~5 L2 round trips per 32-token batch
+// (4 sub-batch row fetches + the rescan re-fetch, which missed L1) and register
+// double-buffering could not hold enough rows in flight.  Here the phi rows go
+// global -> shared by the bulk-copy engine (cp.async.bulk, completion on an
+// mbarrier), NS batches ahead per warp, with no register cost:
+//  * work = batches of <= 32 consecutive tokens of one document; warp g of the
+//    persistent grid owns a contiguous range of batches;
+//  * lane j issues the 16*KQ-byte bulk copy of token j's phiT32 row (natural topic
+//    order, fp32) into the warp's slot; lane 0 arms the slot's mbarrier with the
+//    batch's byte count;
+//  * compute is lane-per-token from shared memory: K products theta/S * g in
+//    16-byte granules, running prefix in registers, u * total, the crossing granule,
+//    the in-granule scan (all from shared memory: no re-fetch), the margin check,
+//    z and the count atomics -- no shuffles;
+//  * theta/S of the warp's current document sits in shared memory (fp32), reloaded
+//    when the batch's document changes.
+// Same screen / fp64-fallback contract as zscreen_kernel.
+struct ZBatch {
+  std::int64_t t0;
+  int m, n;
+};
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "ZW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra ZW_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int KQ>
+__global__ void __launch_bounds__(256) zstage_kernel(LdaArgs a, const std::int64_t* iter_p, const ZBatch* batches,
+                                                     std::int64_t nbatch, int ns, int stride16) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned row_bytes = 16u * KQ;
+  const std::size_t slot_bytes = static_cast<std::size_t>(32) * stride16 * 16;
+  // CTA area: S (fp64, K).  Warp area: bars[ns], w[ns][32], theta/S[4KQ], rows[ns].
+  double* Ssm = reinterpret_cast<double*>(smem_raw);
+  const std::size_t cta_bytes = (static_cast<std::size_t>(a.K) * 8 + 127) / 128 * 128;
+  const std::size_t warp_hdr = (static_cast<std::size_t>(ns) * (16 + 128) + 16 * KQ + 127) / 128 * 128;
+  unsigned char* wbase = smem_raw + cta_bytes + warp * (warp_hdr + ns * slot_bytes);
+  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(wbase);
+  int* wsm = reinterpret_cast<int*>(wbase + 16 * ns);
+  float* th = reinterpret_cast<float*>(wbase + 16 * ns + 128 * ns);
+  unsigned char* rows = wbase + warp_hdr;
+
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) Ssm[k] = a.S[k];
+  if (lane == 0)
+    for (int i = 0; i < ns; ++i) mbar_init(bar + i, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const std::int64_t iter = *iter_p;
+  const std::int64_t tw = static_cast<std::int64_t>(gridDim.x) * nw;
+  const std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * nw + warp;
+  const std::int64_t b_first = nbatch * g / tw, b_last = nbatch * (g + 1) / tw;
+  const std::int64_t count = b_last - b_first;
+
+  auto issue = [&](std::int64_t c, int slot) {
+    const ZBatch zb = batches[b_first + c];
+    const int wv = lane < zb.n ? __ldg(a.w + zb.t0 + lane) : 0;
+    wsm[slot * 32 + lane] = wv;
+    if (lane == 0) mbar_expect_tx(bar + slot, row_bytes * static_cast<unsigned>(zb.n));
+    __syncwarp();
+    if (lane < zb.n)
+      bulk_g2s(rows + slot * slot_bytes + static_cast<std::size_t>(lane) * stride16 * 16,
+               a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32, row_bytes, bar + slot);
+  };
+  for (std::int64_t c = 0; c < count && c < ns; ++c) issue(c, static_cast<int>(c));
+
+  int curm = -1;
+  for (std::int64_t c = 0; c < count; ++c) {
+    const int slot = static_cast<int>(c % ns);
+    const unsigned parity = static_cast<unsigned>((c / ns) & 1);
+    const ZBatch zb = batches[b_first + c];
+    if (zb.m != curm) {
+      __syncwarp();
+      const double* thg = a.theta + static_cast<std::int64_t>(zb.m) * a.K;
+      for (int k = lane; k < 4 * KQ; k += 32) th[k] = k < a.K ? static_cast<float>(thg[k] / Ssm[k]) : 0.0f;
+      curm = zb.m;
+      __syncwarp();
+    }
+    mbar_wait(bar + slot, parity);
+    if (lane < zb.n) {
+      const std::int64_t t = zb.t0 + lane;
+      const int wv = wsm[slot * 32 + lane];
+      const float* row = reinterpret_cast<const float*>(rows + slot * slot_bytes + static_cast<std::size_t>(lane) * stride16 * 16);
+      Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)), static_cast<std::uint64_t>(iter)));
+      const float u01 = static_cast<float>(rng.next_unit());
+      float P[KQ];
+      float run = 0.0f;
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(row + 4 * q);
+        const float4 x = *reinterpret_cast<const float4*>(th + 4 * q);
+        float sq = x.x * f.x;
+        sq = __fmaf_rn(x.y, f.y, sq);
+        sq = __fmaf_rn(x.z, f.z, sq);
+        sq = __fmaf_rn(x.w, f.w, sq);
+        run += sq;
+        P[q] = run;
+      }
+      const float total = run;
+      const float uf = u01 * total;
+      const float mg = a.screen_margin * total;
+      int k = -1;
+      if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
+        int cs = KQ - 1;
+        float lo = 0.0f;
+#pragma unroll
+        for (int q = KQ - 1; q >= 0; --q)
+          if (uf < P[q]) cs = q;
+#pragma unroll
+        for (int q = 0; q < KQ - 1; ++q)
+          if (q < cs) lo = P[q];
+        const float4 f = *reinterpret_cast<const float4*>(row + 4 * cs);
+        const float4 x = *reinterpret_cast<const float4*>(th + 4 * cs);
+        const float fv[4] = {f.x, f.y, f.z, f.w};
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+        float acc = lo, prev = lo;
+        int j = -1;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const float nx = __fmaf_rn(xv[jj], fv[jj], acc);
+          if (j < 0) {
+            if (uf < nx) {
+              j = jj;
+              prev = acc;
+            }
+            acc = nx;
+          }
+        }
+        const int kk = 4 * cs + j;
+        if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
+      }
+      if (k >= 0) {
+        a.z[t] = k;
+        atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
+        atomicAdd(&a.nmk[static_cast<std::int64_t>(zb.m) * a.K + k], 1);
+      } else {
+        const int slotq = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
+        a.fq[slotq] = make_int2(static_cast<int>(t), zb.m);
+      }
+    }
+    __syncwarp();
+    // the slot's generic reads are done: order them before the next bulk write into it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (c + ns < count) issue(c + ns, slot);
+  }
+}
+
 // fp64 product-form draw for the tokens the screen could not decide (~2K * 2^-16
 // of them): one warp per queued token.  Lane l owns the contiguous candidates
 // [l*c, (l+1)*c), c = ceil(K/32); warp scan of the lane sums, the owner rescans
@@ -1702,6 +1879,17 @@ class Lda final : public Model {
     screen_ = !exact_ && !(sc && std::string(sc) == "0");
     choose_screen();
     Kp32_ = CW32_ * G32_ * RS_;
+    if (stage_ && screen_) {
+      std::vector<ZBatch> hb;
+      for (std::int64_t m = 0; m < Ml_; ++m)
+        for (std::int64_t t = off_host_[m]; t < off_host_[m + 1]; t += 32)
+          hb.push_back(ZBatch{t, static_cast<int>(m), static_cast<int>(std::min<std::int64_t>(32, off_host_[m + 1] - t))});
+      nbatch_ = static_cast<std::int64_t>(hb.size());
+      batches_.alloc(std::max<std::size_t>(hb.size(), 1));
+      if (!hb.empty())
+        BNMC_CUDA(cudaMemcpy(batches_.p, hb.data(), sizeof(ZBatch) * hb.size(), cudaMemcpyHostToDevice));
+      plan_stage();
+    }
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
@@ -2062,6 +2250,23 @@ class Lda final : public Model {
   // shared memory doubled the L1 register-writeback traffic, the limiter); K > 512:
   // G = 32 x CW = 8, theta in shared memory.  BNMC_ZSCREEN=g<G>w<CW>[s|r] overrides.
   void choose_screen() {
+    // Off by default: measured slower on NIPS (160 us vs 107 us; r01 v19) -- 32 bulk
+    // copies of 400 B per batch, the bulk-copy issue rate bounds it.  BNMC_ZSTAGE=1.
+    stage_ = false;
+    if (const char* e = std::getenv("BNMC_ZSTAGE")) stage_ = std::string(e) == "1" && K_ <= 128;
+    if (stage_) {
+      kq_ = 0;
+      for (int q : kStageKQ)
+        if (q * 4 >= K_) {
+          kq_ = q;
+          break;
+        }
+      G32_ = 1;
+      CW32_ = 8;
+      RS_ = (kq_ + 1) / 2;  // Kp32 = 8 RS >= 4 KQ: the bulk copy never leaves the row
+      transposed_ = false;
+      return;
+    }
     transposed_ = K_ <= 128;
     G32_ = 32;
     CW32_ = 8;
@@ -2141,8 +2346,53 @@ class Lda final : public Model {
     }
   }
 
+  template <int KQ>
+  void zstage_launch(const LdaArgs& a, cudaStream_t st) {
+    if (!stage_attr_) {
+      BNMC_CUDA(cudaFuncSetAttribute(zstage_kernel<KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(stage_smem_)));
+      stage_attr_ = true;
+    }
+    zstage_kernel<KQ><<<stage_grid_, 32 * stage_warps_, stage_smem_, st>>>(
+        a, out.iter, batches_.p, nbatch_, stage_slots_, stage_stride16_);
+  }
+
+  template <int... Q>
+  void zstage_dispatch(const LdaArgs& a, cudaStream_t st, std::integer_sequence<int, Q...>) {
+    bool done = false;
+    ((!done && Q == kq_ ? (zstage_launch<Q>(a, st), done = true) : false), ...);
+  }
+
+  // Shared-memory plan of zstage_kernel: W warps x NS slots of 32 rows.
+  void plan_stage() {
+    stage_stride16_ = kq_ | 1;  // odd 16-byte row stride: conflict-free lane-per-row reads
+    const std::size_t slot = static_cast<std::size_t>(32) * stage_stride16_ * 16;
+    const std::size_t cta = (static_cast<std::size_t>(K_) * 8 + 127) / 128 * 128;
+    int dev = 0, smem_max = 0, sms = 148;
+    BNMC_CUDA(cudaGetDevice(&dev));
+    BNMC_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    stage_warps_ = 8;
+    if (const char* e = std::getenv("BNMC_ZSTAGE_WARPS")) stage_warps_ = std::min(8, std::max(1, std::atoi(e)));
+    auto hdr = [&](int ns) { return (static_cast<std::size_t>(ns) * (16 + 128) + 16 * kq_ + 127) / 128 * 128; };
+    auto need = [&](int w, int ns) { return cta + w * (hdr(ns) + ns * slot); };
+    stage_slots_ = 2;
+    while (stage_slots_ < 8 && need(stage_warps_, stage_slots_ + 1) <= static_cast<std::size_t>(smem_max))
+      ++stage_slots_;
+    if (const char* e = std::getenv("BNMC_ZSTAGE_SLOTS")) stage_slots_ = std::min(16, std::max(1, std::atoi(e)));
+    while (stage_warps_ > 1 && need(stage_warps_, stage_slots_) > static_cast<std::size_t>(smem_max)) --stage_warps_;
+    stage_smem_ = need(stage_warps_, stage_slots_);
+    require(stage_smem_ <= static_cast<std::size_t>(smem_max), BNMC_GPU_ERR_ARG, "z-step staging does not fit shared memory");
+    stage_grid_ = static_cast<unsigned>(sms);
+  }
+
   void launch_zscreen(const LdaArgs& a, cudaStream_t st) {
     BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+    if (stage_) {
+      zstage_dispatch(a, st, std::integer_sequence<int, 1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32>{});
+      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
+      return;
+    }
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
@@ -2256,6 +2506,14 @@ class Lda final : public Model {
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
   int Kp32_ = 0, RS_ = 1, G32_ = 8, CW32_ = 4;
   bool tfr_ = true, transposed_ = false, phi_v1_ = false, theta_v1_ = false;
+  // TMA-staged z-step (zstage_kernel)
+  static constexpr int kStageKQ[] = {1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32};
+  bool stage_ = false, stage_attr_ = false;
+  int kq_ = 0, stage_stride16_ = 1, stage_warps_ = 8, stage_slots_ = 2;
+  std::size_t stage_smem_ = 0;
+  unsigned stage_grid_ = 148;
+  DevBuf<ZBatch> batches_;
+  std::int64_t nbatch_ = 0;
   DevBuf<float> phiT32_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
