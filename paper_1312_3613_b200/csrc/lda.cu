@@ -73,14 +73,15 @@ struct LdaArgs {
   double* S;         // [K]
   double* phi_term;  // [K]
   double* tpart;     // [Ml] theta-factor pieces
-  double* zpart;     // [nb_doc] z-factor pieces (sum_k n[d,k] log theta[d,k])
+  double* zpart;     // [nbw] z-factor pieces (sum n[d,k] log theta[d,k]) per wterm block
   double* logg;      // [V][Kp] log of this sweep's gamma draws (phi block v2)
   double* logS;      // [K] log of the gamma row sums
   int logg_valid;    // logg/logS belong to the current phi (set inside a v2 sweep)
   float screen_margin;  // kScreenMargin (BNMC_SCREEN_MARGIN overrides: tests force the fallback)
   int2* fq;          // screen fallback queue: (local token, local document) [Nl]
   int* fq_len;
-  double* wpart;     // [nb_phi] w-factor pieces
+  double* wpart;     // [nbw] w-factor pieces per wterm block
+  int nbw;           // wterm_kernel blocks
   double* doc_part;  // [Ml][3] (eval path)
   double* red;       // [4]
   double alpha, beta;
@@ -1499,8 +1500,8 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
     __threadfence();
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, f = 0.0;
     for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += __ldcg(&a.tpart[m]);
-    for (std::int64_t u = threadIdx.x; u < a.nb_doc; u += blockDim.x) s1 += __ldcg(&a.zpart[u]);
-    for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) s2 += __ldcg(&a.wpart[b]);
+    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s1 += __ldcg(&a.zpart[b]);
+    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s2 += __ldcg(&a.wpart[b]);
     for (int k = threadIdx.x; k < a.K; k += blockDim.x) f += __ldcg(&a.phi_term[k]);
     s0 = block_sum(s0, scratch);
     s1 = block_sum(s1, scratch);
@@ -1517,45 +1518,65 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
 }
 
 template <bool FINAL>
-__global__ void wterm_kernel(LdaArgs a, Outputs o, int advance) {
+__global__ void __launch_bounds__(256) wterm_kernel(LdaArgs a, Outputs o, int advance) {
   __shared__ double scratch[32];
-  const int b = blockIdx.x;
-  if (b >= a.nb_phi) {
-    const std::int64_t d0 = static_cast<std::int64_t>(b - a.nb_phi) * a.docs_per_block;
-    const std::int64_t d1 = min(a.Ml, d0 + a.docs_per_block);
-    const std::int64_t c0 = d0 * a.K, c1 = d1 * a.K;
-    double acc = 0.0;
-    for (std::int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-      const int n = a.nmk[c];
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  const std::int64_t g0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // w-factor over the topic-word cells (static cell -> thread assignment: deterministic);
+  // 4 cells per thread iteration with their loads issued together
+  double accw = 0.0;
+  const std::int64_t ncw = static_cast<std::int64_t>(a.V) * a.K;
+  if (a.logg_valid) {
+    for (std::int64_t c0 = g0; c0 < ncw; c0 += 4 * stride) {
+      int n[4];
+      double lg[4];
+      int kk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const std::int64_t c = c0 + j * stride;
+        n[j] = 0;
+        lg[j] = 0.0;
+        kk[j] = 0;
+        if (c < ncw) {
+          const std::int64_t v = c / a.K;
+          kk[j] = static_cast<int>(c - v * a.K);
+          const std::size_t i = static_cast<std::size_t>(v) * a.Kp + kk[j];
+          n[j] = a.nkw[i];
+          lg[j] = a.logg[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n[j]) accw += static_cast<double>(n[j]) * (lg[j] - a.logS[kk[j]]);  // log phi = log g - log S
+    }
+  } else {
+    for (std::int64_t c = g0; c < ncw; c += stride) {
+      const std::int64_t v = c / a.K;
+      const int k = static_cast<int>(c - v * a.K);
+      const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
+      const int n = a.nkw[i];
       if (n) {
-        const double x = a.theta[c];
-        acc += static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY);
-      }
-    }
-    acc = block_sum(acc, scratch);
-    if (threadIdx.x == 0) a.zpart[b - a.nb_phi] = acc;
-    loglik_finish<FINAL>(a, o, advance, scratch);
-    return;
-  }
-  const int v0 = b * a.rows_per_block;
-  const int v1 = min(a.V, v0 + a.rows_per_block);
-  const int cells = (v1 - v0) * a.K;
-  double acc = 0.0;
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-    const int v = v0 + c / a.K, k = c % a.K;
-    const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
-    const int n = a.nkw[i];
-    if (n) {
-      if (a.logg_valid) {
-        acc += static_cast<double>(n) * (a.logg[i] - a.logS[k]);  // log phi = log g - log S
-      } else {
         const double p = a.phiT[i] / a.S[k];  // phi = g / S (S = 1 once normalised)
-        acc += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
+        accw += static_cast<double>(n) * (p > 0.0 ? log(p) : -INFINITY);
       }
     }
   }
-  acc = block_sum(acc, scratch);
-  if (threadIdx.x == 0) a.wpart[b] = acc;
+  // z-factor over the doc-topic cells
+  double accz = 0.0;
+  const std::int64_t ncz = a.Ml * a.K;
+  for (std::int64_t c = g0; c < ncz; c += stride) {
+    const int n = a.nmk[c];
+    if (n) {
+      const double x = a.theta[c];
+      accz += static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY);
+    }
+  }
+  accw = block_sum(accw, scratch);
+  accz = block_sum(accz, scratch);
+  if (threadIdx.x == 0) {
+    a.wpart[blockIdx.x] = accw;
+    a.zpart[blockIdx.x] = accz;
+  }
   loglik_finish<FINAL>(a, o, advance, scratch);
 }
 
@@ -1613,8 +1634,8 @@ __global__ void reduce_kernel(LdaArgs a, Outputs o = Outputs{}, int advance = 0)
     }
   } else {
     for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += a.tpart[m];
-    for (std::int64_t u = threadIdx.x; u < a.nb_doc; u += blockDim.x) s1 += a.zpart[u];
-    for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) s2 += a.wpart[b];
+    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s1 += a.zpart[b];
+    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s2 += a.wpart[b];
   }
   s0 = block_sum(s0, scratch);
   s1 = block_sum(s1, scratch);
@@ -1898,10 +1919,11 @@ class Lda final : public Model {
     tpart_.alloc(std::max<std::int64_t>(Ml_, 1));
     docs_per_block_ = std::max<std::int64_t>(1, 4096 / K_);
     nb_doc_ = (Ml_ + docs_per_block_ - 1) / docs_per_block_;
-    zpart_.alloc(std::max<std::int64_t>(nb_doc_, 1));
+    nbw_ = 148 * 4;
+    zpart_.alloc(nbw_);
     fq_.alloc(std::max<std::int64_t>(Nl_, 1));
     fq_len_.alloc(1);
-    wpart_.alloc(nb_phi_);
+    wpart_.alloc(nbw_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     nvb_ = (V_ + kPhiRows - 1) / kPhiRows;
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
@@ -2075,7 +2097,7 @@ class Lda final : public Model {
       launch_zstep(a, st);
       mark(st, "zstep");
     }
-    const unsigned nbw = static_cast<unsigned>(nb_phi_ + nb_doc_);
+    const unsigned nbw = static_cast<unsigned>(nbw_);
     if (comm_.world > 1) {
       wterm_kernel<false><<<nbw, 256, 0, st>>>(a, out, 0);
       mark(st, "wterm");
@@ -2493,6 +2515,7 @@ class Lda final : public Model {
     a.nb_phi = nb_phi_;
     a.docs_per_block = docs_per_block_;
     a.nb_doc = nb_doc_;
+    a.nbw = nbw_;
     a.screen_margin = screen_margin_;
     a.fq = fq_.p;
     a.fq_len = fq_len_.p;
@@ -2523,6 +2546,7 @@ class Lda final : public Model {
   int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
   std::vector<std::int64_t> units_host_;
   std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0;
+  int nbw_ = 1;
   float screen_margin_ = kScreenMargin;
   DevBuf<int2> fq_;
   DevBuf<int> fq_len_;

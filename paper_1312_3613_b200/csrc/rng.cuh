@@ -39,10 +39,17 @@ __host__ __device__ __forceinline__ std::uint64_t derive(std::uint64_t key, std:
 struct Stream {
   std::uint64_t key;
   std::uint64_t counter;
+  std::uint64_t pos;  // key + kGolden * counter (mod 2^64), advanced by addition
 
-  __device__ __forceinline__ explicit Stream(std::uint64_t k) : key(k), counter(0) {}
+  __device__ __forceinline__ explicit Stream(std::uint64_t k) : key(k), counter(0), pos(k) {}
 
-  __device__ __forceinline__ std::uint64_t next_u64() { return mix(key + kGolden * ++counter); }
+  // mix(key + kGolden * ++counter) (rng.hpp:40); the product is carried incrementally
+  // (one 64-bit add instead of a 64-bit multiply per draw; identical modulo 2^64).
+  __device__ __forceinline__ std::uint64_t next_u64() {
+    ++counter;
+    pos += kGolden;
+    return mix(pos);
+  }
 
   __device__ __forceinline__ double next_unit() {
     return (static_cast<double>(next_u64() >> 11) + 0.5) * 0x1p-53;
