@@ -52,6 +52,14 @@ __host__ __device__ __forceinline__ int phys32(int k, int R, int G, int CW) {
   return (r * G + gl) * CW + j;
 }
 
+// Programmatic dependent launch: kernels launched with launch_pdl may start while
+// their stream predecessor drains; they wait here before touching its results
+// (a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the stream successor's blocks be scheduled once every block of this grid has
+// passed this point (they still wait for this grid's completion in pdl_wait).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct LdaArgs {
   int K, Kp, V;
   std::int64_t Ml, Nl;
@@ -207,6 +215,7 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
     }
   }
   const int col32 = a.phiT32 ? phys32(k, a.R32, a.G32, a.CW32) : 0;
+  pdl_trigger();
   const std::uint64_t kkey = fold(keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
                                         static_cast<std::uint64_t>(iter)),
                                   static_cast<std::uint64_t>(k));
@@ -270,6 +279,9 @@ constexpr int kColStripes = 16;
 __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __shared__ double sg_s[8][33], sl_s[8][33];
   __shared__ bool last;
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.fq_len) *a.fq_len = 0;  // this sweep's fallback queue
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
   const std::int64_t chunk = (a.nvb + kColStripes - 1) / kColStripes;
@@ -1015,6 +1027,8 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
   const int warp = threadIdx.x >> 5;
   float* csum = thf + G * KLP + warp * 32 * CSP;     // [32][CSP] chunk sums of the batch
+  pdl_wait();
+  pdl_trigger();
   const std::int64_t iter = *iter_p;
   const int rl = min(R, max(0, (a.K - gl * KL + CW - 1) / CW));
 
@@ -1328,6 +1342,8 @@ __global__ void __launch_bounds__(256) zstage_kernel(LdaArgs a, const std::int64
 // dist.cpp:202-215).  Tokens whose product weights underflow take the sequential
 // log-space draw.
 __global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
+  pdl_wait();
+  pdl_trigger();
   const std::int64_t iter = *iter_p;
   const int lane = threadIdx.x & 31;
   const int n = *a.fq_len;
@@ -1520,6 +1536,7 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
 template <bool FINAL>
 __global__ void __launch_bounds__(256) wterm_kernel(LdaArgs a, Outputs o, int advance) {
   __shared__ double scratch[32];
+  pdl_wait();
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   const std::int64_t g0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   // w-factor over the topic-word cells (static cell -> thread assignment: deterministic);
@@ -1975,6 +1992,7 @@ class Lda final : public Model {
     const char* pv = std::getenv("BNMC_PHI_V1");
     phi_v1_ = pv && std::string(pv) == "1";
     if (const char* e = std::getenv("BNMC_SCREEN_MARGIN")) screen_margin_ = static_cast<float>(std::atof(e));
+    if (const char* e = std::getenv("BNMC_PDL")) pdl_ = std::string(e) != "0";
     const char* tv = std::getenv("BNMC_THETA_V1");
     theta_v1_ = tv && std::string(tv) == "1";
     configure_kernels();
@@ -2073,7 +2091,8 @@ class Lda final : public Model {
       } else {
         phi_gamma2_kernel<<<blocks_for(nvb_ * K_, 256), 256, 0, st>>>(a, out.iter);
         mark(st, "phi_gamma");
-        phi_colsum2_kernel<<<dim3((K_ + 31) / 32, kColStripes), 256, 0, st>>>(a);
+        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, kColStripes), dim3(256), 0, st, a);
+        fq_reset_ = true;
       }
       mark(st, "phi_colsum");
       if (exact_) {
@@ -2106,7 +2125,7 @@ class Lda final : public Model {
       finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
       mark(st, "reduce_finalize");
     } else {
-      wterm_kernel<true><<<nbw, 256, 0, st>>>(a, out, 1);
+      launch_pdl(wterm_kernel<true>, dim3(nbw), dim3(256), 0, st, a, out, 1);
       mark(st, "wterm_finalize");
     }
     BNMC_CUDA(cudaGetLastError());
@@ -2355,7 +2374,7 @@ class Lda final : public Model {
   void zscreen_t_launch(const LdaArgs& a, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
     const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + (kZThreads / 32) * 32 * (4 * R + 4));
-    zscreen_t_kernel<R, TFR><<<g, kZThreads, sm, st>>>(a, out.iter);
+    launch_pdl(zscreen_t_kernel<R, TFR>, dim3(g), dim3(kZThreads), sm, st, a, static_cast<const std::int64_t*>(out.iter));
   }
 
   template <bool TFR>
@@ -2409,7 +2428,8 @@ class Lda final : public Model {
   }
 
   void launch_zscreen(const LdaArgs& a, cudaStream_t st) {
-    BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+    if (!fq_reset_) BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+    fq_reset_ = false;
     if (stage_) {
       zstage_dispatch(a, st, std::integer_sequence<int, 1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32>{});
       zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
@@ -2418,7 +2438,7 @@ class Lda final : public Model {
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
-      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
+      launch_pdl(zfallback_kernel, dim3(148 * 8), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter), out.err);
       return;
     }
     const int key = G32_ * 100 + CW32_ * 10 + (tfr_ ? 1 : 0);
@@ -2548,6 +2568,25 @@ class Lda final : public Model {
   std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0;
   int nbw_ = 1;
   float screen_margin_ = kScreenMargin;
+  bool fq_reset_ = false;  // phi_colsum2 of this sweep zeroes the fallback queue
+
+  // cudaLaunchKernelEx with programmatic stream serialization (PDL): the kernel's
+  // launch overlaps the predecessor's tail; it calls pdl_wait() before its inputs.
+  template <class... KArgs, class... Args>
+  void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_ ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BNMC_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  }
+  bool pdl_ = true;
   DevBuf<int2> fq_;
   DevBuf<int> fq_len_;
   bool data_on_device_ = false;
