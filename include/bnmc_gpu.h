@@ -14,6 +14,7 @@
  *                          include/bnmc/store.hpp:74-83
  *   bnmc_gpu_sweep         Engine::sweep             include/bnmc/sampler.hpp:60 (src/sampler.cpp:390-405)
  *   bnmc_gpu_run           Engine::run's sweep loop  include/bnmc/sampler.hpp:63 (src/sampler.cpp:426-455)
+ *   bnmc_gpu_run_trace     Engine::run (Trace: samples, MAP, log-joints, timings) sampler.hpp:63
  *   bnmc_gpu_eval_log_joint Engine::eval_log_joint   include/bnmc/sampler.hpp:56 (src/sampler.cpp:44-46)
  *   bnmc_gpu_download      writes back the unobserved variables of the ParamStore
  *   bnmc_gpu_prior_init    prior_init                include/bnmc/sampler.hpp:97-99 (src/sampler.cpp:542-555)
@@ -120,6 +121,23 @@ int bnmc_gpu_download(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
 int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_accepted);
 /* n sweeps iter0..iter0+n-1 with one host sync; per-sweep outputs optional. */
 int bnmc_gpu_run(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n, double* log_joints, int* accepted);
+/* Engine::run (sampler.cpp:426-455) with a device-resident trace: burn-in + n kept
+ * sweeps; the MAP state is tracked on the device (a conditional device copy after
+ * every kept sweep whose log-joint beats the best so far, strict >, as the
+ * reference), thinned samples (kept index % thin == 0) are written into
+ * samples[i], the MAP state into map_state at the end.  No host round trip per
+ * sweep except for the thinned downloads.  timing_ms[i] = device time of kept
+ * sweep i (the reference times sweep() only).  Optional outputs may be NULL. */
+typedef struct bnmc_gpu_trace {
+  int64_t burnin, n, thin;
+  double* log_joints;              /* [n] */
+  double* timing_ms;               /* [n] */
+  int* accepted;                   /* [n] MH accept flags */
+  const bnmc_gpu_store* samples;   /* [ceil(n / thin)] host views to write */
+  const bnmc_gpu_store* map_state; /* host view to write */
+  double* map_log_joint;           /* -inf when no kept sweep */
+} bnmc_gpu_trace;
+int bnmc_gpu_run_trace(bnmc_gpu_ctx* ctx, int64_t iter0, bnmc_gpu_trace* trace);
 /* Asynchronous variant of bnmc_gpu_run (no host sync); pair with bnmc_gpu_synchronize. */
 int bnmc_gpu_enqueue(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n);
 int bnmc_gpu_synchronize(bnmc_gpu_ctx* ctx, double* last_log_joint, int* last_accepted);

@@ -156,33 +156,34 @@ class Engine {
     return lj;
   }
 
-  // Engine::run: burn-in + n kept sweeps; state copies only for thinned / MAP snapshots.
+  // Engine::run: burn-in + n kept sweeps through bnmc_gpu_run_trace -- the MAP state
+  // is tracked on the device, thinned samples are downloaded into copies of the store.
   Trace run(ParamStore& store, long long n) {
     bind(store);
     Trace t;
     t.seed = cfg_.seed;
-    t.map_log_joint = -std::numeric_limits<double>::infinity();
-    for (long long it = 0; it < cfg_.burnin + n; ++it) {
-      const auto t0 = std::chrono::steady_clock::now();
-      double lj = 0.0;
-      int acc = 0;
-      check(bnmc_gpu_sweep(ctx_.get(), it, &lj, &acc), ctx_.get());
-      const auto t1 = std::chrono::steady_clock::now();
-      if (it < cfg_.burnin) continue;
-      const long long s = it - cfg_.burnin;
-      t.log_joint.push_back(lj);
-      t.timing_ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
-      const bool snap = s % cfg_.thin == 0, better = lj > t.map_log_joint;
-      if (snap || better) {
-        download(store);
-        Snapshot sn{store.real, store.ival};
-        if (snap) t.samples.push_back(sn);
-        if (better) {
-          t.map_log_joint = lj;
-          t.map_state = sn;
-        }
-      }
-    }
+    const long long thin = cfg_.thin > 0 ? cfg_.thin : 1;
+    const long long ns = n > 0 ? (n + thin - 1) / thin : 0;
+    std::vector<ParamStore> samples(static_cast<std::size_t>(ns), store);
+    ParamStore map_store = store;
+    std::vector<bnmc_gpu_store> views;
+    views.reserve(samples.size());
+    for (auto& s : samples) views.push_back(s.view());
+    bnmc_gpu_store mv = map_store.view();
+    t.log_joint.assign(static_cast<std::size_t>(n > 0 ? n : 0), 0.0);
+    t.timing_ms.assign(t.log_joint.size(), 0.0);
+    bnmc_gpu_trace tr{};
+    tr.burnin = cfg_.burnin;
+    tr.n = n;
+    tr.thin = thin;
+    tr.log_joints = t.log_joint.data();
+    tr.timing_ms = t.timing_ms.data();
+    tr.samples = views.empty() ? nullptr : views.data();
+    tr.map_state = &mv;
+    tr.map_log_joint = &t.map_log_joint;
+    check(bnmc_gpu_run_trace(ctx_.get(), 0, &tr), ctx_.get());
+    for (auto& s : samples) t.samples.push_back(Snapshot{s.real, s.ival});
+    if (n > 0) t.map_state = Snapshot{map_store.real, map_store.ival};
     download(store);
     return t;
   }

@@ -6,6 +6,7 @@
 // kernel advances it, so n sweeps are n graph launches with no host round trip;
 // log-joints land in a device ring read back at synchronisation points.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -140,6 +141,30 @@ void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, in
       BNMC_CUDA(cudaMemcpyAsync(acc + first, c->acc.p, sizeof(int) * (n - first), cudaMemcpyDeviceToHost, c->stream));
   }
   BNMC_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// MAP tracking on the device (bnmc_gpu_run_trace): the sweep just advanced *iter;
+// its log-joint sits in lj[(*iter - 1) % kRing].
+__global__ void map_check_kernel(const double* lj, const std::int64_t* iter, double* map_lj, int* flag) {
+  const double v = lj[(*iter - 1) & (kRing - 1)];
+  const bool better = v > *map_lj;  // strict, NaN never better (sampler.cpp:449)
+  if (better) *map_lj = v;
+  *flag = better ? 1 : 0;
+}
+
+struct CopyTab {
+  const unsigned* src[8];
+  unsigned* dst[8];
+  std::size_t words[8];
+  int n;
+};
+
+__global__ void cond_copy_kernel(CopyTab t, const int* flag) {
+  if (!*flag) return;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  for (int b = 0; b < t.n; ++b)
+    for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < t.words[b]; i += stride)
+      t.dst[b][i] = t.src[b][i];
 }
 
 }  // namespace
@@ -322,6 +347,91 @@ int bnmc_gpu_run(bnmc_gpu_ctx* c, std::int64_t iter0, std::int64_t n, double* lo
       check_device_error(c);
       done += chunk;
     }
+  });
+}
+
+int bnmc_gpu_run_trace(bnmc_gpu_ctx* c, std::int64_t iter0, bnmc_gpu_trace* tr) {
+  if (!c || !tr) return fail(c, BNMC_GPU_ERR_ARG, "null context or trace");
+  return guarded(c, [&] {
+    require(iter0 >= 0 && tr->n >= 0 && tr->burnin >= 0 && tr->thin >= 1, BNMC_GPU_ERR_ARG,
+            "bad trace arguments (n, burnin >= 0, thin >= 1)");
+    auto bufs = c->model->state_buffers();
+    require(bufs.size() <= 8, BNMC_GPU_ERR_RUNTIME, "too many state buffers");
+    // device MAP copy of the state + best log-joint + flag
+    std::vector<DevBuf<unsigned>> map(bufs.size());
+    CopyTab tab{};
+    tab.n = static_cast<int>(bufs.size());
+    for (std::size_t i = 0; i < bufs.size(); ++i) {
+      map[i].alloc((bufs[i].bytes + 3) / 4);
+      tab.words[i] = bufs[i].bytes / 4;
+    }
+    DevBuf<double> map_lj;
+    DevBuf<int> flag;
+    map_lj.alloc(1);
+    flag.alloc(1);
+    const double ninf = -INFINITY;
+    BNMC_CUDA(cudaMemcpyAsync(map_lj.p, &ninf, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    std::vector<cudaEvent_t> ev;
+    auto cleanup = [&] {
+      for (auto e : ev) cudaEventDestroy(e);
+    };
+    try {
+      set_iter(c, iter0);
+      for (std::int64_t i = 0; i < tr->burnin; ++i) launch_sweep(c);
+      if (tr->timing_ms) {
+        ev.resize(static_cast<std::size_t>(2 * tr->n));
+        for (auto& e : ev) BNMC_CUDA(cudaEventCreate(&e));
+      }
+      std::int64_t read = 0;  // kept log-joints already copied out
+      auto drain = [&](std::int64_t upto) {
+        if (upto > read) {
+          read_ring(c, iter0 + tr->burnin + read, upto - read, tr->log_joints ? tr->log_joints + read : nullptr,
+                    tr->accepted ? tr->accepted + read : nullptr);
+          read = upto;
+        }
+      };
+      std::int64_t sample = 0;
+      for (std::int64_t s = 0; s < tr->n; ++s) {
+        if (s - read >= kRing) drain(s);
+        if (tr->timing_ms) BNMC_CUDA(cudaEventRecord(ev[2 * s], c->stream));
+        launch_sweep(c);
+        if (tr->timing_ms) BNMC_CUDA(cudaEventRecord(ev[2 * s + 1], c->stream));
+        if (tr->map_state || tr->map_log_joint) {
+          map_check_kernel<<<1, 1, 0, c->stream>>>(c->lj.p, c->iter.p, map_lj.p, flag.p);
+          for (std::size_t i = 0; i < bufs.size(); ++i) {
+            tab.src[i] = static_cast<const unsigned*>(*bufs[i].p);
+            tab.dst[i] = map[i].p;
+          }
+          cond_copy_kernel<<<148 * 4, 256, 0, c->stream>>>(tab, flag.p);
+        }
+        if (tr->samples && s % tr->thin == 0) c->model->download(tr->samples[sample++], c->stream);
+      }
+      drain(tr->n);
+      check_device_error(c);
+      if (tr->timing_ms)
+        for (std::int64_t s = 0; s < tr->n; ++s) {
+          float ms = 0.f;
+          BNMC_CUDA(cudaEventElapsedTime(&ms, ev[2 * s], ev[2 * s + 1]));
+          tr->timing_ms[s] = ms;
+        }
+      if (tr->map_log_joint)
+        BNMC_CUDA(cudaMemcpy(tr->map_log_joint, map_lj.p, sizeof(double), cudaMemcpyDeviceToHost));
+      if (tr->map_state && tr->n > 0) {
+        // download() reads the model's state buffers: swap the MAP copies in and out
+        for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
+        try {
+          c->model->download(*tr->map_state, c->stream);
+        } catch (...) {
+          for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
+          throw;
+        }
+        for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 

@@ -116,6 +116,14 @@ struct Model {
   virtual void lda_generate(std::uint64_t, double, double, cudaStream_t) {
     throw Error(BNMC_GPU_ERR_ARG, "generate is only defined for LDA");
   }
+  // The device buffers that fully determine the latent state (what download()
+  // reads).  The trace run keeps a device copy of the MAP state by copying them
+  // and downloads it by swapping the pointers in (bnmc_gpu_run_trace).
+  struct StateBuf {
+    void** p;
+    std::size_t bytes;
+  };
+  virtual std::vector<StateBuf> state_buffers() { return {}; }
   Outputs out{};
 
   // Per-phase timing (bnmc_gpu_sweep_phases): when `marks` is set, every phase

@@ -368,6 +368,13 @@ class Gmm final : public Model {
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
 
+  std::vector<StateBuf> state_buffers() override {
+    return {{reinterpret_cast<void**>(&z_.p), sizeof(int) * static_cast<std::size_t>(N_)},
+            {reinterpret_cast<void**>(&pi_.p), sizeof(double) * static_cast<std::size_t>(K_)},
+            {reinterpret_cast<void**>(&mu_.p), sizeof(double) * static_cast<std::size_t>(K_)},
+            {reinterpret_cast<void**>(&s2_.p), sizeof(double) * static_cast<std::size_t>(K_)}};
+  }
+
   void enqueue_sweep(cudaStream_t st) override {
     GmmArgs a = args();
     mark(st, "begin");

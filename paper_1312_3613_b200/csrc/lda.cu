@@ -2157,6 +2157,13 @@ class Lda final : public Model {
     after_state_change(st);
   }
 
+  std::vector<StateBuf> state_buffers() override {
+    return {{reinterpret_cast<void**>(&z_.p), sizeof(int) * static_cast<std::size_t>(Nl_)},
+            {reinterpret_cast<void**>(&theta_.p), sizeof(double) * static_cast<std::size_t>(Ml_ * K_)},
+            {reinterpret_cast<void**>(&phiT_.p), phiT_.bytes()},
+            {reinterpret_cast<void**>(&S_.p), S_.bytes()}};
+  }
+
   void lda_counts(std::int32_t* nkw_host, std::int32_t* nmk_host, cudaStream_t st) override {
     if (nkw_host) {
       // Topic-word counts of the current z, recomputed (then summed over ranks).

@@ -319,6 +319,10 @@ class Mh final : public Model {
     if (!logistic_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
   }
 
+  std::vector<StateBuf> state_buffers() override {
+    return {{reinterpret_cast<void**>(&w_.p), sizeof(double) * static_cast<std::size_t>(K_ + 2)}};
+  }
+
   void enqueue_sweep(cudaStream_t st) override {
     MhArgs a = args();
     mark(st, "begin");

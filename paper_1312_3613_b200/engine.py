@@ -56,6 +56,12 @@ class _Store(ctypes.Structure):
                 ("len", POINTER(c_int64)), ("observed", POINTER(c_char))]
 
 
+class _Trace(ctypes.Structure):
+    _fields_ = [("burnin", c_int64), ("n", c_int64), ("thin", c_int64), ("log_joints", POINTER(c_double)),
+                ("timing_ms", POINTER(c_double)), ("accepted", POINTER(c_int)), ("samples", POINTER(_Store)),
+                ("map_state", POINTER(_Store)), ("map_log_joint", POINTER(c_double))]
+
+
 _lib = None
 
 
@@ -82,6 +88,7 @@ def lib():
     L.bnmc_gpu_sweep.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_int)]
     L.bnmc_gpu_run.argtypes = [c_void_p, c_int64, c_int64, POINTER(c_double), POINTER(c_int)]
     L.bnmc_gpu_enqueue.argtypes = [c_void_p, c_int64, c_int64]
+    L.bnmc_gpu_run_trace.argtypes = [c_void_p, c_int64, POINTER(_Trace)]
     L.bnmc_gpu_synchronize.argtypes = [c_void_p, POINTER(c_double), POINTER(c_int)]
     L.bnmc_gpu_eval_log_joint.argtypes = [c_void_p, POINTER(c_double)]
     L.bnmc_gpu_prior_init.argtypes = [c_void_p, c_uint64]
@@ -407,32 +414,39 @@ class Engine:
 
     def run(self, store: ParamStore, n: int) -> dict:
         """Engine::run (sampler.cpp:426-455): burn-in + n kept sweeps, thinned samples,
-        MAP state; per-sweep log-joints come from the device, states only on snapshots."""
+        MAP state, per-sweep log-joints and timings -- through bnmc_gpu_run_trace, which
+        keeps the MAP state on the device (no host round trip per sweep); only the
+        thinned samples are downloaded as they are taken."""
         if self._bound is not store:
             self.upload(store)
         cfg = self.cfg
+        if n < 0 or cfg.thin < 1:
+            raise BnmcError("run needs n >= 0 and thin >= 1")
         unobs = [v for v in store.names if not store.observed[v]]
+        n_samples = (n + cfg.thin - 1) // cfg.thin
+        samples = [store.copy() for _ in range(n_samples)]
+        map_store = store.copy()
+        views = (_Store * max(n_samples, 1))()
+        keep = []
+        for i, smp in enumerate(samples):
+            v = smp._view()
+            views[i] = v
+            keep.append(v)
+        mv = map_store._view()
+        lj = np.full(max(n, 1), np.nan)
+        tm = np.zeros(max(n, 1))
+        acc = np.zeros(max(n, 1), dtype=np.int32)
+        map_lj = c_double(-np.inf)
+        tr = _Trace(cfg.burnin, n, cfg.thin, _p(lj, c_double), _p(tm, c_double), _p(acc, c_int),
+                    ctypes.cast(views, POINTER(_Store)), ctypes.pointer(mv), ctypes.pointer(map_lj))
+        _raise(lib().bnmc_gpu_run_trace(self._h, 0, ctypes.byref(tr)), self._h)
         trace = dict(model=self.model, method=self.spec["method"], seed=cfg.seed, var_names=unobs,
-                     samples=[], log_joint=[], map_state={}, map_log_joint=-np.inf, timing_ms=[])
-        import time
-        for it in range(cfg.burnin + n):
-            t0 = time.perf_counter()
-            lj, _ = self.sweep_device(it)
-            t1 = time.perf_counter()
-            if it < cfg.burnin:
-                continue
-            s = it - cfg.burnin
-            trace["log_joint"].append(lj)
-            trace["timing_ms"].append((t1 - t0) * 1e3)
-            snap = None
-            if s % cfg.thin == 0 or lj > trace["map_log_joint"]:
-                self.download(store)
-                snap = {v: store[v].copy() for v in unobs}
-            if s % cfg.thin == 0:
-                trace["samples"].append(snap)
-            if lj > trace["map_log_joint"]:
-                trace["map_log_joint"] = lj
-                trace["map_state"] = snap
+                     samples=[{v: smp[v].copy() for v in unobs} for smp in samples],
+                     log_joint=lj[:n].tolist(), timing_ms=tm[:n].tolist(),
+                     map_state={v: map_store[v].copy() for v in unobs} if n > 0 else {},
+                     map_log_joint=map_lj.value)
+        if self.spec["method"] == "mh":
+            trace["accepted"] = acc[:n].astype(bool).tolist()
         self.download(store)
         return trace
 

@@ -333,3 +333,66 @@ def test_lda_layouts_vs_restatement(g, restatement, monkeypatch, K, env):
     np.add.at(want, (z, w), 1)
     assert np.array_equal(nkw, want)
     e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# Engine::run with the device-resident trace (bnmc_gpu_run_trace)
+# ----------------------------------------------------------------------------------------
+def _stepwise_run(e, s, burnin, n, thin, names):
+    """Engine::run (sampler.cpp:426-455) restated over single device sweeps."""
+    lj, samples, map_lj, map_state = [], [], -np.inf, None
+    for it in range(burnin + n):
+        v = e.sweep(s, it)
+        if it < burnin:
+            continue
+        k = it - burnin
+        lj.append(v)
+        if k % thin == 0:
+            samples.append({x: s[x].copy() for x in names})
+        if v > map_lj:
+            map_lj, map_state = v, {x: s[x].copy() for x in names}
+    return lj, samples, map_lj, map_state
+
+
+@pytest.mark.parametrize("model", ["lda", "gmm", "regression"])
+def test_run_trace_matches_stepwise(g, model):
+    if model == "lda":
+        fx = golden("lda_desk")
+        mk = lambda: lda_engine(g, fx)  # noqa: E731
+        names = ["phi", "theta", "z"]
+    elif model == "gmm":
+        fx = golden("gmm_small")
+
+        def mk():
+            e = g.Engine("gmm", {"N": int(fx["N"]), "K": 4}, g.RunConfig(seed=int(fx["seed"]), burnin=2, thin=3))
+            s = e.allocate()
+            s["x"], s["z"], s["pi"], s["mu"], s["sigma2"] = fx["x"], fx["z0"], fx["pi0"], fx["mu0"], fx["sigma20"]
+            return e, s
+        names = ["pi", "mu", "sigma2", "z"]
+    else:
+        fx = golden("mh_linreg")
+
+        def mk():
+            N, K = int(fx["N"]), int(fx["K"])
+            e = g.Engine("regression", {"N": N, "K": K, "l": -1.0, "u": 1.0},
+                         g.RunConfig(seed=int(fx["seed"]), burnin=2, thin=3))
+            s = e.allocate()
+            s["x"], s["y"], s["w"], s["b"], s["tau"] = fx["x"], fx["y"], fx["w0"], [fx["b0"]], [fx["tau0"]]
+            return e, s
+        names = ["w", "b", "tau"]
+    burnin, n, thin = 2, 7, 3
+    e1, s1 = mk()
+    e1.cfg.burnin, e1.cfg.thin = burnin, thin
+    tr = e1.run(s1, n)
+    e2, s2 = mk()
+    lj, samples, map_lj, map_state = _stepwise_run(e2, s2, burnin, n, thin, names)
+    assert tr["log_joint"] == lj
+    assert len(tr["samples"]) == len(samples) == 3
+    for a, b in zip(tr["samples"], samples):
+        for x in names:
+            assert np.array_equal(a[x], b[x]), x
+    assert tr["map_log_joint"] == map_lj
+    for x in names:
+        assert np.array_equal(tr["map_state"][x], map_state[x]), x
+        assert np.array_equal(s1[x], s2[x]), x  # the store holds the final state
+    assert len(tr["timing_ms"]) == n and all(t > 0 for t in tr["timing_ms"])
