@@ -1018,15 +1018,26 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
 // Every lane does useful work in (2), instead of 1 lane in 4 for the in-group
 // search, and no cross-lane scans are needed (ncu r01 v10: the grouped search was
 // ~2/3 of the z-step's ~31 warp instructions per token).
+// csum row layout: 16 floats per token row, 16-byte group q of row r stored at group
+// q ^ ((r >> 1) & 3): the products phase's float4 writes (2 rows x 4 lanes per
+// quarter warp) and the search phase's float4 reads (8 rows, one group) both touch
+// 8 distinct bank groups -- no conflicts (ncu r01 v15: 1.05 M conflicting store
+// wavefronts with a padded row layout).
+__device__ __forceinline__ int cs_idx(int row, int c) {
+  return row * 16 + ((((c >> 2) ^ (row >> 1)) & 3) << 2) + (c & 3);
+}
+
 template <int R, bool TFR>
 __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  constexpr int G = 4, CW = 8, KL = CW * R, KLP = KL + 4, C = G * R, CSP = C + 4;
+  constexpr int G = 4, CW = 8, KL = CW * R, KLP = KL + 4, C = G * R;
+  static_assert(C <= 16, "csum rows hold 16 chunk sums");
   constexpr int kWarps = kZThreads / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* thf = reinterpret_cast<float*>(smem_raw);  // [G][KLP] theta/S, fp32
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
   const int warp = threadIdx.x >> 5;
-  float* csum = thf + G * KLP + warp * 32 * CSP;     // [32][CSP] chunk sums of the batch
+  float* csum = thf + G * KLP + warp * 32 * 16;      // [32][16] chunk sums of the batch (cs_idx)
+  int* cnt_s = reinterpret_cast<int*>(thf + G * KLP + kWarps * 32 * 16);  // [K] this unit's doc-topic counts
   pdl_wait();
   pdl_trigger();
   const std::int64_t iter = *iter_p;
@@ -1035,8 +1046,10 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
   for (std::int64_t unit = blockIdx.x; unit < a.n_units; unit += gridDim.x) {
     const std::int64_t m = a.units[unit * 3], t0 = a.units[unit * 3 + 1], t1 = a.units[unit * 3 + 2];
     const double* thg = a.theta + m * a.K;
-    for (int k = threadIdx.x; k < G * KL; k += blockDim.x)
+    for (int k = threadIdx.x; k < G * KL; k += blockDim.x) {
       thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+      if (k < a.K) cnt_s[k] = 0;
+    }
     __syncthreads();
     float tf[TFR ? KL : 1];
     if constexpr (TFR) {
@@ -1046,7 +1059,6 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
         tf[i] = t.x, tf[i + 1] = t.y, tf[i + 2] = t.z, tf[i + 3] = t.w;
       }
     }
-    int* cnt = a.nmk + m * a.K;
     for (std::int64_t b0 = t0 + warp * 32; b0 < t1; b0 += kWarps * 32) {
       const std::int64_t t = b0 + lane;
       const bool valid = t < t1;
@@ -1081,12 +1093,11 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
           for (int j = 1; j < CW; ++j) sr = __fmaf_rn(x[j], ph[r].v[j], sr);
           cs[r] = sr;
         }
-        float* dst = csum + src * CSP + gl * R;
         if constexpr (R == 4) {
-          *reinterpret_cast<float4*>(dst) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+          *reinterpret_cast<float4*>(csum + cs_idx(src, gl * R)) = make_float4(cs[0], cs[1], cs[2], cs[3]);
         } else {
 #pragma unroll
-          for (int r = 0; r < R; ++r) dst[r] = cs[r];
+          for (int r = 0; r < R; ++r) csum[cs_idx(src, gl * R + r)] = cs[r];
         }
       }
       __syncwarp();
@@ -1099,7 +1110,7 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
         float run = 0.0f;
 #pragma unroll
         for (int c = 0; c < C; c += 4) {
-          const float4 y = *reinterpret_cast<const float4*>(csum + lane * CSP + c);
+          const float4 y = *reinterpret_cast<const float4*>(csum + cs_idx(lane, c));
           run += y.x;
           P[c] = run;
           run += y.y;
@@ -1147,7 +1158,7 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
         if (k >= 0) {
           a.z[t] = k;
           atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
-          atomicAdd(&cnt[k], 1);
+          atomicAdd(&cnt_s[k], 1);  // shared: flushed to nmk once per unit
         } else {
           const int slot = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
           a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
@@ -1156,6 +1167,10 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
       __syncwarp();
     }
     __syncthreads();
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+      const int n = cnt_s[k];
+      if (n) atomicAdd(&a.nmk[m * a.K + k], n);
+    }
   }
 }
 
@@ -2380,7 +2395,7 @@ class Lda final : public Model {
   template <int R, bool TFR>
   void zscreen_t_launch(const LdaArgs& a, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
-    const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + (kZThreads / 32) * 32 * (4 * R + 4));
+    const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + (kZThreads / 32) * 32 * 16) + sizeof(int) * K_;
     launch_pdl(zscreen_t_kernel<R, TFR>, dim3(g), dim3(kZThreads), sm, st, a, static_cast<const std::int64_t*>(out.iter));
   }
 
