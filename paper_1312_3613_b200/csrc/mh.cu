@@ -67,9 +67,9 @@ __global__ void propose_kernel(MhArgs a, const std::int64_t* iter_p) {
 
 // Sum over local rows of the row log-likelihood at parameters p (K + 2 values).
 // A group of 8 lanes per row: lane gl reads the row's 4-feature chunks gl, gl+8, ...
-// with one 256-bit load each (8 lanes = 256 contiguous bytes per request, 4 rows per
-// warp), keeps its slice of w in registers, and the dot product is a fixed 3-step
-// butterfly; lane 0 of the group evaluates the row's log-likelihood.
+// with one 256-bit load each (8 lanes = 256 contiguous bytes per request), keeps its
+// slice of w in registers, and the dot product is a fixed 3-step butterfly; a group
+// takes 4 consecutive rows per iteration and lane r evaluates row r's log-likelihood.
 constexpr int kRowGroup = 8;
 constexpr int kMaxChunks = 8;  // K <= 4 * 8 * kMaxChunks = 256 on the vector path
 
@@ -102,24 +102,42 @@ __global__ void __launch_bounds__(kThreads) lik_kernel(MhArgs a, const double* p
     }
     const std::int64_t g = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) / kRowGroup;
     const std::int64_t ng = static_cast<std::int64_t>(gridDim.x) * blockDim.x / kRowGroup;
-    for (std::int64_t i = g; i < a.N; i += ng) {
-      const double* xi = a.x + i * a.K;
-      double s = 0.0;
+    // kRows consecutive rows per group iteration: all their loads are issued before
+    // any reduction (kRows * CPL 256-bit loads in flight per lane), and the rows'
+    // log-likelihoods (exp/log1p chains) run on kRows different lanes of the group
+    // instead of serially on lane 0.
+    constexpr int kRows = 4;
+    for (std::int64_t i0 = g * kRows; i0 < a.N; i0 += ng * kRows) {
+      double xv[kRows][CPL][4];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int ch = gl + kRowGroup * c;
-        if (ch < chunks) {
-          double x0, x1, x2, x3;
-          ldg256(xi + 4 * ch, x0, x1, x2, x3);
-          s += wr[c][0] * x0;
-          s += wr[c][1] * x1;
-          s += wr[c][2] * x2;
-          s += wr[c][3] * x3;
+      for (int r = 0; r < kRows; ++r) {
+        const double* xi = a.x + (i0 + r) * a.K;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int ch = gl + kRowGroup * c;
+          if (ch < chunks && i0 + r < a.N) {
+            ldg256(xi + 4 * ch, xv[r][c][0], xv[r][c][1], xv[r][c][2], xv[r][c][3]);
+          } else {
+            xv[r][c][0] = xv[r][c][1] = xv[r][c][2] = xv[r][c][3] = 0.0;
+          }
         }
       }
+      double mine = 0.0;
 #pragma unroll
-      for (int o = kRowGroup / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gm, s, o, kRowGroup);
-      if (gl == 0) acc += row_loglik(a, s + b, __ldg(a.y + i), tau);
+      for (int r = 0; r < kRows; ++r) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          s += wr[c][0] * xv[r][c][0];
+          s += wr[c][1] * xv[r][c][1];
+          s += wr[c][2] * xv[r][c][2];
+          s += wr[c][3] * xv[r][c][3];
+        }
+#pragma unroll
+        for (int o = kRowGroup / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gm, s, o, kRowGroup);
+        if (gl == r) mine = s;
+      }
+      if (gl < kRows && i0 + gl < a.N) acc += row_loglik(a, mine + b, __ldg(a.y + i0 + gl), tau);
     }
   } else {
     // any K: warp per row, lanes stride the features
