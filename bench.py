@@ -17,8 +17,9 @@ Prints ONE JSON line (rank 0).  Fields beyond the base contract:
   cpu_baseline the compiled reference (oracle/_ref) timed on this host's cores on a
                bounded sample of the same workload
   e2e          the same metric through the public API with HOST buffers: every step
-               uploads the caller's latent state, sweeps, and downloads the state +
-               log-joint (Engine::sweep borrow semantics), pinned host memory
+               uploads what the sweep reads from the caller's store (LDA: z; its phi and
+               theta blocks redraw phi and theta first), sweeps, and downloads the whole
+               latent state + log-joint (Engine::sweep borrow semantics), pinned memory
 Multi-GPU (torchrun): documents sharded across ranks (weak scaling: each rank holds a
 NIPS-shaped shard), one NCCL all-reduce of the K x V counts per sweep inside the graph.
 """
@@ -374,10 +375,14 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
                 store.__dict__.setdefault("_pins", []).append(t)
         lat = [n for n in store.names if not store.observed[n]]
         if model == "lda":
-            up = sum(store.arrays[n].nbytes for n in lat) // world
+            # per step: this rank's z slice up (the sweep reads only z of the latent state:
+            # bnmc_gpu_upload_sweep_inputs); z and theta slices + the global phi + lj down
+            nz = sites_local * 8
+            up = nz
+            down = nz + (sites_local // L) * K * 8 + K * V * 8 + 8
         else:
             up = sum(store.arrays[n].nbytes for n in lat)
-        down = up + 8
+            down = up + 8
         eng.sweep(store, it)  # bind (uploads the observed data once, outside the timed region)
         it += 1
         if dist:
@@ -395,7 +400,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             e2e_s = float(t.item())
         e2e = {"value": sites_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(up),
                "d2h_bytes_per_step": int(down), "ms_per_step": e2e_s * 1e3,
-               "path": "Engine.sweep(store, iter): bnmc_gpu_upload_state + bnmc_gpu_sweep + bnmc_gpu_download"}
+               "path": "Engine.sweep(store, iter) with pinned host arrays: bnmc_gpu_upload_sweep_inputs + "
+                       "bnmc_gpu_sweep + bnmc_gpu_download"}
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "1B corpus is generated and kept on the device (host cannot hold it)"}

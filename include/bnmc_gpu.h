@@ -113,6 +113,10 @@ int bnmc_gpu_upload(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
 /* Copies only the latent (unobserved) variables; observed data already on the
  * device is kept.  The per-call path of a bound store (Engine::sweep borrow). */
 int bnmc_gpu_upload_state(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
+/* Copies only the latent variables the next sweep reads (LDA: z -- the phi and theta
+ * blocks redraw phi and theta from the counts first; other models: all latent
+ * variables).  The per-call upload of Engine::sweep on a bound store. */
+int bnmc_gpu_upload_sweep_inputs(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
 /* Writes the device state back into the unobserved variables of `store`
  * (observed variables are never written, test_runtime.cpp:214-233). */
 int bnmc_gpu_download(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);

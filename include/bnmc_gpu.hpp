@@ -132,7 +132,7 @@ class Engine {
 
   // Engine::sweep: the store is advanced in place; returns the post-sweep log-joint.
   double sweep(ParamStore& store, long long iter, bool* mh_accepted = nullptr) {
-    bind(store);
+    bind(store, /*sweep_inputs=*/true);
     double lj = 0.0;
     int acc = 0;
     check(bnmc_gpu_sweep(ctx_.get(), iter, &lj, &acc), ctx_.get());
@@ -191,11 +191,13 @@ class Engine {
   bnmc_gpu_ctx* handle() { return ctx_.get(); }
 
  private:
-  void bind(ParamStore& store) {
+  void bind(ParamStore& store, bool sweep_inputs = false) {
     bnmc_gpu_store v = store.view();
     if (bound_ != &store) {
       check(bnmc_gpu_upload(ctx_.get(), &v), ctx_.get());
       bound_ = &store;
+    } else if (sweep_inputs) {
+      check(bnmc_gpu_upload_sweep_inputs(ctx_.get(), &v), ctx_.get());
     } else {
       check(bnmc_gpu_upload_state(ctx_.get(), &v), ctx_.get());
     }

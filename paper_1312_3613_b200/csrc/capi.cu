@@ -275,6 +275,15 @@ int bnmc_gpu_upload_state(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
   });
 }
 
+int bnmc_gpu_upload_sweep_inputs(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
+            "store view is incomplete");
+    c->model->upload_sweep_inputs(*s, c->stream);  // range errors surface at the sweep's check
+  });
+}
+
 int bnmc_gpu_sweep_phases(bnmc_gpu_ctx* c, std::int64_t iter, double* ms, const char** names, int cap,
                           int* n_out) {
   if (!c || !ms || !n_out) return fail(c, BNMC_GPU_ERR_ARG, "null argument");

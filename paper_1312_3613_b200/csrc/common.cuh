@@ -104,6 +104,9 @@ struct Model {
   // Uploads only the latent (unobserved) variables: the observed data already on
   // the device is kept (the engine never writes observed arrays).
   virtual void upload_state(const bnmc_gpu_store& s, cudaStream_t st) { upload(s, st); }
+  // Uploads the latent variables the next sweep actually reads (a bound store's
+  // per-call path of Engine::sweep); the default is every latent variable.
+  virtual void upload_sweep_inputs(const bnmc_gpu_store& s, cudaStream_t st) { upload_state(s, st); }
   // Enqueues one sweep (reads the iteration from *out.iter, advances it).
   virtual void enqueue_sweep(cudaStream_t st) = 0;
   // Enqueues Engine::eval_log_joint of the current state into lj[iter % kRing]

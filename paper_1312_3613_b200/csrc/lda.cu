@@ -2028,6 +2028,33 @@ class Lda final : public Model {
     upload_impl(s, st, !data_on_device_);
   }
 
+  // The LDA sweep reads only z of the latent state: its phi and theta blocks redraw
+  // phi and theta from the counts of z before anything reads them (plan order phi,
+  // theta, z; sampler.cpp:52-218).  So a bound store's sweep uploads z alone and
+  // rebuilds the counts; phiT / S keep the last sweep's values (download-consistent).
+  void upload_sweep_inputs(const bnmc_gpu_store& s, cudaStream_t st) override {
+    if (!data_on_device_) {
+      upload_impl(s, st, true);
+      return;
+    }
+    check_len(s, var_z_, N_, "z");
+    require(s.ival[var_z_] != nullptr, BNMC_GPU_ERR_RUNTIME, "store arrays missing");
+    if (Nl_ > 0) {
+      if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
+      BNMC_CUDA(cudaMemcpyAsync(stage64_.p, s.ival[var_z_] + tok0_, sizeof(std::int64_t) * Nl_,
+                                cudaMemcpyHostToDevice, st));
+      i64_to_i32_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(stage64_.p, z_.p, Nl_, 0, K_, out.err);
+    }
+    LdaArgs a = args();
+    nkw_.zero(st);
+    nmk_.zero(st);
+    if (Nl_ > 0) {
+      count_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(a, out.err);
+      doc_counts_kernel<<<grid_docs(), 256, 0, st>>>(a, nmk_.p);
+    }
+    BNMC_CUDA(cudaGetLastError());
+  }
+
   void upload_impl(const bnmc_gpu_store& s, cudaStream_t st, bool with_data) {
     require(s.n_vars > std::max(std::max(var_phi_, var_theta_), std::max(var_z_, var_w_)),
             BNMC_GPU_ERR_RUNTIME, "store has the wrong number of variables");

@@ -81,6 +81,7 @@ def lib():
     L.bnmc_gpu_destroy.argtypes = [c_void_p]
     L.bnmc_gpu_upload.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_upload_state.argtypes = [c_void_p, POINTER(_Store)]
+    L.bnmc_gpu_upload_sweep_inputs.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_sweep_phases.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_char_p), c_int,
                                         POINTER(c_int)]
     L.bnmc_gpu_nccl_unique_id.argtypes = [c_void_p]
@@ -368,7 +369,8 @@ class Engine:
         if self._bound is not store:
             self.upload(store)
         else:
-            self.upload_state(store)
+            st = store._view()  # only what the sweep reads (bnmc_gpu_upload_sweep_inputs)
+            _raise(lib().bnmc_gpu_upload_sweep_inputs(self._h, ctypes.byref(st)), self._h)
         lj, acc = c_double(), c_int()
         _raise(lib().bnmc_gpu_sweep(self._h, it, ctypes.byref(lj), ctypes.byref(acc)), self._h)
         self.download(store)
