@@ -42,7 +42,7 @@ namespace bnmc_gpu {
 namespace {
 
 constexpr int kZThreads = 256;
-constexpr int kChunk = 512;  // tokens per z-step work unit
+constexpr int kChunk = 2048;  // max tokens per z-step work unit
 
 // Column of logical candidate k in a phiT32 row (see zscreen_kernel): lane gl of a
 // G-lane group owns candidates [CW*R*gl, CW*R*(gl+1)); its round-r chunk of CW is
@@ -1031,7 +1031,7 @@ template <int R, bool TFR>
 __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaArgs a, const std::int64_t* iter_p) {
   constexpr int G = 4, CW = 8, KL = CW * R, KLP = KL + 4, C = G * R;
   static_assert(C <= 16, "csum rows hold 16 chunk sums");
-  constexpr int kWarps = kZThreads / 32;
+  const int kWarps = blockDim.x >> 5;  // sized to the work units (zscreen_t_launch)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* thf = reinterpret_cast<float*>(smem_raw);  // [G][KLP] theta/S, fp32
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
@@ -1913,7 +1913,10 @@ class Lda final : public Model {
     nb_phi_ = (V_ + rows_per_block_ - 1) / rows_per_block_;
     theta_threads_ = std::min(256, ((K_ + 31) / 32) * 32);
 
-    // z-step work units: chunks of <= kChunk tokens of one document.
+    // z-step work units: chunks of <= kChunk tokens of one document (whole documents
+    // up to kChunk: one theta setup per document).  The transposed z-step's CTA has
+    // one warp per 32-token batch of a mean unit (<= 8), so short documents (KOS: 136
+    // tokens) do not leave most warps of a 256-thread CTA idle.
     for (std::int64_t m = 0; m < Ml_; ++m)
       for (std::int64_t t = off_host_[m]; t < off_host_[m + 1]; t += kChunk) {
         units_host_.push_back(m);
@@ -1921,6 +1924,11 @@ class Lda final : public Model {
         units_host_.push_back(std::min(t + kChunk, off_host_[m + 1]));
       }
     n_units_ = static_cast<std::int64_t>(units_host_.size() / 3);
+    {
+      const double mean = n_units_ > 0 ? static_cast<double>(Nl_) / static_cast<double>(n_units_) : 32.0;
+      zt_warps_ = std::min(8, std::max(1, static_cast<int>(std::ceil(mean / 32.0))));
+      if (const char* e = std::getenv("BNMC_ZT_WARPS")) zt_warps_ = std::min(8, std::max(1, std::atoi(e)));
+    }
 
     w_.alloc(std::max<std::int64_t>(Nl_, 1));
     z_.alloc(std::max<std::int64_t>(Nl_, 1));
@@ -2422,8 +2430,8 @@ class Lda final : public Model {
   template <int R, bool TFR>
   void zscreen_t_launch(const LdaArgs& a, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
-    const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + (kZThreads / 32) * 32 * 16) + sizeof(int) * K_;
-    launch_pdl(zscreen_t_kernel<R, TFR>, dim3(g), dim3(kZThreads), sm, st, a, static_cast<const std::int64_t*>(out.iter));
+    const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + zt_warps_ * 32 * 16) + sizeof(int) * K_;
+    launch_pdl(zscreen_t_kernel<R, TFR>, dim3(g), dim3(32 * zt_warps_), sm, st, a, static_cast<const std::int64_t*>(out.iter));
   }
 
   template <bool TFR>
@@ -2636,6 +2644,7 @@ class Lda final : public Model {
     BNMC_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
   }
   bool pdl_ = true;
+  int zt_warps_ = 8;
   DevBuf<int2> fq_;
   DevBuf<int> fq_len_;
   bool data_on_device_ = false;
