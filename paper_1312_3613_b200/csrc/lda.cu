@@ -185,8 +185,9 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
 // consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
 // uniform]), so the draws are the reference's.
 constexpr int kGammaTab = 64;
-constexpr int kPhiRows = 8;  // L: cells per thread
+constexpr int kPhiRowsMax = 8;  // L: cells per thread (8, or fewer for small K x V)
 
+template <int kPhiRows>
 __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::int64_t* iter_p) {
   __shared__ double tab_d[kGammaTab], tab_c[kGammaTab], tab_inv[kGammaTab];
   __shared__ int cnt_s[kPhiRows][256];  // the thread's counts, loaded up front
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
 // spart[s][k]; the last stripe block of kb to finish (atomic ticket) adds the
 // stripes in stripe order.  The ticket decides who adds, never the order, so the
 // result is deterministic.
-constexpr int kColStripes = 16;
+constexpr int kColStripes = 64;
 
 __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __shared__ double sg_s[8][33], sl_s[8][33];
@@ -287,11 +288,26 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   const std::int64_t chunk = (a.nvb + kColStripes - 1) / kColStripes;
   const std::int64_t b0 = blockIdx.y * chunk, b1 = min(a.nvb, b0 + chunk);
   double sg = 0.0, sl = 0.0;
-  if (k < a.K)
-    for (std::int64_t b = b0 + ty; b < b1; b += 8) {
+  if (k < a.K) {
+    std::int64_t b = b0 + ty;
+    for (; b + 24 < b1; b += 32) {  // 4 independent loads in flight per operand
+      double g4[4], l4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        g4[j] = a.gpart[(b + 8 * j) * a.K + k];
+        l4[j] = a.lpart[(b + 8 * j) * a.K + k];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sg += g4[j];
+        sl += l4[j];
+      }
+    }
+    for (; b < b1; b += 8) {
       sg += a.gpart[b * a.K + k];
       sl += a.lpart[b * a.K + k];
     }
+  }
   sg_s[ty][tx] = sg;
   sl_s[ty][tx] = sl;
   __syncthreads();
@@ -1965,7 +1981,15 @@ class Lda final : public Model {
     fq_len_.alloc(1);
     wpart_.alloc(nbw_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
-    nvb_ = (V_ + kPhiRows - 1) / kPhiRows;
+    // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
+    // vs 42 at 1): enough threads to fill the GPU while the per-thread rejection loop
+    // still amortises over several cells
+    phi_rows_ = 4;
+    if (const char* e = std::getenv("BNMC_PHI_ROWS")) {
+      const int r = std::atoi(e);
+      if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
+    }
+    nvb_ = (V_ + phi_rows_ - 1) / phi_rows_;
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
     ticket_.alloc((K_ + 31) / 32 + 1);
     ticket_.zero(nullptr);
@@ -2139,7 +2163,13 @@ class Lda final : public Model {
         mark(st, "phi_gamma");
         phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
       } else {
-        phi_gamma2_kernel<<<blocks_for(nvb_ * K_, 256), 256, 0, st>>>(a, out.iter);
+        const unsigned nbg = blocks_for(nvb_ * K_, 256);
+        switch (phi_rows_) {
+          case 1: phi_gamma2_kernel<1><<<nbg, 256, 0, st>>>(a, out.iter); break;
+          case 2: phi_gamma2_kernel<2><<<nbg, 256, 0, st>>>(a, out.iter); break;
+          case 4: phi_gamma2_kernel<4><<<nbg, 256, 0, st>>>(a, out.iter); break;
+          default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
+        }
         mark(st, "phi_gamma");
         launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, kColStripes), dim3(256), 0, st, a);
         fq_reset_ = true;
@@ -2654,6 +2684,7 @@ class Lda final : public Model {
   DevBuf<std::int64_t> units_;
   DevBuf<std::int64_t> off_;
   std::int64_t nvb_ = 1;
+  int phi_rows_ = kPhiRowsMax;
   DevBuf<double> gpart_, lpart_, spart_, logg_, logS_;
   DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
