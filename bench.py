@@ -255,11 +255,14 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             store = None
         b, e = g.partition(np.arange(docs + 1, dtype=np.int64) * L, world, rank)
         sites_local = (e - b) * L
-        per_sweep_kernels = 9
+        # phi_gamma2, phi_colsum2, theta2, z-step screen, z-step fallback, wterm<FINAL>
+        per_sweep_kernels = 6
         dominant = "zstep"
-        # per token: phi row 8K + w 4 + z 4 + topic-word count 4 + doc-topic count 4,
-        # theta row 8K per work unit (<= 512 tokens of one document)
-        bytes_per_site_dom = 8 * K + 16 + 8 * K / min(L, 512)
+        # SURVEY 8(d), per token: phi row 8K (fp64) + w 4 + z 4 + topic-word count 4 +
+        # doc-topic count 4, theta row 8K per work unit (a document, <= 2048 tokens)
+        bytes_per_site_dom = 8 * K + 16 + 8 * K / min(L, 2048)
+        # what the implementation moves per token: the fp32 screen row (4K) + the same 16
+        impl_bytes_per_site = 4 * K + 16
         bytes_per_site_sweep = 8 * K + 16 * K / L + 16 + 20 * K * V / (docs * L)
         config = {"workload": f"lda-{args.workload}", "model": "lda (proj/models/lda.bn)", "docs": docs,
                   "vocab": V, "topics": K, "doc_len": L, "tokens": sites_total, "seed": args.seed,
@@ -277,7 +280,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         sites_total = sites_local = N * world  # replicas
         sites_local = N
         per_sweep_kernels, dominant = 6, "z"
-        bytes_per_site_dom = bytes_per_site_sweep = 16
+        bytes_per_site_dom = bytes_per_site_sweep = impl_bytes_per_site = 16
         host_corpus = True
         config = {"workload": "gmm-100k", "model": "gmm (proj/models/gmm.bn)", "points": N, "components": K,
                   "seed": args.seed, "parallelism": f"replicas x{world}"}
@@ -297,7 +300,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         eng.upload(store)
         sites_total, sites_local = Nt, Nt // world
         per_sweep_kernels, dominant = 3, "lik"
-        bytes_per_site_dom = bytes_per_site_sweep = 8 * Kf + 8
+        bytes_per_site_dom = bytes_per_site_sweep = impl_bytes_per_site = 8 * Kf + 8
         host_corpus = True
         config = {"workload": "logreg-mh-10m", "model": "logistic regression MH", "rows": Nt, "features": Kf,
                   "seed": args.seed, "parallelism": f"rows sharded x{world}"}
@@ -352,7 +355,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     phases = {k: float(np.mean(v)) for k, v in phase_ms.items()}
     dom_ms = phases.get(dominant)
     peak, peak_src = measured_peak_hbm()
-    roofline = None
+    roofline = roofline_l2 = None
     if dom_ms:
         achieved = sites_local * bytes_per_site_dom / (dom_ms / 1e3) / 1e9
         traffic = ncu_traffic(dominant)
@@ -362,8 +365,23 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
                     "kernel_ms": round(dom_ms, 5), "share_of_sweep": round(dom_ms / sum(phases.values()), 3),
                     "sweep_effective_frac": round(value / world * bytes_per_site_sweep / 1e9 / peak, 4),
                     "sweep_bytes_per_site": round(bytes_per_site_sweep, 2),
-                    "note": "KOS/NIPS working sets fit the 126 MB L2 within a sweep; L2 is flushed before every "
-                            "timed sweep, so reads start in HBM"}
+                    "note": "KOS/NIPS working sets fit the 126 MB L2 within a sweep (L2 is flushed before every "
+                            "timed sweep, so reads start in HBM): frac > 1 means the kernel is fed from L2 -- "
+                            "see roofline_l2"}
+        # Secondary roofline: the bytes the implementation moves / the kernel time against
+        # the device's L2 -> SM read bandwidth, measured here (bnmc_gpu_probe_read_bandwidth
+        # over a 48 MB buffer); the HBM read bandwidth is measured the same way for context.
+        try:
+            l2_bw = g.read_bandwidth(48 << 20, 50)
+            hbm_bw = g.read_bandwidth(4 << 30, 5)
+            ach_impl = sites_local * impl_bytes_per_site / (dom_ms / 1e3) / 1e9
+            roofline_l2 = {"bound": "l2", "kernel": dominant, "achieved": round(ach_impl, 1),
+                           "peak": round(l2_bw, 1), "unit": "GB/s", "frac": round(ach_impl / l2_bw, 4),
+                           "implementation_bytes_per_site": impl_bytes_per_site,
+                           "peak_source": "measured in this run: 256-bit read stream over a 48 MB buffer",
+                           "hbm_read_measured": round(hbm_bw, 1)}
+        except Exception as ex:  # reported, never fatal
+            roofline_l2 = {"error": str(ex)}
 
     # --- e2e through the public API with host buffers ---
     e2e = None
@@ -411,7 +429,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (gen_lda process, numpy; device prior_init)" if model == "lda" else "synthetic",
            "config": {**config, "l2": "flushed before every timed sweep (256 MiB write)"},
-           "roofline": roofline, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
+           "roofline": roofline, "roofline_l2": roofline_l2, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
            "e2e": e2e, "gpu_launches": per_sweep_kernels * args.steps,
            "clocks": clk.summary(), "wall_s_timed": wall, "setup_s": setup_s, "last_log_joint": lj_last}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

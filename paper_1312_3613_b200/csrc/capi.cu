@@ -17,6 +17,7 @@ namespace bnmc_gpu {
 void probe_rng(const std::uint64_t*, std::int64_t, std::int64_t, std::uint64_t*, double*, double*);
 void probe_gamma(const std::uint64_t*, const double*, std::int64_t, double*, std::uint64_t*);
 void probe_log_weights(const std::uint64_t*, const double*, std::int64_t, std::int64_t, std::int64_t*);
+double probe_read_bandwidth(std::size_t, int);
 void dirichlet_batch(std::int64_t, std::int64_t, const double*, std::uint64_t, double*);
 double lpp(const double*, const double*, std::int64_t, std::int64_t, const std::int64_t*,
            const std::int64_t*, std::int64_t);
@@ -522,6 +523,11 @@ int bnmc_gpu_probe_rng(const std::uint64_t* keys, std::int64_t n, std::int64_t p
 int bnmc_gpu_probe_gamma(const std::uint64_t* keys, const double* shapes, std::int64_t n, double* out,
                          std::uint64_t* counters) {
   return guarded(nullptr, [&] { probe_gamma(keys, shapes, n, out, counters); });
+}
+
+int bnmc_gpu_probe_read_bandwidth(int64_t bytes, int32_t reps, double* gbps) {
+  if (bytes <= 0 || reps <= 0 || !gbps) return fail(nullptr, BNMC_GPU_ERR_ARG, "bad probe arguments");
+  return guarded(nullptr, [&] { *gbps = probe_read_bandwidth(static_cast<std::size_t>(bytes), reps); });
 }
 
 int bnmc_gpu_probe_log_weights(const std::uint64_t* keys, const double* logw, std::int64_t rows,

@@ -216,4 +216,41 @@ double lpp(const double* phi, const double* theta, std::int64_t K, std::int64_t 
   return total;
 }
 
+// Read-bandwidth probe (bench.py's secondary roofline): every thread streams 256-bit
+// loads over a `bytes` buffer, `reps` passes, fixed grid (148 x 8 x 256 threads).
+// A buffer well inside the 126 MB L2 measures L2 -> SM read bandwidth; a multi-GB
+// buffer measures HBM.  Returns GB/s of the timed passes (after one warm pass).
+__global__ void read_bw_kernel(const double4* p, std::size_t n, double* sink) {
+  double acc = 0.0;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p + i));
+    acc += (v.x + v.y) + (v.z + v.w);
+  }
+  if (acc == 12345.678) *sink = acc;  // keeps the loads alive
+}
+
+double probe_read_bandwidth(std::size_t bytes, int reps) {
+  const std::size_t n = std::max<std::size_t>(bytes / sizeof(double4), 1);
+  DevBuf<double4> buf;
+  DevBuf<double> sink;
+  buf.alloc(n);
+  sink.alloc(1);
+  buf.zero(nullptr);
+  cudaEvent_t e0, e1;
+  BNMC_CUDA(cudaEventCreate(&e0));
+  BNMC_CUDA(cudaEventCreate(&e1));
+  read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, sink.p);
+  BNMC_CUDA(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, sink.p);
+  BNMC_CUDA(cudaEventRecord(e1));
+  BNMC_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  BNMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return static_cast<double>(n) * sizeof(double4) * reps / (ms * 1e-3) / 1e9;
+}
+
 }  // namespace bnmc_gpu

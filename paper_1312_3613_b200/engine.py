@@ -103,6 +103,7 @@ def lib():
                                      POINTER(c_double)]
     L.bnmc_gpu_probe_gamma.argtypes = [POINTER(c_uint64), POINTER(c_double), c_int64, POINTER(c_double),
                                        POINTER(c_uint64)]
+    L.bnmc_gpu_probe_read_bandwidth.argtypes = [c_int64, c_int32, POINTER(c_double)]
     L.bnmc_gpu_probe_log_weights.argtypes = [POINTER(c_uint64), POINTER(c_double), c_int64, c_int64,
                                              POINTER(c_int64)]
     if L.bnmc_gpu_abi_version() != ABI_VERSION:
@@ -226,6 +227,13 @@ class ParamStore:
         st = _Store(n, real, ival, lens, obs)
         st._keep = (real, ival, lens, obs)
         return st
+
+
+def read_bandwidth(nbytes: int, reps: int = 20) -> float:
+    """Device read bandwidth in GB/s over an `nbytes` buffer (bnmc_gpu_probe_read_bandwidth)."""
+    out = c_double()
+    _raise(lib().bnmc_gpu_probe_read_bandwidth(int(nbytes), int(reps), ctypes.byref(out)))
+    return out.value
 
 
 def nccl_unique_id() -> bytes:
