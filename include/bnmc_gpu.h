@@ -44,7 +44,11 @@ typedef enum {
   BNMC_GPU_LDA = 1,       /* proj/models/lda.bn, Gibbs: blocks phi, theta, z */
   BNMC_GPU_GMM = 2,       /* proj/models/gmm.bn, Gibbs: blocks pi, mu, sigma2, z */
   BNMC_GPU_MH_LINREG = 3, /* proj/models/regression.bn, method MH (one block w, b, tau) */
-  BNMC_GPU_MH_LOGREG = 4  /* logistic twin of regression.bn (no reference model) */
+  BNMC_GPU_MH_LOGREG = 4, /* logistic twin of regression.bn (no reference model) */
+  BNMC_GPU_CATMIX = 5,    /* proj/models/catmix.bn, Gibbs: theta, phi, z.  K, V, N */
+  BNMC_GPU_NAIVEBAYES = 6,/* proj/models/naivebayes.bn, Gibbs: pC, pF (c, f observed).  K, N */
+  BNMC_GPU_HMM = 7,       /* proj/models/hmm.bn, Gibbs: T, bias, s (sequential scan).  K = S states, N */
+  BNMC_GPU_MH_POLYREG = 8 /* proj/models/polyreg.bn, method MH (one block w, bias).  K = M order, N */
 } bnmc_gpu_kind;
 
 typedef enum {
@@ -80,7 +84,8 @@ typedef struct bnmc_gpu_desc {
   double hyper[8];
   /* Reference variable ids (declaration order; they are RNG key components):
    * LDA {phi, theta, z, w}; GMM {pi, mu, sigma2, z, x}; LINREG {w, b, tau, x, y};
-   * LOGREG {w, b, x, y}. */
+   * LOGREG {w, b, x, y}; CATMIX {theta, phi, z, x}; NAIVEBAYES {pC, c, pF, f};
+   * HMM {T, bias, s, flips}; POLYREG {w, bias, x, y}. */
   int32_t var_ids[8];
   double mh_scale;      /* RunConfig::mh_scale (PlanConfig, plan.hpp:31-33) */
   int32_t rank;         /* this process's shard (documents / rows) */

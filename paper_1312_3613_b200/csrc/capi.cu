@@ -230,7 +230,11 @@ int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
       case BNMC_GPU_LDA: c->model = make_lda(*desc, c->comm, o); break;
       case BNMC_GPU_GMM: c->model = make_gmm(*desc, c->comm, o); break;
       case BNMC_GPU_MH_LINREG:
-      case BNMC_GPU_MH_LOGREG: c->model = make_mh(*desc, c->comm, o); break;
+      case BNMC_GPU_MH_LOGREG:
+      case BNMC_GPU_MH_POLYREG: c->model = make_mh(*desc, c->comm, o); break;
+      case BNMC_GPU_CATMIX:
+      case BNMC_GPU_NAIVEBAYES:
+      case BNMC_GPU_HMM: c->model = make_zoo(*desc, c->comm, o); break;
       default: throw Error(BNMC_GPU_ERR_ARG, "unknown model kind");
     }
     BNMC_CUDA(cudaStreamSynchronize(c->stream));

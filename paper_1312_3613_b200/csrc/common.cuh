@@ -153,6 +153,7 @@ struct Comm {
 std::unique_ptr<Model> make_lda(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
 std::unique_ptr<Model> make_gmm(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
 std::unique_ptr<Model> make_mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
+std::unique_ptr<Model> make_zoo(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
 
 // Balanced-token document partition (shared by the C-ABI and the models).
 void partition_docs(const std::int64_t* off, std::int64_t M, int world, int rank, std::int64_t* b,

@@ -40,6 +40,9 @@ struct MhArgs {
   std::uint64_t seed;
   int var_w, var_b, var_tau;
   int logistic;
+  int notau;        // logistic or polyreg: no tau variable (polyreg: y ~ N(mean, 1.0))
+  const double* xr; // fx factor input: raw x (polyreg: N scalars) or the feature matrix
+  std::int64_t nfx; // its length
 };
 
 __device__ __forceinline__ double softplus(double s) {
@@ -57,7 +60,7 @@ __global__ void propose_kernel(MhArgs a, const std::int64_t* iter_p) {
     } else if (t == a.K) {
       Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(a.var_b), 0, static_cast<std::uint64_t>(iter)));
       v += a.mh_scale * r.next_gaussian();
-    } else if (!a.logistic) {
+    } else if (!a.notau) {
       Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(a.var_tau), 0, static_cast<std::uint64_t>(iter)));
       v += a.mh_scale * r.next_gaussian();
     }
@@ -161,10 +164,10 @@ __global__ void fx_kernel(MhArgs a, double* part) {
   __shared__ double scratch[32];
   double acc = 0.0;
   const double c = -log(a.hi - a.lo);
-  const std::int64_t n = a.N * a.K;
+  const std::int64_t n = a.nfx;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-    const double v = a.x[i];
+    const double v = a.xr[i];
     acc += (!(a.hi > a.lo) || v < a.lo || v > a.hi) ? -INFINITY : c;
   }
   acc = block_sum(acc, scratch);
@@ -176,8 +179,8 @@ __device__ double priors(const MhArgs& a, const double* p, double* fw, double* f
   for (int j = 0; j < a.K; ++j) s += log_pdf_gaussian(p[j], 0.0, a.w_var);
   *fw = s;
   *fb = log_pdf_gaussian(p[a.K], 0.0, a.b_var);
-  *ftau = a.logistic ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
-  return a.logistic ? (*fw + *fb) : ((*fw + *fb) + *ftau);
+  *ftau = a.notau ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
+  return a.notau ? (*fw + *fb) : ((*fw + *fb) + *ftau);
 }
 
 __device__ double sum_parts(const double* part, int n, double* scratch) {
@@ -208,7 +211,7 @@ __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_t
       double fw, fb, ft;
       const double pr = priors(a, a.wp, &fw, &fb, &ft);
       const double after = pr + lik_all;
-      const double before = a.logistic ? ((a.state[1] + a.state[2]) + a.state[0])
+      const double before = a.notau ? ((a.state[1] + a.state[2]) + a.state[0])
                                        : (((a.state[1] + a.state[2]) + a.state[3]) + a.state[0]);
       const double delta = after - before;
       Stream acc(keyed(a.seed, kAccept, static_cast<std::uint64_t>(a.var_w), static_cast<std::uint64_t>(it)));
@@ -221,7 +224,7 @@ __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_t
       }
     }
     take_s = take;
-    const double lj = a.logistic ? (((a.state[1] + a.state[2]) + fx) + a.state[0])
+    const double lj = a.notau ? (((a.state[1] + a.state[2]) + fx) + a.state[0])
                                  : ((((a.state[1] + a.state[2]) + a.state[3]) + fx) + a.state[0]);
     o.lj[it & (kRing - 1)] = lj;
     o.acc[it & (kRing - 1)] = take;
@@ -249,8 +252,8 @@ __global__ void prior_kernel(MhArgs a, std::uint64_t seed) {
       Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_b), 0));
       a.w[t] = 0.0 + sqrt(a.b_var) * r.next_gaussian();
     } else {
-      if (a.logistic) {
-        a.w[t] = 0.0;
+      if (a.notau) {
+        a.w[t] = a.logistic ? 0.0 : 1.0;  // polyreg: the fixed unit variance of y
       } else {
         Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_tau), 0));
         a.w[t] = a.tau_b / draw_gamma(r, a.tau_a);
@@ -265,11 +268,23 @@ __global__ void sum_to_kernel(const double* part, int n, double* out) {
   if (threadIdx.x == 0) *out = s;
 }
 
+// polyreg.bn's design matrix: X[i][j] = pow(x_i, j + 1), the terms of the mean
+// sum(j in 1..M, w(j) * pow(x(i), j + 1)) (models/polyreg.bn).
+__global__ void poly_features_kernel(const double* x, double* X, std::int64_t n, int K) {
+  for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < n * K;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t i = e / K;
+    const int j = static_cast<int>(e - i * K);
+    X[e] = pow(x[i], static_cast<double>(j + 1));
+  }
+}
+
 class Mh final : public Model {
  public:
   Mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o) : comm_(c) {
     out = o;
     logistic_ = d.kind == BNMC_GPU_MH_LOGREG;
+    poly_ = d.kind == BNMC_GPU_MH_POLYREG;
     require(d.K >= 1 && d.N >= 0, BNMC_GPU_ERR_ARG, "MH needs K >= 1 features");
     K_ = static_cast<int>(d.K);
     N_ = d.N;
@@ -279,14 +294,19 @@ class Mh final : public Model {
     const double* h = d.hyper;
     lo_ = h[0];
     hi_ = h[1];
-    w_var_ = h[2] > 0 ? h[2] : 10.0;
-    b_var_ = h[3] > 0 ? h[3] : 10.0;
+    w_var_ = h[2] > 0 ? h[2] : (poly_ ? 1.0 : 10.0);
+    b_var_ = h[3] > 0 ? h[3] : (poly_ ? 1.0 : 10.0);
+    if (poly_ && !(hi_ > lo_)) {
+      lo_ = 0.0;  // x ~ Uniform(0.0, 2.0) (models/polyreg.bn)
+      hi_ = 2.0;
+    }
     tau_a_ = h[4] > 0 ? h[4] : 3.0;
     tau_b_ = h[5] > 0 ? h[5] : 1.0;
     mh_scale_ = d.mh_scale;
     seed_ = d.seed;
     for (int i = 0; i < 5; ++i) var_[i] = d.var_ids[i];
     x_.alloc(std::max<std::int64_t>(Nl_ * K_, 1));
+    if (poly_) xraw_.alloc(std::max<std::int64_t>(Nl_, 1));
     y_.alloc(std::max<std::int64_t>(Nl_, 1));
     w_.alloc(K_ + 2);
     wp_.alloc(K_ + 2);
@@ -306,18 +326,24 @@ class Mh final : public Model {
 
   void upload_impl(const bnmc_gpu_store& s, cudaStream_t st, bool with_data) {
     const int vw = var_[0], vb = var_[1];
-    const int vtau = logistic_ ? -1 : var_[2];
-    const int vx = logistic_ ? var_[2] : var_[3], vy = logistic_ ? var_[3] : var_[4];
-    require(s.len[vw] == K_ && s.len[vb] == 1 && s.len[vx] == N_ * K_ && s.len[vy] == N_ &&
+    const bool notau = logistic_ || poly_;
+    const int vtau = notau ? -1 : var_[2];
+    const int vx = notau ? var_[2] : var_[3], vy = notau ? var_[3] : var_[4];
+    require(s.len[vw] == K_ && s.len[vb] == 1 && s.len[vx] == N_ * (poly_ ? 1 : K_) && s.len[vy] == N_ &&
                 (vtau < 0 || s.len[vtau] == 1),
             BNMC_GPU_ERR_RUNTIME, "MH store arrays have the wrong flat lengths");
     std::vector<double> p(K_ + 2, 0.0);
     for (int j = 0; j < K_; ++j) p[j] = s.real[vw][j];
     p[K_] = s.real[vb][0];
-    p[K_ + 1] = vtau >= 0 ? s.real[vtau][0] : 0.0;
+    p[K_ + 1] = vtau >= 0 ? s.real[vtau][0] : (poly_ ? 1.0 : 0.0);
     BNMC_CUDA(cudaMemcpyAsync(w_.p, p.data(), sizeof(double) * (K_ + 2), cudaMemcpyHostToDevice, st));
     if (Nl_ > 0 && with_data) {
-      BNMC_CUDA(cudaMemcpyAsync(x_.p, s.real[vx] + r0_ * K_, sizeof(double) * Nl_ * K_, cudaMemcpyHostToDevice, st));
+      if (poly_) {
+        BNMC_CUDA(cudaMemcpyAsync(xraw_.p, s.real[vx] + r0_, sizeof(double) * Nl_, cudaMemcpyHostToDevice, st));
+        poly_features_kernel<<<kBlocks, kThreads, 0, st>>>(xraw_.p, x_.p, Nl_, K_);
+      } else {
+        BNMC_CUDA(cudaMemcpyAsync(x_.p, s.real[vx] + r0_ * K_, sizeof(double) * Nl_ * K_, cudaMemcpyHostToDevice, st));
+      }
       BNMC_CUDA(cudaMemcpyAsync(y_.p, s.real[vy] + r0_, sizeof(double) * Nl_, cudaMemcpyHostToDevice, st));
     }
     data_ = true;
@@ -334,7 +360,7 @@ class Mh final : public Model {
     if (!(obs && obs[vw]))
       for (int j = 0; j < K_; ++j) s.real[vw][j] = p[j];
     if (!(obs && obs[vb])) s.real[vb][0] = p[K_];
-    if (!logistic_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
+    if (!logistic_ && !poly_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
   }
 
   std::vector<StateBuf> state_buffers() override {
@@ -437,20 +463,23 @@ class Mh final : public Model {
     a.seed = seed_;
     a.var_w = var_[0];
     a.var_b = var_[1];
-    a.var_tau = logistic_ ? -1 : var_[2];
+    a.var_tau = (logistic_ || poly_) ? -1 : var_[2];
     a.logistic = logistic_ ? 1 : 0;
+    a.notau = (logistic_ || poly_) ? 1 : 0;
+    a.xr = poly_ ? xraw_.p : x_.p;
+    a.nfx = poly_ ? Nl_ : Nl_ * K_;
     return a;
   }
 
   Comm comm_;
   bool data_ = false;
-  bool logistic_ = false;
+  bool logistic_ = false, poly_ = false;
   int K_ = 0;
   std::int64_t N_ = 0, r0_ = 0, r1_ = 0, Nl_ = 0;
   double lo_, hi_, w_var_, b_var_, tau_a_, tau_b_, mh_scale_;
   std::uint64_t seed_ = 0;
   int var_[5] = {0, 1, 2, 3, 4};
-  DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_;
+  DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_, xraw_;
 };
 
 }  // namespace

@@ -27,7 +27,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BNMC_GPU_LIB") or os.path.join(HERE, "libbnmc_gpu.so")
 ABI_VERSION = 1
 
-LDA, GMM, MH_LINREG, MH_LOGREG = 1, 2, 3, 4
+LDA, GMM, MH_LINREG, MH_LOGREG, CATMIX, NAIVEBAYES, HMM, MH_POLYREG = 1, 2, 3, 4, 5, 6, 7, 8
 OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH = 1, 2, 4
 
 
@@ -140,6 +140,14 @@ MODELS = {
     "regression": dict(kind=MH_LINREG, method="mh", vars=["w", "b", "tau", "x", "y"], ints=set(),
                        observed={"x", "y"}),
     "logreg": dict(kind=MH_LOGREG, method="mh", vars=["w", "b", "x", "y"], ints=set(), observed={"x", "y"}),
+    # the rest of the reference zoo
+    "catmix": dict(kind=CATMIX, method="gibbs", vars=["theta", "phi", "z", "x"], ints={"z", "x"},
+                   observed={"x"}),
+    "naivebayes": dict(kind=NAIVEBAYES, method="gibbs", vars=["pC", "c", "pF", "f"], ints={"c", "f"},
+                       observed={"c", "f"}),
+    "hmm": dict(kind=HMM, method="gibbs", vars=["T", "bias", "s", "flips"], ints={"s", "flips"},
+                observed={"flips"}),
+    "polyreg": dict(kind=MH_POLYREG, method="mh", vars=["w", "bias", "x", "y"], ints=set(), observed={"x", "y"}),
 }
 
 
@@ -168,6 +176,18 @@ def layout_lengths(model: str, hyper: dict) -> dict:
     if model == "gmm":
         N, K = int(hyper["N"]), int(hyper["K"])
         return {"pi": K, "mu": K, "sigma2": K, "z": N, "x": N}
+    if model == "catmix":
+        N, K, V = int(hyper["N"]), int(hyper["K"]), int(hyper["V"])
+        return {"theta": K * V, "phi": K, "z": N, "x": N}
+    if model == "naivebayes":
+        N, K = int(hyper["N"]), int(hyper["K"])
+        return {"pC": 1, "c": N, "pF": 2 * K, "f": N * K}
+    if model == "hmm":
+        N, S = int(hyper["N"]), int(hyper["S"])
+        return {"T": S * S, "bias": S, "s": N, "flips": N}
+    if model == "polyreg":
+        N, M = int(hyper["N"]), int(hyper["M"])
+        return {"w": M, "bias": 1, "x": N, "y": N}
     if model in ("regression", "logreg"):
         N, K = int(hyper["N"]), int(hyper["K"])
         d = {"w": K, "b": 1, "x": N * K, "y": N}
@@ -299,6 +319,18 @@ class Engine:
             for i, v in enumerate([hyper.get("alpha", 0.1), hyper.get("mu0", 0.0), hyper.get("v0", 10.0),
                                    hyper.get("a0", 1.0), hyper.get("b0", 1.0)]):
                 d.hyper[i] = float(v)
+        elif model == "catmix":
+            d.K, d.V, d.N = int(hyper["K"]), int(hyper["V"]), int(hyper["N"])
+            d.hyper[0], d.hyper[1] = float(hyper.get("alpha", 0.5)), float(hyper.get("beta", 0.5))
+        elif model == "naivebayes":
+            d.K, d.N = int(hyper["K"]), int(hyper["N"])
+        elif model == "hmm":
+            d.K, d.N = int(hyper["S"]), int(hyper["N"])
+            d.hyper[0] = float(hyper.get("v", 0.1))
+        elif model == "polyreg":
+            d.K, d.N = int(hyper["M"]), int(hyper["N"])
+            for i, v in enumerate([0.0, 2.0, 1.0, 1.0]):
+                d.hyper[i] = v
         else:
             d.K, d.N = int(hyper["K"]), int(hyper["N"])
             for i, v in enumerate([hyper.get("l", -1.0), hyper.get("u", 1.0), hyper.get("w_var", 10.0),

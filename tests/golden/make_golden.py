@@ -131,6 +131,45 @@ def mh_fixture(F: Reference, name, N, K, seed, steps):
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 
+def zoo_fixture(F: Reference, name, model, hyper, data, seed, sweeps, method="gibbs", mh_scale=0.5):
+    """catmix / naivebayes / hmm / polyreg: observed data from numpy,
+    the reference's prior_init, then `sweeps` reference sweeps (state + log-joint each)."""
+    e = F.open(model, hyper, method=method, seed=seed, mh_scale=mh_scale)
+    for k, v in data.items():
+        e.set(k, v)
+    e.prior_init(seed)
+    import paper_1312_3613_b200.engine as eng  # names only (no device): variable order
+    names = eng.MODELS[model]["vars"]
+    latent = [n for n in names if n not in eng.MODELS[model]["observed"]]
+    out = dict(seed=seed, hyper=np.array(repr(hyper)), mh_scale=mh_scale, lj0=e.log_joint(),
+               **{f"data_{k}": v for k, v in data.items()}, **{f"{n}0": e.get(n) for n in latent})
+    hist = {n: [] for n in latent}
+    ljs, accs = [], []
+    for it in range(sweeps):
+        lj, a = e.sweep(it)
+        for n in latent:
+            hist[n].append(e.get(n))
+        ljs.append(lj)
+        accs.append(a)
+    out.update({n: np.stack(v) for n, v in hist.items()})
+    out.update(lj=np.array(ljs), accepted=np.array(accs))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
+def zoo(F: Reference):
+    rs = np.random.default_rng(99)
+    zoo_fixture(F, "catmix_small", "catmix", {"N": 500, "K": 4, "V": 12},
+                {"x": rs.integers(0, 12, 500)}, seed=31, sweeps=4)
+    zoo_fixture(F, "naivebayes_small", "naivebayes", {"N": 400, "K": 6},
+                {"c": rs.integers(0, 2, 400), "f": (rs.random(2400) < 0.3).astype(np.int64)}, seed=37, sweeps=4)
+    flips = (rs.random(300) < np.repeat([0.2, 0.8, 0.5], 100)).astype(np.int64)
+    zoo_fixture(F, "hmm_small", "hmm", {"N": 300, "S": 3}, {"flips": flips}, seed=41, sweeps=4)
+    x = rs.uniform(0.0, 2.0, 800)
+    y = 0.5 + 0.3 * x - 0.7 * x ** 2 + 0.2 * x ** 3 + rs.normal(size=800)
+    zoo_fixture(F, "polyreg_small", "polyreg", {"N": 800, "M": 3}, {"x": x, "y": y}, seed=43, sweeps=12,
+                method="mh", mh_scale=0.05)
+
+
 def describe(F: Reference):
     # Block order of the LDA plan (phi, theta, z) as the reference reports it.
     with open(os.path.join(HERE, "describe_lda.txt"), "w") as f:
@@ -145,6 +184,7 @@ if __name__ == "__main__":
     lda_fixture(F, "lda_k1", M=5, V=30, K=1, L=12, seed=5, sweeps=2)
     gmm_fixture(F, "gmm_small", N=3000, seed=17, sweeps=5)
     mh_fixture(F, "mh_linreg", N=1500, K=16, seed=23, steps=12)
+    zoo(F)
     describe(F)
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -396,3 +396,57 @@ def test_run_trace_matches_stepwise(g, model):
         assert np.array_equal(tr["map_state"][x], map_state[x]), x
         assert np.array_equal(s1[x], s2[x]), x  # the store holds the final state
     assert len(tr["timing_ms"]) == n and all(t > 0 for t in tr["timing_ms"])
+
+
+# ----------------------------------------------------------------------------------------
+# the rest of the zoo: catmix, naivebayes, hmm (sequential scan), polyreg MH
+# ----------------------------------------------------------------------------------------
+ZOO = [("catmix_small", "catmix"), ("naivebayes_small", "naivebayes"), ("hmm_small", "hmm"),
+       ("polyreg_small", "polyreg")]
+
+
+def _zoo_engine(g, fx, model):
+    import ast
+    hyper = ast.literal_eval(str(fx["hyper"]))
+    cfg = g.RunConfig(seed=int(fx["seed"]), mh_scale=float(fx["mh_scale"]))
+    e = g.Engine(model, hyper, cfg)
+    s = e.allocate()
+    for k in fx.files:
+        if k.startswith("data_"):
+            s[k[5:]] = fx[k]
+    latent = [n for n in s.names if not s.observed[n]]
+    return e, s, latent
+
+
+@pytest.mark.parametrize("name,model", ZOO)
+def test_zoo_prior_init_matches_reference(g, name, model):
+    fx = golden(name)
+    e, s, latent = _zoo_engine(g, fx, model)
+    e.prior_init(s, int(fx["seed"]))
+    for n in latent:
+        if s[n].dtype == np.int64:
+            assert np.array_equal(s[n], fx[n + "0"]), n
+        else:
+            assert rel(s[n], fx[n + "0"]) < RTOL_PARAM, n
+    e.close()
+
+
+@pytest.mark.parametrize("name,model", ZOO)
+def test_zoo_sweeps_vs_reference(g, name, model):
+    fx = golden(name)
+    e, s, latent = _zoo_engine(g, fx, model)
+    for n in latent:
+        s[n] = fx[n + "0"]
+    assert abs(e.eval_log_joint(s) - fx["lj0"]) <= RTOL_LJ * abs(fx["lj0"])
+    for it in range(len(fx["lj"])):
+        acc = []
+        lj = e.sweep(s, it, acc)
+        if model == "polyreg":
+            assert acc[0] == bool(fx["accepted"][it]), f"accept decision differs at step {it}"
+        for n in latent:
+            if s[n].dtype == np.int64:
+                assert np.array_equal(s[n], fx[n][it]), f"{n} differs at sweep {it}: {(s[n] != fx[n][it]).sum()}"
+            else:
+                assert rel(s[n], fx[n][it]) < RTOL_PARAM, (n, it, rel(s[n], fx[n][it]))
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it]), (it, lj, fx["lj"][it])
+    e.close()

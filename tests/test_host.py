@@ -54,7 +54,9 @@ def test_unsupported_model_rejected():
     import paper_1312_3613_b200 as g
 
     with pytest.raises(ValueError):
-        g.Engine("hmm", {})
+        g.Engine("nosuchmodel", {})
+    with pytest.raises(ValueError):
+        g.Engine("hmm", {"N": 4, "S": 2}, g.RunConfig(method="mh"))  # hmm.bn's plan is Gibbs
     with pytest.raises(ValueError):
         g.Engine("lda", {"K": 2, "V": 3, "M": 1, "N": [2]}, g.RunConfig(method="mh"))
 
