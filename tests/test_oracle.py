@@ -185,3 +185,31 @@ def test_observed_phi_protocol(restatement, reference):
         lj2 = restatement.lda_sweep(K, V, off, w, z, phi, theta, 5, it, observe_phi=True)
         assert lj == lj2 and np.array_equal(e.get("z"), z)
         assert np.array_equal(e.get("phi"), true_phi) and np.array_equal(phi, true_phi)
+
+
+@pytest.mark.parametrize("name,model,method", [("catmix_small", "catmix", "gibbs"),
+                                               ("naivebayes_small", "naivebayes", "gibbs"),
+                                               ("hmm_small", "hmm", "gibbs"),
+                                               ("polyreg_small", "polyreg", "mh")])
+def test_zoo_goldens_vs_live_reference(reference, name, model, method):
+    """The zoo fixtures (tests/golden/make_golden.py) are outputs of the compiled
+    reference: re-run its prior_init and two sweeps and compare bitwise."""
+    import ast
+
+    import numpy as np
+
+    fx = golden(name)
+    hyper = ast.literal_eval(str(fx["hyper"]))
+    e = reference.open(model, hyper, method=method, seed=int(fx["seed"]), mh_scale=float(fx["mh_scale"]))
+    for k in fx.files:
+        if k.startswith("data_"):
+            e.set(k[5:], fx[k])
+    e.prior_init(int(fx["seed"]))
+    latent = [k[:-1] for k in fx.files if k.endswith("0") and k[:-1] in fx.files and k != "lj0"]
+    for n in latent:
+        assert np.array_equal(e.get(n), fx[n + "0"]), n
+    for it in range(2):
+        lj, acc = e.sweep(it)
+        assert lj == fx["lj"][it] and acc == bool(fx["accepted"][it])
+        for n in latent:
+            assert np.array_equal(e.get(n), fx[n][it]), (n, it)
