@@ -55,7 +55,12 @@ typedef enum {
   BNMC_GPU_OBSERVE_PHI = 1u << 0,    /* LDA: phi clamped (RunConfig::observe_extra = {"phi"}) */
   BNMC_GPU_EXACT_WEIGHTS = 1u << 1,  /* LDA: log-space weights exactly as the reference
                                         (default: product-form theta*phi, same draws) */
-  BNMC_GPU_NO_GRAPH = 1u << 2        /* launch kernels directly instead of a CUDA graph */
+  BNMC_GPU_NO_GRAPH = 1u << 2,       /* launch kernels directly instead of a CUDA graph */
+  BNMC_GPU_GIBBS = 1u << 3,          /* regression / polyreg: Method::Gibbs plan -- one MH
+                                        block per non-conjugate variable (w, b), conjugate
+                                        tau (plan.cpp:139-164) -- instead of one MH block */
+  BNMC_GPU_MWG = 1u << 4             /* regression / polyreg: Method::MWG plan -- single-site
+                                        blocks per element (run_mwg_block, sampler.cpp:342-388) */
 } bnmc_gpu_flag;
 
 typedef enum {

@@ -190,7 +190,8 @@ __device__ double sum_parts(const double* part, int n, double* scratch) {
 }
 
 // mode 0: initialise the cache from the current state (no step);
-// mode 1: MH step; mode 2: log-joint of the current state only.
+// mode 1: MH step; mode 2: log-joint of the current state only;
+// mode 3: as 0, and advance the iteration (end of a Gibbs / MWG sweep).
 __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_total) {
   __shared__ double scratch[32];
   __shared__ int take_s;
@@ -200,7 +201,7 @@ __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_t
     const std::int64_t it = *o.iter;
     const double lik_all = lik_total ? *lik_total : lik;
     int take = 0;
-    if (mode == 0) {
+    if (mode == 0 || mode == 3) {
       double fw, fb, ft;
       priors(a, a.w, &fw, &fb, &ft);
       a.state[0] = lik_all;
@@ -227,8 +228,8 @@ __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_t
     const double lj = a.notau ? (((a.state[1] + a.state[2]) + fx) + a.state[0])
                                  : ((((a.state[1] + a.state[2]) + a.state[3]) + fx) + a.state[0]);
     o.lj[it & (kRing - 1)] = lj;
-    o.acc[it & (kRing - 1)] = take;
-    if (mode == 1) *o.iter = it + 1;
+    o.acc[it & (kRing - 1)] = mode == 3 ? static_cast<int>(a.state[5]) : take;
+    if (mode == 1 || mode == 3) *o.iter = it + 1;
   }
   __syncthreads();
   if (mode == 1 && take_s)
@@ -268,6 +269,155 @@ __global__ void sum_to_kernel(const double* part, int n, double* out) {
   if (threadIdx.x == 0) *out = s;
 }
 
+// ---------------------------------------------------------------------------------
+// MWG plan of regression.bn / polyreg.bn (RunConfig::method = mwg): w[t] and b are
+// single-site random-walk blocks (run_mwg_block, sampler.cpp:342-388), in declaration
+// order, each element against its own conditional numerator 0 + log p(elem) +
+// sum_i log p(y_i | ...); regression.bn's tau is conjugate (InverseGammaVariance,
+// sampler.cpp:122-130, 206-208).  Element e's proposal cur + mh_scale * N(0,1) and its
+// accept uniform come from ONE stream keyed(seed,1,var,t,iter) (gaussian, then unit).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void mwg_element(const MhArgs& a, int e, int& var, std::uint64_t& t, double& pvar) {
+  if (e < a.K) {
+    var = a.var_w;
+    t = static_cast<std::uint64_t>(e);
+    pvar = a.w_var;
+  } else {
+    var = a.var_b;
+    t = 0;
+    pvar = a.b_var;
+  }
+}
+
+__device__ __forceinline__ double mwg_proposal(const MhArgs& a, int e, std::int64_t iter, Stream& r) {
+  int var;
+  std::uint64_t t;
+  double pvar;
+  mwg_element(a, e, var, t, pvar);
+  r = Stream(keyed(a.seed, kProposal, static_cast<std::uint64_t>(var), t, static_cast<std::uint64_t>(iter)));
+  return a.w[e] + a.mh_scale * r.next_gaussian();
+}
+
+// Per block: sum_i ll(y_i | mean_i) at the current state (part[2b]) and with element e
+// moved to its proposal (part[2b+1]); RSS: sum_i (y_i - mean_i)^2 instead (tau block).
+template <bool RSS>
+__global__ void __launch_bounds__(kThreads) mwg_lik_kernel(MhArgs a, const std::int64_t* iter_p, int e, double* part) {
+  __shared__ double scratch[32];
+  __shared__ double dlt;
+  if (threadIdx.x == 0) {
+    Stream r(0);
+    dlt = RSS ? 0.0 : mwg_proposal(a, e, *iter_p, r) - a.w[e];
+  }
+  __syncthreads();
+  const double b = a.w[a.K], tau = a.w[a.K + 1], d = dlt;
+  const int lane = threadIdx.x & 31;
+  double acc0 = 0.0, acc1 = 0.0;
+  const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (std::int64_t i = warp; i < a.N; i += nwarps) {
+    const double* xi = a.x + i * a.K;
+    double sdot = 0.0;
+    for (int j = lane; j < a.K; j += 32) sdot += a.w[j] * __ldg(xi + j);
+    sdot = warp_sum(sdot);
+    if (lane == 0) {
+      const double m0 = sdot + b, yi = __ldg(a.y + i);
+      if (RSS) {
+        acc0 += (yi - m0) * (yi - m0);
+      } else {
+        const double m1 = e < a.K ? (sdot + d * __ldg(xi + e)) + b : sdot + (b + d);
+        acc0 += row_loglik(a, m0, yi, tau);
+        acc1 += row_loglik(a, m1, yi, tau);
+      }
+    }
+  }
+  acc0 = block_sum(acc0, scratch);
+  acc1 = block_sum(acc1, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = acc0;
+    part[2 * blockIdx.x + 1] = acc1;
+  }
+}
+
+__global__ void mwg_accept_kernel(MhArgs a, const std::int64_t* iter_p, int e, const double* part) {
+  __shared__ double scratch[32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {
+    s0 += part[2 * b];
+    s1 += part[2 * b + 1];
+  }
+  s0 = block_sum(s0, scratch);
+  s1 = block_sum(s1, scratch);
+  if (threadIdx.x == 0) {
+    int var;
+    std::uint64_t t;
+    double pvar;
+    mwg_element(a, e, var, t, pvar);
+    Stream r(0);
+    const double cur = a.w[e];
+    const double prop = mwg_proposal(a, e, *iter_p, r);
+    const double before = (0.0 + log_pdf_gaussian(cur, 0.0, pvar)) + s0;
+    const double after = (0.0 + log_pdf_gaussian(prop, 0.0, pvar)) + s1;
+    if (isfinite(after) && log(r.next_unit()) < after - before) a.w[e] = prop;
+  }
+}
+
+// tau ~ InverseGamma(tau_a + n/2, tau_b + rss/2), stream keyed(seed,4,var_tau,iter).derive(0)
+__global__ void mwg_tau_kernel(MhArgs a, const std::int64_t* iter_p, const double* part) {
+  __shared__ double scratch[32];
+  double rss = 0.0;
+  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) rss += part[2 * b];
+  rss = block_sum(rss, scratch);
+  if (threadIdx.x == 0) {
+    const std::uint64_t key = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_tau),
+                                    static_cast<std::uint64_t>(*iter_p));
+    Stream r(derive(key, 0));
+    const double n = static_cast<double>(a.N);
+    a.w[a.K + 1] = (a.tau_b + 0.5 * rss) / draw_gamma(r, a.tau_a + 0.5 * n);
+  }
+}
+
+// Gibbs plan (Method::Gibbs, plan.cpp:139-164): a non-conjugate real variable is ONE
+// random-walk MH block (run_mh_block, sampler.cpp:284-340) over its elements
+// [e0, e1) of the parameter vector: proposals keyed(seed,1,var,t,iter), blanket = the
+// variable's prior factor + the y factor, accept keyed(seed,2,var,iter).
+__global__ void blk_propose_kernel(MhArgs a, const std::int64_t* iter_p, int e0, int e1, int var) {
+  const std::int64_t iter = *iter_p;
+  for (int e = threadIdx.x; e < a.K + 2; e += blockDim.x) {
+    double v = a.w[e];
+    if (e >= e0 && e < e1) {
+      Stream r(keyed(a.seed, kProposal, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(e - e0),
+                     static_cast<std::uint64_t>(iter)));
+      v += a.mh_scale * r.next_gaussian();
+    }
+    a.wp[e] = v;
+  }
+}
+
+// before = prior(cur) + lik(cur), after = prior(prop) + lik(prop); the prior factor's
+// elements are summed in order (eval_density of the var's factor)
+__global__ void blk_accept_kernel(MhArgs a, const std::int64_t* iter_p, int e0, int e1, int var, double pvar,
+                                  const double* part_cur, const double* part_prop) {
+  __shared__ double scratch[32];
+  __shared__ int take_s;
+  const double l0 = sum_parts(part_cur, kBlocks, scratch);
+  const double l1 = sum_parts(part_prop, kBlocks, scratch);
+  if (threadIdx.x == 0) {
+    double p0 = 0.0, p1 = 0.0;
+    for (int e = e0; e < e1; ++e) {
+      p0 += log_pdf_gaussian(a.w[e], 0.0, pvar);
+      p1 += log_pdf_gaussian(a.wp[e], 0.0, pvar);
+    }
+    const double before = p0 + l0, after = p1 + l1;
+    Stream acc(keyed(a.seed, kAccept, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(*iter_p)));
+    const int take = isfinite(after) && log(acc.next_unit()) < after - before;
+    take_s = take;
+    a.state[5] = take;  // Engine::sweep reports the last MH block's decision
+  }
+  __syncthreads();
+  if (take_s)
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) a.w[e] = a.wp[e];
+}
+
 // polyreg.bn's design matrix: X[i][j] = pow(x_i, j + 1), the terms of the mean
 // sum(j in 1..M, w(j) * pow(x(i), j + 1)) (models/polyreg.bn).
 __global__ void poly_features_kernel(const double* x, double* X, std::int64_t n, int K) {
@@ -285,6 +435,10 @@ class Mh final : public Model {
     out = o;
     logistic_ = d.kind == BNMC_GPU_MH_LOGREG;
     poly_ = d.kind == BNMC_GPU_MH_POLYREG;
+    gibbs_ = (d.flags & BNMC_GPU_GIBBS) != 0;
+    mwg_ = (d.flags & BNMC_GPU_MWG) != 0;
+    require(!(gibbs_ || mwg_) || (!logistic_ && c.world == 1), BNMC_GPU_ERR_ARG,
+            "the Gibbs / MWG plans serve regression.bn / polyreg.bn on one GPU");
     require(d.K >= 1 && d.N >= 0, BNMC_GPU_ERR_ARG, "MH needs K >= 1 features");
     K_ = static_cast<int>(d.K);
     N_ = d.N;
@@ -307,6 +461,7 @@ class Mh final : public Model {
     for (int i = 0; i < 5; ++i) var_[i] = d.var_ids[i];
     x_.alloc(std::max<std::int64_t>(Nl_ * K_, 1));
     if (poly_) xraw_.alloc(std::max<std::int64_t>(Nl_, 1));
+    if (gibbs_ || mwg_) mwg_part_.alloc(2 * kBlocks);
     y_.alloc(std::max<std::int64_t>(Nl_, 1));
     w_.alloc(K_ + 2);
     wp_.alloc(K_ + 2);
@@ -370,6 +525,38 @@ class Mh final : public Model {
   void enqueue_sweep(cudaStream_t st) override {
     MhArgs a = args();
     mark(st, "begin");
+    if (gibbs_ || mwg_) {
+      if (mwg_) {
+        // Method::MWG: single-site blocks w[0..K-1], b in declaration order
+        for (int e = 0; e <= K_; ++e) {
+          mwg_lik_kernel<false><<<kBlocks, kThreads, 0, st>>>(a, out.iter, e, mwg_part_.p);
+          mwg_accept_kernel<<<1, 256, 0, st>>>(a, out.iter, e, mwg_part_.p);
+        }
+        mark(st, "mwg_w_b");
+      } else {
+        // Method::Gibbs: one random-walk MH block per variable, w then b
+        const int ranges[2][3] = {{0, K_, var_[0]}, {K_, K_ + 1, var_[1]}};
+        const double pv[2] = {w_var_, b_var_};
+        for (int bi = 0; bi < 2; ++bi) {
+          blk_propose_kernel<<<1, 128, 0, st>>>(a, out.iter, ranges[bi][0], ranges[bi][1], ranges[bi][2]);
+          launch_lik(a, w_.p, st, mwg_part_.p);
+          launch_lik(a, wp_.p, st, part_.p);
+          blk_accept_kernel<<<1, 256, 0, st>>>(a, out.iter, ranges[bi][0], ranges[bi][1], ranges[bi][2], pv[bi],
+                                               mwg_part_.p, part_.p);
+        }
+        mark(st, "mh_w_b");
+      }
+      if (!poly_) {
+        mwg_lik_kernel<true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, 0, mwg_part_.p);
+        mwg_tau_kernel<<<1, 256, 0, st>>>(a, out.iter, mwg_part_.p);
+        mark(st, "tau");
+      }
+      launch_lik(a, w_.p, st);
+      accept_kernel<<<1, 256, 0, st>>>(a, out, 3, nullptr);
+      mark(st, "log_joint");
+      BNMC_CUDA(cudaGetLastError());
+      return;
+    }
     propose_kernel<<<1, 128, 0, st>>>(a, out.iter);
     mark(st, "propose");
     launch_lik(a, wp_.p, st);
@@ -401,19 +588,20 @@ class Mh final : public Model {
 
  private:
 
-  void launch_lik(const MhArgs& a, const double* p, cudaStream_t st) {
+  void launch_lik(const MhArgs& a, const double* p, cudaStream_t st, double* dst = nullptr) {
     const std::size_t sm = sizeof(double) * (K_ + 2);
     const int cpl = (K_ / 4 + kRowGroup - 1) / kRowGroup;
+    double* o = dst ? dst : part_.p;
     if (K_ % 4 == 0 && cpl <= 1)
-      lik_kernel<true, 1><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+      lik_kernel<true, 1><<<kBlocks, kThreads, sm, st>>>(a, p, o);
     else if (K_ % 4 == 0 && cpl <= 2)
-      lik_kernel<true, 2><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+      lik_kernel<true, 2><<<kBlocks, kThreads, sm, st>>>(a, p, o);
     else if (K_ % 4 == 0 && cpl <= 4)
-      lik_kernel<true, 4><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+      lik_kernel<true, 4><<<kBlocks, kThreads, sm, st>>>(a, p, o);
     else if (K_ % 4 == 0 && cpl <= kMaxChunks)
-      lik_kernel<true, 8><<<kBlocks, kThreads, sm, st>>>(a, p, part_.p);
+      lik_kernel<true, 8><<<kBlocks, kThreads, sm, st>>>(a, p, o);
     else
-      lik_kernel<false><<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, p, part_.p);
+      lik_kernel<false><<<kBlocks, kThreads, sizeof(double) * (K_ + 2), st>>>(a, p, o);
   }
 
   void accept_kernel_cached(const MhArgs& a, cudaStream_t st) {
@@ -473,13 +661,13 @@ class Mh final : public Model {
 
   Comm comm_;
   bool data_ = false;
-  bool logistic_ = false, poly_ = false;
+  bool logistic_ = false, poly_ = false, gibbs_ = false, mwg_ = false;
   int K_ = 0;
   std::int64_t N_ = 0, r0_ = 0, r1_ = 0, Nl_ = 0;
   double lo_, hi_, w_var_, b_var_, tau_a_, tau_b_, mh_scale_;
   std::uint64_t seed_ = 0;
   int var_[5] = {0, 1, 2, 3, 4};
-  DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_, xraw_;
+  DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_, xraw_, mwg_part_;
 };
 
 }  // namespace

@@ -28,7 +28,7 @@ LIB_PATH = os.environ.get("BNMC_GPU_LIB") or os.path.join(HERE, "libbnmc_gpu.so"
 ABI_VERSION = 1
 
 LDA, GMM, MH_LINREG, MH_LOGREG, CATMIX, NAIVEBAYES, HMM, MH_POLYREG = 1, 2, 3, 4, 5, 6, 7, 8
-OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH = 1, 2, 4
+OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH, GIBBS, MWG = 1, 2, 4, 8, 16
 
 
 class BnmcError(RuntimeError):
@@ -281,8 +281,12 @@ class Engine:
         self.cfg = cfg or RunConfig()
         spec = MODELS[model]
         method = self.cfg.method or spec["method"]
-        if method != spec["method"]:
-            raise ValueError(f"the GPU path runs {model} with method '{spec['method']}', not '{method}'")
+        # regression.bn / polyreg.bn also run their Gibbs plan (an MH block per variable,
+        # conjugate tau) and their MWG plan (single-site blocks): BNMC_GPU_GIBBS / _MWG
+        methods = {spec["method"], "gibbs", "mwg"} if model in ("regression", "polyreg") else {spec["method"]}
+        if method not in methods:
+            raise ValueError(f"the GPU path runs {model} with method {sorted(methods)}, not '{method}'")
+        self.method = method
         self.spec = spec
         L = lib()
         d = _Desc()
@@ -301,6 +305,10 @@ class Engine:
             flags |= EXACT_WEIGHTS
         if not self.cfg.use_graph:
             flags |= NO_GRAPH
+        if method == "gibbs" and spec["method"] == "mh":
+            flags |= GIBBS
+        if method == "mwg":
+            flags |= MWG
         d.flags = flags
         self._offsets = None
         if model == "lda":
@@ -482,12 +490,12 @@ class Engine:
         tr = _Trace(cfg.burnin, n, cfg.thin, _p(lj, c_double), _p(tm, c_double), _p(acc, c_int),
                     ctypes.cast(views, POINTER(_Store)), ctypes.pointer(mv), ctypes.pointer(map_lj))
         _raise(lib().bnmc_gpu_run_trace(self._h, 0, ctypes.byref(tr)), self._h)
-        trace = dict(model=self.model, method=self.spec["method"], seed=cfg.seed, var_names=unobs,
+        trace = dict(model=self.model, method=self.method, seed=cfg.seed, var_names=unobs,
                      samples=[{v: smp[v].copy() for v in unobs} for smp in samples],
                      log_joint=lj[:n].tolist(), timing_ms=tm[:n].tolist(),
                      map_state={v: map_store[v].copy() for v in unobs} if n > 0 else {},
                      map_log_joint=map_lj.value)
-        if self.spec["method"] == "mh":
+        if self.method != "gibbs" or self.spec["method"] == "mh":
             trace["accepted"] = acc[:n].astype(bool).tolist()
         self.download(store)
         return trace

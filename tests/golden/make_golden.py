@@ -141,7 +141,7 @@ def zoo_fixture(F: Reference, name, model, hyper, data, seed, sweeps, method="gi
     import paper_1312_3613_b200.engine as eng  # names only (no device): variable order
     names = eng.MODELS[model]["vars"]
     latent = [n for n in names if n not in eng.MODELS[model]["observed"]]
-    out = dict(seed=seed, hyper=np.array(repr(hyper)), mh_scale=mh_scale, lj0=e.log_joint(),
+    out = dict(seed=seed, hyper=np.array(repr(hyper)), method=np.array(method), mh_scale=mh_scale, lj0=e.log_joint(),
                **{f"data_{k}": v for k, v in data.items()}, **{f"{n}0": e.get(n) for n in latent})
     hist = {n: [] for n in latent}
     ljs, accs = [], []
@@ -168,6 +168,17 @@ def zoo(F: Reference):
     y = 0.5 + 0.3 * x - 0.7 * x ** 2 + 0.2 * x ** 3 + rs.normal(size=800)
     zoo_fixture(F, "polyreg_small", "polyreg", {"N": 800, "M": 3}, {"x": x, "y": y}, seed=43, sweeps=12,
                 method="mh", mh_scale=0.05)
+    # Gibbs plans of the MH models: single-site MWG for w and b, conjugate tau
+    zoo_fixture(F, "polyreg_gibbs", "polyreg", {"N": 600, "M": 3}, {"x": x[:600], "y": y[:600]}, seed=47,
+                sweeps=6, method="gibbs", mh_scale=0.05)
+    xr = rs.uniform(-1.0, 1.0, (700, 5))
+    yr = xr @ np.array([0.5, -1.0, 0.3, 0.0, 2.0]) + 0.2 + 0.3 * rs.normal(size=700)
+    zoo_fixture(F, "regression_gibbs", "regression", {"K": 5, "N": 700, "l": -1.0, "u": 1.0},
+                {"x": xr.ravel(), "y": yr}, seed=53, sweeps=6, method="gibbs", mh_scale=0.1)
+    zoo_fixture(F, "polyreg_mwg", "polyreg", {"N": 600, "M": 3}, {"x": x[:600], "y": y[:600]}, seed=59,
+                sweeps=4, method="mwg", mh_scale=0.05)
+    zoo_fixture(F, "regression_mwg", "regression", {"K": 5, "N": 700, "l": -1.0, "u": 1.0},
+                {"x": xr.ravel(), "y": yr}, seed=61, sweeps=4, method="mwg", mh_scale=0.1)
 
 
 def describe(F: Reference):

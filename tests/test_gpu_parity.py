@@ -402,13 +402,15 @@ def test_run_trace_matches_stepwise(g, model):
 # the rest of the zoo: catmix, naivebayes, hmm (sequential scan), polyreg MH
 # ----------------------------------------------------------------------------------------
 ZOO = [("catmix_small", "catmix"), ("naivebayes_small", "naivebayes"), ("hmm_small", "hmm"),
-       ("polyreg_small", "polyreg")]
+       ("polyreg_small", "polyreg"), ("polyreg_gibbs", "polyreg"), ("regression_gibbs", "regression"),
+       ("polyreg_mwg", "polyreg"), ("regression_mwg", "regression")]
 
 
 def _zoo_engine(g, fx, model):
     import ast
     hyper = ast.literal_eval(str(fx["hyper"]))
-    cfg = g.RunConfig(seed=int(fx["seed"]), mh_scale=float(fx["mh_scale"]))
+    method = str(fx["method"]) if "method" in fx.files else ""
+    cfg = g.RunConfig(seed=int(fx["seed"]), mh_scale=float(fx["mh_scale"]), method=method)
     e = g.Engine(model, hyper, cfg)
     s = e.allocate()
     for k in fx.files:
@@ -441,7 +443,7 @@ def test_zoo_sweeps_vs_reference(g, name, model):
     for it in range(len(fx["lj"])):
         acc = []
         lj = e.sweep(s, it, acc)
-        if model == "polyreg":
+        if model in ("polyreg", "regression"):  # the (last) MH block's decision
             assert acc[0] == bool(fx["accepted"][it]), f"accept decision differs at step {it}"
         for n in latent:
             if s[n].dtype == np.int64:

@@ -190,7 +190,11 @@ def test_observed_phi_protocol(restatement, reference):
 @pytest.mark.parametrize("name,model,method", [("catmix_small", "catmix", "gibbs"),
                                                ("naivebayes_small", "naivebayes", "gibbs"),
                                                ("hmm_small", "hmm", "gibbs"),
-                                               ("polyreg_small", "polyreg", "mh")])
+                                               ("polyreg_small", "polyreg", "mh"),
+                                               ("polyreg_gibbs", "polyreg", "gibbs"),
+                                               ("regression_gibbs", "regression", "gibbs"),
+                                               ("polyreg_mwg", "polyreg", "mwg"),
+                                               ("regression_mwg", "regression", "mwg")])
 def test_zoo_goldens_vs_live_reference(reference, name, model, method):
     """The zoo fixtures (tests/golden/make_golden.py) are outputs of the compiled
     reference: re-run its prior_init and two sweeps and compare bitwise."""
