@@ -99,27 +99,29 @@ __global__ void draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // pi block: Dirichlet over a single row, cells derive(0, c); left-to-right sum.
-    const std::uint64_t kp = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_pi),
-                                   static_cast<std::uint64_t>(iter));
+  // Independent per-component streams: thread k draws the pi cell's gamma and mu_k (the
+  // draws were serial on one thread: ~2 gamma chains of latency per component).
+  __shared__ double g[kMaxK];
+  const std::uint64_t kp = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_pi),
+                                 static_cast<std::uint64_t>(iter));
+  const std::uint64_t km = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_mu),
+                                 static_cast<std::uint64_t>(iter));
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    // pi block: Dirichlet over a single row, cells derive(0, c)
+    Stream r(derive(kp, 0, static_cast<std::uint64_t>(k)));
+    g[k] = draw_gamma(r, a.alpha + cnt[k]);
+    // mu block
+    Stream q(derive(km, static_cast<std::uint64_t>(k)));
+    const double prec = 1.0 / a.v0 + P[k];
+    const double wsum = a.mu0 / a.v0 + W[k];
+    const double post_var = 1.0 / prec;
+    a.mu[k] = post_var * wsum + sqrt(post_var) * q.next_gaussian();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // left-to-right row sum (batch.cpp:55-58)
     double sum = 0.0;
-    for (int k = 0; k < a.K; ++k) {
-      Stream r(derive(kp, 0, static_cast<std::uint64_t>(k)));
-      a.pi[k] = draw_gamma(r, a.alpha + cnt[k]);
-      sum += a.pi[k];
-    }
-    for (int k = 0; k < a.K; ++k) a.pi[k] /= sum;
-    // mu block.
-    const std::uint64_t km = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_mu),
-                                   static_cast<std::uint64_t>(iter));
-    for (int k = 0; k < a.K; ++k) {
-      Stream r(derive(km, static_cast<std::uint64_t>(k)));
-      const double prec = 1.0 / a.v0 + P[k];
-      const double wsum = a.mu0 / a.v0 + W[k];
-      const double post_var = 1.0 / prec;
-      a.mu[k] = post_var * wsum + sqrt(post_var) * r.next_gaussian();
-    }
+    for (int k = 0; k < a.K; ++k) sum += g[k];
+    for (int k = 0; k < a.K; ++k) a.pi[k] = g[k] / sum;
   }
 }
 
@@ -136,14 +138,12 @@ __global__ void draw_s2_kernel(GmmArgs a, const std::int64_t* iter_p) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const std::uint64_t ks = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_s2),
-                                   static_cast<std::uint64_t>(iter));
-    for (int k = 0; k < a.K; ++k) {
-      Stream r(derive(ks, static_cast<std::uint64_t>(k)));
-      const double scale = a.b0 + 0.5 * rss[k];
-      a.s2[k] = scale / draw_gamma(r, a.a0 + 0.5 * cnt[k]);
-    }
+  const std::uint64_t ks = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_s2),
+                                 static_cast<std::uint64_t>(iter));
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    Stream r(derive(ks, static_cast<std::uint64_t>(k)));
+    const double scale = a.b0 + 0.5 * rss[k];
+    a.s2[k] = scale / draw_gamma(r, a.a0 + 0.5 * cnt[k]);
   }
 }
 
