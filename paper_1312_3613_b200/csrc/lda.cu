@@ -68,6 +68,8 @@ struct LdaArgs {
   const std::int64_t* off;   // local offsets, off[0] = 0
   const std::int64_t* units; // z-step work units: [n_units][3] = doc, t0, t1
   std::int64_t n_units;
+  const std::int64_t* wunits; // warp-level units (<= 256 tokens of one document)
+  std::int64_t n_wunits;
   std::int64_t tok_base, doc_base;
   double* phiT;
   float* phiT32;     // fp32 copy of phiT [V][Kp32], columns permuted by phys32 (screen only)
@@ -1053,30 +1055,44 @@ __device__ __forceinline__ int cs_idx(int row, int c) {
   return row * 16 + ((((c >> 2) ^ (row >> 1)) & 3) << 2) + (c & 3);
 }
 
-template <int R, bool TFR>
+// WU: warp-level work units (chunks of <= 256 tokens of one document, `wunits`): every
+// warp owns its theta operands, chunk-sum table and doc-topic counts in shared memory
+// and never waits on a CTA barrier; short documents (KOS: 136 tokens) no longer leave
+// warps of a document-wide CTA idle, and long ones are split into warp-sized chunks.
+template <int R, bool TFR, bool WU = false>
 __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaArgs a, const std::int64_t* iter_p) {
   constexpr int G = 4, CW = 8, KL = CW * R, KLP = KL + 4, C = G * R;
   static_assert(C <= 16, "csum rows hold 16 chunk sums");
   const int kWarps = blockDim.x >> 5;  // sized to the work units (zscreen_t_launch)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* thf = reinterpret_cast<float*>(smem_raw);  // [G][KLP] theta/S, fp32
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
   const int warp = threadIdx.x >> 5;
-  float* csum = thf + G * KLP + warp * 32 * 16;      // [32][16] chunk sums of the batch (cs_idx)
-  int* cnt_s = reinterpret_cast<int*>(thf + G * KLP + kWarps * 32 * 16);  // [K] this unit's doc-topic counts
+  // CTA units: [thf G*KLP][csum kWarps*32*16][cnt K];  warp units: per warp the same
+  const int kpad = (a.K + 3) & ~3;
+  float* base = reinterpret_cast<float*>(smem_raw) + (WU ? warp * (G * KLP + 32 * 16 + kpad) : 0);
+  float* thf = base;                                  // [G][KLP] theta/S, fp32
+  float* csum = thf + G * KLP + (WU ? 0 : warp * 32 * 16);  // [32][16] chunk sums of the batch (cs_idx)
+  int* cnt_s = reinterpret_cast<int*>(thf + G * KLP + (WU ? 32 * 16 : kWarps * 32 * 16));  // [K] doc-topic counts
   pdl_wait();
   pdl_trigger();
   const std::int64_t iter = *iter_p;
   const int rl = min(R, max(0, (a.K - gl * KL + CW - 1) / CW));
+  const int tid_u = WU ? lane : static_cast<int>(threadIdx.x);      // thread index within the unit's team
+  const int nthr_u = WU ? 32 : static_cast<int>(blockDim.x);
+  const std::int64_t nunits = WU ? a.n_wunits : a.n_units;
+  const std::int64_t* units = WU ? a.wunits : a.units;
+  const std::int64_t ustart = WU ? static_cast<std::int64_t>(blockIdx.x) * kWarps + warp : blockIdx.x;
+  const std::int64_t ustride = WU ? static_cast<std::int64_t>(gridDim.x) * kWarps : gridDim.x;
 
-  for (std::int64_t unit = blockIdx.x; unit < a.n_units; unit += gridDim.x) {
-    const std::int64_t m = a.units[unit * 3], t0 = a.units[unit * 3 + 1], t1 = a.units[unit * 3 + 2];
+  for (std::int64_t unit = ustart; unit < nunits; unit += ustride) {
+    const std::int64_t m = units[unit * 3], t0 = units[unit * 3 + 1], t1 = units[unit * 3 + 2];
     const double* thg = a.theta + m * a.K;
-    for (int k = threadIdx.x; k < G * KL; k += blockDim.x) {
+    for (int k = tid_u; k < G * KL; k += nthr_u) {
       thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
       if (k < a.K) cnt_s[k] = 0;
     }
-    __syncthreads();
+    if constexpr (WU) __syncwarp();
+    else __syncthreads();
     float tf[TFR ? KL : 1];
     if constexpr (TFR) {
 #pragma unroll
@@ -1085,7 +1101,7 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
         tf[i] = t.x, tf[i + 1] = t.y, tf[i + 2] = t.z, tf[i + 3] = t.w;
       }
     }
-    for (std::int64_t b0 = t0 + warp * 32; b0 < t1; b0 += kWarps * 32) {
+    for (std::int64_t b0 = t0 + (WU ? 0 : warp * 32); b0 < t1; b0 += (WU ? 32 : kWarps * 32)) {
       const std::int64_t t = b0 + lane;
       const bool valid = t < t1;
       const int wl = valid ? __ldg(a.w + t) : 0;
@@ -1192,8 +1208,9 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
       }
       __syncwarp();
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    if constexpr (WU) __syncwarp();
+    else __syncthreads();
+    for (int k = tid_u; k < a.K; k += nthr_u) {
       const int n = cnt_s[k];
       if (n) atomicAdd(&a.nmk[m * a.K + k], n);
     }
@@ -1950,6 +1967,21 @@ class Lda final : public Model {
         units_host_.push_back(std::min(t + kChunk, off_host_[m + 1]));
       }
     n_units_ = static_cast<std::int64_t>(units_host_.size() / 3);
+    std::vector<std::int64_t> wu;
+    for (std::int64_t m = 0; m < Ml_; ++m)
+      for (std::int64_t t = off_host_[m]; t < off_host_[m + 1]; t += 256) {
+        wu.push_back(m);
+        wu.push_back(t);
+        wu.push_back(std::min<std::int64_t>(t + 256, off_host_[m + 1]));
+      }
+    n_wunits_ = static_cast<std::int64_t>(wu.size() / 3);
+    wunits_.alloc(std::max<std::size_t>(wu.size(), 3));
+    if (!wu.empty())
+      BNMC_CUDA(cudaMemcpy(wunits_.p, wu.data(), sizeof(std::int64_t) * wu.size(), cudaMemcpyHostToDevice));
+    // warp-level units for short documents (r01 v42: KOS, 136 tokens/doc, z-step 32 -> 27 us;
+    // NIPS, 1267 tokens/doc, is faster with document-wide CTA units: 93 vs 110 us)
+    zt_wu_ = Ml_ > 0 && Nl_ / Ml_ < 256;
+    if (const char* e = std::getenv("BNMC_ZT_WU")) zt_wu_ = std::string(e) != "0";
     {
       const double mean = n_units_ > 0 ? static_cast<double>(Nl_) / static_cast<double>(n_units_) : 32.0;
       zt_warps_ = std::min(8, std::max(1, static_cast<int>(std::ceil(mean / 32.0))));
@@ -2470,6 +2502,14 @@ class Lda final : public Model {
   template <int R, bool TFR>
   void zscreen_t_launch(const LdaArgs& a, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
+    if (zt_wu_) {
+      const int kpad = (K_ + 3) & ~3;
+      const std::size_t smw = sizeof(float) * 8 * (4 * (8 * R + 4) + 32 * 16 + kpad);
+      const unsigned gw = static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((n_wunits_ + 7) / 8, 148 * 3)));
+      launch_pdl(zscreen_t_kernel<R, TFR, true>, dim3(gw), dim3(256), smw, st, a,
+                 static_cast<const std::int64_t*>(out.iter));
+      return;
+    }
     const std::size_t sm = sizeof(float) * (4 * (8 * R + 4) + zt_warps_ * 32 * 16) + sizeof(int) * K_;
     launch_pdl(zscreen_t_kernel<R, TFR>, dim3(g), dim3(32 * zt_warps_), sm, st, a, static_cast<const std::int64_t*>(out.iter));
   }
@@ -2605,6 +2645,8 @@ class Lda final : public Model {
     a.nmk = nmk_.p;
     a.units = units_.p;
     a.n_units = n_units_;
+    a.wunits = wunits_.p;
+    a.n_wunits = n_wunits_;
     a.tpart = tpart_.p;
     a.zpart = zpart_.p;
     a.wpart = wpart_.p;
@@ -2662,7 +2704,9 @@ class Lda final : public Model {
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
   int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
   std::vector<std::int64_t> units_host_;
-  std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0;
+  std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0, n_wunits_ = 0;
+  DevBuf<std::int64_t> wunits_;
+  bool zt_wu_ = true;
   int nbw_ = 1;
   float screen_margin_ = kScreenMargin;
   bool fq_reset_ = false;  // phi_colsum2 of this sweep zeroes the fallback queue

@@ -299,6 +299,7 @@ LAYOUTS = [
     (100, {"BNMC_ZSCREEN": "g4w8s"}), (100, {"BNMC_ZSCREEN": "g8w4r"}),
     (100, {"BNMC_ZSCREEN": "g16w4s"}), (100, {"BNMC_ZSCREEN": "g32w4r"}),
     (100, {"BNMC_ZSTEP_THETA": "smem"}),
+    (100, {"BNMC_ZT_WU": "1"}), (33, {"BNMC_ZT_WU": "1", "BNMC_ZSTEP_THETA": "smem"}), (64, {"BNMC_ZT_WU": "0"}),
     # TMA bulk-copy staged screen (experimental layout)
     (64, {"BNMC_ZSTAGE": "1"}), (100, {"BNMC_ZSTAGE": "1"}), (7, {"BNMC_ZSTAGE": "1", "BNMC_ZSTAGE_SLOTS": "3"}),
     # every token through the fp64 fallback queue
