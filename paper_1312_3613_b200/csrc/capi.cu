@@ -7,6 +7,7 @@
 // log-joints land in a device ring read back at synchronisation points.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -209,10 +210,18 @@ int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
     c->comm.world = std::max(1, desc->world_size);
     c->comm.rank = desc->rank;
     require(c->comm.rank >= 0 && c->comm.rank < c->comm.world, BNMC_GPU_ERR_ARG, "rank out of range");
-    if (c->comm.world > 1) {
-      require(desc->nccl_id != nullptr, BNMC_GPU_ERR_ARG, "world_size > 1 needs an ncclUniqueId");
+    const char* fn = std::getenv("BNMC_FORCE_NCCL");
+    const bool force = fn && std::string(fn) == "1" && c->comm.world == 1 &&
+                       (desc->kind == BNMC_GPU_LDA || desc->kind == BNMC_GPU_MH_LINREG ||
+                        desc->kind == BNMC_GPU_MH_LOGREG || desc->kind == BNMC_GPU_MH_POLYREG);
+    if (c->comm.world > 1 || force) {
       ncclUniqueId id;
-      std::memcpy(&id, desc->nccl_id, sizeof(id));
+      if (c->comm.world > 1) {
+        require(desc->nccl_id != nullptr, BNMC_GPU_ERR_ARG, "world_size > 1 needs an ncclUniqueId");
+        std::memcpy(&id, desc->nccl_id, sizeof(id));
+      } else {
+        BNMC_NCCL(ncclGetUniqueId(&id));  // a 1-rank communicator (test hook)
+      }
       BNMC_NCCL(ncclCommInitRank(&c->comm.comm, c->comm.world, id, c->comm.rank));
     }
     c->lj.alloc(kRing);

@@ -148,6 +148,9 @@ struct Model {
 struct Comm {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // the NCCL code paths run whenever a communicator exists: world > 1, or a 1-rank
+  // communicator forced with BNMC_FORCE_NCCL=1 (exercises the sharded path on one GPU)
+  bool active() const { return comm != nullptr; }
 };
 
 std::unique_ptr<Model> make_lda(const bnmc_gpu_desc& d, const Comm& c, Outputs o);

@@ -2196,7 +2196,7 @@ class Lda final : public Model {
       BNMC_CUDA(cudaEventRecord(ev_join_, side_));
     }
     if (!observe_phi_) {
-      if (comm_.world > 1) {
+      if (comm_.active()) {
         BNMC_NCCL(ncclAllReduce(nkw_.p, nkw_.p, nkw_.n, ncclInt32, ncclSum, comm_.comm, st));
         mark(st, "allreduce_counts");
       }
@@ -2239,7 +2239,7 @@ class Lda final : public Model {
       mark(st, "zstep");
     }
     const unsigned nbw = static_cast<unsigned>(nbw_);
-    if (comm_.world > 1) {
+    if (comm_.active()) {
       wterm_kernel<false><<<nbw, 256, 0, st>>>(a, out, 0);
       mark(st, "wterm");
       reduce_kernel<false><<<1, 1024, 0, st>>>(a);
@@ -2259,7 +2259,7 @@ class Lda final : public Model {
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
     if (Ml_ > 0) doc_eval_kernel<<<grid_docs(), 256, 0, st>>>(a, out.err);
     reduce_kernel<true><<<1, 1024, 0, st>>>(a);
-    if (comm_.world > 1)
+    if (comm_.active())
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
     finalize_kernel<<<1, 256, 0, st>>>(a, out, 0);
     BNMC_CUDA(cudaGetLastError());
@@ -2295,7 +2295,7 @@ class Lda final : public Model {
       LdaArgs a = args();
       a.nkw = tmp.p;
       if (Nl_ > 0) count_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(a, out.err);
-      if (comm_.world > 1)
+      if (comm_.active())
         BNMC_NCCL(ncclAllReduce(tmp.p, tmp.p, tmp.n, ncclInt32, ncclSum, comm_.comm, st));
       std::vector<int> h(tmp.n);
       BNMC_CUDA(cudaMemcpyAsync(h.data(), tmp.p, tmp.bytes(), cudaMemcpyDeviceToHost, st));

@@ -562,7 +562,7 @@ class Mh final : public Model {
     launch_lik(a, wp_.p, st);
     mark(st, "lik");
     const double* tot = nullptr;
-    if (comm_.world > 1) {
+    if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
       BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
       tot = tot_.p;
@@ -607,7 +607,7 @@ class Mh final : public Model {
   void accept_kernel_cached(const MhArgs& a, cudaStream_t st) {
     launch_lik(a, w_.p, st);
     const double* tot = nullptr;
-    if (comm_.world > 1) {
+    if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
       BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
       tot = tot_.p;
@@ -621,7 +621,7 @@ class Mh final : public Model {
     MhArgs a = args();
     fx_kernel<<<kBlocks, kThreads, 0, st>>>(a, part_.p);
     const double* tot = nullptr;
-    if (comm_.world > 1) {
+    if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p + 1);
       BNMC_NCCL(ncclAllReduce(tot_.p + 1, tot_.p + 1, 1, ncclFloat64, ncclSum, comm_.comm, st));
       tot = tot_.p + 1;

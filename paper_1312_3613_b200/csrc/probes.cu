@@ -220,10 +220,22 @@ double lpp(const double* phi, const double* theta, std::int64_t K, std::int64_t 
 // loads over a `bytes` buffer, `reps` passes, fixed grid (148 x 8 x 256 threads).
 // A buffer well inside the 126 MB L2 measures L2 -> SM read bandwidth; a multi-GB
 // buffer measures HBM.  Returns GB/s of the timed passes (after one warm pass).
-__global__ void read_bw_kernel(const double4* p, std::size_t n, double* sink) {
+__global__ void __launch_bounds__(256) read_bw_kernel(const double4* p, std::size_t n, double* sink) {
+  // 4 independent 256-bit loads in flight per thread per iteration
   double acc = 0.0;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
-  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+  std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(v[j].x), "=d"(v[j].y), "=d"(v[j].z), "=d"(v[j].w)
+                   : "l"(p + i + j * stride));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+  }
+  for (; i < n; i += stride) {
     double4 v;
     asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p + i));
     acc += (v.x + v.y) + (v.z + v.w);
@@ -241,9 +253,9 @@ double probe_read_bandwidth(std::size_t bytes, int reps) {
   cudaEvent_t e0, e1;
   BNMC_CUDA(cudaEventCreate(&e0));
   BNMC_CUDA(cudaEventCreate(&e1));
-  read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, sink.p);
+  read_bw_kernel<<<148 * 16, 256>>>(buf.p, n, sink.p);
   BNMC_CUDA(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, sink.p);
+  for (int r = 0; r < reps; ++r) read_bw_kernel<<<148 * 16, 256>>>(buf.p, n, sink.p);
   BNMC_CUDA(cudaEventRecord(e1));
   BNMC_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;

@@ -453,3 +453,39 @@ def test_zoo_sweeps_vs_reference(g, name, model):
                 assert rel(s[n], fx[n][it]) < RTOL_PARAM, (n, it, rel(s[n], fx[n][it]))
         assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it]), (it, lj, fx["lj"][it])
     e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# the sharded code path (NCCL all-reduces inside the sweep's CUDA graph) on one GPU:
+# BNMC_FORCE_NCCL=1 gives a 1-rank communicator, so every world > 1 branch runs
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["lda_desk", "lda_ragged"])
+def test_lda_nccl_path_vs_reference(g, monkeypatch, name):
+    monkeypatch.setenv("BNMC_FORCE_NCCL", "1")
+    fx = golden(name)
+    e, s = lda_engine(g, fx)
+    assert abs(e.eval_log_joint(s) - fx["lj0"]) <= RTOL_LJ * abs(fx["lj0"])
+    for it in range(len(fx["lj"])):
+        lj = e.sweep(s, it)
+        assert np.array_equal(s["z"], fx["z"][it])
+        assert rel(s["phi"], fx["phi"][it]) < RTOL_PARAM
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
+    lj_dev, _ = e.run_device(len(fx["lj"]), 3)  # graph replays with the captured all-reduces
+    assert np.all(np.isfinite(lj_dev))
+    e.close()
+
+
+def test_mh_nccl_path_vs_reference(g, monkeypatch):
+    monkeypatch.setenv("BNMC_FORCE_NCCL", "1")
+    fx = golden("mh_linreg")
+    N, K = int(fx["N"]), int(fx["K"])
+    e = g.Engine("regression", {"N": N, "K": K, "l": -1.0, "u": 1.0}, g.RunConfig(seed=int(fx["seed"])))
+    s = e.allocate()
+    s["x"], s["y"], s["w"], s["b"], s["tau"] = fx["x"], fx["y"], fx["w0"], [fx["b0"]], [fx["tau0"]]
+    assert abs(e.eval_log_joint(s) - fx["lj0"]) <= RTOL_LJ * abs(fx["lj0"])
+    for it in range(len(fx["lj"])):
+        acc = []
+        lj = e.sweep(s, it, acc)
+        assert acc[0] == bool(fx["accepted"][it])
+        assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
+    e.close()
