@@ -166,6 +166,21 @@ int bnmc_gpu_eval_log_joint(bnmc_gpu_ctx* ctx, double* log_joint);
 /* prior_init(skip_observed = true) on the device (sampler.cpp:542-555). */
 int bnmc_gpu_prior_init(bnmc_gpu_ctx* ctx, uint64_t seed);
 
+/* Checkpoint / resume (the reference has none): the device state
+ * of the model (state_buffers: LDA z, theta, phi draws + row sums; GMM z, pi, mu,
+ * sigma2; MH w, b, tau; zoo models likewise) and the next iteration, in a binary file.
+ * Loading into a context of the same model, sizes, shard and seed resumes the chain
+ * exactly: the RNG streams are keyed by (seed, iteration, site). */
+int bnmc_gpu_save_checkpoint(bnmc_gpu_ctx* ctx, const char* path);
+int bnmc_gpu_load_checkpoint(bnmc_gpu_ctx* ctx, const char* path);
+/* The iteration the next sweep will run (after a load: the checkpoint's). */
+int bnmc_gpu_checkpoint_iter(const bnmc_gpu_ctx* ctx, int64_t* next_iter);
+/* LDA binary corpus (.bnc) -- SURVEY.md 8f row 1, the format for corpora the JSON path
+ * (data.cpp:27-136) cannot carry: "BNMCCORP", uint32 version = 1, uint32 0, int64 M,
+ * int64 N, int64 V, int64 offsets[M + 1], int32 w[N].  This shard's tokens are streamed
+ * to the device (range-checked); the offsets must equal the context's.  Observed data
+ * only: follow with bnmc_gpu_prior_init (or an upload of the latent state). */
+int bnmc_gpu_lda_load_corpus(bnmc_gpu_ctx* ctx, const char* path);
 /* LDA diagnostics: topic-word counts of the current z, row-major K x V (global,
  * after the all-reduce), and this shard's doc-topic counts (local docs x K). */
 int bnmc_gpu_lda_counts(bnmc_gpu_ctx* ctx, int32_t* nkw, int32_t* nmk);

@@ -7,6 +7,7 @@
 // log-joints land in a device ring read back at synchronisation points.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -455,6 +456,112 @@ int bnmc_gpu_run_trace(bnmc_gpu_ctx* c, std::int64_t iter0, bnmc_gpu_trace* tr) 
       throw;
     }
     cleanup();
+  });
+}
+
+namespace {
+struct CkptHeader {
+  char magic[8];
+  std::uint32_t version;
+  std::int32_t kind;
+  std::int64_t K, V, M, N;
+  std::uint64_t seed;
+  std::int64_t next_iter;
+  std::int32_t rank, world;
+  std::uint32_t nbufs, pad;
+};
+
+struct FileCloser {
+  std::FILE* f;
+  ~FileCloser() {
+    if (f) std::fclose(f);
+  }
+};
+
+CkptHeader ckpt_header(const bnmc_gpu_ctx* c, std::uint32_t nbufs) {
+  CkptHeader h{};
+  std::memcpy(h.magic, "BNMCCKPT", 8);
+  h.version = 1;
+  h.kind = c->desc.kind;
+  h.K = c->desc.K;
+  h.V = c->desc.V;
+  h.M = c->desc.M;
+  h.N = c->desc.N;
+  h.seed = c->desc.seed;
+  h.next_iter = c->next_iter;
+  h.rank = c->comm.rank;
+  h.world = c->comm.world;
+  h.nbufs = nbufs;
+  return h;
+}
+}  // namespace
+
+int bnmc_gpu_save_checkpoint(bnmc_gpu_ctx* c, const char* path) {
+  if (!c || !path) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+    check_device_error(c);
+    auto bufs = c->model->state_buffers();
+    require(!bufs.empty(), BNMC_GPU_ERR_ARG, "this model has no checkpointable state");
+    std::FILE* f = std::fopen(path, "wb");
+    require(f != nullptr, BNMC_GPU_ERR_RUNTIME, std::string("cannot write ") + path);
+    FileCloser fc{f};
+    const CkptHeader h = ckpt_header(c, static_cast<std::uint32_t>(bufs.size()));
+    require(std::fwrite(&h, sizeof(h), 1, f) == 1, BNMC_GPU_ERR_RUNTIME, "checkpoint write failed");
+    std::vector<unsigned char> host;
+    for (const auto& b : bufs) {
+      const std::uint64_t n = b.bytes;
+      host.resize(static_cast<std::size_t>(n));
+      if (n) BNMC_CUDA(cudaMemcpy(host.data(), *b.p, n, cudaMemcpyDeviceToHost));
+      require(std::fwrite(&n, 8, 1, f) == 1 && (n == 0 || std::fwrite(host.data(), 1, n, f) == n), BNMC_GPU_ERR_RUNTIME,
+              "checkpoint write failed");
+    }
+  });
+}
+
+int bnmc_gpu_load_checkpoint(bnmc_gpu_ctx* c, const char* path) {
+  if (!c || !path) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+    auto bufs = c->model->state_buffers();
+    std::FILE* f = std::fopen(path, "rb");
+    require(f != nullptr, BNMC_GPU_ERR_RUNTIME, std::string("cannot read ") + path);
+    FileCloser fc{f};
+    CkptHeader h{};
+    require(std::fread(&h, sizeof(h), 1, f) == 1 && std::memcmp(h.magic, "BNMCCKPT", 8) == 0 && h.version == 1,
+            BNMC_GPU_ERR_RUNTIME, "not a bnmc checkpoint");
+    const CkptHeader want = ckpt_header(c, static_cast<std::uint32_t>(bufs.size()));
+    require(h.kind == want.kind && h.K == want.K && h.V == want.V && h.M == want.M && h.N == want.N &&
+                h.rank == want.rank && h.world == want.world && h.nbufs == want.nbufs,
+            BNMC_GPU_ERR_RUNTIME, "checkpoint was written by a different model / shard");
+    require(h.seed == want.seed, BNMC_GPU_ERR_RUNTIME,
+            "checkpoint seed differs (the RNG streams are keyed by the seed: the chain would not resume)");
+    std::vector<unsigned char> host;
+    for (const auto& b : bufs) {
+      std::uint64_t n = 0;
+      require(std::fread(&n, 8, 1, f) == 1 && n == b.bytes, BNMC_GPU_ERR_RUNTIME, "checkpoint buffer size mismatch");
+      host.resize(static_cast<std::size_t>(n));
+      require(n == 0 || std::fread(host.data(), 1, n, f) == n, BNMC_GPU_ERR_RUNTIME, "truncated checkpoint");
+      if (n) BNMC_CUDA(cudaMemcpy(*b.p, host.data(), n, cudaMemcpyHostToDevice));
+    }
+    c->model->on_state_restored(c->stream);
+    c->next_iter = -1;
+    set_iter(c, h.next_iter < 0 ? 0 : h.next_iter);
+    check_device_error(c);
+  });
+}
+
+int bnmc_gpu_checkpoint_iter(const bnmc_gpu_ctx* c, int64_t* next_iter) {
+  if (!c || !next_iter) return fail(nullptr, BNMC_GPU_ERR_ARG, "null argument");
+  *next_iter = c->next_iter;
+  return BNMC_GPU_OK;
+}
+
+int bnmc_gpu_lda_load_corpus(bnmc_gpu_ctx* c, const char* path) {
+  if (!c || !path) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    c->model->lda_load_corpus(path, c->stream);
+    check_device_error(c);
   });
 }
 

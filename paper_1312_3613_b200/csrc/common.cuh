@@ -127,6 +127,13 @@ struct Model {
     std::size_t bytes;
   };
   virtual std::vector<StateBuf> state_buffers() { return {}; }
+  // After state_buffers() were overwritten (checkpoint restore): rebuild whatever the
+  // model derives from them (counts, caches).
+  virtual void on_state_restored(cudaStream_t) {}
+  // LDA: stream this shard's tokens of a binary corpus file into device memory.
+  virtual void lda_load_corpus(const char*, cudaStream_t) {
+    throw Error(BNMC_GPU_ERR_ARG, "binary corpora are only defined for LDA");
+  }
   Outputs out{};
 
   // Per-phase timing (bnmc_gpu_sweep_phases): when `marks` is set, every phase

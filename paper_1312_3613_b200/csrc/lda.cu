@@ -1785,6 +1785,12 @@ __global__ void i64_to_i32_kernel(const std::int64_t* in, int* out, std::int64_t
   }
 }
 
+__global__ void i32_check_kernel(const int* v, std::int64_t n, int hi, int* err) {
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    if (v[i] < 0 || v[i] >= hi) atomicOr(err, kErrBin);
+}
+
 __global__ void i32_to_i64_kernel(const int* in, std::int64_t* out, std::int64_t n) {
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -2277,6 +2283,62 @@ class Lda final : public Model {
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
     after_state_change(st);
+  }
+
+  // Checkpoint restore: phiT holds this sweep's gamma draws g with their row sums S;
+  // normalise in place (phi = g / S, the value download() reports) and rebuild the
+  // counts and phi terms as after an upload.
+  void on_state_restored(cudaStream_t st) override {
+    LdaArgs a = args();
+    phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
+    after_state_change(st);
+  }
+
+  // Binary corpus (.bnc, see include/bnmc_gpu.h): this shard's token range of w is
+  // streamed through a pinned buffer into the device (int32, range-checked); the
+  // document offsets must equal the ones the context was created with.
+  void lda_load_corpus(const char* path, cudaStream_t st) override {
+    std::FILE* f = std::fopen(path, "rb");
+    require(f != nullptr, BNMC_GPU_ERR_RUNTIME, std::string("cannot open corpus ") + path);
+    struct Closer {
+      std::FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[8];
+    std::uint32_t ver = 0, pad = 0;
+    std::int64_t M = 0, N = 0, V = 0;
+    require(std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, "BNMCCORP", 8) == 0, BNMC_GPU_ERR_RUNTIME,
+            "not a bnmc corpus file");
+    require(std::fread(&ver, 4, 1, f) == 1 && std::fread(&pad, 4, 1, f) == 1 && ver == 1, BNMC_GPU_ERR_RUNTIME,
+            "unsupported corpus version");
+    require(std::fread(&M, 8, 1, f) == 1 && std::fread(&N, 8, 1, f) == 1 && std::fread(&V, 8, 1, f) == 1,
+            BNMC_GPU_ERR_RUNTIME, "truncated corpus header");
+    require(M == M_ && N == N_ && V == V_, BNMC_GPU_ERR_RUNTIME, "corpus sizes differ from the model's (M, N, V)");
+    std::vector<std::int64_t> off(static_cast<std::size_t>(M) + 1);
+    require(std::fread(off.data(), 8, off.size(), f) == off.size(), BNMC_GPU_ERR_RUNTIME, "truncated corpus offsets");
+    for (std::int64_t m = 0; m <= Ml_; ++m)
+      require(off[d0_ + m] - tok0_ == off_host_[m], BNMC_GPU_ERR_RUNTIME, "corpus document offsets differ");
+    const long base = static_cast<long>(8 + 8 + 24 + 8 * (M + 1));
+    require(std::fseek(f, base + static_cast<long>(4 * tok0_), SEEK_SET) == 0, BNMC_GPU_ERR_RUNTIME, "corpus seek failed");
+    const std::int64_t chunk = 16 << 20;  // tokens per staged copy
+    int* pinned = nullptr;
+    BNMC_CUDA(cudaMallocHost(&pinned, sizeof(int) * static_cast<std::size_t>(std::min(chunk, std::max<std::int64_t>(Nl_, 1)))));
+    struct Pin {
+      int* p;
+      ~Pin() { cudaFreeHost(p); }
+    } pin{pinned};
+    if (stage64_.n < static_cast<std::size_t>(std::max<std::int64_t>(Nl_, 1))) stage64_.alloc(std::max<std::int64_t>(Nl_, 1));
+    for (std::int64_t t = 0; t < Nl_; t += chunk) {
+      const std::int64_t n = std::min(chunk, Nl_ - t);
+      require(std::fread(pinned, 4, static_cast<std::size_t>(n), f) == static_cast<std::size_t>(n), BNMC_GPU_ERR_RUNTIME,
+              "truncated corpus tokens");
+      BNMC_CUDA(cudaMemcpyAsync(w_.p + t, pinned, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+      BNMC_CUDA(cudaStreamSynchronize(st));  // the pinned buffer is reused
+    }
+    i32_check_kernel<<<std::max(1u, std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16)), 256, 0, st>>>(w_.p, Nl_, V_, out.err);
+    data_on_device_ = true;
+    BNMC_CUDA(cudaGetLastError());
+    BNMC_CUDA(cudaStreamSynchronize(st));
   }
 
   std::vector<StateBuf> state_buffers() override {

@@ -518,6 +518,8 @@ class Mh final : public Model {
     if (!logistic_ && !poly_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
   }
 
+  void on_state_restored(cudaStream_t st) override { refresh(st); }
+
   std::vector<StateBuf> state_buffers() override {
     return {{reinterpret_cast<void**>(&w_.p), sizeof(double) * static_cast<std::size_t>(K_ + 2)}};
   }

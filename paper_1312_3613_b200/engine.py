@@ -95,6 +95,10 @@ def lib():
     L.bnmc_gpu_prior_init.argtypes = [c_void_p, c_uint64]
     L.bnmc_gpu_lda_counts.argtypes = [c_void_p, POINTER(c_int32), POINTER(c_int32)]
     L.bnmc_gpu_lda_generate.argtypes = [c_void_p, c_uint64, c_double, c_double]
+    L.bnmc_gpu_save_checkpoint.argtypes = [c_void_p, c_char_p]
+    L.bnmc_gpu_load_checkpoint.argtypes = [c_void_p, c_char_p]
+    L.bnmc_gpu_checkpoint_iter.argtypes = [c_void_p, POINTER(c_int64)]
+    L.bnmc_gpu_lda_load_corpus.argtypes = [c_void_p, c_char_p]
     L.bnmc_gpu_partition.argtypes = [POINTER(c_int64), c_int64, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]
     L.bnmc_gpu_lpp.argtypes = [POINTER(c_double), POINTER(c_double), c_int64, c_int64, POINTER(c_int64),
                                POINTER(c_int64), c_int64, POINTER(c_double)]
@@ -247,6 +251,20 @@ class ParamStore:
         st = _Store(n, real, ival, lens, obs)
         st._keep = (real, ival, lens, obs)
         return st
+
+
+def write_corpus(path: str, offsets, w, V: int):
+    """The binary LDA corpus format of bnmc_gpu_lda_load_corpus (include/bnmc_gpu.h)."""
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    ww = np.ascontiguousarray(w, dtype=np.int32)
+    if off[0] != 0 or off[-1] != ww.size:
+        raise BnmcError("offsets must run from 0 to len(w)")
+    with open(path, "wb") as f:
+        f.write(b"BNMCCORP")
+        f.write(np.array([1, 0], dtype=np.uint32).tobytes())
+        f.write(np.array([off.size - 1, ww.size, V], dtype=np.int64).tobytes())
+        f.write(off.tobytes())
+        f.write(ww.tobytes())
 
 
 def read_bandwidth(nbytes: int, reps: int = 20) -> float:
@@ -510,6 +528,30 @@ class Engine:
         nmk = np.empty(max(Ml, 1) * K, dtype=np.int32)
         _raise(lib().bnmc_gpu_lda_counts(self._h, _p(nkw, c_int32), _p(nmk, c_int32)), self._h)
         return nkw.reshape(K, V), nmk[: Ml * K].reshape(Ml, K)
+
+    # -- checkpoint / binary corpus ------------------------------------------------------
+    def save_checkpoint(self, path: str):
+        """Device state + next iteration to a binary file (bnmc_gpu_save_checkpoint)."""
+        _raise(lib().bnmc_gpu_save_checkpoint(self._h, os.fsencode(path)), self._h)
+
+    def load_checkpoint(self, path: str) -> int:
+        """Restore a checkpoint of the same model / sizes / seed; returns the iteration the
+        next sweep runs (the chain resumes exactly)."""
+        _raise(lib().bnmc_gpu_load_checkpoint(self._h, os.fsencode(path)), self._h)
+        it = c_int64()
+        _raise(lib().bnmc_gpu_checkpoint_iter(self._h, ctypes.byref(it)), self._h)
+        self._bound = None
+        return it.value
+
+    def lda_load_corpus(self, path: str):
+        """Stream a binary corpus (write_corpus) into device memory (bnmc_gpu_lda_load_corpus)."""
+        _raise(lib().bnmc_gpu_lda_load_corpus(self._h, os.fsencode(path)), self._h)
+        self._bound = None
+
+    def prior_init_device(self, seed: int):
+        """prior_init on the device-resident state (no host store involved)."""
+        _raise(lib().bnmc_gpu_prior_init(self._h, seed), self._h)
+        self._bound = None
 
     def lda_generate(self, seed: int, phi_conc: float = 0.05, theta_conc: float = 0.3):
         _raise(lib().bnmc_gpu_lda_generate(self._h, seed, phi_conc, theta_conc), self._h)

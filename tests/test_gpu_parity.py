@@ -489,3 +489,95 @@ def test_mh_nccl_path_vs_reference(g, monkeypatch):
         assert acc[0] == bool(fx["accepted"][it])
         assert abs(lj - fx["lj"][it]) <= RTOL_LJ * abs(fx["lj"][it])
     e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# checkpoint / resume and the binary corpus
+# ----------------------------------------------------------------------------------------
+def _resume_case(g, tmp_path, make, names, n_before=2, n_after=2):
+    e1, s1 = make()
+    for it in range(n_before):
+        e1.sweep(s1, it)
+    ck = str(tmp_path / "state.ckpt")
+    e1.save_checkpoint(ck)
+    for it in range(n_before, n_before + n_after):
+        e1.sweep(s1, it)
+    e2, s2 = make()
+    e2.upload(s2)                       # observed data (and a stale latent state)
+    assert e2.load_checkpoint(ck) == n_before
+    e2.run_device(n_before, n_after)
+    e2.download(s2)
+    for x in names:
+        assert np.array_equal(s1[x], s2[x]), x
+    e1.close()
+    e2.close()
+
+
+def test_checkpoint_resume_lda(g, tmp_path):
+    fx = golden("lda_desk")
+    _resume_case(g, tmp_path, lambda: lda_engine(g, fx), ["z", "phi", "theta"])
+
+
+def test_checkpoint_resume_gmm_mh_hmm(g, tmp_path):
+    gm = golden("gmm_small")
+
+    def mk_gmm():
+        e = g.Engine("gmm", {"N": int(gm["N"]), "K": 4}, g.RunConfig(seed=int(gm["seed"])))
+        s = e.allocate()
+        s["x"], s["z"], s["pi"], s["mu"], s["sigma2"] = gm["x"], gm["z0"], gm["pi0"], gm["mu0"], gm["sigma20"]
+        return e, s
+    _resume_case(g, tmp_path, mk_gmm, ["z", "pi", "mu", "sigma2"])
+    mh = golden("mh_linreg")
+
+    def mk_mh():
+        e = g.Engine("regression", {"N": int(mh["N"]), "K": int(mh["K"]), "l": -1.0, "u": 1.0},
+                     g.RunConfig(seed=int(mh["seed"])))
+        s = e.allocate()
+        s["x"], s["y"], s["w"], s["b"], s["tau"] = mh["x"], mh["y"], mh["w0"], [mh["b0"]], [mh["tau0"]]
+        return e, s
+    _resume_case(g, tmp_path, mk_mh, ["w", "b", "tau"])
+    hm = golden("hmm_small")
+
+    def mk_hmm():
+        e, s, latent = _zoo_engine(g, hm, "hmm")
+        for n in latent:
+            s[n] = hm[n + "0"]
+        return e, s
+    _resume_case(g, tmp_path, mk_hmm, ["T", "bias", "s"])
+
+
+def test_checkpoint_rejects_other_seed(g, tmp_path):
+    fx = golden("lda_desk")
+    e1, s1 = lda_engine(g, fx)
+    e1.sweep(s1, 0)
+    ck = str(tmp_path / "a.ckpt")
+    e1.save_checkpoint(ck)
+    K, V, M = int(fx["K"]), int(fx["V"]), int(fx["M"])
+    e2 = g.Engine("lda", {"K": K, "V": V, "M": M, "N": np.diff(fx["offsets"]).tolist()}, g.RunConfig(seed=1))
+    with pytest.raises(g.BnmcError):
+        e2.load_checkpoint(ck)
+
+
+def test_binary_corpus_device_workflow(g, tmp_path):
+    """write_corpus -> bnmc_gpu_lda_load_corpus -> device prior_init -> sweeps: the same
+    state as the reference's prior_init and sweeps (the 1B workflow, host never holds z)."""
+    fx = golden("lda_desk")
+    K, V, M = int(fx["K"]), int(fx["V"]), int(fx["M"])
+    path = str(tmp_path / "desk.bnc")
+    g.write_corpus(path, fx["offsets"], fx["w"], V)
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": np.diff(fx["offsets"]).tolist()},
+                 g.RunConfig(seed=int(fx["seed"])))
+    e.lda_load_corpus(path)
+    e.prior_init_device(int(fx["seed"]))
+    s = e.allocate()
+    e.download(s)
+    assert np.array_equal(s["z"], fx["z0"])
+    assert rel(s["phi"], fx["phi0"]) < RTOL_PARAM and rel(s["theta"], fx["theta0"]) < RTOL_PARAM
+    lj, _ = e.run_device(0, len(fx["lj"]))
+    e.download(s)
+    assert np.array_equal(s["z"], fx["z"][-1])
+    assert abs(lj[-1] - fx["lj"][-1]) <= RTOL_LJ * abs(fx["lj"][-1])
+    bad = str(tmp_path / "bad.bnc")
+    g.write_corpus(bad, fx["offsets"], np.full(len(fx["w"]), V + 3), V)
+    with pytest.raises(g.BnmcError):
+        e.lda_load_corpus(bad)
