@@ -577,6 +577,41 @@ def map_estimate(model: str, observe_extra, hyper: dict, store: ParamStore, n: i
     return store
 
 
+def lpp_curve(phi_samples, timing_ms, heldout_hyper: dict, heldout_w, heldout_docs, fit_sweeps: int, seed: int,
+              cfg: RunConfig | None = None):
+    """lpp_curve (bench.cpp:30-77), the Fig. 3 protocol, on the device: for checkpoints
+    c = 1, 2, 4, ... (and the last sample) clamp phi to training sample c - 1, prior_init
+    the held-out documents' theta and z with seed + c, map_estimate them over `fit_sweeps`
+    Gibbs sweeps (blocks theta, z), and score log_predictive_probability on the held-out
+    tokens.  heldout_docs = (w, offsets) of the held-out tokens.  Returns
+    [{"samples": c, "lpp": ..., "seconds": sum of the first c sweep times}]."""
+    n = len(phi_samples)
+    checkpoints = []
+    c = 1
+    while c <= n:
+        checkpoints.append(c)
+        c *= 2
+    if not checkpoints or checkpoints[-1] != n:
+        checkpoints.append(n)
+    K, V = int(heldout_hyper["K"]), int(heldout_hyper["V"])
+    hw, hoff = heldout_docs
+    out = []
+    for c in checkpoints:
+        phi = np.asarray(phi_samples[c - 1], dtype=np.float64)
+        run = RunConfig(**{**(cfg or RunConfig()).__dict__, "seed": seed + c, "method": "gibbs",
+                           "observe_extra": ["phi"]})
+        with Engine("lda", heldout_hyper, run) as e:
+            store = e.allocate()
+            store["w"] = heldout_w
+            store["phi"] = phi
+            e.prior_init(store, seed + c)  # skip_observed: theta and z only
+        map_estimate("lda", {"phi"}, heldout_hyper, store, fit_sweeps, run)
+        lpp = log_predictive_probability(phi, store["theta"], K, V, hw, hoff)
+        secs = float(np.sum(np.asarray(timing_ms[:c], dtype=np.float64)) / 1000.0) if timing_ms is not None else 0.0
+        out.append({"samples": c, "lpp": lpp, "seconds": secs})
+    return out
+
+
 # -- primitive operators (device) -------------------------------------------------------
 def probe_rng(keys, per: int):
     keys = np.ascontiguousarray(keys, dtype=np.uint64)

@@ -581,3 +581,32 @@ def test_binary_corpus_device_workflow(g, tmp_path):
     g.write_corpus(bad, fx["offsets"], np.full(len(fx["w"]), V + 3), V)
     with pytest.raises(g.BnmcError):
         e.lda_load_corpus(bad)
+
+
+def test_lpp_curve_vs_restatement(g, restatement, reference):
+    """lpp_curve (bench.cpp:30-77, the Fig. 3 protocol) on the device against the same
+    protocol composed from the restatement: clamped phi, prior_init(seed + c) of theta
+    and z, fit sweeps keeping the MAP state (strict >), log10 predictive probability."""
+    K, V, Mh, L, seed, fit = 5, 60, 8, 20, 7, 4
+    w_tr, _, _ = reference.gen_lda(30, V, K, 25, 3)
+    phis = [restatement.lda_prior_init(K, V, np.arange(31, dtype=np.int64) * 25, w_tr, 100 + i)[0] for i in range(5)]
+    rs = np.random.default_rng(4)
+    hw = rs.integers(0, V, Mh * L).astype(np.int64)              # held-out documents (fit)
+    hoff = np.arange(Mh + 1, dtype=np.int64) * L
+    tw = rs.integers(0, V, Mh * 6).astype(np.int64)              # held-out test tokens
+    toff = np.arange(Mh + 1, dtype=np.int64) * 6
+    hyper = {"K": K, "V": V, "M": Mh, "N": [L] * Mh}
+    got = g.lpp_curve(phis, [1.0] * 5, hyper, hw, (tw, toff), fit, seed)
+    assert [p["samples"] for p in got] == [1, 2, 4, 5]
+    for p in got:
+        c = p["samples"]
+        phi = phis[c - 1].copy()
+        _, theta, z = restatement.lda_prior_init(K, V, hoff, hw, seed + c)
+        best, best_theta = -np.inf, None
+        for it in range(fit):
+            lj = restatement.lda_sweep(K, V, hoff, hw, z, phi, theta, seed + c, it, observe_phi=True)
+            if lj > best:
+                best, best_theta = lj, theta.copy()
+        want = restatement.lda_lpp(phi, best_theta, K, V, tw, toff)
+        assert abs(p["lpp"] - want) <= 1e-10 * abs(want), (c, p["lpp"], want)
+        assert p["seconds"] == c / 1000.0
