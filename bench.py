@@ -418,8 +418,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             e2e_s = float(t.item())
         e2e = {"value": sites_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(up),
                "d2h_bytes_per_step": int(down), "ms_per_step": e2e_s * 1e3,
-               "path": "Engine.sweep(store, iter) with pinned host arrays: bnmc_gpu_upload_sweep_inputs + "
-                       "bnmc_gpu_sweep + bnmc_gpu_download"}
+               "path": "Engine.sweep(store, iter) with pinned host arrays: bnmc_gpu_sweep_store (upload of "
+                       "what the sweep reads, sweep, write-back; phi/theta copies overlap the z-step)"}
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "1B corpus is generated and kept on the device (host cannot hold it)"}

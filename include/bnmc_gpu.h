@@ -133,6 +133,12 @@ int bnmc_gpu_download(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
 
 /* One sweep (all plan blocks + log-joint) for iteration `iter`; synchronous. */
 int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_accepted);
+/* Engine::sweep on a caller's store in one call: upload what the sweep reads
+ * (bnmc_gpu_upload_sweep_inputs), sweep, and write the latent state back -- LDA copies
+ * phi and theta back while the z-step still runs.  On an error the store's latent
+ * variables are unspecified. */
+int bnmc_gpu_sweep_store(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store, int64_t iter, double* log_joint,
+                         int* mh_accepted);
 /* n sweeps iter0..iter0+n-1 with one host sync; per-sweep outputs optional. */
 int bnmc_gpu_run(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n, double* log_joints, int* accepted);
 /* Engine::run (sampler.cpp:426-455) with a device-resident trace: burn-in + n kept

@@ -132,11 +132,17 @@ class Engine {
 
   // Engine::sweep: the store is advanced in place; returns the post-sweep log-joint.
   double sweep(ParamStore& store, long long iter, bool* mh_accepted = nullptr) {
-    bind(store, /*sweep_inputs=*/true);
     double lj = 0.0;
     int acc = 0;
-    check(bnmc_gpu_sweep(ctx_.get(), iter, &lj, &acc), ctx_.get());
-    download(store);
+    if (bound_ != &store) {
+      bind(store);
+      check(bnmc_gpu_sweep(ctx_.get(), iter, &lj, &acc), ctx_.get());
+      download(store);
+    } else {
+      // upload what the sweep reads, sweep, write back in one call (bnmc_gpu_sweep_store)
+      bnmc_gpu_store v = store.view();
+      check(bnmc_gpu_sweep_store(ctx_.get(), &v, iter, &lj, &acc), ctx_.get());
+    }
     if (mh_accepted) *mh_accepted = acc != 0;
     return lj;
   }

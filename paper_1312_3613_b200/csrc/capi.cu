@@ -358,6 +358,27 @@ int bnmc_gpu_sweep(bnmc_gpu_ctx* c, std::int64_t iter, double* log_joint, int* m
   });
 }
 
+int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t iter, double* log_joint,
+                         int* mh_accepted) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    require(iter >= 0, BNMC_GPU_ERR_ARG, "iteration must be non-negative");
+    require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
+            "store view is incomplete");
+    c->model->upload_sweep_inputs(*s, c->stream);
+    set_iter(c, iter);
+    launch_sweep(c);
+    if (!c->model->download_overlapped(*s, c->stream)) {
+      read_ring(c, iter, 1, log_joint, mh_accepted);
+      check_device_error(c);
+      c->model->download(*s, c->stream);
+      return;
+    }
+    read_ring(c, iter, 1, log_joint, mh_accepted);  // synchronises the stream (and the copies)
+    check_device_error(c);
+  });
+}
+
 int bnmc_gpu_run(bnmc_gpu_ctx* c, std::int64_t iter0, std::int64_t n, double* log_joints, int* accepted) {
   if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
   return guarded(c, [&] {

@@ -127,6 +127,10 @@ struct Model {
     std::size_t bytes;
   };
   virtual std::vector<StateBuf> state_buffers() { return {}; }
+  // Download whose copies of variables finished early in the sweep overlap the rest of
+  // it (the sweep was just enqueued on `st`); returns false when the model has no such
+  // schedule (the caller then downloads after the sweep).
+  virtual bool download_overlapped(const bnmc_gpu_store&, cudaStream_t) { return false; }
   // After state_buffers() were overwritten (checkpoint restore): rebuild whatever the
   // model derives from them (counts, caches).
   virtual void on_state_restored(cudaStream_t) {}

@@ -2092,12 +2092,20 @@ class Lda final : public Model {
     theta_v1_ = tv && std::string(tv) == "1";
     configure_kernels();
     BNMC_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    BNMC_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_phi_ready_, cudaEventDisableTiming));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_theta_ready_, cudaEventDisableTiming));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_copy_done_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   }
 
   ~Lda() override {
     if (side_) cudaStreamDestroy(side_);
+    if (copy_) cudaStreamDestroy(copy_);
+    if (ev_phi_ready_) cudaEventDestroy(ev_phi_ready_);
+    if (ev_theta_ready_) cudaEventDestroy(ev_theta_ready_);
+    if (ev_copy_done_) cudaEventDestroy(ev_copy_done_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
   }
@@ -2168,6 +2176,44 @@ class Lda final : public Model {
     after_state_change(st);
   }
 
+  // An event other streams can wait on: inside a stream capture it must be an external
+  // event node (cudaEventRecordExternal), outside a plain record (direct launches).
+  static void record_external(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    BNMC_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) BNMC_CUDA(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+    else BNMC_CUDA(cudaEventRecord(ev, st));
+  }
+
+  // phi and theta are final early in the sweep (after the phi block / the theta block):
+  // their transpose + device-to-host copies run on a copy stream while the z-step and
+  // the log-joint run; z follows the sweep on the main stream.
+  bool download_overlapped(const bnmc_gpu_store& s, cudaStream_t st) override {
+    if (marks || observe_phi_ || Ml_ == 0) return false;
+    const char* obs = s.observed;
+    if (!(obs && obs[var_phi_]) && s.real[var_phi_]) {
+      if (stage_phi_.n == 0) stage_phi_.alloc(static_cast<std::size_t>(K_) * V_);
+      BNMC_CUDA(cudaStreamWaitEvent(copy_, ev_phi_ready_, 0));
+      transpose_kernel<<<dim3((K_ + 31) / 32, (V_ + 31) / 32), dim3(32, 8), 0, copy_>>>(phiT_.p, stage_phi_.p, V_, K_, Kp_, V_, S_.p);
+      BNMC_CUDA(cudaMemcpyAsync(s.real[var_phi_], stage_phi_.p, stage_phi_.bytes(), cudaMemcpyDeviceToHost, copy_));
+    }
+    if (!(obs && obs[var_theta_]) && s.real[var_theta_]) {
+      BNMC_CUDA(cudaStreamWaitEvent(copy_, ev_theta_ready_, 0));
+      BNMC_CUDA(cudaMemcpyAsync(s.real[var_theta_] + d0_ * K_, theta_.p, sizeof(double) * Ml_ * K_,
+                                cudaMemcpyDeviceToHost, copy_));
+    }
+    BNMC_CUDA(cudaEventRecord(ev_copy_done_, copy_));
+    if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) {
+      if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
+      i32_to_i64_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(z_.p, stage64_.p, Nl_);
+      BNMC_CUDA(cudaMemcpyAsync(s.ival[var_z_] + tok0_, stage64_.p, sizeof(std::int64_t) * Nl_,
+                                cudaMemcpyDeviceToHost, st));
+    }
+    BNMC_CUDA(cudaStreamWaitEvent(st, ev_copy_done_, 0));  // the sweep call completes with both
+    BNMC_CUDA(cudaGetLastError());
+    return true;
+  }
+
   void download(const bnmc_gpu_store& s, cudaStream_t st) override {
     const char* obs = s.observed;
     if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) {
@@ -2199,6 +2245,7 @@ class Lda final : public Model {
       BNMC_CUDA(cudaEventRecord(ev_fork_, st));
       BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
       launch_theta(a, side_);
+      record_external(ev_theta_ready_, side_);
       BNMC_CUDA(cudaEventRecord(ev_join_, side_));
     }
     if (!observe_phi_) {
@@ -2229,6 +2276,9 @@ class Lda final : public Model {
         fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
         mark(st, "phi_norm");
       }
+      // phi (phiT, S) is final from here: an overlapped download may start (external
+      // event node in the captured graph)
+      if (!timed) record_external(ev_phi_ready_, st);
     } else {
       // phi clamped: no phi block consumes the counts; the z-step's counts of this
       // sweep feed only the w-factor.
@@ -2759,7 +2809,8 @@ class Lda final : public Model {
   DevBuf<ZBatch> batches_;
   std::int64_t nbatch_ = 0;
   DevBuf<float> phiT32_;
-  cudaStream_t side_ = nullptr;
+  cudaStream_t side_ = nullptr, copy_ = nullptr;
+  cudaEvent_t ev_phi_ready_ = nullptr, ev_theta_ready_ = nullptr, ev_copy_done_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;

@@ -82,6 +82,7 @@ def lib():
     L.bnmc_gpu_upload.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_upload_state.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_upload_sweep_inputs.argtypes = [c_void_p, POINTER(_Store)]
+    L.bnmc_gpu_sweep_store.argtypes = [c_void_p, POINTER(_Store), c_int64, POINTER(c_double), POINTER(c_int)]
     L.bnmc_gpu_sweep_phases.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_char_p), c_int,
                                         POINTER(c_int)]
     L.bnmc_gpu_nccl_unique_id.argtypes = [c_void_p]
@@ -432,14 +433,17 @@ class Engine:
         Borrow semantics of the reference: the caller's latent state is read on every
         call (the caller may have changed it) and written back after the sweep; the
         observed data is uploaded once per bound store."""
+        lj, acc = c_double(), c_int()
         if self._bound is not store:
             self.upload(store)
+            _raise(lib().bnmc_gpu_sweep(self._h, it, ctypes.byref(lj), ctypes.byref(acc)), self._h)
+            self.download(store)
         else:
-            st = store._view()  # only what the sweep reads (bnmc_gpu_upload_sweep_inputs)
-            _raise(lib().bnmc_gpu_upload_sweep_inputs(self._h, ctypes.byref(st)), self._h)
-        lj, acc = c_double(), c_int()
-        _raise(lib().bnmc_gpu_sweep(self._h, it, ctypes.byref(lj), ctypes.byref(acc)), self._h)
-        self.download(store)
+            # upload what the sweep reads, sweep, write back (phi / theta copies overlap
+            # the z-step): bnmc_gpu_sweep_store
+            st = store._view()
+            _raise(lib().bnmc_gpu_sweep_store(self._h, ctypes.byref(st), it, ctypes.byref(lj), ctypes.byref(acc)),
+                   self._h)
         if mh_accepted is not None:
             mh_accepted.append(bool(acc.value))
         return lj.value
