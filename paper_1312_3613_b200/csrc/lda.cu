@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.fq_len) *a.fq_len = 0;  // this sweep's fallback queue
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
-  const std::int64_t chunk = (a.nvb + kColStripes - 1) / kColStripes;
+  const int stripes = static_cast<int>(gridDim.y);
+  const std::int64_t chunk = (a.nvb + stripes - 1) / stripes;
   const std::int64_t b0 = blockIdx.y * chunk, b1 = min(a.nvb, b0 + chunk);
   double sg = 0.0, sl = 0.0;
   if (k < a.K) {
@@ -331,14 +332,14 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const int t = atomicAdd(&a.ticket[blockIdx.x], 1);
-    last = t == kColStripes - 1;
+    last = t == stripes - 1;
     if (last) a.ticket[blockIdx.x] = 0;  // every stripe has arrived: reset for the next sweep
   }
   __syncthreads();
   if (!last || ty != 0 || k >= a.K) return;
   __threadfence();
   double g = 0.0, l = 0.0;
-  for (int s = 0; s < kColStripes; ++s) {
+  for (int s = 0; s < stripes; ++s) {
     g += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2]);
     l += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2 + 1]);
   }
@@ -2023,7 +2024,9 @@ class Lda final : public Model {
     tpart_.alloc(std::max<std::int64_t>(Ml_, 1));
     docs_per_block_ = std::max<std::int64_t>(1, 4096 / K_);
     nb_doc_ = (Ml_ + docs_per_block_ - 1) / docs_per_block_;
+    // grid sizes of the small reductions, scaled to the work (r01 v47 tuning)
     nbw_ = 148 * 4;
+    if (const char* e = std::getenv("BNMC_WTERM_BLOCKS")) nbw_ = std::max(1, std::atoi(e));
     zpart_.alloc(nbw_);
     fq_.alloc(std::max<std::int64_t>(Nl_, 1));
     fq_len_.alloc(1);
@@ -2038,6 +2041,8 @@ class Lda final : public Model {
       if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
     }
     nvb_ = (V_ + phi_rows_ - 1) / phi_rows_;
+    col_stripes_ = static_cast<int>(std::min<std::int64_t>(kColStripes, std::max<std::int64_t>(4, nvb_ / 96)));
+    if (const char* e = std::getenv("BNMC_COL_STRIPES")) col_stripes_ = std::min(kColStripes, std::max(1, std::atoi(e)));
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
     ticket_.alloc((K_ + 31) / 32 + 1);
     ticket_.zero(nullptr);
@@ -2266,7 +2271,7 @@ class Lda final : public Model {
           default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
         }
         mark(st, "phi_gamma");
-        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, kColStripes), dim3(256), 0, st, a);
+        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, col_stripes_), dim3(256), 0, st, a);
         fq_reset_ = true;
       }
       mark(st, "phi_colsum");
@@ -2820,7 +2825,7 @@ class Lda final : public Model {
   std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0, n_wunits_ = 0;
   DevBuf<std::int64_t> wunits_;
   bool zt_wu_ = true;
-  int nbw_ = 1;
+  int nbw_ = 1, col_stripes_ = kColStripes;
   float screen_margin_ = kScreenMargin;
   bool fq_reset_ = false;  // phi_colsum2 of this sweep zeroes the fallback queue
 
