@@ -1275,7 +1275,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <int KQ>
 __global__ void __launch_bounds__(256) zstage_kernel(LdaArgs a, const std::int64_t* iter_p, const ZBatch* batches,
                                                      std::int64_t nbatch, int ns, int stride16) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned row_bytes = 16u * KQ;
   const std::size_t slot_bytes = static_cast<std::size_t>(32) * stride16 * 16;
