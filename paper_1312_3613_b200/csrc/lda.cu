@@ -1945,6 +1945,10 @@ class Lda final : public Model {
     Ml_ = d1_ - d0_;
     tok0_ = d.doc_offsets[d0_];
     Nl_ = d.doc_offsets[d1_] - tok0_;
+    // per-GPU token and document indices are 32-bit in the fallback queue and the
+    // z-step's work units: shard larger corpora across more GPUs
+    require(Nl_ < (1ll << 31) && Ml_ < (1ll << 31), BNMC_GPU_ERR_ARG,
+            "LDA shard too large: < 2^31 tokens and documents per GPU");
     off_host_.resize(static_cast<std::size_t>(Ml_) + 1);
     for (std::int64_t m = 0; m <= Ml_; ++m) off_host_[m] = d.doc_offsets[d0_ + m] - tok0_;
 
