@@ -96,6 +96,23 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
+// N block sums with one pair of barriers. scratch: >= 32 * N doubles. Results valid in
+// every thread; fixed order as block_sum.
+template <int N>
+__device__ __forceinline__ void block_sum_n(double (&v)[N], double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) scratch[i * 32 + wid] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_sum(lane < nw ? scratch[i * 32 + lane] : 0.0);
+}
+
 // Model-specific device state behind one context.
 struct Model {
   virtual ~Model() = default;

@@ -91,6 +91,7 @@ struct LdaArgs {
   int2* fq;          // screen fallback queue: (local token, local document) [Nl]
   int* fq_len;
   double* wpart;     // [nbw] w-factor pieces per wterm block
+  double* ttpart;    // [nbw] per wterm block: its slice of tpart (single-rank path)
   int nbw;           // wterm_kernel blocks
   double* doc_part;  // [Ml][3] (eval path)
   double* red;       // [4]
@@ -298,22 +299,30 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   double sg = 0.0, sl = 0.0;
   if (k < a.K) {
     std::int64_t b = b0 + ty;
-    for (; b + 24 < b1; b += 32) {  // 4 independent loads in flight per operand
-      double g4[4], l4[4];
+    for (; b + 56 < b1; b += 64) {  // 8 independent loads in flight per operand
+      double g8[8], l8[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        g4[j] = a.gpart[(b + 8 * j) * a.K + k];
-        l4[j] = a.lpart[(b + 8 * j) * a.K + k];
+      for (int j = 0; j < 8; ++j) {
+        g8[j] = a.gpart[(b + 8 * j) * a.K + k];
+        l8[j] = a.lpart[(b + 8 * j) * a.K + k];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        sg += g4[j];
-        sl += l4[j];
+      for (int j = 0; j < 8; ++j) {
+        sg += g8[j];
+        sl += l8[j];
       }
     }
-    for (; b < b1; b += 8) {
-      sg += a.gpart[b * a.K + k];
-      sl += a.lpart[b * a.K + k];
+    double g8[8], l8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // the remaining < 8 rows of this thread, loads issued together
+      const std::int64_t bj = b + 8 * j;
+      g8[j] = bj < b1 ? a.gpart[bj * a.K + k] : 0.0;
+      l8[j] = bj < b1 ? a.lpart[bj * a.K + k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sg += g8[j];
+      sl += l8[j];
     }
   }
   sg_s[ty][tx] = sg;
@@ -336,12 +345,34 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
     if (last) a.ticket[blockIdx.x] = 0;  // every stripe has arrived: reset for the next sweep
   }
   __syncthreads();
-  if (!last || ty != 0 || k >= a.K) return;
+  if (!last) return;
   __threadfence();
+  // stripes s = ty, ty + 8, ... per warp (all loads in flight: stripes <= 64), then the
+  // 8 warp sums in order: fixed order, one L2 round trip
+  sg = sl = 0.0;
+  if (k < a.K) {
+    double g8[8], l8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int st = ty + 8 * j;
+      g8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2]) : 0.0;
+      l8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2 + 1]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sg += g8[j];
+      sl += l8[j];
+    }
+  }
+  __syncthreads();
+  sg_s[ty][tx] = sg;
+  sl_s[ty][tx] = sl;
+  __syncthreads();
+  if (ty != 0 || k >= a.K) return;
   double g = 0.0, l = 0.0;
-  for (int s = 0; s < stripes; ++s) {
-    g += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2]);
-    l += __ldcg(&a.spart[(static_cast<std::size_t>(s) * a.K + k) * 2 + 1]);
+  for (int j = 0; j < 8; ++j) {
+    g += sg_s[j][tx];
+    l += sl_s[j][tx];
   }
   a.S[k] = g;
   const double lS = log(g);
@@ -1573,15 +1604,28 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
     __syncthreads();
     if (!last) return;
     __threadfence();
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, f = 0.0;
-    for (std::int64_t m = threadIdx.x; m < a.Ml; m += blockDim.x) s0 += __ldcg(&a.tpart[m]);
-    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s1 += __ldcg(&a.zpart[b]);
-    for (int b = threadIdx.x; b < a.nbw; b += blockDim.x) s2 += __ldcg(&a.wpart[b]);
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) f += __ldcg(&a.phi_term[k]);
-    s0 = block_sum(s0, scratch);
-    s1 = block_sum(s1, scratch);
-    s2 = block_sum(s2, scratch);
-    f = block_sum(f, scratch);
+    // every block's partials, up to 4 per thread and operand in flight (one L2
+    // round trip for nbw <= 1024), then one combined block reduction
+    double s[4] = {0.0, 0.0, 0.0, 0.0};  // theta, z, w pieces; phi factor
+    for (int b0 = threadIdx.x; b0 < a.nbw; b0 += 4 * blockDim.x) {
+      double t4[4], z4[4], w4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int b = b0 + j * blockDim.x;
+        t4[j] = b < a.nbw ? __ldcg(&a.ttpart[b]) : 0.0;
+        z4[j] = b < a.nbw ? __ldcg(&a.zpart[b]) : 0.0;
+        w4[j] = b < a.nbw ? __ldcg(&a.wpart[b]) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s[0] += t4[j];
+        s[1] += z4[j];
+        s[2] += w4[j];
+      }
+    }
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) s[3] += __ldcg(&a.phi_term[k]);
+    block_sum_n<4>(s, scratch);
+    const double s0 = s[0], s1 = s[1], s2 = s[2], f = s[3];
     if (threadIdx.x == 0) {
       const double lj = ((f + s0) + s1) + s2;
       const std::int64_t it = *o.iter;
@@ -1593,40 +1637,48 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
 }
 
 template <bool FINAL>
-__global__ void __launch_bounds__(256) wterm_kernel(LdaArgs a, Outputs o, int advance) {
-  __shared__ double scratch[32];
+__global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int advance) {
+  __shared__ double scratch[4 * 32];
   pdl_wait();
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   const std::int64_t g0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  // w-factor over the topic-word cells (static cell -> thread assignment: deterministic);
-  // 4 cells per thread iteration with their loads issued together
+  // w-factor over the topic-word cells, static cell -> thread assignment (deterministic).
+  // The padded [V][Kp] arrays are read as 4-cell vectors (Kp % 4 == 0: a vector never
+  // crosses a row; padding cells have n = 0 and logS is zero-padded to Kp), two vectors
+  // per thread in flight; no per-cell index arithmetic beyond one modulo per vector.
   double accw = 0.0;
-  const std::int64_t ncw = static_cast<std::int64_t>(a.V) * a.K;
   if (a.logg_valid) {
-    for (std::int64_t c0 = g0; c0 < ncw; c0 += 4 * stride) {
-      int n[4];
-      double lg[4];
-      int kk[4];
+    const std::int64_t nvec = static_cast<std::int64_t>(a.V) * a.Kp / 4;
+    const bool narrow = nvec < (std::int64_t{1} << 29);  // 4 * nvec fits 31 bits
+    const int4* n4 = reinterpret_cast<const int4*>(a.nkw);
+    const double2* l2 = reinterpret_cast<const double2*>(a.logg);
+    for (std::int64_t c0 = g0; c0 < nvec; c0 += 2 * stride) {
+      int4 n[2];
+      double2 la[2], lb[2];
+      int k0[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 2; ++j) {
         const std::int64_t c = c0 + j * stride;
-        n[j] = 0;
-        lg[j] = 0.0;
-        kk[j] = 0;
-        if (c < ncw) {
-          const std::int64_t v = c / a.K;
-          kk[j] = static_cast<int>(c - v * a.K);
-          const std::size_t i = static_cast<std::size_t>(v) * a.Kp + kk[j];
-          n[j] = a.nkw[i];
-          lg[j] = a.logg[i];
+        n[j] = make_int4(0, 0, 0, 0);
+        k0[j] = 0;
+        if (c < nvec) {
+          n[j] = n4[c];
+          la[j] = l2[2 * c];
+          lb[j] = l2[2 * c + 1];
+          k0[j] = narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
+                         : static_cast<int>((4 * c) % a.Kp);
         }
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (n[j]) accw += static_cast<double>(n[j]) * (lg[j] - a.logS[kk[j]]);  // log phi = log g - log S
+      for (int j = 0; j < 2; ++j) {  // log phi = log g - log S
+        if (n[j].x) accw += static_cast<double>(n[j].x) * (la[j].x - __ldg(&a.logS[k0[j]]));
+        if (n[j].y) accw += static_cast<double>(n[j].y) * (la[j].y - __ldg(&a.logS[k0[j] + 1]));
+        if (n[j].z) accw += static_cast<double>(n[j].z) * (lb[j].x - __ldg(&a.logS[k0[j] + 2]));
+        if (n[j].w) accw += static_cast<double>(n[j].w) * (lb[j].y - __ldg(&a.logS[k0[j] + 3]));
+      }
     }
   } else {
-    for (std::int64_t c = g0; c < ncw; c += stride) {
+    for (std::int64_t c = g0; c < static_cast<std::int64_t>(a.V) * a.K; c += stride) {
       const std::int64_t v = c / a.K;
       const int k = static_cast<int>(c - v * a.K);
       const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
@@ -1637,21 +1689,35 @@ __global__ void __launch_bounds__(256) wterm_kernel(LdaArgs a, Outputs o, int ad
       }
     }
   }
-  // z-factor over the doc-topic cells
+  // z-factor over the doc-topic cells: the flat [Ml][K] arrays as 4-cell vectors
+  // (cudaMalloc bases are 256-byte aligned), the ragged tail scalar
   double accz = 0.0;
-  const std::int64_t ncz = a.Ml * a.K;
-  for (std::int64_t c = g0; c < ncz; c += stride) {
-    const int n = a.nmk[c];
-    if (n) {
-      const double x = a.theta[c];
-      accz += static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY);
-    }
+  const std::int64_t ncz = a.Ml * a.K, nvz = ncz / 4;
+  const int4* m4 = reinterpret_cast<const int4*>(a.nmk);
+  const double2* t2 = reinterpret_cast<const double2*>(a.theta);
+  auto zterm = [](int n, double x) {
+    return n ? static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY) : 0.0;
+  };
+  for (std::int64_t c = g0; c < nvz; c += stride) {
+    const int4 n = m4[c];
+    const double2 x = t2[2 * c], y = t2[2 * c + 1];
+    accz += zterm(n.x, x.x);
+    accz += zterm(n.y, x.y);
+    accz += zterm(n.z, y.x);
+    accz += zterm(n.w, y.y);
   }
-  accw = block_sum(accw, scratch);
-  accz = block_sum(accz, scratch);
+  if (g0 < ncz - 4 * nvz) accz += zterm(a.nmk[4 * nvz + g0], a.theta[4 * nvz + g0]);
+  // the theta factor's per-document pieces, spread over the grid (single-rank path:
+  // the last block then reads nbw partials instead of Ml)
+  double acct = 0.0;
+  if constexpr (FINAL)
+    for (std::int64_t m = g0; m < a.Ml; m += stride) acct += a.tpart[m];
+  double v[3] = {accw, accz, acct};
+  block_sum_n<3>(v, scratch);
   if (threadIdx.x == 0) {
-    a.wpart[blockIdx.x] = accw;
-    a.zpart[blockIdx.x] = accz;
+    a.wpart[blockIdx.x] = v[0];
+    a.zpart[blockIdx.x] = v[1];
+    if (FINAL) a.ttpart[blockIdx.x] = v[2];
   }
   loglik_finish<FINAL>(a, o, advance, scratch);
 }
@@ -2035,6 +2101,7 @@ class Lda final : public Model {
     fq_.alloc(std::max<std::int64_t>(Nl_, 1));
     fq_len_.alloc(1);
     wpart_.alloc(nbw_);
+    ttpart_.alloc(nbw_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
     // vs 42 at 1): enough threads to fill the GPU while the per-thread rejection loop
@@ -2052,7 +2119,8 @@ class Lda final : public Model {
     ticket_.zero(nullptr);
     gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     logg_.alloc(static_cast<std::size_t>(V_) * Kp_);
-    logS_.alloc(K_);
+    logS_.alloc(Kp_);
+    logS_.zero(nullptr);  // padding columns stay 0 (wterm_kernel reads 4-cell vectors)
     lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
@@ -2771,6 +2839,7 @@ class Lda final : public Model {
     a.tpart = tpart_.p;
     a.zpart = zpart_.p;
     a.wpart = wpart_.p;
+    a.ttpart = ttpart_.p;
     a.alpha = alpha_;
     a.beta = beta_;
     a.phi_norm = phi_norm_;
@@ -2861,7 +2930,7 @@ class Lda final : public Model {
   DevBuf<std::int64_t> off_;
   std::int64_t nvb_ = 1;
   int phi_rows_ = kPhiRowsMax;
-  DevBuf<double> gpart_, lpart_, spart_, logg_, logS_;
+  DevBuf<double> gpart_, lpart_, spart_, logg_, logS_, ttpart_;
   DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
       zpart_, wpart_;

@@ -99,6 +99,8 @@ def full(rep, dst, key):
         ia, ie = sh.index("Source"), sh.index("Instructions Executed")
         c = collections.Counter()
         for r in srows[2:]:
+            if len(r) <= max(ia, ie) or not r[ie].isdigit():
+                continue
             toks = r[ia].strip().split()
             if not toks:
                 continue
