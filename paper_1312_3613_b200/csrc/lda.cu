@@ -1636,6 +1636,10 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
   }
 }
 
+// wterm_kernel: 4-cell vectors per thread in flight (1..4 measured equal, r01 v52: the
+// kernel is bound by its launch and last-block tail, not its loads)
+constexpr int kWU = 2;
+
 template <bool FINAL>
 __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int advance) {
   __shared__ double scratch[4 * 32];
@@ -1652,29 +1656,29 @@ __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int
     const bool narrow = nvec < (std::int64_t{1} << 29);  // 4 * nvec fits 31 bits
     const int4* n4 = reinterpret_cast<const int4*>(a.nkw);
     const double2* l2 = reinterpret_cast<const double2*>(a.logg);
-    for (std::int64_t c0 = g0; c0 < nvec; c0 += 2 * stride) {
-      int4 n[2];
-      double2 la[2], lb[2];
-      int k0[2];
+    for (std::int64_t c0 = g0; c0 < nvec; c0 += kWU * stride) {
+      int4 n[kWU];
+      double2 la[kWU], lb[kWU];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < kWU; ++j) {
         const std::int64_t c = c0 + j * stride;
         n[j] = make_int4(0, 0, 0, 0);
-        k0[j] = 0;
         if (c < nvec) {
           n[j] = n4[c];
           la[j] = l2[2 * c];
           lb[j] = l2[2 * c + 1];
-          k0[j] = narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
-                         : static_cast<int>((4 * c) % a.Kp);
         }
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {  // log phi = log g - log S
-        if (n[j].x) accw += static_cast<double>(n[j].x) * (la[j].x - __ldg(&a.logS[k0[j]]));
-        if (n[j].y) accw += static_cast<double>(n[j].y) * (la[j].y - __ldg(&a.logS[k0[j] + 1]));
-        if (n[j].z) accw += static_cast<double>(n[j].z) * (lb[j].x - __ldg(&a.logS[k0[j] + 2]));
-        if (n[j].w) accw += static_cast<double>(n[j].w) * (lb[j].y - __ldg(&a.logS[k0[j] + 3]));
+      for (int j = 0; j < kWU; ++j) {  // log phi = log g - log S
+        const std::int64_t c = c0 + j * stride;
+        if (c >= nvec || (n[j].x | n[j].y | n[j].z | n[j].w) == 0) continue;
+        const int k0 = narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
+                              : static_cast<int>((4 * c) % a.Kp);
+        if (n[j].x) accw += static_cast<double>(n[j].x) * (la[j].x - __ldg(&a.logS[k0]));
+        if (n[j].y) accw += static_cast<double>(n[j].y) * (la[j].y - __ldg(&a.logS[k0 + 1]));
+        if (n[j].z) accw += static_cast<double>(n[j].z) * (lb[j].x - __ldg(&a.logS[k0 + 2]));
+        if (n[j].w) accw += static_cast<double>(n[j].w) * (lb[j].y - __ldg(&a.logS[k0 + 3]));
       }
     }
   } else {
