@@ -394,15 +394,19 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         lat = [n for n in store.names if not store.observed[n]]
         if model == "lda":
             # per step: this rank's z slice up (the sweep reads only z of the latent state:
-            # bnmc_gpu_upload_sweep_inputs); z and theta slices + the global phi + lj down
-            nz = sites_local * 8
-            up = nz
-            down = nz + (sites_local // L) * K * 8 + K * V * 8 + 8
+            # bnmc_gpu_upload_sweep_inputs), z and theta slices + the global phi + lj down --
+            # counted by the library
+            # (bnmc_gpu_transfer_stats) after the bind call below
+            up = down = 0
         else:
             up = sum(store.arrays[n].nbytes for n in lat)
             down = up + 8
         eng.sweep(store, it)  # bind (uploads the observed data once, outside the timed region)
         it += 1
+        if model == "lda":
+            eng.sweep(store, it)
+            it += 1
+            up, down = eng.transfer_stats()  # the bytes the library actually moves per call
         if dist:
             dist.barrier()
         torch.cuda.synchronize()

@@ -139,6 +139,10 @@ int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_a
  * variables are unspecified. */
 int bnmc_gpu_sweep_store(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store, int64_t iter, double* log_joint,
                          int* mh_accepted);
+/* Host <-> device bytes moved by the last bnmc_gpu_sweep_store call (LDA: z up; z,
+ * theta, phi and the log-joint / accept ring entry down).  Models other than LDA
+ * report only the ring entry. */
+int bnmc_gpu_transfer_stats(bnmc_gpu_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* n sweeps iter0..iter0+n-1 with one host sync; per-sweep outputs optional. */
 int bnmc_gpu_run(bnmc_gpu_ctx* ctx, int64_t iter0, int64_t n, double* log_joints, int* accepted);
 /* Engine::run (sampler.cpp:426-455) with a device-resident trace: burn-in + n kept

@@ -365,9 +365,11 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     require(iter >= 0, BNMC_GPU_ERR_ARG, "iteration must be non-negative");
     require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
             "store view is incomplete");
+    c->model->h2d_bytes = c->model->d2h_bytes = 0;
     c->model->upload_sweep_inputs(*s, c->stream);
     set_iter(c, iter);
     launch_sweep(c);
+    c->model->d2h_bytes += static_cast<std::int64_t>(sizeof(double) + sizeof(int));  // the ring entry
     if (!c->model->download_overlapped(*s, c->stream)) {
       read_ring(c, iter, 1, log_joint, mh_accepted);
       check_device_error(c);
@@ -376,6 +378,15 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     }
     read_ring(c, iter, 1, log_joint, mh_accepted);  // synchronises the stream (and the copies)
     check_device_error(c);
+  });
+}
+
+int bnmc_gpu_transfer_stats(bnmc_gpu_ctx* c, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  if (!c || !h2d_bytes || !d2h_bytes) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  return guarded(c, [&] {
+    require(c->model != nullptr, BNMC_GPU_ERR_RUNTIME, "no model");
+    *h2d_bytes = c->model->h2d_bytes;
+    *d2h_bytes = c->model->d2h_bytes;
   });
 }
 

@@ -116,6 +116,9 @@ __device__ __forceinline__ void block_sum_n(double (&v)[N], double* scratch) {
 // Model-specific device state behind one context.
 struct Model {
   virtual ~Model() = default;
+  // host <-> device bytes of the current Engine::sweep call (bnmc_gpu_transfer_stats);
+  // counted by the models that implement the bound-store path
+  std::int64_t h2d_bytes = 0, d2h_bytes = 0;
   virtual void upload(const bnmc_gpu_store& s, cudaStream_t st) = 0;
   virtual void download(const bnmc_gpu_store& s, cudaStream_t st) = 0;
   // Uploads only the latent (unobserved) variables: the observed data already on

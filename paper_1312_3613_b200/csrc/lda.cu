@@ -2212,6 +2212,7 @@ class Lda final : public Model {
       if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
       BNMC_CUDA(cudaMemcpyAsync(stage64_.p, s.ival[var_z_] + tok0_, sizeof(std::int64_t) * Nl_,
                                 cudaMemcpyHostToDevice, st));
+      h2d_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * Nl_;
       i64_to_i32_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(stage64_.p, z_.p, Nl_, 0, K_, out.err);
     }
     LdaArgs a = args();
@@ -2269,6 +2270,14 @@ class Lda final : public Model {
   // phi and theta are final early in the sweep (after the phi block / the theta block):
   // their transpose + device-to-host copies run on a copy stream while the z-step and
   // the log-joint run; z follows the sweep on the main stream.
+  // Writes z back into the int64 store slice `dst` (enqueued on st).
+  void download_z(std::int64_t* dst, cudaStream_t st) {
+    if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
+    i32_to_i64_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(z_.p, stage64_.p, Nl_);
+    BNMC_CUDA(cudaMemcpyAsync(dst, stage64_.p, sizeof(std::int64_t) * Nl_, cudaMemcpyDeviceToHost, st));
+    d2h_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * Nl_;
+  }
+
   bool download_overlapped(const bnmc_gpu_store& s, cudaStream_t st) override {
     if (marks || observe_phi_ || Ml_ == 0) return false;
     const char* obs = s.observed;
@@ -2277,19 +2286,16 @@ class Lda final : public Model {
       BNMC_CUDA(cudaStreamWaitEvent(copy_, ev_phi_ready_, 0));
       transpose_kernel<<<dim3((K_ + 31) / 32, (V_ + 31) / 32), dim3(32, 8), 0, copy_>>>(phiT_.p, stage_phi_.p, V_, K_, Kp_, V_, S_.p);
       BNMC_CUDA(cudaMemcpyAsync(s.real[var_phi_], stage_phi_.p, stage_phi_.bytes(), cudaMemcpyDeviceToHost, copy_));
+      d2h_bytes += static_cast<std::int64_t>(stage_phi_.bytes());
     }
     if (!(obs && obs[var_theta_]) && s.real[var_theta_]) {
       BNMC_CUDA(cudaStreamWaitEvent(copy_, ev_theta_ready_, 0));
       BNMC_CUDA(cudaMemcpyAsync(s.real[var_theta_] + d0_ * K_, theta_.p, sizeof(double) * Ml_ * K_,
                                 cudaMemcpyDeviceToHost, copy_));
+      d2h_bytes += static_cast<std::int64_t>(sizeof(double)) * Ml_ * K_;
     }
     BNMC_CUDA(cudaEventRecord(ev_copy_done_, copy_));
-    if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) {
-      if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
-      i32_to_i64_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(z_.p, stage64_.p, Nl_);
-      BNMC_CUDA(cudaMemcpyAsync(s.ival[var_z_] + tok0_, stage64_.p, sizeof(std::int64_t) * Nl_,
-                                cudaMemcpyDeviceToHost, st));
-    }
+    if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) download_z(s.ival[var_z_] + tok0_, st);
     BNMC_CUDA(cudaStreamWaitEvent(st, ev_copy_done_, 0));  // the sweep call completes with both
     BNMC_CUDA(cudaGetLastError());
     return true;
@@ -2297,12 +2303,7 @@ class Lda final : public Model {
 
   void download(const bnmc_gpu_store& s, cudaStream_t st) override {
     const char* obs = s.observed;
-    if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) {
-      if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
-      i32_to_i64_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(z_.p, stage64_.p, Nl_);
-      BNMC_CUDA(cudaMemcpyAsync(s.ival[var_z_] + tok0_, stage64_.p, sizeof(std::int64_t) * Nl_,
-                                cudaMemcpyDeviceToHost, st));
-    }
+    if (!(obs && obs[var_z_]) && s.ival[var_z_] && Nl_ > 0) download_z(s.ival[var_z_] + tok0_, st);
     if (!(obs && obs[var_theta_]) && s.real[var_theta_] && Ml_ > 0)
       BNMC_CUDA(cudaMemcpyAsync(s.real[var_theta_] + d0_ * K_, theta_.p, sizeof(double) * Ml_ * K_,
                                 cudaMemcpyDeviceToHost, st));

@@ -83,6 +83,7 @@ def lib():
     L.bnmc_gpu_upload_state.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_upload_sweep_inputs.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_sweep_store.argtypes = [c_void_p, POINTER(_Store), c_int64, POINTER(c_double), POINTER(c_int)]
+    L.bnmc_gpu_transfer_stats.argtypes = [c_void_p, POINTER(c_int64), POINTER(c_int64)]
     L.bnmc_gpu_sweep_phases.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_char_p), c_int,
                                         POINTER(c_int)]
     L.bnmc_gpu_nccl_unique_id.argtypes = [c_void_p]
@@ -447,6 +448,12 @@ class Engine:
         if mh_accepted is not None:
             mh_accepted.append(bool(acc.value))
         return lj.value
+
+    def transfer_stats(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes of the last bound-store sweep call."""
+        up, down = c_int64(), c_int64()
+        _raise(lib().bnmc_gpu_transfer_stats(self._h, ctypes.byref(up), ctypes.byref(down)), self._h)
+        return up.value, down.value
 
     def sweep_device(self, it: int):
         """One sweep on the device-resident state (no host copies); returns (lj, accepted)."""

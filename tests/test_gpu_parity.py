@@ -161,6 +161,48 @@ def test_lda_bad_assignment_raises(g):
         e.upload(s)
 
 
+@pytest.mark.parametrize("K", [7, 300])
+def test_lda_bound_store_transfers(g, K):
+    """Engine::sweep on a bound store: the bytes moved per call (z up; z, theta, phi and
+    the ring entry down), the caller's edits between calls are what the next sweep
+    reads, and an out-of-range edit raises through the device check."""
+    rs = np.random.default_rng(K)
+    V, M, L = 50, 12, 30
+    N = M * L
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+    e = g.Engine("lda", hyper, g.RunConfig(seed=3))
+    s = e.allocate()
+    s["w"] = rs.integers(0, V, N)
+    e.prior_init(s, 3)
+    e.sweep(s, 0)  # binds
+    e.sweep(s, 1)
+    up, down = e.transfer_stats()
+    assert up == N * 8
+    assert down == N * 8 + M * K * 8 + K * V * 8 + 8 + 4
+    # the caller's edit is what the next sweep reads: same result as a fresh engine
+    z = s["z"].copy()
+    z[::3] = (z[::3] + 1) % K
+    s["z"] = z
+    e2 = g.Engine("lda", hyper, g.RunConfig(seed=3))
+    s2 = e2.allocate()
+    for n in s.names:
+        s2[n] = s[n].copy()
+    lj = e.sweep(s, 2)
+    lj2 = e2.sweep(s2, 2)
+    assert lj == lj2 and np.array_equal(s["z"], s2["z"]) and np.array_equal(s["phi"], s2["phi"])
+    bad = s["z"].copy()
+    bad[5] = K
+    s["z"] = bad
+    with pytest.raises(g.BnmcError):
+        e.sweep(s, 3)
+    bad[5] = -1
+    s["z"] = bad
+    with pytest.raises(g.BnmcError):
+        e.sweep(s, 3)
+    e.close()
+    e2.close()
+
+
 def _gen_lda(restatement, reference, M, V, K, L, seed):
     w, _, _ = reference.gen_lda(M, V, K, L, seed)
     off = np.arange(M + 1, dtype=np.int64) * L
