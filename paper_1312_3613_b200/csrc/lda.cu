@@ -74,6 +74,12 @@ struct LdaArgs {
   double* phiT;
   float* phiT32;     // fp32 copy of phiT [V][Kp32], columns permuted by phys32 (screen only)
   int Kp32, G32, R32, CW32; // screen layout: Kp32 = CW32 * G32 * R32
+  unsigned short* phiT16;    // fp16 row-scaled copy [V][Kp16], columns permuted by phys16 (level-1 screen)
+  int Kp16, RH;              // Kp16 = 64 RH
+  float* thS32;              // [Ml][K8] theta/S in fp32 (level-1 units -> level 2)
+  int2* q2;                  // level-2 queue (t, m)
+  int* q2_len;
+  int col_stripes;           // phi_colsum2 stripe blocks (extra y-blocks convert phiT16 rows)
   double* logphiT;   // exact mode only
   double* theta;
   int* nkw;          // [V][Kp]
@@ -285,15 +291,29 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
 // result is deterministic.
 constexpr int kColStripes = 64;
 
+__device__ void h16_rows(const LdaArgs& a, std::int64_t w0, std::int64_t nw);
+
+// Blocks with blockIdx.y >= col_stripes convert the new phi rows to fp16 for the
+// level-1 screen (h16_rows) -- the conversion needs the rows, not S, so it runs beside
+// the column sums instead of after them.
 __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __shared__ double sg_s[8][33], sl_s[8][33];
   __shared__ bool last;
   pdl_wait();
   pdl_trigger();
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.fq_len) *a.fq_len = 0;  // this sweep's fallback queue
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // this sweep's redraw queues
+    if (a.fq_len) *a.fq_len = 0;
+    if (a.q2_len) *a.q2_len = 0;
+  }
+  const int stripes = a.col_stripes;
+  if (static_cast<int>(blockIdx.y) >= stripes) {
+    const std::int64_t hb = static_cast<std::int64_t>(blockIdx.y - stripes) * gridDim.x + blockIdx.x;
+    const std::int64_t nhb = static_cast<std::int64_t>(gridDim.y - stripes) * gridDim.x;
+    h16_rows(a, hb * 8 + (threadIdx.x >> 5), nhb * 8);
+    return;
+  }
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
-  const int stripes = static_cast<int>(gridDim.y);
   const std::int64_t chunk = (a.nvb + stripes - 1) / stripes;
   const std::int64_t b0 = blockIdx.y * chunk, b1 = min(a.nvb, b0 + chunk);
   double sg = 0.0, sl = 0.0;
@@ -1250,6 +1270,426 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
 }
 
 // ---------------------------------------------------------------------------------
+// z block, two-level screen (experimental, BNMC_ZSCREEN_H=1): fp16 rows, then fp32, then fp64
+// ---------------------------------------------------------------------------------
+// The z-step moves one phi row per token from L2 (ncu r01: at the L2 read bandwidth),
+// so the row bytes set its time.  Level 1 reads the rows in fp16 (phiT16: 2 bytes per
+// candidate, half of phiT32) with theta/S in fp16 and FHFMA (fp16 x fp16 products,
+// exact in fp32, fp32 accumulation):
+//  * per-row scale c_v and per-document scale a_d (powers of two) put each row's and
+//    document's maximum in [2^14, 2^15) -- the draw does not depend on them (both
+//    scale every weight of the token alike);
+//  * error of every level-1 prefix / total / u * total against the exact scaled value:
+//    quantisation of both factors 2^-11 + 2^-11 relative (normal range) or 2^-25
+//    absolute per factor (fp16 subnormals), fp32 rounding <= 24 * 2^-24 relative, so
+//    <= 2^-9.9 * value + A with A = 2^-24 (32768 K + Theta_d), Theta_d = sum of the
+//    document's fp16 theta values (every fp16 value <= 2^15);
+//  * a token is decided when u * total lies >= mg1 = 2^-8.5 * uf + 4 A inside its
+//    candidate's interval (covers both boundaries' and uf's errors);
+//    otherwise it is queued for level 2 (q2).
+// Level 2 (zscreen_q_kernel) redraws the queued tokens with the fp32 transposed screen
+// (phiT32 rows, theta/S rows the level-1 units left in thS32) and queues what is still
+// ambiguous for the fp64 draw (zfallback_kernel).  The pick is the fp64 product-form
+// draw in every case.
+__host__ __device__ __forceinline__ int phys16(int k, int RH) {
+  const int c = k >> 4, j = k & 15, gl = c / RH, r = c - gl * RH;
+  return ((r << 2) + gl) * 16 + j;
+}
+
+__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
+  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+  return c;
+}
+
+struct Oct16 {
+  unsigned v[8];  // 16 halves
+};
+
+__device__ __forceinline__ Oct16 ldg256h(const unsigned short* p) {
+  Oct16 o;
+  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(o.v[0]), "=r"(o.v[1]), "=r"(o.v[2]), "=r"(o.v[3]), "=r"(o.v[4]), "=r"(o.v[5]), "=r"(o.v[6]),
+        "=r"(o.v[7])
+      : "l"(p));
+  return o;
+}
+
+// fp16 rows of the current phi numerator (phiT32 -> phiT16, row-scaled); warps w0,
+// w0 + nw, ... of the caller each take one row at a time.  K <= 128.
+__device__ void h16_rows(const LdaArgs& a, std::int64_t w0, std::int64_t nw) {
+  // lane L holds phiT32 physical columns 4L .. 4L + 3 (one coalesced 16-byte load per
+  // row; Kp32 <= 128); two rows per warp iteration
+  const int lane = threadIdx.x & 31;
+  const int p0 = 4 * lane;
+  int kl[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // logical candidate of physical column p0 + j (phys32 inverse)
+    const int p = p0 + j, c = p / a.CW32, jj = p - c * a.CW32, r = c / a.G32, gl = c - r * a.G32;
+    kl[j] = (gl * a.R32 + r) * a.CW32 + jj;
+  }
+  const bool mine = p0 < a.Kp32;
+  for (std::int64_t v0 = w0; v0 < a.V; v0 += 2 * nw) {
+    float4 x[2];
+    float mx[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const std::int64_t v = v0 + i * nw;
+      x[i] = (mine && v < a.V) ? *reinterpret_cast<const float4*>(a.phiT32 + static_cast<std::size_t>(v) * a.Kp32 + p0)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {  // (padding columns hold 0)
+      mx[i] = fmaxf(fmaxf(x[i].x, x[i].y), fmaxf(x[i].z, x[i].w));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const std::int64_t v = v0 + i * nw;
+      if (!mine || v >= a.V) continue;
+      const int e = mx[i] > 0.0f ? min(127, max(-126, 14 - ilogbf(mx[i]))) : 0;
+      const float sc = ldexpf(1.0f, e);
+      unsigned short* out = a.phiT16 + static_cast<std::size_t>(v) * a.Kp16;
+      const float xv[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (kl[j] < a.K) out[phys16(kl[j], a.RH)] = __half_as_ushort(__float2half_rn(xv[j] * sc));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) phi_h16_kernel(LdaArgs a) {
+  const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
+  h16_rows(a, static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5), nw);
+}
+
+// max / sum over a unit's team (a warp for warp units, the CTA otherwise)
+template <bool WU>
+__device__ __forceinline__ float team_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if constexpr (WU) return v;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  v = lane < nw ? red[lane] : 0.0f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <bool WU>
+__device__ __forceinline__ float team_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if constexpr (WU) return v;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  v = lane < nw ? red[lane] : 0.0f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr float kL1Rel = 0.0027622f;  // level-1 margin relative to u * total (>= 2^-8.5)
+
+// Level 1.  RH: 16-candidate rounds per lane (K <= 64 * RH); units as zscreen_t_kernel.
+// Shared memory per team: thh [4][16 RH + 8] halves (fp16 theta/S * a_d), csum
+// [warps][32][16] floats, cnt [K] ints, red [32] floats.
+template <int RH, bool WU>
+__global__ void __launch_bounds__(kZThreads, 3) zscreen_h_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  constexpr int G = 4, KLH = 16 * RH, KLHP = KLH + 8, C = G * RH;
+  static_assert(C <= 16, "csum rows hold 16 chunk sums");
+  const int kWarps = blockDim.x >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
+  const int warp = threadIdx.x >> 5;
+  const int kpad = (a.K + 3) & ~3;
+  // team area: [thh G*KLHP halves][csum][cnt kpad][red 32]
+  const std::size_t team_floats = G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16) + kpad + 32;
+  float* base = reinterpret_cast<float*>(smem_raw) + (WU ? warp * team_floats : 0);
+  unsigned short* thh = reinterpret_cast<unsigned short*>(base);
+  float* csum = base + G * KLHP / 2 + (WU ? 0 : warp * 32 * 16);
+  int* cnt_s = reinterpret_cast<int*>(base + G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16));
+  float* red = base + G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16) + kpad;
+  pdl_wait();
+  pdl_trigger();
+  const std::int64_t iter = *iter_p;
+  const int rl = min(RH, max(0, (a.K - gl * KLH + 15) / 16));
+  const int tid_u = WU ? lane : static_cast<int>(threadIdx.x);
+  const int nthr_u = WU ? 32 : static_cast<int>(blockDim.x);
+  const std::int64_t nunits = WU ? a.n_wunits : a.n_units;
+  const std::int64_t* units = WU ? a.wunits : a.units;
+  const std::int64_t ustart = WU ? static_cast<std::int64_t>(blockIdx.x) * kWarps + warp : blockIdx.x;
+  const std::int64_t ustride = WU ? static_cast<std::int64_t>(gridDim.x) * kWarps : gridDim.x;
+  const int K8 = (a.K + 7) & ~7;
+
+  for (std::int64_t unit = ustart; unit < nunits; unit += ustride) {
+    const std::int64_t m = units[unit * 3], t0 = units[unit * 3 + 1], t1 = units[unit * 3 + 2];
+    const double* thg = a.theta + m * a.K;
+    float* ths = a.thS32 + m * K8;  // theta/S in fp32 for level 2 (natural order, zero-padded)
+    // theta/S (fp32) and its maximum; the document scale a_d; fp16 operands and Theta_d
+    float mx = 0.0f;
+    for (int k = tid_u; k < G * KLH; k += nthr_u) {
+      const float x = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+      if (k < K8) ths[k] = x;
+      mx = fmaxf(mx, x);
+      if (k < a.K) cnt_s[k] = 0;
+    }
+    mx = team_max<WU>(mx, red);
+    const float ad = ldexpf(1.0f, mx > 0.0f ? min(127, max(-126, 14 - ilogbf(mx))) : 0);
+    float th_sum = 0.0f;
+    for (int k = tid_u; k < G * KLH; k += nthr_u) {
+      const float x = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+      const __half h = __float2half_rn(x * ad);
+      thh[(k / KLH) * KLHP + k % KLH] = __half_as_ushort(h);
+      th_sum += __half2float(h);
+    }
+    th_sum = team_sum<WU>(th_sum, red);
+    const float A = 0x1p-24f * (32768.0f * static_cast<float>(a.K) + th_sum);
+    if constexpr (WU) __syncwarp();
+    else __syncthreads();
+    unsigned tw[KLH / 2];
+#pragma unroll
+    for (int i = 0; i < KLH / 2; i += 4) {
+      const uint4 t = *reinterpret_cast<const uint4*>(thh + gl * KLHP + 2 * i);
+      tw[i] = t.x, tw[i + 1] = t.y, tw[i + 2] = t.z, tw[i + 3] = t.w;
+    }
+    const std::int64_t bstep = WU ? 32 : kWarps * 32;
+    std::int64_t b0 = t0 + (WU ? 0 : warp * 32);
+    int wl_next = b0 + lane < t1 ? __ldg(a.w + b0 + lane) : 0;
+    for (; b0 < t1; b0 += bstep) {
+      const std::int64_t t = b0 + lane;
+      const bool valid = t < t1;
+      const int wl = wl_next;
+      wl_next = b0 + bstep + lane < t1 ? __ldg(a.w + b0 + bstep + lane) : 0;  // next batch, in flight
+      // (1) level-1 chunk sums: 4 lanes per token, 16 candidates per round; the rows of
+      // sub-batch s + 1 are in flight while sub-batch s is summed
+      const std::int64_t left = (t1 - b0 + 7) / 8;
+      const int nsub = left < 4 ? static_cast<int>(left) : 4;  // warp-uniform
+      Oct16 cur[RH], nxt[RH];
+      auto fetch = [&](int s2, Oct16 (&ph)[RH]) {
+        const int wv = __shfl_sync(0xffffffffu, wl, s2 * 8 + gid);
+        const unsigned short* row = a.phiT16 + static_cast<std::size_t>(wv) * a.Kp16;
+#pragma unroll
+        for (int r = 0; r < RH; ++r) {
+          if (r < rl) ph[r] = ldg256h(row + 16 * (r * G + gl));
+          else ph[r] = Oct16{};
+        }
+      };
+      fetch(0, cur);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (s >= nsub) break;  // warp-uniform
+        if (s + 1 < nsub) fetch(s + 1, nxt);
+        const int src = s * 8 + gid;
+#pragma unroll
+        for (int r = 0; r < RH; ++r) {
+          float sr = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            sr = fhfma(static_cast<unsigned short>(tw[8 * r + j] & 0xffffu), static_cast<unsigned short>(cur[r].v[j] & 0xffffu), sr);
+            sr = fhfma(static_cast<unsigned short>(tw[8 * r + j] >> 16), static_cast<unsigned short>(cur[r].v[j] >> 16), sr);
+          }
+          csum[cs_idx(src, gl * RH + r)] = sr;
+        }
+#pragma unroll
+        for (int r = 0; r < RH; ++r) cur[r] = nxt[r];
+      }
+      __syncwarp();
+      // (2) search: lane = token
+      if (valid) {
+        Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
+                        static_cast<std::uint64_t>(iter)));
+        const float u01 = static_cast<float>(rng.next_unit());
+        float P[C];
+        float run = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; c += 4) {
+          const float4 y = *reinterpret_cast<const float4*>(csum + cs_idx(lane, c));
+          run += y.x;
+          P[c] = run;
+          run += y.y;
+          P[c + 1] = run;
+          run += y.z;
+          P[c + 2] = run;
+          run += y.w;
+          P[c + 3] = run;
+        }
+        const float total = run;
+        const float uf = u01 * total;
+        const float mg = kL1Rel * uf + 4.0f * A;
+        int k = -1;
+        if (uf < total && total < 0x1p100f) {
+          int cs = C - 1;
+          float lo = 0.0f;
+#pragma unroll
+          for (int c = C - 1; c >= 0; --c)
+            if (uf < P[c]) cs = c;
+#pragma unroll
+          for (int c = 0; c < C - 1; ++c)
+            if (c < cs) lo = P[c];
+          const int og = cs / RH, orr = cs - og * RH;
+          const Oct16 p = ldg256h(a.phiT16 + static_cast<std::size_t>(wl) * a.Kp16 + 16 * (orr * G + og));
+          const uint4 y0 = *reinterpret_cast<const uint4*>(thh + og * KLHP + 16 * orr);
+          const uint4 y1 = *reinterpret_cast<const uint4*>(thh + og * KLHP + 16 * orr + 8);
+          const unsigned tv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+          float acc = lo, prev = lo;
+          int j = -1;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const unsigned ta = tv[jj >> 1], pa = p.v[jj >> 1];
+            const float nx = fhfma(static_cast<unsigned short>((jj & 1) ? ta >> 16 : ta & 0xffffu),
+                                   static_cast<unsigned short>((jj & 1) ? pa >> 16 : pa & 0xffffu), acc);
+            if (j < 0) {
+              if (uf < nx) {
+                j = jj;
+                prev = acc;
+              }
+              acc = nx;
+            }
+          }
+          const int kk = 16 * cs + j;
+          if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
+        }
+        if (k >= 0) {
+          a.z[t] = k;
+          atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
+          atomicAdd(&cnt_s[k], 1);
+        } else {
+          const int slot = atomicAdd(a.q2_len, 1);  // level 2 (zscreen_q_kernel)
+          a.q2[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
+        }
+      }
+      __syncwarp();
+    }
+    if constexpr (WU) __syncwarp();
+    else __syncthreads();
+    for (int k = tid_u; k < a.K; k += nthr_u) {
+      const int n = cnt_s[k];
+      if (n) atomicAdd(&a.nmk[m * a.K + k], n);
+    }
+  }
+}
+
+// Level 2: the fp32 transposed screen (zscreen_t_kernel's arithmetic and margin) over
+// the level-1 queue.  Each token brings its own document: the theta/S operands come
+// from thS32 (written by the level-1 unit), counts go straight to nmk.  R: rounds of
+// the phiT32 layout (G = 4 x CW = 8).
+template <int R>
+__global__ void __launch_bounds__(256) zscreen_q_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  constexpr int G = 4, CW = 8, C = G * R;
+  __shared__ __align__(16) float csum_all[8][32 * 16];
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G, warp = threadIdx.x >> 5;
+  float* csum = csum_all[warp];
+  pdl_wait();
+  pdl_trigger();
+  const std::int64_t iter = *iter_p;
+  const int n = *a.q2_len;
+  const int K8 = (a.K + 7) & ~7;
+  const int rl = min(R, max(0, (a.K - gl * CW * R + CW - 1) / CW));
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int b0 = (blockIdx.x * (blockDim.x >> 5) + warp) * 32; b0 < n; b0 += nwarps * 32) {
+    const int i = b0 + lane;
+    const bool valid = i < n;
+    const int2 q = valid ? a.q2[i] : make_int2(0, 0);
+    const int wl = valid ? __ldg(a.w + q.x) : 0;
+#pragma unroll 1
+    for (int s = 0; s < 4; ++s) {
+      if (b0 + s * 8 >= n) break;  // warp-uniform
+      const int src = s * 8 + gid;
+      const int wv = __shfl_sync(0xffffffffu, wl, src);
+      const int mv = __shfl_sync(0xffffffffu, q.y, src);
+      const float* row = a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
+      const float* th = a.thS32 + static_cast<std::size_t>(mv) * K8;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float sr = 0.0f;
+        if (r < rl) {
+          const Oct p = ldg256f(row + CW * (r * G + gl));
+          const int k0 = CW * (gl * R + r);  // logical candidates of this chunk
+          const float4 x0 = *reinterpret_cast<const float4*>(th + k0);
+          const float4 x1 = *reinterpret_cast<const float4*>(th + k0 + 4);
+          const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          sr = x[0] * p.v[0];
+#pragma unroll
+          for (int j = 1; j < CW; ++j) sr = __fmaf_rn(x[j], p.v[j], sr);
+        }
+        csum[cs_idx(src, gl * R + r)] = sr;
+      }
+    }
+    __syncwarp();
+    if (valid) {
+      const std::int64_t t = q.x, m = q.y;
+      Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
+                      static_cast<std::uint64_t>(iter)));
+      const float u01 = static_cast<float>(rng.next_unit());
+      float P[C];
+      float run = 0.0f;
+#pragma unroll
+      for (int c = 0; c < C; c += 4) {
+        const float4 y = *reinterpret_cast<const float4*>(csum + cs_idx(lane, c));
+        run += y.x;
+        P[c] = run;
+        run += y.y;
+        P[c + 1] = run;
+        run += y.z;
+        P[c + 2] = run;
+        run += y.w;
+        P[c + 3] = run;
+      }
+      const float total = run;
+      const float uf = u01 * total;
+      const float mg = a.screen_margin * total;
+      int k = -1;
+      if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
+        int cs = C - 1;
+        float lo = 0.0f;
+#pragma unroll
+        for (int c = C - 1; c >= 0; --c)
+          if (uf < P[c]) cs = c;
+#pragma unroll
+        for (int c = 0; c < C - 1; ++c)
+          if (c < cs) lo = P[c];
+        const int og = cs / R, orr = cs - og * R;
+        const Oct p = ldg256f(a.phiT32 + static_cast<std::size_t>(wl) * a.Kp32 + CW * (orr * G + og));
+        const float* th = a.thS32 + static_cast<std::size_t>(m) * K8 + CW * cs;
+        const float4 y0 = *reinterpret_cast<const float4*>(th);
+        const float4 y1 = *reinterpret_cast<const float4*>(th + 4);
+        const float tv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+        float acc = lo, prev = lo;
+        int j = -1;
+#pragma unroll
+        for (int jj = 0; jj < CW; ++jj) {
+          const float nx = __fmaf_rn(tv[jj], p.v[jj], acc);
+          if (j < 0) {
+            if (uf < nx) {
+              j = jj;
+              prev = acc;
+            }
+            acc = nx;
+          }
+        }
+        const int kk = CW * cs + j;
+        if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
+      }
+      if (k >= 0) {
+        a.z[t] = k;
+        atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
+        atomicAdd(&a.nmk[m * a.K + k], 1);
+      } else {
+        const int slot = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
+        a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // z block, TMA-staged screen (experimental, BNMC_ZSTAGE=1; slower, see choose_screen)
 // ---------------------------------------------------------------------------------
 // ncu r01 v15 (zscreen_t): every warp serialised ~5 L2 round trips per 32-token batch
@@ -2091,6 +2531,23 @@ class Lda final : public Model {
       plan_stage();
     }
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
+    // two-level screen (fp16 rows, then fp32): experimental, BNMC_ZSCREEN_H=1.  Measured
+    // slower (r01, NIPS): level 1 takes 79 us against the fp32 screen's 85 us -- half the
+    // row bytes, but the kernel is bound by its per-batch latency chain, not bytes --
+    // and level 2 (4.6 % of the tokens, one latency chain per scattered batch) plus
+    // the row conversion add ~24 us.
+    const char* zh = std::getenv("BNMC_ZSCREEN_H");
+    h16_ = screen_ && transposed_ && !stage_ && K_ <= 128 && zh && std::string(zh) == "1";
+    if (h16_) {
+      RH_ = (K_ + 63) / 64;
+      Kp16_ = 64 * RH_;
+      phiT16_.alloc(static_cast<std::size_t>(V_) * Kp16_);
+      thS32_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(Ml_, 1)) * ((K_ + 7) & ~7));
+      q2_.alloc(std::max<std::int64_t>(Nl_, 1));
+      q2_len_.alloc(1);
+      const int gx = (K_ + 31) / 32;
+      h16_blocks_ = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((V_ + 8 * gx - 1) / (8 * gx), 296 / gx)));
+    }
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
@@ -2142,6 +2599,8 @@ class Lda final : public Model {
     wpart_.zero(s0);
     phiT_.zero(s0);
     phiT32_.zero(s0);
+    phiT16_.zero(s0);
+    q2_len_.zero(s0);
     nkw_.zero(s0);
     w_.zero(s0);
     z_.zero(s0);
@@ -2339,6 +2798,7 @@ class Lda final : public Model {
         phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
         mark(st, "phi_gamma");
         phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
+        if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
       } else {
         const unsigned nbg = blocks_for(nvb_ * K_, 256);
         switch (phi_rows_) {
@@ -2348,7 +2808,8 @@ class Lda final : public Model {
           default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
         }
         mark(st, "phi_gamma");
-        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, col_stripes_), dim3(256), 0, st, a);
+        // (+ h16_blocks_ y-blocks converting the rows for the level-1 screen)
+        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, col_stripes_ + (h16_ ? h16_blocks_ : 0)), dim3(256), 0, st, a);
         fq_reset_ = true;
       }
       mark(st, "phi_colsum");
@@ -2375,6 +2836,13 @@ class Lda final : public Model {
       }
       launch_zstep(a, st);
       mark(st, "zstep");
+      if (timed && std::getenv("BNMC_SCREEN_STATS")) {  // diagnostics: queue lengths of this sweep
+        int n2 = -1, n3 = -1;
+        BNMC_CUDA(cudaStreamSynchronize(st));
+        if (h16_) BNMC_CUDA(cudaMemcpy(&n2, q2_len_.p, sizeof(int), cudaMemcpyDeviceToHost));
+        BNMC_CUDA(cudaMemcpy(&n3, fq_len_.p, sizeof(int), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[bnmc] z-step queues: level2 %d fp64 %d of %lld tokens\n", n2, n3, static_cast<long long>(Nl_));
+      }
     }
     const unsigned nbw = static_cast<unsigned>(nbw_);
     if (comm_.active()) {
@@ -2549,6 +3017,7 @@ class Lda final : public Model {
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
     if (screen_) phi_f32_kernel<<<148 * 8, 256, 0, st>>>(a);
+    if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
@@ -2718,6 +3187,45 @@ class Lda final : public Model {
     }
   }
 
+  template <int RH, bool WU>
+  void zscreen_h_launch(const LdaArgs& a, cudaStream_t st) {
+    const int kpad = (K_ + 3) & ~3;
+    const std::size_t hw = 4 * (16 * RH + 8) / 2;  // thh, in floats
+    if (WU) {
+      const std::size_t sm = sizeof(float) * 8 * (hw + 32 * 16 + kpad + 32);
+      const unsigned gw = static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((n_wunits_ + 7) / 8, 148 * 3)));
+      launch_pdl(zscreen_h_kernel<RH, true>, dim3(gw), dim3(256), sm, st, a, static_cast<const std::int64_t*>(out.iter));
+      return;
+    }
+    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
+    const std::size_t sm = sizeof(float) * (hw + zt_warps_ * 32 * 16 + kpad + 32);
+    launch_pdl(zscreen_h_kernel<RH, false>, dim3(g), dim3(32 * zt_warps_), sm, st, a, static_cast<const std::int64_t*>(out.iter));
+  }
+
+  template <int R>
+  void zscreen_q_launch(const LdaArgs& a, cudaStream_t st) {
+    // one wave of warps covers ~200 k queued tokens (NIPS: ~87 k): the kernel is one
+    // latency chain per batch, so warps, not blocks per SM, set its time
+    launch_pdl(zscreen_q_kernel<R>, dim3(148 * 6), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter));
+  }
+
+  // Level 1 (fp16 rows) then level 2 (fp32 rows, the level-1 queue).
+  void launch_zscreen_h(const LdaArgs& a, cudaStream_t st) {
+    if (RH_ == 1) {
+      if (zt_wu_) zscreen_h_launch<1, true>(a, st);
+      else zscreen_h_launch<1, false>(a, st);
+    } else {
+      if (zt_wu_) zscreen_h_launch<2, true>(a, st);
+      else zscreen_h_launch<2, false>(a, st);
+    }
+    switch (RS_) {
+      case 1: zscreen_q_launch<1>(a, st); break;
+      case 2: zscreen_q_launch<2>(a, st); break;
+      case 3: zscreen_q_launch<3>(a, st); break;
+      default: zscreen_q_launch<4>(a, st); break;
+    }
+  }
+
   template <int KQ>
   void zstage_launch(const LdaArgs& a, cudaStream_t st) {
     if (!stage_attr_) {
@@ -2759,8 +3267,16 @@ class Lda final : public Model {
   }
 
   void launch_zscreen(const LdaArgs& a, cudaStream_t st) {
-    if (!fq_reset_) BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+    if (!fq_reset_) {
+      BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
+      if (h16_) BNMC_CUDA(cudaMemsetAsync(q2_len_.p, 0, sizeof(int), st));
+    }
     fq_reset_ = false;
+    if (h16_) {
+      launch_zscreen_h(a, st);
+      launch_pdl(zfallback_kernel, dim3(148 * 8), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter), out.err);
+      return;
+    }
     if (stage_) {
       zstage_dispatch(a, st, std::integer_sequence<int, 1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32>{});
       zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
@@ -2827,6 +3343,13 @@ class Lda final : public Model {
     a.G32 = G32_;
     a.R32 = RS_;
     a.CW32 = CW32_;
+    a.phiT16 = h16_ ? phiT16_.p : nullptr;
+    a.Kp16 = Kp16_;
+    a.RH = RH_;
+    a.thS32 = h16_ ? thS32_.p : nullptr;
+    a.q2 = h16_ ? q2_.p : nullptr;
+    a.q2_len = h16_ ? q2_len_.p : nullptr;
+    a.col_stripes = col_stripes_;
     a.logphiT = exact_ ? logphiT_.p : nullptr;
     a.theta = theta_.p;
     a.nkw = nkw_.p;
@@ -2892,6 +3415,13 @@ class Lda final : public Model {
   DevBuf<ZBatch> batches_;
   std::int64_t nbatch_ = 0;
   DevBuf<float> phiT32_;
+  // two-level screen (zscreen_h_kernel + zscreen_q_kernel), K <= 128
+  bool h16_ = false;
+  int RH_ = 1, Kp16_ = 64, h16_blocks_ = 1;
+  DevBuf<unsigned short> phiT16_;
+  DevBuf<float> thS32_;
+  DevBuf<int2> q2_;
+  DevBuf<int> q2_len_;
   cudaStream_t side_ = nullptr, copy_ = nullptr;
   cudaEvent_t ev_phi_ready_ = nullptr, ev_theta_ready_ = nullptr, ev_copy_done_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;

@@ -210,10 +210,14 @@ def _gen_lda(restatement, reference, M, V, K, L, seed):
     return w, off, phi, theta, z
 
 
-@pytest.mark.parametrize("cfg", [("kos", 3430, 6906, 50, 136), ("nips", 1500, 12419, 100, 1267)])
-def test_lda_full_size_one_sweep(g, restatement, reference, cfg):
+@pytest.mark.parametrize("cfg,env", [(("kos", 3430, 6906, 50, 136), {}), (("nips", 1500, 12419, 100, 1267), {}),
+                                     (("nips", 1500, 12419, 100, 1267), {"BNMC_ZSCREEN_H": "1"})],
+                         ids=["kos", "nips", "nips-two-level-screen"])
+def test_lda_full_size_one_sweep(g, restatement, reference, monkeypatch, cfg, env):
     """KOS / NIPS-shaped corpora: one sweep from the reference's prior_init
     state; z and the counts must be bit-exact (0 mismatches), floats within tolerance."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     name, M, V, K, L = cfg
     seed = 42
     w, off, phi, theta, z = _gen_lda(restatement, reference, M, V, K, L, seed)
@@ -350,6 +354,11 @@ LAYOUTS = [
     (100, {"BNMC_ZSTEP_SCREEN": "0"}), (1000, {"BNMC_ZSTEP_SCREEN": "0"}),
     # phi / theta block v1 kernels
     (100, {"BNMC_PHI_V1": "1", "BNMC_THETA_V1": "1"}),
+    # two-level screen: fp16 rows (level 1), fp32 queue (level 2), fp64 queue
+    (5, {"BNMC_ZSCREEN_H": "1"}), (33, {"BNMC_ZSCREEN_H": "1"}), (64, {"BNMC_ZSCREEN_H": "1"}),
+    (100, {"BNMC_ZSCREEN_H": "1"}), (128, {"BNMC_ZSCREEN_H": "1"}),
+    (100, {"BNMC_ZSCREEN_H": "1", "BNMC_ZT_WU": "1"}), (50, {"BNMC_ZSCREEN_H": "1", "BNMC_ZT_WU": "0"}),
+    (100, {"BNMC_ZSCREEN_H": "1", "BNMC_PHI_V1": "1"}),
 ]
 
 
