@@ -74,6 +74,7 @@ template <class F>
 int guarded(bnmc_gpu_ctx* ctx, F&& f) {
   try {
     if (ctx) BNMC_CUDA(cudaSetDevice(ctx->device));
+    if (ctx && ctx->model) ++ctx->model->epoch;  // any call may change the device state
     f();
     return BNMC_GPU_OK;
   } catch (const Error& e) {
@@ -365,19 +366,31 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     require(iter >= 0, BNMC_GPU_ERR_ARG, "iteration must be non-negative");
     require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
             "store view is incomplete");
-    c->model->h2d_bytes = c->model->d2h_bytes = 0;
-    c->model->upload_sweep_inputs(*s, c->stream);
-    set_iter(c, iter);
-    launch_sweep(c);
-    c->model->d2h_bytes += static_cast<std::int64_t>(sizeof(double) + sizeof(int));  // the ring entry
-    if (!c->model->download_overlapped(*s, c->stream)) {
-      read_ring(c, iter, 1, log_joint, mh_accepted);
+    Model* m = c->model.get();
+    m->h2d_bytes = m->d2h_bytes = 0;
+    // speculative when no other call ran since the last sweep_store (see Model::epoch)
+    const bool spec = m->spec_epoch + 1 == m->epoch && m->spec_begin(*s, c->stream);
+    if (!spec) m->upload_sweep_inputs(*s, c->stream);
+    auto sweep_and_write_back = [&](bool verify) {
+      set_iter(c, iter);
+      launch_sweep(c);
+      if (verify) m->spec_verify(c->stream);
+      if (!m->download_overlapped(*s, c->stream)) {
+        read_ring(c, iter, 1, log_joint, mh_accepted);
+        check_device_error(c);
+        m->download(*s, c->stream);
+        return;
+      }
+      read_ring(c, iter, 1, log_joint, mh_accepted);  // synchronises the stream (and the copies)
       check_device_error(c);
-      c->model->download(*s, c->stream);
-      return;
+    };
+    sweep_and_write_back(spec);
+    if (spec && m->spec_failed()) {  // the caller changed the store: redo from its state
+      m->spec_adopt(c->stream);
+      sweep_and_write_back(false);
     }
-    read_ring(c, iter, 1, log_joint, mh_accepted);  // synchronises the stream (and the copies)
-    check_device_error(c);
+    m->d2h_bytes += static_cast<std::int64_t>(sizeof(double) + sizeof(int));  // the ring entry
+    m->spec_epoch = m->epoch;
   });
 }
 

@@ -119,6 +119,21 @@ struct Model {
   // host <-> device bytes of the current Engine::sweep call (bnmc_gpu_transfer_stats);
   // counted by the models that implement the bound-store path
   std::int64_t h2d_bytes = 0, d2h_bytes = 0;
+  // Speculative bound-store sweeps (bnmc_gpu_sweep_store).  `epoch` counts C-ABI calls
+  // on the context; `spec_epoch` is the epoch of the last completed sweep_store.  When
+  // nothing ran in between, the device state is the one the caller's store was last
+  // written from, so the sweep may start from it while the store's latent state
+  // crosses PCIe; the upload is then compared with that state and, if the caller
+  // changed it, the sweep is redone from the upload.
+  std::uint64_t epoch = 0, spec_epoch = ~std::uint64_t{0};
+  // enqueue the upload of the sweep inputs into staging (side stream); false: no speculation
+  virtual bool spec_begin(const bnmc_gpu_store&, cudaStream_t) { return false; }
+  // enqueue: wait for the upload, compare it with the state the sweep started from
+  virtual void spec_verify(cudaStream_t) {}
+  // after a stream sync: did the store differ (the speculative sweep must be redone)?
+  virtual bool spec_failed() { return false; }
+  // the staged upload becomes the state (with upload_sweep_inputs' checks and counts)
+  virtual void spec_adopt(cudaStream_t) {}
   virtual void upload(const bnmc_gpu_store& s, cudaStream_t st) = 0;
   virtual void download(const bnmc_gpu_store& s, cudaStream_t st) = 0;
   // Uploads only the latent (unobserved) variables: the observed data already on

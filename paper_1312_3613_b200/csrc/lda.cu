@@ -2302,6 +2302,27 @@ __global__ void i32_check_kernel(const int* v, std::int64_t n, int hi, int* err)
     if (v[i] < 0 || v[i] >= hi) atomicOr(err, kErrBin);
 }
 
+// z write-back: int64 staging for the store and the copy the next speculative
+// sweep_store compares the store with (zprev)
+__global__ void z_writeback_kernel(const int* in, std::int64_t* out, int* keep, std::int64_t n) {
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const int v = in[i];
+    out[i] = v;
+    keep[i] = v;
+  }
+}
+
+// Speculative sweep_store: did the caller's store (uploaded to `up`) differ from the
+// state the sweep started from (`prev`)?
+__global__ void spec_check_kernel(const std::int64_t* up, const int* prev, std::int64_t n, int* flag) {
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  bool diff = false;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    diff |= up[i] != static_cast<std::int64_t>(prev[i]);
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
 __global__ void i32_to_i64_kernel(const int* in, std::int64_t* out, std::int64_t n) {
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -2638,6 +2659,11 @@ class Lda final : public Model {
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_copy_done_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    BNMC_CUDA(cudaStreamCreateWithFlags(&up_, cudaStreamNonBlocking));
+    BNMC_CUDA(cudaEventCreateWithFlags(&ev_up_, cudaEventDisableTiming));
+    BNMC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&spec_flag_host_), sizeof(int)));
+    spec_flag_.alloc(1);
+    if (const char* e = std::getenv("BNMC_SPECULATE")) speculate_ = std::string(e) != "0";
   }
 
   ~Lda() override {
@@ -2648,6 +2674,9 @@ class Lda final : public Model {
     if (ev_copy_done_) cudaEventDestroy(ev_copy_done_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (up_) cudaStreamDestroy(up_);
+    if (ev_up_) cudaEventDestroy(ev_up_);
+    if (spec_flag_host_) cudaFreeHost(spec_flag_host_);
   }
 
   void upload(const bnmc_gpu_store& s, cudaStream_t st) override { upload_impl(s, st, true); }
@@ -2672,8 +2701,13 @@ class Lda final : public Model {
       BNMC_CUDA(cudaMemcpyAsync(stage64_.p, s.ival[var_z_] + tok0_, sizeof(std::int64_t) * Nl_,
                                 cudaMemcpyHostToDevice, st));
       h2d_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * Nl_;
-      i64_to_i32_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(stage64_.p, z_.p, Nl_, 0, K_, out.err);
     }
+    adopt_z(stage64_.p, st);
+  }
+
+  // z := the uploaded int64 assignments (range-checked), counts rebuilt from them
+  void adopt_z(const std::int64_t* dev64, cudaStream_t st) {
+    if (Nl_ > 0) i64_to_i32_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(dev64, z_.p, Nl_, 0, K_, out.err);
     LdaArgs a = args();
     nkw_.zero(st);
     nmk_.zero(st);
@@ -2683,6 +2717,33 @@ class Lda final : public Model {
     }
     BNMC_CUDA(cudaGetLastError());
   }
+
+  // Speculative bound-store sweep (Model::spec_begin): the sweep starts from the device
+  // state -- the z this context last wrote back to the caller (zprev_), with its counts
+  // -- while the caller's z crosses PCIe on up_; spec_verify compares the two after
+  // the sweep, and a difference makes sweep_store adopt the upload and redo the sweep.
+  // Single-rank only (a redo must not be a per-rank decision); BNMC_SPECULATE=0 disables it.
+  bool spec_begin(const bnmc_gpu_store& s, cudaStream_t st) override {
+    if (!speculate_ || comm_.active() || Nl_ == 0 || !zprev_valid_) return false;
+    if ((s.observed && s.observed[var_z_]) || !s.ival[var_z_]) return false;
+    check_len(s, var_z_, N_, "z");
+    if (up64_.n < static_cast<std::size_t>(Nl_)) up64_.alloc(Nl_);
+    BNMC_CUDA(cudaMemsetAsync(spec_flag_.p, 0, sizeof(int), st));
+    BNMC_CUDA(cudaMemcpyAsync(up64_.p, s.ival[var_z_] + tok0_, sizeof(std::int64_t) * Nl_, cudaMemcpyHostToDevice, up_));
+    BNMC_CUDA(cudaEventRecord(ev_up_, up_));
+    h2d_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * Nl_;
+    return true;
+  }
+
+  void spec_verify(cudaStream_t st) override {
+    BNMC_CUDA(cudaStreamWaitEvent(st, ev_up_, 0));
+    spec_check_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 8), 256, 0, st>>>(up64_.p, zprev_.p, Nl_, spec_flag_.p);
+    BNMC_CUDA(cudaMemcpyAsync(spec_flag_host_, spec_flag_.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+
+  bool spec_failed() override { return *spec_flag_host_ != 0; }
+
+  void spec_adopt(cudaStream_t st) override { adopt_z(up64_.p, st); }
 
   void upload_impl(const bnmc_gpu_store& s, cudaStream_t st, bool with_data) {
     require(s.n_vars > std::max(std::max(var_phi_, var_theta_), std::max(var_z_, var_w_)),
@@ -2732,7 +2793,9 @@ class Lda final : public Model {
   // Writes z back into the int64 store slice `dst` (enqueued on st).
   void download_z(std::int64_t* dst, cudaStream_t st) {
     if (stage64_.n < static_cast<std::size_t>(Nl_)) stage64_.alloc(Nl_);
-    i32_to_i64_kernel<<<blocks_for(Nl_, 256), 256, 0, st>>>(z_.p, stage64_.p, Nl_);
+    if (zprev_.n < static_cast<std::size_t>(Nl_)) zprev_.alloc(Nl_);
+    z_writeback_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(z_.p, stage64_.p, zprev_.p, Nl_);
+    zprev_valid_ = true;
     BNMC_CUDA(cudaMemcpyAsync(dst, stage64_.p, sizeof(std::int64_t) * Nl_, cudaMemcpyDeviceToHost, st));
     d2h_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * Nl_;
   }
@@ -3423,6 +3486,13 @@ class Lda final : public Model {
   DevBuf<int2> q2_;
   DevBuf<int> q2_len_;
   cudaStream_t side_ = nullptr, copy_ = nullptr;
+  // speculative sweep_store
+  cudaStream_t up_ = nullptr;
+  cudaEvent_t ev_up_ = nullptr;
+  DevBuf<std::int64_t> up64_;
+  DevBuf<int> zprev_, spec_flag_;
+  int* spec_flag_host_ = nullptr;
+  bool zprev_valid_ = false, speculate_ = true;
   cudaEvent_t ev_phi_ready_ = nullptr, ev_theta_ready_ = nullptr, ev_copy_done_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;

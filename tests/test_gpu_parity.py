@@ -203,6 +203,46 @@ def test_lda_bound_store_transfers(g, K):
     e2.close()
 
 
+def test_lda_speculative_sweep_store(g, monkeypatch):
+    """Repeated Engine::sweep calls on a bound store start from the device state while
+    the store's z is uploaded (sweep_store speculation).  Results must equal the
+    non-speculative path's call by call, including when the caller edits z between
+    calls (the upload differs -> redo from it) or writes an invalid value (-> error)."""
+    rs = np.random.default_rng(5)
+    K, V, M, L = 20, 60, 16, 40
+    N = M * L
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+
+    def make():
+        e = g.Engine("lda", hyper, g.RunConfig(seed=9))
+        s = e.allocate()
+        s["w"] = np.random.default_rng(1).integers(0, V, N)
+        e.prior_init(s, 9)
+        return e, s
+
+    e1, s1 = make()  # speculative (default)
+    monkeypatch.setenv("BNMC_SPECULATE", "0")
+    e2, s2 = make()
+    monkeypatch.delenv("BNMC_SPECULATE")
+    for it in range(8):
+        if it in (4, 6):  # the caller edits the store between calls
+            z = s1["z"].copy()
+            z[rs.integers(0, N, 7)] = rs.integers(0, K, 7)
+            s1["z"] = z
+            s2["z"] = z.copy()
+        lj1, lj2 = e1.sweep(s1, it), e2.sweep(s2, it)
+        assert lj1 == lj2, it
+        for n in ("z", "phi", "theta"):
+            assert np.array_equal(s1[n], s2[n]), (it, n)
+    bad = s1["z"].copy()
+    bad[3] = K
+    s1["z"] = bad
+    with pytest.raises(g.BnmcError):
+        e1.sweep(s1, 8)
+    e1.close()
+    e2.close()
+
+
 def _gen_lda(restatement, reference, M, V, K, L, seed):
     w, _, _ = reference.gen_lda(M, V, K, L, seed)
     off = np.arange(M + 1, dtype=np.int64) * L
