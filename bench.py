@@ -199,6 +199,14 @@ def gen_lda_corpus(docs, vocab, topics, doc_len, seed):
     return w
 
 
+E2E_NOTES = {
+    "lda": "; the sweep starts from the written-back state while z uploads (compared on the device "
+           "after the sweep, redone if the caller changed it); phi/theta copies overlap the z-step",
+    "logreg": "; w, b uploaded every call, the likelihood refresh pass skipped when they equal the "
+              "written-back state",
+}
+
+
 def pinned_like(arr):
     import torch
 
@@ -398,12 +406,14 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             # counted by the library
             # (bnmc_gpu_transfer_stats) after the bind call below
             up = down = 0
+        elif model == "logreg":
+            up = down = 0  # counted by the library below (w, b up; w, b + lj down)
         else:
             up = sum(store.arrays[n].nbytes for n in lat)
             down = up + 8
         eng.sweep(store, it)  # bind (uploads the observed data once, outside the timed region)
         it += 1
-        if model == "lda":
+        if model in ("lda", "logreg"):
             eng.sweep(store, it)
             it += 1
             up, down = eng.transfer_stats()  # the bytes the library actually moves per call
@@ -423,7 +433,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         e2e = {"value": sites_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(up),
                "d2h_bytes_per_step": int(down), "ms_per_step": e2e_s * 1e3,
                "path": "Engine.sweep(store, iter) with pinned host arrays: bnmc_gpu_sweep_store (upload of "
-                       "what the sweep reads, sweep, write-back; phi/theta copies overlap the z-step)"}
+                       "what the sweep reads, sweep, write-back)" + E2E_NOTES.get(model, "")}
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "1B corpus is generated and kept on the device (host cannot hold it)"}

@@ -369,8 +369,10 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     Model* m = c->model.get();
     m->h2d_bytes = m->d2h_bytes = 0;
     // speculative when no other call ran since the last sweep_store (see Model::epoch)
-    const bool spec = m->spec_epoch + 1 == m->epoch && m->spec_begin(*s, c->stream);
+    m->quiet = m->spec_epoch + 1 == m->epoch;
+    const bool spec = m->quiet && m->spec_begin(*s, c->stream);
     if (!spec) m->upload_sweep_inputs(*s, c->stream);
+    m->quiet = false;
     auto sweep_and_write_back = [&](bool verify) {
       set_iter(c, iter);
       launch_sweep(c);

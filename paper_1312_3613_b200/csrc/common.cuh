@@ -126,6 +126,9 @@ struct Model {
   // crosses PCIe; the upload is then compared with that state and, if the caller
   // changed it, the sweep is redone from the upload.
   std::uint64_t epoch = 0, spec_epoch = ~std::uint64_t{0};
+  // set by sweep_store around upload_sweep_inputs / spec_begin: no other call ran since
+  // the previous sweep_store, so the device state is the one last written back
+  bool quiet = false;
   // enqueue the upload of the sweep inputs into staging (side stream); false: no speculation
   virtual bool spec_begin(const bnmc_gpu_store&, cudaStream_t) { return false; }
   // enqueue: wait for the upload, compare it with the state the sweep started from

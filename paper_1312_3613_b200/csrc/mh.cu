@@ -17,6 +17,7 @@
 //                    = Fw + Fb + Ftau + Fx + Fy in the reference's order.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 #include "dist.cuh"
@@ -432,6 +433,7 @@ __global__ void poly_features_kernel(const double* x, double* X, std::int64_t n,
 class Mh final : public Model {
  public:
   Mh(const bnmc_gpu_desc& d, const Comm& c, Outputs o) : comm_(c) {
+    if (const char* e = std::getenv("BNMC_SPECULATE")) skip_unchanged_ = std::string(e) != "0";
     out = o;
     logistic_ = d.kind == BNMC_GPU_MH_LOGREG;
     poly_ = d.kind == BNMC_GPU_MH_POLYREG;
@@ -487,11 +489,10 @@ class Mh final : public Model {
     require(s.len[vw] == K_ && s.len[vb] == 1 && s.len[vx] == N_ * (poly_ ? 1 : K_) && s.len[vy] == N_ &&
                 (vtau < 0 || s.len[vtau] == 1),
             BNMC_GPU_ERR_RUNTIME, "MH store arrays have the wrong flat lengths");
-    std::vector<double> p(K_ + 2, 0.0);
-    for (int j = 0; j < K_; ++j) p[j] = s.real[vw][j];
-    p[K_] = s.real[vb][0];
-    p[K_ + 1] = vtau >= 0 ? s.real[vtau][0] : (poly_ ? 1.0 : 0.0);
+    const std::vector<double> p = store_params(s);
     BNMC_CUDA(cudaMemcpyAsync(w_.p, p.data(), sizeof(double) * (K_ + 2), cudaMemcpyHostToDevice, st));
+    h2d_bytes += static_cast<std::int64_t>(sizeof(double)) * (K_ + 2);
+    last_valid_ = false;
     if (Nl_ > 0 && with_data) {
       if (poly_) {
         BNMC_CUDA(cudaMemcpyAsync(xraw_.p, s.real[vx] + r0_, sizeof(double) * Nl_, cudaMemcpyHostToDevice, st));
@@ -506,16 +507,46 @@ class Mh final : public Model {
     refresh(st);
   }
 
+  // (w, b, tau) as the store holds them (tau: 0 / 1 placeholders without it)
+  std::vector<double> store_params(const bnmc_gpu_store& s) const {
+    const int vw = var_[0], vb = var_[1];
+    const int vtau = (logistic_ || poly_) ? -1 : var_[2];
+    std::vector<double> p(K_ + 2, 0.0);
+    for (int j = 0; j < K_; ++j) p[j] = s.real[vw][j];
+    p[K_] = s.real[vb][0];
+    p[K_ + 1] = vtau >= 0 ? s.real[vtau][0] : (poly_ ? 1.0 : 0.0);
+    return p;
+  }
+
+  // Engine::sweep on a bound store: the parameters are uploaded every call; when they
+  // are bit for bit the state this context last wrote back and nothing ran since
+  // (Model::quiet), the cached log-likelihood of the device state is current and the
+  // refresh pass over the data (as long as the sweep's own likelihood pass) is skipped.
+  void upload_sweep_inputs(const bnmc_gpu_store& s, cudaStream_t st) override {
+    const std::vector<double> p = store_params(s);
+    if (!(quiet && skip_unchanged_ && last_valid_ &&
+          std::memcmp(p.data(), last_.data(), sizeof(double) * p.size()) == 0)) {
+      upload_state(s, st);
+      return;
+    }
+    BNMC_CUDA(cudaMemcpyAsync(w_.p, p.data(), sizeof(double) * (K_ + 2), cudaMemcpyHostToDevice, st));
+    BNMC_CUDA(cudaStreamSynchronize(st));  // p is a host temporary
+    h2d_bytes += static_cast<std::int64_t>(sizeof(double)) * (K_ + 2);
+  }
+
   void download(const bnmc_gpu_store& s, cudaStream_t st) override {
     std::vector<double> p(K_ + 2);
     BNMC_CUDA(cudaMemcpyAsync(p.data(), w_.p, sizeof(double) * (K_ + 2), cudaMemcpyDeviceToHost, st));
     BNMC_CUDA(cudaStreamSynchronize(st));
+    d2h_bytes += static_cast<std::int64_t>(sizeof(double)) * (K_ + 2);
     const char* obs = s.observed;
     const int vw = var_[0], vb = var_[1];
     if (!(obs && obs[vw]))
       for (int j = 0; j < K_; ++j) s.real[vw][j] = p[j];
     if (!(obs && obs[vb])) s.real[vb][0] = p[K_];
     if (!logistic_ && !poly_ && !(obs && obs[var_[2]])) s.real[var_[2]][0] = p[K_ + 1];
+    last_ = store_params(s);  // what the store holds now (observed entries: the caller's)
+    last_valid_ = std::memcmp(last_.data(), p.data(), sizeof(double) * p.size()) == 0;
   }
 
   void on_state_restored(cudaStream_t st) override { refresh(st); }
@@ -669,6 +700,9 @@ class Mh final : public Model {
   double lo_, hi_, w_var_, b_var_, tau_a_, tau_b_, mh_scale_;
   std::uint64_t seed_ = 0;
   int var_[5] = {0, 1, 2, 3, 4};
+  std::vector<double> last_;  // the store's (w, b, tau) after the last write-back
+  bool last_valid_ = false;   // ... and they equal the device state
+  bool skip_unchanged_ = true;  // BNMC_SPECULATE=0: always refresh on a bound-store upload
   DevBuf<double> x_, y_, w_, wp_, part_, state_, tot_, xraw_, mwg_part_;
 };
 

@@ -243,6 +243,41 @@ def test_lda_speculative_sweep_store(g, monkeypatch):
     e2.close()
 
 
+def test_mh_bound_store_unchanged_skip(g, monkeypatch):
+    """MH on a bound store skips the upload and the likelihood refresh when the store
+    still holds the state last written back; results equal the always-upload path's
+    call by call, including after the caller edits a weight."""
+    rs = np.random.default_rng(2)
+    N, K = 5000, 6
+    x = rs.uniform(-1, 1, size=(N, K))
+    y = (rs.random(N) < 0.5).astype(np.float64)
+    hyper = {"N": N, "K": K, "l": -1.0, "u": 1.0}
+
+    def make():
+        e = g.Engine("logreg", hyper, g.RunConfig(seed=4, mh_scale=0.05))
+        s = e.allocate()
+        s["x"], s["y"] = x.ravel(), y
+        e.prior_init(s, 4)
+        return e, s
+
+    e1, s1 = make()
+    monkeypatch.setenv("BNMC_SPECULATE", "0")
+    e2, s2 = make()
+    monkeypatch.delenv("BNMC_SPECULATE")
+    for it in range(10):
+        if it == 6:
+            for s in (s1, s2):
+                w = s["w"].copy()
+                w[1] += 0.25
+                s["w"] = w
+        acc1, acc2 = [], []
+        lj1, lj2 = e1.sweep(s1, it, acc1), e2.sweep(s2, it, acc2)
+        assert lj1 == lj2 and acc1 == acc2, it
+        assert np.array_equal(s1["w"], s2["w"]) and np.array_equal(s1["b"], s2["b"]), it
+    e1.close()
+    e2.close()
+
+
 def _gen_lda(restatement, reference, M, V, K, L, seed):
     w, _, _ = reference.gen_lda(M, V, K, L, seed)
     off = np.arange(M + 1, dtype=np.int64) * L
