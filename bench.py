@@ -399,24 +399,15 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
                 arr, t = pinned_like(store.arrays[name])
                 store.arrays[name] = arr
                 store.__dict__.setdefault("_pins", []).append(t)
-        lat = [n for n in store.names if not store.observed[n]]
-        if model == "lda":
-            # per step: this rank's z slice up (the sweep reads only z of the latent state:
-            # bnmc_gpu_upload_sweep_inputs), z and theta slices + the global phi + lj down --
-            # counted by the library
-            # (bnmc_gpu_transfer_stats) after the bind call below
-            up = down = 0
-        elif model == "logreg":
-            up = down = 0  # counted by the library below (w, b up; w, b + lj down)
-        else:
-            up = sum(store.arrays[n].nbytes for n in lat)
-            down = up + 8
+        # bytes per step, counted by the library (bnmc_gpu_transfer_stats) on the call after
+        # the bind: LDA this rank's z slice up (the sweep reads only z of the latent state),
+        # z and theta slices + the global phi + lj down; MH w, b up and down; GMM z, pi,
+        # mu, sigma2 up and down
         eng.sweep(store, it)  # bind (uploads the observed data once, outside the timed region)
         it += 1
-        if model in ("lda", "logreg"):
-            eng.sweep(store, it)
-            it += 1
-            up, down = eng.transfer_stats()  # the bytes the library actually moves per call
+        eng.sweep(store, it)
+        it += 1
+        up, down = eng.transfer_stats()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()

@@ -342,12 +342,11 @@ class Gmm final : public Model {
     BNMC_CUDA(cudaMemcpyAsync(mu_.p, s.real[vmu], sizeof(double) * K_, cudaMemcpyHostToDevice, st));
     BNMC_CUDA(cudaMemcpyAsync(s2_.p, s.real[vs2], sizeof(double) * K_, cudaMemcpyHostToDevice, st));
     if (N_ > 0) {
-      DevBuf<std::int64_t> tmp;
-      tmp.alloc(N_);
-      BNMC_CUDA(cudaMemcpyAsync(tmp.p, s.ival[vz], sizeof(std::int64_t) * N_, cudaMemcpyHostToDevice, st));
-      z_from_i64<<<kBlocks, kThreads, 0, st>>>(tmp.p, z_.p, N_, K_, out.err);
-      BNMC_CUDA(cudaStreamSynchronize(st));
+      if (stage64_.n < static_cast<std::size_t>(N_)) stage64_.alloc(N_);  // kept: no per-call cudaMalloc/cudaFree
+      BNMC_CUDA(cudaMemcpyAsync(stage64_.p, s.ival[vz], sizeof(std::int64_t) * N_, cudaMemcpyHostToDevice, st));
+      z_from_i64<<<kBlocks, kThreads, 0, st>>>(stage64_.p, z_.p, N_, K_, out.err);
     }
+    h2d_bytes += static_cast<std::int64_t>(sizeof(double)) * 3 * K_ + static_cast<std::int64_t>(sizeof(std::int64_t)) * N_;
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
 
@@ -359,12 +358,13 @@ class Gmm final : public Model {
     if (want(vmu)) BNMC_CUDA(cudaMemcpyAsync(s.real[vmu], mu_.p, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
     if (want(vs2)) BNMC_CUDA(cudaMemcpyAsync(s.real[vs2], s2_.p, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
     if (want(vz) && N_ > 0) {
-      DevBuf<std::int64_t> tmp;
-      tmp.alloc(N_);
-      z_to_i64<<<kBlocks, kThreads, 0, st>>>(z_.p, tmp.p, N_);
-      BNMC_CUDA(cudaMemcpyAsync(s.ival[vz], tmp.p, sizeof(std::int64_t) * N_, cudaMemcpyDeviceToHost, st));
-      BNMC_CUDA(cudaStreamSynchronize(st));
+      if (stage64_.n < static_cast<std::size_t>(N_)) stage64_.alloc(N_);
+      z_to_i64<<<kBlocks, kThreads, 0, st>>>(z_.p, stage64_.p, N_);
+      BNMC_CUDA(cudaMemcpyAsync(s.ival[vz], stage64_.p, sizeof(std::int64_t) * N_, cudaMemcpyDeviceToHost, st));
+      d2h_bytes += static_cast<std::int64_t>(sizeof(std::int64_t)) * N_;
     }
+    for (int v : {vpi, vmu, vs2})
+      if (want(v)) d2h_bytes += static_cast<std::int64_t>(sizeof(double)) * K_;
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
 
@@ -441,6 +441,7 @@ class Gmm final : public Model {
   int var_[5] = {0, 1, 2, 3, 4};
   DevBuf<double> x_, pi_, mu_, s2_, part_, lpart_;
   DevBuf<int> z_;
+  DevBuf<std::int64_t> stage64_;  // z upload / write-back staging (int64 store layout)
 };
 
 }  // namespace
