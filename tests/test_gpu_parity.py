@@ -736,3 +736,49 @@ def test_lpp_curve_vs_restatement(g, restatement, reference):
         want = restatement.lda_lpp(phi, best_theta, K, V, tw, toff)
         assert abs(p["lpp"] - want) <= 1e-10 * abs(want), (c, p["lpp"], want)
         assert p["seconds"] == c / 1000.0
+
+
+# ----------------------------------------------------------------------------------------
+# statistical checks (SURVEY.md 8c parity plan, step 3): posterior summaries over many
+# sweeps -- the logistic likelihood has no reference model, so its MH chain is pinned by
+# recovering a synthetic truth; GMM recovers its centres (acceptance crit. 4 pattern)
+# ----------------------------------------------------------------------------------------
+def test_logreg_posterior_recovers_truth(g):
+    rs = np.random.default_rng(11)
+    N, K = 20000, 4
+    wt, bt = np.array([0.8, -0.5, 0.3, 0.0]), 0.2
+    x = rs.uniform(-1, 1, size=(N, K))
+    y = (rs.uniform(size=N) < 1 / (1 + np.exp(-(x @ wt + bt)))).astype(np.float64)
+    cfg = g.RunConfig(seed=21, mh_scale=0.01, burnin=1500, thin=5)
+    e = g.Engine("logreg", {"N": N, "K": K, "l": -1.0, "u": 1.0}, cfg)
+    s = e.allocate()
+    s["x"], s["y"] = x.ravel(), y
+    e.prior_init(s, 21)
+    tr = e.run(s, 6000)
+    acc = np.mean(tr["accepted"])
+    assert 0.05 < acc < 0.9, acc
+    ws = np.array([smp["w"] for smp in tr["samples"]])
+    bs = np.array([smp["b"][0] for smp in tr["samples"]])
+    # posterior sd at N = 2e4 is ~0.03 per coefficient: 0.12 is ~4 sd
+    assert np.max(np.abs(ws.mean(axis=0) - wt)) < 0.12, ws.mean(axis=0)
+    assert abs(bs.mean() - bt) < 0.12, bs.mean()
+    e.close()
+
+
+def test_gmm_posterior_recovers_centres(g):
+    rs = np.random.default_rng(12)
+    N = 20000
+    centres, sds = np.array([-6.0, -2.0, 2.0, 6.0]), np.array([0.5, 0.5, 0.5, 0.5])
+    zt = rs.integers(0, 4, N)
+    x = centres[zt] + sds[zt] * rs.normal(size=N)
+    cfg = g.RunConfig(seed=22, burnin=800, thin=2)
+    e = g.Engine("gmm", {"N": N, "K": 4}, cfg)
+    s = e.allocate()
+    s["x"] = x
+    e.prior_init(s, 22)
+    tr = e.run(s, 200)
+    mus = np.sort(np.array([smp["mu"] for smp in tr["samples"]]), axis=1)
+    s2 = np.array([smp["sigma2"] for smp in tr["samples"]])
+    assert np.max(np.abs(mus.mean(axis=0) - centres)) < 0.05, mus.mean(axis=0)
+    assert np.all(np.abs(np.sort(s2.mean(axis=0)) - 0.25) < 0.05), s2.mean(axis=0)
+    e.close()
