@@ -524,7 +524,8 @@ class Mh final : public Model {
   // refresh pass over the data (as long as the sweep's own likelihood pass) is skipped.
   void upload_sweep_inputs(const bnmc_gpu_store& s, cudaStream_t st) override {
     const std::vector<double> p = store_params(s);
-    if (!(quiet && skip_unchanged_ && last_valid_ &&
+    // (single rank: the refresh's all-reduce must not become a per-rank decision)
+    if (!(quiet && skip_unchanged_ && last_valid_ && !comm_.active() &&
           std::memcmp(p.data(), last_.data(), sizeof(double) * p.size()) == 0)) {
       upload_state(s, st);
       return;
