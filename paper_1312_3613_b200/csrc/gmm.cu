@@ -347,7 +347,7 @@ class Gmm final : public Model {
       z_from_i64<<<kBlocks, kThreads, 0, st>>>(stage64_.p, z_.p, N_, K_, out.err);
     }
     h2d_bytes += static_cast<std::int64_t>(sizeof(double)) * 3 * K_ + static_cast<std::int64_t>(sizeof(std::int64_t)) * N_;
-    BNMC_CUDA(cudaStreamSynchronize(st));
+    // stream-ordered: the sweep (or the caller's next synchronous call) sees the upload
   }
 
   void download(const bnmc_gpu_store& s, cudaStream_t st) override {
