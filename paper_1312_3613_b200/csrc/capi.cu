@@ -163,8 +163,8 @@ struct CopyTab {
   int n;
 };
 
-__global__ void cond_copy_kernel(CopyTab t, const int* flag) {
-  if (!*flag) return;
+__global__ void cond_copy_kernel(CopyTab t, const int* flag) {  // flag == nullptr: always
+  if (flag && !*flag) return;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
   for (int b = 0; b < t.n; ++b)
     for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < t.words[b]; i += stride)
@@ -443,8 +443,37 @@ int bnmc_gpu_run_trace(bnmc_gpu_ctx* c, std::int64_t iter0, bnmc_gpu_trace* tr) 
     const double ninf = -INFINITY;
     BNMC_CUDA(cudaMemcpyAsync(map_lj.p, &ninf, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     std::vector<cudaEvent_t> ev;
+    // Thinned samples: the state is copied on the device into one of two snapshot slots
+    // (stream order), and the slot is written into the caller's sample store by the
+    // model's download on a copy stream at the next sample point -- while the sweeps
+    // launched since run on the GPU -- instead of a synchronous download per sample.
+    std::vector<DevBuf<unsigned>> slot[2];
+    cudaEvent_t ev_snap[2] = {nullptr, nullptr};
+    cudaStream_t cp = nullptr;
+    std::int64_t pending = -1;  // sample index whose snapshot awaits its download
+    int pending_slot = 0;
     auto cleanup = [&] {
       for (auto e : ev) cudaEventDestroy(e);
+      for (auto e : ev_snap)
+        if (e) cudaEventDestroy(e);
+      if (cp) cudaStreamDestroy(cp);
+    };
+    auto with_state = [&](std::vector<DevBuf<unsigned>>& bufs_in, auto&& f) {
+      // the model's download reads its state buffers: swap a copy in and out
+      for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&bufs_in[i].p));
+      try {
+        f();
+      } catch (...) {
+        for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&bufs_in[i].p));
+        throw;
+      }
+      for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&bufs_in[i].p));
+    };
+    auto flush_sample = [&] {
+      if (pending < 0) return;
+      BNMC_CUDA(cudaStreamWaitEvent(cp, ev_snap[pending_slot], 0));
+      with_state(slot[pending_slot], [&] { c->model->download(tr->samples[pending], cp); });
+      pending = -1;
     };
     try {
       set_iter(c, iter0);
@@ -475,8 +504,29 @@ int bnmc_gpu_run_trace(bnmc_gpu_ctx* c, std::int64_t iter0, bnmc_gpu_trace* tr) 
           }
           cond_copy_kernel<<<148 * 4, 256, 0, c->stream>>>(tab, flag.p);
         }
-        if (tr->samples && s % tr->thin == 0) c->model->download(tr->samples[sample++], c->stream);
+        if (tr->samples && s % tr->thin == 0) {
+          flush_sample();  // the previous sample, overlapping the sweep just launched
+          const int j = static_cast<int>(sample & 1);
+          if (slot[j].empty()) {
+            slot[j] = std::vector<DevBuf<unsigned>>(bufs.size());
+            for (std::size_t i = 0; i < bufs.size(); ++i) slot[j][i].alloc((bufs[i].bytes + 3) / 4);
+            if (!cp) BNMC_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+            BNMC_CUDA(cudaEventCreateWithFlags(&ev_snap[j], cudaEventDisableTiming));
+          }
+          CopyTab snap{};
+          snap.n = static_cast<int>(bufs.size());
+          for (std::size_t i = 0; i < bufs.size(); ++i) {
+            snap.src[i] = static_cast<const unsigned*>(*bufs[i].p);
+            snap.dst[i] = slot[j][i].p;
+            snap.words[i] = bufs[i].bytes / 4;
+          }
+          cond_copy_kernel<<<148 * 4, 256, 0, c->stream>>>(snap, nullptr);
+          BNMC_CUDA(cudaEventRecord(ev_snap[j], c->stream));
+          pending = sample++;
+          pending_slot = j;
+        }
       }
+      flush_sample();
       drain(tr->n);
       check_device_error(c);
       if (tr->timing_ms)
@@ -488,15 +538,7 @@ int bnmc_gpu_run_trace(bnmc_gpu_ctx* c, std::int64_t iter0, bnmc_gpu_trace* tr) 
       if (tr->map_log_joint)
         BNMC_CUDA(cudaMemcpy(tr->map_log_joint, map_lj.p, sizeof(double), cudaMemcpyDeviceToHost));
       if (tr->map_state && tr->n > 0) {
-        // download() reads the model's state buffers: swap the MAP copies in and out
-        for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
-        try {
-          c->model->download(*tr->map_state, c->stream);
-        } catch (...) {
-          for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
-          throw;
-        }
-        for (std::size_t i = 0; i < bufs.size(); ++i) std::swap(*bufs[i].p, *reinterpret_cast<void**>(&map[i].p));
+        with_state(map, [&] { c->model->download(*tr->map_state, c->stream); });
       }
     } catch (...) {
       cleanup();

@@ -234,6 +234,16 @@ class ParamStore:
         s.observed = dict(self.observed)
         return s
 
+    def _latent_copy(self):
+        """A store for the engine to write a snapshot into: fresh (uninitialised) arrays
+        for the unobserved variables, the observed arrays shared (the engine never writes
+        observed variables)."""
+        s = ParamStore.__new__(ParamStore)
+        s.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("arrays", "observed")})
+        s.arrays = {k: (v if self.observed[k] else np.empty_like(v)) for k, v in self.arrays.items()}
+        s.observed = dict(self.observed)
+        return s
+
     def _view(self):
         n = len(self.names)
         real = (POINTER(c_double) * n)()
@@ -503,8 +513,8 @@ class Engine:
             raise BnmcError("run needs n >= 0 and thin >= 1")
         unobs = [v for v in store.names if not store.observed[v]]
         n_samples = (n + cfg.thin - 1) // cfg.thin
-        samples = [store.copy() for _ in range(n_samples)]
-        map_store = store.copy()
+        samples = [store._latent_copy() for _ in range(n_samples)]
+        map_store = store._latent_copy()
         views = (_Store * max(n_samples, 1))()
         keep = []
         for i, smp in enumerate(samples):
@@ -520,9 +530,9 @@ class Engine:
                     ctypes.cast(views, POINTER(_Store)), ctypes.pointer(mv), ctypes.pointer(map_lj))
         _raise(lib().bnmc_gpu_run_trace(self._h, 0, ctypes.byref(tr)), self._h)
         trace = dict(model=self.model, method=self.method, seed=cfg.seed, var_names=unobs,
-                     samples=[{v: smp[v].copy() for v in unobs} for smp in samples],
+                     samples=[{v: smp[v] for v in unobs} for smp in samples],
                      log_joint=lj[:n].tolist(), timing_ms=tm[:n].tolist(),
-                     map_state={v: map_store[v].copy() for v in unobs} if n > 0 else {},
+                     map_state={v: map_store[v] for v in unobs} if n > 0 else {},
                      map_log_joint=map_lj.value)
         if self.method != "gibbs" or self.spec["method"] == "mh":
             trace["accepted"] = acc[:n].astype(bool).tolist()
