@@ -135,8 +135,9 @@ int bnmc_gpu_download(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
 int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_accepted);
 /* Engine::sweep on a caller's store in one call: upload what the sweep reads
  * (bnmc_gpu_upload_sweep_inputs), sweep, and write the latent state back -- LDA copies
- * phi and theta back while the z-step still runs.  LDA, single rank: when no other call
- * ran on the context since the previous sweep_store, the sweep starts from the device
+ * phi and theta back while the z-step still runs.  LDA: when no other call ran on the
+ * context since the previous sweep_store (on every rank: the decision is collective), the
+ * sweep starts from the device
  * state (the z last written back to the caller) while the store's z is uploaded; the
  * upload is then compared with that z and, if the caller changed the store, the sweep
  * is redone from the upload -- results equal the non-speculative path's

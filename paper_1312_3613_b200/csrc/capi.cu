@@ -370,7 +370,7 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     m->h2d_bytes = m->d2h_bytes = 0;
     // speculative when no other call ran since the last sweep_store (see Model::epoch)
     m->quiet = m->spec_epoch + 1 == m->epoch;
-    const bool spec = m->quiet && m->spec_begin(*s, c->stream);
+    const bool spec = m->spec_begin(*s, c->stream);  // (collective for sharded models)
     if (!spec) m->upload_sweep_inputs(*s, c->stream);
     m->quiet = false;
     auto sweep_and_write_back = [&](bool verify) {

@@ -2722,10 +2722,21 @@ class Lda final : public Model {
   // state -- the z this context last wrote back to the caller (zprev_), with its counts
   // -- while the caller's z crosses PCIe on up_; spec_verify compares the two after
   // the sweep, and a difference makes sweep_store adopt the upload and redo the sweep.
-  // Single-rank only (a redo must not be a per-rank decision); BNMC_SPECULATE=0 disables it.
+  // Sharded: whether to speculate and whether to redo are collective decisions (an int
+  // all-reduce each), so every rank runs the same sweeps and NCCL calls.
+  // BNMC_SPECULATE=0 disables it.
   bool spec_begin(const bnmc_gpu_store& s, cudaStream_t st) override {
-    if (!speculate_ || comm_.active() || Nl_ == 0 || !zprev_valid_) return false;
-    if ((s.observed && s.observed[var_z_]) || !s.ival[var_z_]) return false;
+    bool ok = quiet && speculate_ && Nl_ > 0 && zprev_valid_ && !(s.observed && s.observed[var_z_]) &&
+              s.ival[var_z_] != nullptr;
+    if (comm_.active()) {
+      *spec_flag_host_ = ok ? 1 : 0;
+      BNMC_CUDA(cudaMemcpyAsync(spec_flag_.p, spec_flag_host_, sizeof(int), cudaMemcpyHostToDevice, st));
+      BNMC_NCCL(ncclAllReduce(spec_flag_.p, spec_flag_.p, 1, ncclInt32, ncclMin, comm_.comm, st));
+      BNMC_CUDA(cudaMemcpyAsync(spec_flag_host_, spec_flag_.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      BNMC_CUDA(cudaStreamSynchronize(st));
+      ok = *spec_flag_host_ == 1;
+    }
+    if (!ok) return false;
     check_len(s, var_z_, N_, "z");
     if (up64_.n < static_cast<std::size_t>(Nl_)) up64_.alloc(Nl_);
     BNMC_CUDA(cudaMemsetAsync(spec_flag_.p, 0, sizeof(int), st));
@@ -2738,6 +2749,7 @@ class Lda final : public Model {
   void spec_verify(cudaStream_t st) override {
     BNMC_CUDA(cudaStreamWaitEvent(st, ev_up_, 0));
     spec_check_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 8), 256, 0, st>>>(up64_.p, zprev_.p, Nl_, spec_flag_.p);
+    if (comm_.active()) BNMC_NCCL(ncclAllReduce(spec_flag_.p, spec_flag_.p, 1, ncclInt32, ncclMax, comm_.comm, st));
     BNMC_CUDA(cudaMemcpyAsync(spec_flag_host_, spec_flag_.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   }
 

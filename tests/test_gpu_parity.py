@@ -203,7 +203,8 @@ def test_lda_bound_store_transfers(g, K):
     e2.close()
 
 
-def test_lda_speculative_sweep_store(g, monkeypatch):
+@pytest.mark.parametrize("nccl", [False, True], ids=["single", "nccl-path"])
+def test_lda_speculative_sweep_store(g, monkeypatch, nccl):
     """Repeated Engine::sweep calls on a bound store start from the device state while
     the store's z is uploaded (sweep_store speculation).  Results must equal the
     non-speculative path's call by call, including when the caller edits z between
@@ -220,6 +221,8 @@ def test_lda_speculative_sweep_store(g, monkeypatch):
         e.prior_init(s, 9)
         return e, s
 
+    if nccl:  # the collective speculate / redo decisions, on a 1-rank communicator
+        monkeypatch.setenv("BNMC_FORCE_NCCL", "1")
     e1, s1 = make()  # speculative (default)
     monkeypatch.setenv("BNMC_SPECULATE", "0")
     e2, s2 = make()
