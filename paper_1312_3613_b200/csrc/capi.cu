@@ -54,6 +54,8 @@ struct bnmc_gpu_ctx {
   DevBuf<std::int64_t> iter;
   DevBuf<int> err;
   std::int64_t* host_iter = nullptr;  // pinned
+  int* host_err = nullptr;            // pinned: the device error word, fetched by read_ring
+  bool err_fetched = false;           // host_err holds the word as of the last stream sync
   std::int64_t next_iter = -1;        // device *iter value after the enqueued work
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -75,6 +77,7 @@ int guarded(bnmc_gpu_ctx* ctx, F&& f) {
   try {
     if (ctx) BNMC_CUDA(cudaSetDevice(ctx->device));
     if (ctx && ctx->model) ++ctx->model->epoch;  // any call may change the device state
+    if (ctx) ctx->err_fetched = false;
     f();
     return BNMC_GPU_OK;
   } catch (const Error& e) {
@@ -88,8 +91,13 @@ int guarded(bnmc_gpu_ctx* ctx, F&& f) {
 
 void check_device_error(bnmc_gpu_ctx* c) {
   int e = 0;
-  BNMC_CUDA(cudaMemcpyAsync(&e, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->err_fetched) {  // read_ring already brought the word back with its sync
+    e = *c->host_err;
+    c->err_fetched = false;
+  } else {
+    BNMC_CUDA(cudaMemcpyAsync(&e, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  }
   if (e) {
     BNMC_CUDA(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
     BNMC_CUDA(cudaStreamSynchronize(c->stream));
@@ -109,6 +117,7 @@ void set_iter(bnmc_gpu_ctx* c, std::int64_t it) {
 }
 
 void launch_sweep(bnmc_gpu_ctx* c) {
+  c->err_fetched = false;  // work enqueued after the last fetch of the error word
   if (c->desc.flags & BNMC_GPU_NO_GRAPH) {
     c->model->enqueue_sweep(c->stream);
   } else {
@@ -144,7 +153,9 @@ void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, in
     if (n > first)
       BNMC_CUDA(cudaMemcpyAsync(acc + first, c->acc.p, sizeof(int) * (n - first), cudaMemcpyDeviceToHost, c->stream));
   }
+  BNMC_CUDA(cudaMemcpyAsync(c->host_err, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   BNMC_CUDA(cudaStreamSynchronize(c->stream));
+  c->err_fetched = true;
 }
 
 // MAP tracking on the device (bnmc_gpu_run_trace): the sweep just advanced *iter;
@@ -235,6 +246,7 @@ int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
     c->iter.zero(c->stream);
     c->err.zero(c->stream);
     BNMC_CUDA(cudaMallocHost(&c->host_iter, sizeof(std::int64_t)));
+    BNMC_CUDA(cudaMallocHost(&c->host_err, sizeof(int)));
     c->next_iter = 0;
     Outputs o{c->lj.p, c->acc.p, c->iter.p, c->err.p};
     switch (desc->kind) {
@@ -267,6 +279,7 @@ void bnmc_gpu_destroy(bnmc_gpu_ctx* c) {
   c->model.reset();
   if (c->comm.comm) ncclCommDestroy(c->comm.comm);
   if (c->host_iter) cudaFreeHost(c->host_iter);
+  if (c->host_err) cudaFreeHost(c->host_err);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
