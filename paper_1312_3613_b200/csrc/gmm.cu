@@ -77,28 +77,34 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(GmmArgs a, int* err) {
   }
 }
 
-__device__ double reduce_part(const GmmArgs& a, int k, int j, double* scratch) {
+// All K x J sums over the kBlocks partials at once (J <= 3; K * J <= blockDim): thread t
+// sums (k, j) = t mod (K J) over every groups-th partial, then threads t < K J add the
+// groups' sums in group order -- fixed order, one barrier pair instead of one block
+// reduction per (k, j) (the per-(k, j) reductions were ~1 us each, serialised).
+__device__ void reduce_parts(const GmmArgs& a, int J, double* out, double* tmp) {
+  const int n = a.K * J, t = threadIdx.x;
+  const int groups = static_cast<int>(blockDim.x) / n, grp = t / n, q = t - grp * n;
   double s = 0.0;
-  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x)
-    s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
-  return block_sum(s, scratch);
-}
-
-__global__ void draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
-  __shared__ double scratch[32];
-  __shared__ double cnt[kMaxK], P[kMaxK], W[kMaxK];
-  const std::int64_t iter = *iter_p;
-  for (int k = 0; k < a.K; ++k) {
-    const double c = reduce_part(a, k, 0, scratch);
-    const double p = reduce_part(a, k, 1, scratch);
-    const double w = reduce_part(a, k, 2, scratch);
-    if (threadIdx.x == 0) {
-      cnt[k] = c;
-      P[k] = p;
-      W[k] = w;
-    }
+  if (grp < groups) {
+    const int k = q / J, j = q - (q / J) * J;
+#pragma unroll 4
+    for (int b = grp; b < kBlocks; b += groups) s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
+  }
+  tmp[t] = s;
+  __syncthreads();
+  if (t < n) {
+    double r = 0.0;
+    for (int g = 0; g < groups; ++g) r += tmp[g * n + t];
+    out[t] = r;
   }
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double sums[3 * kMaxK], tmp[kThreads];
+  const std::int64_t iter = *iter_p;
+  reduce_parts(a, 3, sums, tmp);
+  const double* cnt = sums;  // [k * 3 + 0]: count, 1: precision sum, 2: weighted x sum
   // Independent per-component streams: thread k draws the pi cell's gamma and mu_k (the
   // draws were serial on one thread: ~2 gamma chains of latency per component).
   __shared__ double g[kMaxK];
@@ -109,11 +115,11 @@ __global__ void draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
     // pi block: Dirichlet over a single row, cells derive(0, c)
     Stream r(derive(kp, 0, static_cast<std::uint64_t>(k)));
-    g[k] = draw_gamma(r, a.alpha + cnt[k]);
+    g[k] = draw_gamma(r, a.alpha + cnt[3 * k]);
     // mu block
     Stream q(derive(km, static_cast<std::uint64_t>(k)));
-    const double prec = 1.0 / a.v0 + P[k];
-    const double wsum = a.mu0 / a.v0 + W[k];
+    const double prec = 1.0 / a.v0 + cnt[3 * k + 1];
+    const double wsum = a.mu0 / a.v0 + cnt[3 * k + 2];
     const double post_var = 1.0 / prec;
     a.mu[k] = post_var * wsum + sqrt(post_var) * q.next_gaussian();
   }
@@ -125,25 +131,16 @@ __global__ void draw_pi_mu_kernel(GmmArgs a, const std::int64_t* iter_p) {
   }
 }
 
-__global__ void draw_s2_kernel(GmmArgs a, const std::int64_t* iter_p) {
-  __shared__ double scratch[32];
-  __shared__ double cnt[kMaxK], rss[kMaxK];
+__global__ void __launch_bounds__(kThreads) draw_s2_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double sums[2 * kMaxK], tmp[kThreads];
   const std::int64_t iter = *iter_p;
-  for (int k = 0; k < a.K; ++k) {
-    const double c = reduce_part(a, k, 0, scratch);
-    const double s = reduce_part(a, k, 1, scratch);
-    if (threadIdx.x == 0) {
-      cnt[k] = c;
-      rss[k] = s;
-    }
-  }
-  __syncthreads();
+  reduce_parts(a, 2, sums, tmp);
   const std::uint64_t ks = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_s2),
                                  static_cast<std::uint64_t>(iter));
   for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
     Stream r(derive(ks, static_cast<std::uint64_t>(k)));
-    const double scale = a.b0 + 0.5 * rss[k];
-    a.s2[k] = scale / draw_gamma(r, a.a0 + 0.5 * cnt[k]);
+    const double scale = a.b0 + 0.5 * sums[2 * k + 1];
+    a.s2[k] = scale / draw_gamma(r, a.a0 + 0.5 * sums[2 * k]);
   }
 }
 
@@ -221,22 +218,36 @@ __global__ void finalize_kernel(GmmArgs a, Outputs o, int advance) {
   }
   lz = block_sum(lz, scratch);
   lx = block_sum(lx, scratch);
+  // the per-component prior terms (transcendentals) in parallel, one thread per k; the
+  // sums below run in k order as the reference's sequential loops
+  __shared__ double tpi[kMaxK], tmu[kMaxK], ts2[kMaxK], lga[2];
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    tpi[k] = (a.alpha - 1.0) * log(a.pi[k]);
+    tmu[k] = log_pdf_gaussian(a.mu[k], a.mu0, a.v0);
+    ts2[k] = log_pdf_inverse_gamma(a.s2[k], a.a0, a.b0);
+  }
+  if (threadIdx.x == 32) lga[0] = lgamma(a.alpha);
+  if (threadIdx.x == 64) {
+    double asum = 0.0;
+    for (int k = 0; k < a.K; ++k) asum += a.alpha;
+    lga[1] = lgamma(asum);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    // p(pi): Dirichlet(alpha,...,alpha) log-pdf (dist.cpp:115-130), sequential.
-    double sum = 0.0, lp = 0.0, norm = 0.0, asum = 0.0;
+    // p(pi): Dirichlet(alpha,...,alpha) log-pdf (dist.cpp:115-130)
+    double sum = 0.0, lp = 0.0, norm = 0.0;
     bool bad = false;
     for (int k = 0; k < a.K; ++k) {
       const double x = a.pi[k];
       bad |= !(x > 0.0);
       sum += x;
-      lp += (a.alpha - 1.0) * log(x);
-      norm += lgamma(a.alpha);
-      asum += a.alpha;
+      lp += tpi[k];
+      norm += lga[0];
     }
-    const double fpi = (bad || fabs(sum - 1.0) > 1e-9) ? -INFINITY : lp - norm + lgamma(asum);
+    const double fpi = (bad || fabs(sum - 1.0) > 1e-9) ? -INFINITY : lp - norm + lga[1];
     double fmu = 0.0, fs2 = 0.0;
-    for (int k = 0; k < a.K; ++k) fmu += log_pdf_gaussian(a.mu[k], a.mu0, a.v0);
-    for (int k = 0; k < a.K; ++k) fs2 += log_pdf_inverse_gamma(a.s2[k], a.a0, a.b0);
+    for (int k = 0; k < a.K; ++k) fmu += tmu[k];
+    for (int k = 0; k < a.K; ++k) fs2 += ts2[k];
     const double lj = (((fpi + fmu) + fs2) + lz) + lx;
     const std::int64_t it = *o.iter;
     o.lj[it & (kRing - 1)] = lj;
