@@ -12,6 +12,10 @@
 //                      with keyed(seed,3,var_z,i,iter) (sampler.cpp:222-265);
 //                      accumulates the log-joint pieces of z and x
 //   finalize_kernel    log-joint in the reference's factor order.
+// K <= 8 (default): three kernels -- draw_params_kernel (pi, mu, sigma2 from the
+// sufficient statistics the previous z kernel left, centred on the mu it used), the z
+// kernel (draws z, accumulates the log-joint pieces and the statistics of the new z),
+// finalize -- instead of two extra passes over the data per sweep.
 // Every reduction runs over a fixed grid with a fixed tree: results are
 // reproducible run to run.  Replicas only across GPUs.
 #include <algorithm>
@@ -36,6 +40,7 @@ struct GmmArgs {
   double* mu;
   double* s2;
   double* part;  // [kBlocks][K][3]
+  double* mu_at_stats;  // [K] (fused path) the mu the z kernel's shifted sums are centred on
   double* lpart; // [kBlocks][2]
   double alpha, mu0, v0, a0, b0;
   std::uint64_t seed;
@@ -144,7 +149,14 @@ __global__ void __launch_bounds__(kThreads) draw_s2_kernel(GmmArgs a, const std:
   }
 }
 
-template <bool SAMPLE>
+// FUSE (K <= kFuseK): the z kernel also leaves, per block and component, the sufficient
+// statistics of the NEW z centred on the current mu -- n, S1 = sum (x - c), S2 = sum
+// (x - c)^2, c = mu[k] -- so the next sweep's pi / mu / sigma2 draws need no data pass:
+// P = n / sigma2, W = (S1 + n c) / sigma2 and rss = S2 - 2 d S1 + n d^2 with
+// d = mu_new - c (the shift keeps the cancellation to the size of d, a posterior sd).
+constexpr int kFuseK = 8;
+
+template <bool SAMPLE, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64_t* iter_p, int* err) {
   __shared__ double scratch[32];
   __shared__ double lpi[kMaxK], mu[kMaxK], var[kMaxK], lvar[kMaxK];
@@ -158,6 +170,9 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
   __syncthreads();
   const std::uint64_t zp = fold(fold(fold(1, a.seed), kDiscrete), static_cast<std::uint64_t>(a.var_z));
   double lz = 0.0, lx = 0.0;
+  double fn[FUSE ? kFuseK : 1], f1[FUSE ? kFuseK : 1], f2[FUSE ? kFuseK : 1];
+#pragma unroll
+  for (int v = 0; v < (FUSE ? kFuseK : 1); ++v) fn[v] = f1[v] = f2[v] = 0.0;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const double xi = a.x[i];
@@ -200,12 +215,76 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
     lz += lpi[k];
     const double d = xi - mu[k];
     lx += var[k] > 0.0 ? -0.5 * (d * d / var[k] + lvar[k] + kLog2Pi) : -INFINITY;
+    if constexpr (FUSE) {
+#pragma unroll
+      for (int v = 0; v < kFuseK; ++v)
+        if (v == k) {
+          fn[v] += 1.0;
+          f1[v] += d;
+          f2[v] += d * d;
+        }
+    }
   }
   lz = block_sum(lz, scratch);
   lx = block_sum(lx, scratch);
   if (threadIdx.x == 0) {
     a.lpart[blockIdx.x * 2 + 0] = lz;
     a.lpart[blockIdx.x * 2 + 1] = lx;
+  }
+  if constexpr (FUSE) {
+    __shared__ double sc3[3 * 32];
+#pragma unroll
+    for (int v = 0; v < kFuseK; ++v) {
+      if (v >= a.K) break;
+      double t[3] = {fn[v], f1[v], f2[v]};
+      block_sum_n<3>(t, sc3);
+      if (threadIdx.x == 0) {
+        double* p = a.part + (static_cast<std::size_t>(blockIdx.x) * a.K + v) * 3;
+        p[0] = t[0];
+        p[1] = t[1];
+        p[2] = t[2];
+      }
+    }
+    if (blockIdx.x == 0)
+      for (int v = threadIdx.x; v < a.K; v += blockDim.x) a.mu_at_stats[v] = mu[v];
+  }
+}
+
+// Fused path: pi, mu and sigma2 in one block from the z kernel's shifted sums.
+__global__ void __launch_bounds__(kThreads) draw_params_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double sums[3 * kMaxK], tmp[kThreads], g[kMaxK];
+  const std::int64_t iter = *iter_p;
+  reduce_parts(a, 3, sums, tmp);
+  const std::uint64_t kp = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_pi),
+                                 static_cast<std::uint64_t>(iter));
+  const std::uint64_t km = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_mu),
+                                 static_cast<std::uint64_t>(iter));
+  const std::uint64_t ks = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_s2),
+                                 static_cast<std::uint64_t>(iter));
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+    const double n = sums[3 * k], S1 = sums[3 * k + 1], S2 = sums[3 * k + 2];
+    const double c = a.mu_at_stats[k], v = a.s2[k];
+    // pi block: Dirichlet over a single row, cells derive(0, k)
+    Stream r(derive(kp, 0, static_cast<std::uint64_t>(k)));
+    g[k] = draw_gamma(r, a.alpha + n);
+    // mu block (sampler.cpp:199-204): P = sum 1/sigma2, W = sum x/sigma2 over the cluster
+    Stream q(derive(km, static_cast<std::uint64_t>(k)));
+    const double prec = 1.0 / a.v0 + n * (1.0 / v);
+    const double wsum = a.mu0 / a.v0 + (S1 + n * c) / v;
+    const double post_var = 1.0 / prec;
+    const double mu_new = post_var * wsum + sqrt(post_var) * q.next_gaussian();
+    a.mu[k] = mu_new;
+    // sigma2 block with the new mu: rss = sum (x - mu_new)^2 from the shifted sums
+    const double dd = mu_new - c;
+    const double rss = fmax(0.0, S2 - 2.0 * dd * S1 + n * dd * dd);
+    Stream t(derive(ks, static_cast<std::uint64_t>(k)));
+    a.s2[k] = (a.b0 + 0.5 * rss) / draw_gamma(t, a.a0 + 0.5 * n);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // left-to-right row sum (batch.cpp:55-58)
+    double sum = 0.0;
+    for (int k = 0; k < a.K; ++k) sum += g[k];
+    for (int k = 0; k < a.K; ++k) a.pi[k] = g[k] / sum;
   }
 }
 
@@ -331,6 +410,9 @@ class Gmm final : public Model {
     mu_.alloc(K_);
     s2_.alloc(K_);
     part_.alloc(static_cast<std::size_t>(kBlocks) * K_ * 3);
+    mu_at_stats_.alloc(K_);
+    fuse_ = K_ <= kFuseK;
+    if (const char* e = std::getenv("BNMC_GMM_FUSED")) fuse_ = fuse_ && std::string(e) != "0";
     lpart_.alloc(kBlocks * 2);
     part_.zero(nullptr);
     lpart_.zero(nullptr);
@@ -358,6 +440,7 @@ class Gmm final : public Model {
       z_from_i64<<<kBlocks, kThreads, 0, st>>>(stage64_.p, z_.p, N_, K_, out.err);
     }
     h2d_bytes += static_cast<std::int64_t>(sizeof(double)) * 3 * K_ + static_cast<std::int64_t>(sizeof(std::int64_t)) * N_;
+    refresh_stats(st);
     // stream-ordered: the sweep (or the caller's next synchronous call) sees the upload
   }
 
@@ -389,6 +472,17 @@ class Gmm final : public Model {
   void enqueue_sweep(cudaStream_t st) override {
     GmmArgs a = args();
     mark(st, "begin");
+    if (fuse_) {
+      // the statistics of the current z were left by the last z kernel (or refresh_stats)
+      draw_params_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
+      mark(st, "draw_pi_mu_sigma2");
+      z_kernel<true, true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+      mark(st, "z_stats");
+      finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 1);
+      mark(st, "finalize");
+      BNMC_CUDA(cudaGetLastError());
+      return;
+    }
     stats_kernel<kStatsMu><<<kBlocks, kThreads, 0, st>>>(a, out.err);
     mark(st, "stats_mu");
     draw_pi_mu_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
@@ -404,9 +498,22 @@ class Gmm final : public Model {
     BNMC_CUDA(cudaGetLastError());
   }
 
+  // Fused path: the statistics of the current state (after any state change).
+  void refresh_stats(cudaStream_t st) {
+    if (!fuse_ || N_ == 0) return;
+    GmmArgs a = args();
+    z_kernel<false, true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    BNMC_CUDA(cudaGetLastError());
+  }
+
+  void on_state_restored(cudaStream_t st) override {
+    refresh_stats(st);
+    BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
   void enqueue_log_joint(cudaStream_t st) override {
     GmmArgs a = args();
-    z_kernel<false><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    z_kernel<false, false><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
     finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 0);
     BNMC_CUDA(cudaGetLastError());
   }
@@ -415,6 +522,7 @@ class Gmm final : public Model {
     GmmArgs a = args();
     prior_kernel<<<1, 32, 0, st>>>(a, seed);
     prior_z_kernel<<<kBlocks, kThreads, 0, st>>>(a, seed);
+    refresh_stats(st);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
@@ -431,6 +539,7 @@ class Gmm final : public Model {
     a.s2 = s2_.p;
     a.part = part_.p;
     a.lpart = lpart_.p;
+    a.mu_at_stats = mu_at_stats_.p;
     a.alpha = alpha_;
     a.mu0 = mu0_;
     a.v0 = v0_;
@@ -450,7 +559,8 @@ class Gmm final : public Model {
   double alpha_, mu0_, v0_, a0_, b0_;
   std::uint64_t seed_ = 0;
   int var_[5] = {0, 1, 2, 3, 4};
-  DevBuf<double> x_, pi_, mu_, s2_, part_, lpart_;
+  DevBuf<double> x_, pi_, mu_, s2_, part_, lpart_, mu_at_stats_;
+  bool fuse_ = true;  // draw_params_kernel + z_kernel<.., true> (K <= kFuseK; BNMC_GMM_FUSED=0: 6-kernel sweep)
   DevBuf<int> z_;
   DevBuf<std::int64_t> stage64_;  // z upload / write-back staging (int64 store layout)
 };

@@ -329,7 +329,10 @@ def test_lda_device_prior_init_matches_reference(g, restatement):
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
-def test_gmm_sweeps_vs_reference(g):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "six-kernel"])
+def test_gmm_sweeps_vs_reference(g, monkeypatch, fused):
+    if not fused:
+        monkeypatch.setenv("BNMC_GMM_FUSED", "0")
     fx = golden("gmm_small")
     hyper = {"N": int(fx["N"]), "K": 4}
     e = g.Engine("gmm", hyper, g.RunConfig(seed=int(fx["seed"])))
