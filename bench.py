@@ -287,7 +287,9 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         eng.prior_init(store, args.seed)
         sites_total = sites_local = N * world  # replicas
         sites_local = N
-        per_sweep_kernels, dominant = 6, "z"
+        # K <= 8: the fused sweep -- draw_params, z (+ next-sweep statistics), finalize
+        fused = K <= 8 and os.environ.get("BNMC_GMM_FUSED", "1") != "0"
+        per_sweep_kernels, dominant = (3, "z_stats") if fused else (6, "z")
         bytes_per_site_dom = bytes_per_site_sweep = impl_bytes_per_site = 16
         host_corpus = True
         config = {"workload": "gmm-100k", "model": "gmm (proj/models/gmm.bn)", "points": N, "components": K,
