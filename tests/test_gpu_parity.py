@@ -281,6 +281,50 @@ def test_mh_bound_store_unchanged_skip(g, monkeypatch):
     e2.close()
 
 
+def test_cpp_mirror_matches_python_engine(g, tmp_path):
+    """include/bnmc_gpu.hpp driving the GPU path as a reference caller drives bnmc::Engine
+    (prior_init, eval_log_joint, 5 x sweep, run with thin 2): every value equals the
+    Python engine's over the same library."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    K, V, M, L, seed = 6, 50, 8, 40, 17
+    w = np.random.default_rng(3).integers(0, V, M * L).astype(np.int64)
+    wp = tmp_path / "w.bin"
+    w.tofile(wp)
+    exe = tmp_path / "lda_engine_example"
+    lib = os.path.join(ROOT, "paper_1312_3613_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "lda_engine_example.cpp"), "-L", lib, "-lbnmc_gpu",
+                        f"-Wl,-rpath,{lib}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe), str(wp), str(K), str(V), str(L), str(seed)], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stderr
+    got = {}
+    for line in r.stdout.splitlines():
+        parts = line.split()
+        got[" ".join(parts[:-1])] = float(parts[-1])
+
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed, thin=2))
+    s = e.allocate()
+    s["w"] = w
+    e.prior_init(s, seed)
+    assert got["prior"] == e.eval_log_joint(s)
+    for i in range(5):
+        assert got[f"sweep {i}"] == e.sweep(s, i), i
+    tr = e.run(s, 4)
+    for i, v in enumerate(tr["log_joint"]):
+        assert got[f"run {i}"] == v, i
+    assert got["map"] == tr["map_log_joint"]
+    assert got["samples"] == len(tr["samples"]) == 2
+    assert got["eval"] == e.eval_log_joint(s)
+    assert got["z0"] == s["z"][0]
+    e.close()
+
+
 def _gen_lda(restatement, reference, M, V, K, L, seed):
     w, _, _ = reference.gen_lda(M, V, K, L, seed)
     off = np.arange(M + 1, dtype=np.int64) * L

@@ -102,6 +102,11 @@ def test_cpp_mirror_compiles():
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-x", "c", HEADER],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+    # the driver the GPU parity suite runs against the Python engine
+    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "lda_engine_example.cpp"), "-L", lib, "-lbnmc_gpu",
+                        "-o", "/tmp/bnmc_lda_engine_example_test"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
 
 
 def test_bench_corpus_generator_shape():
