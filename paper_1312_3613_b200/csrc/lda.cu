@@ -102,6 +102,7 @@ struct LdaArgs {
   double* doc_part;  // [Ml][3] (eval path)
   double* red;       // [4]
   double alpha, beta;
+  int pow_alpha, pow_beta;  // 1/alpha, 1/beta when exactly an integer in [2, 64] (boost by squaring), else 0
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
@@ -193,6 +194,20 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
 // The stream of every cell is keyed(seed, 4, var_phi, iter).derive(k, v) and is
 // consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
 // uniform]), so the draws are the reference's.
+// The shape < 1 boost g * u^(1/shape) (dist.cpp:139-140) when 1/shape is exactly an
+// integer e (lda.bn's alpha = beta = 0.1: e = 10): u^e by binary powering (4 multiplies
+// for e = 10, <= ~4 ulp from the correctly rounded power -- pow's own error is <= 1 ulp,
+// the exp(log) form below ~40 ulp) instead of a log and an exp per zero-count cell.
+__device__ __forceinline__ double boost_factor(double u, int e, double inv) {
+  if (e == 0) return exp(inv * log(u));
+  double r = 1.0, b = u;
+  for (; e; e >>= 1) {
+    if (e & 1) r *= b;
+    b *= b;
+  }
+  return r;
+}
+
 constexpr int kGammaTab = 64;
 constexpr int kPhiRowsMax = 8;  // L: cells per thread (8, or fewer for small K x V)
 
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
         // rounded pow is <= ~2^-53 * 37 / shape (4e-14 at shape 0.1), far inside the 1e-12
         // contract, and exp + log cost half of pow's double-double path (r01 v33: phi
         // block 83 -> 77 us on NIPS)
-        if (inv != 0.0) g = g * exp(inv * log(r.next_unit()));
+        if (inv != 0.0) g = g * boost_factor(r.next_unit(), a.pow_beta, inv);
         const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
         a.phiT[i] = g;
         if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + col32] = static_cast<float>(g);
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(256) theta2_kernel(LdaArgs a, const std::int64
         // rounded pow is <= ~2^-53 * 37 / shape (4e-14 at shape 0.1), far inside the 1e-12
         // contract, and exp + log cost half of pow's double-double path (r01 v33: phi
         // block 83 -> 77 us on NIPS)
-        if (inv != 0.0) g = g * exp(inv * log(r.next_unit()));
+        if (inv != 0.0) g = g * boost_factor(r.next_unit(), a.pow_alpha, inv);
         g_s[k - k0][threadIdx.x] = g;
         sg += g;
         if (g > 0.0) {
@@ -3400,6 +3415,13 @@ class Lda final : public Model {
     });
   }
 
+  // 1/x when it is exactly an integer in [2, 64] (the boost exponent), else 0
+  static int exact_int_inverse(double x) {
+    if (!(x > 0.0)) return 0;
+    const double inv = 1.0 / x;
+    return (inv == std::floor(inv) && inv >= 2.0 && inv <= 64.0) ? static_cast<int>(inv) : 0;
+  }
+
   LdaArgs args() const {
     LdaArgs a{};
     a.K = K_;
@@ -3445,6 +3467,8 @@ class Lda final : public Model {
     a.ttpart = ttpart_.p;
     a.alpha = alpha_;
     a.beta = beta_;
+    a.pow_alpha = boost_pow_ ? exact_int_inverse(alpha_) : 0;
+    a.pow_beta = boost_pow_ ? exact_int_inverse(beta_) : 0;
     a.phi_norm = phi_norm_;
     a.phi_lgasum = phi_lgasum_;
     a.theta_norm = theta_norm_;
@@ -3547,6 +3571,7 @@ class Lda final : public Model {
   DevBuf<std::int64_t> off_;
   std::int64_t nvb_ = 1;
   int phi_rows_ = kPhiRowsMax;
+  bool boost_pow_ = std::getenv("BNMC_BOOST_POW") == nullptr || std::string(std::getenv("BNMC_BOOST_POW")) != "0";
   DevBuf<double> gpart_, lpart_, spart_, logg_, logS_, ttpart_;
   DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
