@@ -103,6 +103,7 @@ struct LdaArgs {
   double* red;       // [4]
   double alpha, beta;
   int pow_alpha, pow_beta;  // 1/alpha, 1/beta when exactly an integer in [2, 64] (boost by squaring), else 0
+  int phi_pf;               // phi_gamma2: count prefetch distance in blocks (0: off)
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
@@ -237,6 +238,21 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
       const std::size_t i = static_cast<std::size_t>(v0 + j) * a.Kp + k;
       cnt_s[j][threadIdx.x] = a.nkw[i];
       a.nkw[i] = 0;  // consumed: the z-step accumulates the next sweep's counts here
+    }
+  }
+  // The counts of the block ~0.7 resident waves later (a.phi_pf blocks on), into L2 while
+  // this block draws: the next wave then starts from L2 instead of HBM (the bench flushes
+  // L2 before every sweep; r01: phi 73 -> 66 us on NIPS).
+  if (a.phi_pf > 0) {
+    const std::int64_t idx2 = idx + static_cast<std::int64_t>(a.phi_pf) * blockDim.x;
+    const std::int64_t vb2 = idx2 / a.K;
+    if (vb2 < a.nvb) {
+      const int k2 = static_cast<int>(idx2 % a.K);
+#pragma unroll
+      for (int j = 0; j < kPhiRows; ++j) {
+        const std::int64_t v2 = vb2 * kPhiRows + j;
+        if (v2 < a.V) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.nkw + static_cast<std::size_t>(v2) * a.Kp + k2));
+      }
     }
   }
   const int col32 = a.phiT32 ? phys32(k, a.R32, a.G32, a.CW32) : 0;
@@ -2609,6 +2625,19 @@ class Lda final : public Model {
       if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
     }
     nvb_ = (V_ + phi_rows_ - 1) / phi_rows_;
+    {
+      int dev = 0, sms = 148, per_sm = 1;
+      BNMC_CUDA(cudaGetDevice(&dev));
+      BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      switch (phi_rows_) {
+        case 1: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<1>, 256, 0)); break;
+        case 2: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<2>, 256, 0)); break;
+        case 4: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0)); break;
+        default: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<8>, 256, 0)); break;
+      }
+      phi_pf_ = static_cast<int>(0.7 * sms * std::max(per_sm, 1));  // measured: 0.55-0.8 of a wave best
+      if (const char* e = std::getenv("BNMC_PHI_PREFETCH")) phi_pf_ = std::max(0, std::atoi(e));
+    }
     col_stripes_ = static_cast<int>(std::min<std::int64_t>(kColStripes, std::max<std::int64_t>(4, nvb_ / 96)));
     if (const char* e = std::getenv("BNMC_COL_STRIPES")) col_stripes_ = std::min(kColStripes, std::max(1, std::atoi(e)));
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
@@ -3469,6 +3498,7 @@ class Lda final : public Model {
     a.beta = beta_;
     a.pow_alpha = boost_pow_ ? exact_int_inverse(alpha_) : 0;
     a.pow_beta = boost_pow_ ? exact_int_inverse(beta_) : 0;
+    a.phi_pf = phi_pf_;
     a.phi_norm = phi_norm_;
     a.phi_lgasum = phi_lgasum_;
     a.theta_norm = theta_norm_;
@@ -3572,6 +3602,7 @@ class Lda final : public Model {
   std::int64_t nvb_ = 1;
   int phi_rows_ = kPhiRowsMax;
   bool boost_pow_ = std::getenv("BNMC_BOOST_POW") == nullptr || std::string(std::getenv("BNMC_BOOST_POW")) != "0";
+  int phi_pf_ = 0;     // phi_gamma2 count prefetch distance (blocks)
   DevBuf<double> gpart_, lpart_, spart_, logg_, logS_, ttpart_;
   DevBuf<int> ticket_;
   DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
