@@ -161,12 +161,13 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+def ncu_traffic(key: str):
+    """dram bytes per launch of the kernel `workload:kernel` from the committed ncu summaries
+    (profiles/ncu_traffic.json; one `ncu --set full` capture per workload), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(key)
     except Exception:
         return None
 
@@ -368,7 +369,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     roofline = roofline_l2 = None
     if dom_ms:
         achieved = sites_local * bytes_per_site_dom / (dom_ms / 1e3) / 1e9
-        traffic = ncu_traffic(dominant)
+        traffic = ncu_traffic(f"{args.workload}:{dominant}")
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1), "peak": peak,
                     "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
                     "traffic": traffic, "algorithmic_bytes_per_site": round(bytes_per_site_dom, 2),
