@@ -2557,7 +2557,9 @@ class Lda final : public Model {
     if (const char* e = std::getenv("BNMC_ZT_WU")) zt_wu_ = std::string(e) != "0";
     {
       const double mean = n_units_ > 0 ? static_cast<double>(Nl_) / static_cast<double>(n_units_) : 32.0;
-      zt_warps_ = std::min(8, std::max(1, static_cast<int>(std::ceil(mean / 32.0))));
+      // at most 4 warps per document CTA (r01, NIPS z-step: 4 warps 91.5 us, 8 warps 93.5,
+      // 5-6 warps 95; smaller CTAs, same warps per SM)
+      zt_warps_ = std::min(4, std::max(1, static_cast<int>(std::ceil(mean / 32.0))));
       if (const char* e = std::getenv("BNMC_ZT_WARPS")) zt_warps_ = std::min(8, std::max(1, std::atoi(e)));
     }
 
