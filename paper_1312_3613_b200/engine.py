@@ -239,12 +239,27 @@ class ParamStore:
         for the unobserved variables, the observed arrays shared (the engine never writes
         observed variables)."""
         s = ParamStore.__new__(ParamStore)
-        s.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("arrays", "observed")})
+        s.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("arrays", "observed", "_vcache")})
         s.arrays = {k: (v if self.observed[k] else np.empty_like(v)) for k, v in self.arrays.items()}
         s.observed = dict(self.observed)
         return s
 
     def _view(self):
+        # cached per array identity (an array object's buffer and layout never change) and
+        # observed mask; the cache holds the arrays, so an id cannot be reused by a
+        # replacement while the cached view points at the old one (~30 us per call saved
+        # on every Engine.sweep)
+        c = self.__dict__.get("_vcache")
+        if c is not None:
+            arrs, obs, st = c
+            a = self.arrays
+            if all(a[n] is x for n, x in zip(self.names, arrs)) and obs == tuple(self.observed[n] for n in self.names):
+                return st
+        st = self._build_view()  # (may replace non-contiguous arrays by contiguous copies)
+        self._vcache = (tuple(self.arrays[n] for n in self.names), tuple(self.observed[n] for n in self.names), st)
+        return st
+
+    def _build_view(self):
         n = len(self.names)
         real = (POINTER(c_double) * n)()
         ival = (POINTER(c_int64) * n)()

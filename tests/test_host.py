@@ -115,3 +115,25 @@ def test_bench_corpus_generator_shape():
     w = bench.gen_lda_corpus(20, 300, 5, 17, 3)
     assert w.shape == (340,) and w.min() >= 0 and w.max() < 300
     assert np.array_equal(w, bench.gen_lda_corpus(20, 300, 5, 17, 3))
+
+
+def test_store_view_cache_follows_the_arrays():
+    """ParamStore._view is cached per array object and observed mask: replacing an array
+    (through __setitem__ or .arrays) or flipping a mask rebuilds it, in-place writes do not
+    need to (the pointers are unchanged)."""
+    from paper_1312_3613_b200.engine import ParamStore
+
+    s = ParamStore("gmm", {"N": 100, "K": 4})
+    v1 = s._view()
+    assert s._view() is v1
+    s["z"][:] = 1  # in place: same buffer
+    assert s._view() is v1
+    s["z"] = np.zeros(100, dtype=np.int64)
+    v2 = s._view()
+    assert v2 is not v1 and v2.ival[3] is not None
+    assert ctypes.addressof(v2.ival[3].contents) == s["z"].ctypes.data
+    s.arrays["x"] = np.ones(100)
+    v3 = s._view()
+    assert v3 is not v2 and ctypes.addressof(v3.real[4].contents) == s["x"].ctypes.data
+    s.observed["z"] = True
+    assert s._view() is not v3
