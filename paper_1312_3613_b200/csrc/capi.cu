@@ -139,7 +139,7 @@ void launch_sweep(bnmc_gpu_ctx* c) {
   c->next_iter += 1;
 }
 
-void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, int* acc) {
+void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, int* acc, bool sync = true) {
   // Entries it0 .. it0+n-1 (n <= kRing), possibly wrapping.
   const std::int64_t s = it0 & (kRing - 1);
   const std::int64_t first = std::min<std::int64_t>(n, kRing - s);
@@ -154,6 +154,7 @@ void read_ring(bnmc_gpu_ctx* c, std::int64_t it0, std::int64_t n, double* lj, in
       BNMC_CUDA(cudaMemcpyAsync(acc + first, c->acc.p, sizeof(int) * (n - first), cudaMemcpyDeviceToHost, c->stream));
   }
   BNMC_CUDA(cudaMemcpyAsync(c->host_err, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (!sync) return;  // the caller's next stream synchronisation completes the copies
   BNMC_CUDA(cudaStreamSynchronize(c->stream));
   c->err_fetched = true;
 }
@@ -391,9 +392,11 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
       launch_sweep(c);
       if (verify) m->spec_verify(c->stream);
       if (!m->download_overlapped(*s, c->stream)) {
-        read_ring(c, iter, 1, log_joint, mh_accepted);
+        read_ring(c, iter, 1, log_joint, mh_accepted, false);
+        m->download(*s, c->stream);  // synchronises the stream: the ring entry and error word too
+        BNMC_CUDA(cudaStreamSynchronize(c->stream));  // (idle already: guards a model that did not)
+        c->err_fetched = true;
         check_device_error(c);
-        m->download(*s, c->stream);
         return;
       }
       read_ring(c, iter, 1, log_joint, mh_accepted);  // synchronises the stream (and the copies)
