@@ -2620,8 +2620,18 @@ class Lda final : public Model {
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
     // vs 42 at 1): enough threads to fill the GPU while the per-thread rejection loop
-    // still amortises over several cells
+    // still amortises over several cells; 2 when 4 leaves the GPU under one wave
     phi_rows_ = 4;
+    {
+      // a grid below one resident wave at 4 rows (KOS: 337 blocks for 740 slots) draws
+      // 2 rows per thread instead: twice the threads in flight (r01, KOS phi 35.3 -> 32.2 us)
+      int dev = 0, sms = 148, per_sm = 1;
+      BNMC_CUDA(cudaGetDevice(&dev));
+      BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0));
+      const std::int64_t blocks4 = ((V_ + 3) / 4 * K_ + 255) / 256;
+      if (blocks4 < static_cast<std::int64_t>(sms) * std::max(per_sm, 1)) phi_rows_ = 2;
+    }
     if (const char* e = std::getenv("BNMC_PHI_ROWS")) {
       const int r = std::atoi(e);
       if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
