@@ -28,7 +28,8 @@ namespace bnmc_gpu {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBlocks = 148 * 2;
+constexpr int kBlocks = 148 * 2;     // grid of the six-kernel path's data passes
+constexpr int kMaxBlocks = 148 * 4;  // partial slots (the fused z kernel sizes its grid to N)
 constexpr int kMaxK = 64;
 
 struct GmmArgs {
@@ -39,9 +40,10 @@ struct GmmArgs {
   double* pi;
   double* mu;
   double* s2;
-  double* part;  // [kBlocks][K][3]
+  int nb;        // blocks that wrote part / lpart (the grid of the kernels producing them)
+  double* part;  // [nb][K][3]
   double* mu_at_stats;  // [K] (fused path) the mu the z kernel's shifted sums are centred on
-  double* lpart; // [kBlocks][2]
+  double* lpart; // [nb][2]
   double alpha, mu0, v0, a0, b0;
   std::uint64_t seed;
   int var_pi, var_mu, var_s2, var_z;
@@ -93,7 +95,7 @@ __device__ void reduce_parts(const GmmArgs& a, int J, double* out, double* tmp) 
   if (grp < groups) {
     const int k = q / J, j = q - (q / J) * J;
 #pragma unroll 4
-    for (int b = grp; b < kBlocks; b += groups) s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
+    for (int b = grp; b < a.nb; b += groups) s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
   }
   tmp[t] = s;
   __syncthreads();
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) draw_s2_kernel(GmmArgs a, const std:
 // d = mu_new - c (the shift keeps the cancellation to the size of d, a posterior sd).
 constexpr int kFuseK = 8;
 
-template <bool SAMPLE, bool FUSE = false>
+template <bool SAMPLE, bool FUSE = false, int FK = kFuseK>
 __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64_t* iter_p, int* err) {
   __shared__ double scratch[32];
   __shared__ double lpi[kMaxK], mu[kMaxK], var[kMaxK], lvar[kMaxK];
@@ -170,9 +172,9 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
   __syncthreads();
   const std::uint64_t zp = fold(fold(fold(1, a.seed), kDiscrete), static_cast<std::uint64_t>(a.var_z));
   double lz = 0.0, lx = 0.0;
-  double fn[FUSE ? kFuseK : 1], f1[FUSE ? kFuseK : 1], f2[FUSE ? kFuseK : 1];
+  double fn[FUSE ? FK : 1], f1[FUSE ? FK : 1], f2[FUSE ? FK : 1];
 #pragma unroll
-  for (int v = 0; v < (FUSE ? kFuseK : 1); ++v) fn[v] = f1[v] = f2[v] = 0.0;
+  for (int v = 0; v < (FUSE ? FK : 1); ++v) fn[v] = f1[v] = f2[v] = 0.0;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const double xi = a.x[i];
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
     lx += var[k] > 0.0 ? -0.5 * (d * d / var[k] + lvar[k] + kLog2Pi) : -INFINITY;
     if constexpr (FUSE) {
 #pragma unroll
-      for (int v = 0; v < kFuseK; ++v)
+      for (int v = 0; v < FK; ++v)
         if (v == k) {
           fn[v] += 1.0;
           f1[v] += d;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
   if constexpr (FUSE) {
     __shared__ double sc3[3 * 32];
 #pragma unroll
-    for (int v = 0; v < kFuseK; ++v) {
+    for (int v = 0; v < FK; ++v) {
       if (v >= a.K) break;
       double t[3] = {fn[v], f1[v], f2[v]};
       block_sum_n<3>(t, sc3);
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(kThreads) draw_params_kernel(GmmArgs a, const 
 __global__ void finalize_kernel(GmmArgs a, Outputs o, int advance) {
   __shared__ double scratch[32];
   double lz = 0.0, lx = 0.0;
-  for (int b = threadIdx.x; b < kBlocks; b += blockDim.x) {
+  for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
     lz += a.lpart[b * 2 + 0];
     lx += a.lpart[b * 2 + 1];
   }
@@ -409,11 +411,13 @@ class Gmm final : public Model {
     pi_.alloc(K_);
     mu_.alloc(K_);
     s2_.alloc(K_);
-    part_.alloc(static_cast<std::size_t>(kBlocks) * K_ * 3);
+    part_.alloc(static_cast<std::size_t>(kMaxBlocks) * K_ * 3);
     mu_at_stats_.alloc(K_);
     fuse_ = K_ <= kFuseK;
+    // fused path: one point per thread where the grid fits one wave (N = 1e5: 391 blocks)
+    nbz_ = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(kMaxBlocks, (N_ + kThreads - 1) / kThreads)));
     if (const char* e = std::getenv("BNMC_GMM_FUSED")) fuse_ = fuse_ && std::string(e) != "0";
-    lpart_.alloc(kBlocks * 2);
+    lpart_.alloc(kMaxBlocks * 2);
     part_.zero(nullptr);
     lpart_.zero(nullptr);
     z_.zero(nullptr);
@@ -476,7 +480,7 @@ class Gmm final : public Model {
       // the statistics of the current z were left by the last z kernel (or refresh_stats)
       draw_params_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
       mark(st, "draw_pi_mu_sigma2");
-      z_kernel<true, true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+      launch_fused_z<true>(a, st);
       mark(st, "z_stats");
       finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 1);
       mark(st, "finalize");
@@ -498,11 +502,17 @@ class Gmm final : public Model {
     BNMC_CUDA(cudaGetLastError());
   }
 
+  template <bool SAMPLE>
+  void launch_fused_z(const GmmArgs& a, cudaStream_t st) {
+    if (K_ <= 4) z_kernel<SAMPLE, true, 4><<<static_cast<unsigned>(nbz_), kThreads, 0, st>>>(a, out.iter, out.err);
+    else z_kernel<SAMPLE, true, kFuseK><<<static_cast<unsigned>(nbz_), kThreads, 0, st>>>(a, out.iter, out.err);
+  }
+
   // Fused path: the statistics of the current state (after any state change).
   void refresh_stats(cudaStream_t st) {
     if (!fuse_ || N_ == 0) return;
     GmmArgs a = args();
-    z_kernel<false, true><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    launch_fused_z<false>(a, st);
     BNMC_CUDA(cudaGetLastError());
   }
 
@@ -513,7 +523,7 @@ class Gmm final : public Model {
 
   void enqueue_log_joint(cudaStream_t st) override {
     GmmArgs a = args();
-    z_kernel<false, false><<<kBlocks, kThreads, 0, st>>>(a, out.iter, out.err);
+    z_kernel<false, false><<<static_cast<unsigned>(a.nb), kThreads, 0, st>>>(a, out.iter, out.err);
     finalize_kernel<<<1, kThreads, 0, st>>>(a, out, 0);
     BNMC_CUDA(cudaGetLastError());
   }
@@ -537,6 +547,7 @@ class Gmm final : public Model {
     a.pi = pi_.p;
     a.mu = mu_.p;
     a.s2 = s2_.p;
+    a.nb = fuse_ ? nbz_ : kBlocks;
     a.part = part_.p;
     a.lpart = lpart_.p;
     a.mu_at_stats = mu_at_stats_.p;
@@ -560,7 +571,8 @@ class Gmm final : public Model {
   std::uint64_t seed_ = 0;
   int var_[5] = {0, 1, 2, 3, 4};
   DevBuf<double> x_, pi_, mu_, s2_, part_, lpart_, mu_at_stats_;
-  bool fuse_ = true;  // draw_params_kernel + z_kernel<.., true> (K <= kFuseK; BNMC_GMM_FUSED=0: 6-kernel sweep)
+  bool fuse_ = true;
+  int nbz_ = kBlocks;  // fused z kernel grid  // draw_params_kernel + z_kernel<.., true> (K <= kFuseK; BNMC_GMM_FUSED=0: 6-kernel sweep)
   DevBuf<int> z_;
   DevBuf<std::int64_t> stage64_;  // z upload / write-back staging (int64 store layout)
 };
