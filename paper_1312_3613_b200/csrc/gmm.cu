@@ -94,8 +94,15 @@ __device__ void reduce_parts(const GmmArgs& a, int J, double* out, double* tmp) 
   double s = 0.0;
   if (grp < groups) {
     const int k = q / J, j = q - (q / J) * J;
-#pragma unroll 4
-    for (int b = grp; b < a.nb; b += groups) s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
+    int b = grp;
+    for (; b + 7 * groups < a.nb; b += 8 * groups) {  // 8 loads in flight
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a.part[(static_cast<std::size_t>(b + u * groups) * a.K + k) * 3 + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; b < a.nb; b += groups) s += a.part[(static_cast<std::size_t>(b) * a.K + k) * 3 + j];
   }
   tmp[t] = s;
   __syncthreads();
@@ -253,8 +260,10 @@ __global__ void __launch_bounds__(kThreads) z_kernel(GmmArgs a, const std::int64
 }
 
 // Fused path: pi, mu and sigma2 in one block from the z kernel's shifted sums.
-__global__ void __launch_bounds__(kThreads) draw_params_kernel(GmmArgs a, const std::int64_t* iter_p) {
-  __shared__ double sums[3 * kMaxK], tmp[kThreads], g[kMaxK];
+constexpr int kDrawThreads = 1024;  // draw_params_kernel: 1024 threads reduce the partials in ~one round
+
+__global__ void __launch_bounds__(kDrawThreads) draw_params_kernel(GmmArgs a, const std::int64_t* iter_p) {
+  __shared__ double sums[3 * kMaxK], tmp[kDrawThreads], g[kMaxK];
   const std::int64_t iter = *iter_p;
   reduce_parts(a, 3, sums, tmp);
   const std::uint64_t kp = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_pi),
@@ -478,7 +487,7 @@ class Gmm final : public Model {
     mark(st, "begin");
     if (fuse_) {
       // the statistics of the current z were left by the last z kernel (or refresh_stats)
-      draw_params_kernel<<<1, kThreads, 0, st>>>(a, out.iter);
+      draw_params_kernel<<<1, kDrawThreads, 0, st>>>(a, out.iter);
       mark(st, "draw_pi_mu_sigma2");
       launch_fused_z<true>(a, st);
       mark(st, "z_stats");
