@@ -184,6 +184,32 @@ __device__ double priors(const MhArgs& a, const double* p, double* fw, double* f
   return a.notau ? (*fw + *fb) : ((*fw + *fb) + *ftau);
 }
 
+// priors() with the K weight terms evaluated by the block's threads (each term bitwise the
+// sequential one) and summed by thread 0 in j order, as priors() does: same value, no
+// K-long chain of log-pdf evaluations on one thread.  Call with every thread; the result
+// is valid in thread 0.  K > kPriorTerms falls back to priors().
+constexpr int kPriorTerms = 1024;
+
+__device__ double priors_block(const MhArgs& a, const double* p, double* fw, double* fb, double* ftau, double* terms) {
+  if (a.K > kPriorTerms) {
+    double r = 0.0;
+    if (threadIdx.x == 0) r = priors(a, p, fw, fb, ftau);
+    return r;
+  }
+  for (int j = threadIdx.x; j < a.K; j += blockDim.x) terms[j] = log_pdf_gaussian(p[j], 0.0, a.w_var);
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int j = 0; j < a.K; ++j) s += terms[j];
+    *fw = s;
+    *fb = log_pdf_gaussian(p[a.K], 0.0, a.b_var);
+    *ftau = a.notau ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
+    r = a.notau ? (*fw + *fb) : ((*fw + *fb) + *ftau);
+  }
+  return r;
+}
+
 __device__ double sum_parts(const double* part, int n, double* scratch) {
   double s = 0.0;
   for (int b = threadIdx.x; b < n; b += blockDim.x) s += part[b];
@@ -195,23 +221,23 @@ __device__ double sum_parts(const double* part, int n, double* scratch) {
 // mode 3: as 0, and advance the iteration (end of a Gibbs / MWG sweep).
 __global__ void accept_kernel(MhArgs a, Outputs o, int mode, const double* lik_total) {
   __shared__ double scratch[32];
+  __shared__ double terms[kPriorTerms];
   __shared__ int take_s;
   const double lik = sum_parts(a.part, kBlocks, scratch);
   const double fx = a.state[4];
+  double fw = 0.0, fb = 0.0, ft = 0.0, pr = 0.0;
+  if (mode == 0 || mode == 3) pr = priors_block(a, a.w, &fw, &fb, &ft, terms);
+  else if (mode == 1) pr = priors_block(a, a.wp, &fw, &fb, &ft, terms);
   if (threadIdx.x == 0) {
     const std::int64_t it = *o.iter;
     const double lik_all = lik_total ? *lik_total : lik;
     int take = 0;
     if (mode == 0 || mode == 3) {
-      double fw, fb, ft;
-      priors(a, a.w, &fw, &fb, &ft);
       a.state[0] = lik_all;
       a.state[1] = fw;
       a.state[2] = fb;
       a.state[3] = ft;
     } else if (mode == 1) {
-      double fw, fb, ft;
-      const double pr = priors(a, a.wp, &fw, &fb, &ft);
       const double after = pr + lik_all;
       const double before = a.notau ? ((a.state[1] + a.state[2]) + a.state[0])
                                        : (((a.state[1] + a.state[2]) + a.state[3]) + a.state[0]);
