@@ -832,3 +832,34 @@ def test_gmm_posterior_recovers_centres(g):
     assert np.max(np.abs(mus.mean(axis=0) - centres)) < 0.05, mus.mean(axis=0)
     assert np.all(np.abs(np.sort(s2.mean(axis=0)) - 0.25) < 0.05), s2.mean(axis=0)
     e.close()
+
+
+@pytest.mark.parametrize("name,model", [("hmm_small", "hmm"), ("catmix_small", "catmix"),
+                                        ("naivebayes_small", "naivebayes"), ("regression_mwg", "regression")])
+def test_zoo_run_trace_matches_stepwise(g, name, model):
+    """Engine::run through bnmc_gpu_run_trace (device MAP tracking, thinned samples via the
+    device snapshot slots on a copy stream) == stepwise sweeps, for the rest of the zoo."""
+    fx = golden(name)
+    burnin, n, thin = 1, 6, 2
+
+    def mk():
+        e, s, latent = _zoo_engine(g, fx, model)
+        for v in latent:
+            s[v] = fx[v + "0"]
+        return e, s, latent
+
+    e1, s1, latent = mk()
+    e1.cfg.burnin, e1.cfg.thin = burnin, thin
+    tr = e1.run(s1, n)
+    e2, s2, _ = mk()
+    lj, samples, map_lj, map_state = _stepwise_run(e2, s2, burnin, n, thin, latent)
+    assert tr["log_joint"] == lj
+    assert len(tr["samples"]) == len(samples) == 3
+    for a, b in zip(tr["samples"], samples):
+        for x in latent:
+            assert np.array_equal(a[x], b[x]), x
+    assert tr["map_log_joint"] == map_lj
+    for x in latent:
+        assert np.array_equal(tr["map_state"][x], map_state[x]), x
+    e1.close()
+    e2.close()
