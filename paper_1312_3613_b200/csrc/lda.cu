@@ -115,6 +115,8 @@ struct LdaArgs {
   double* spart;     // [kColStripes][K][2]
   int* ticket;       // [ceil(K/32)] last-block tickets of phi_colsum2
   int* ticket2;      // last-block ticket of wterm_kernel<true>
+  int red_only;      // sharded: the last wterm block writes red[0..2] (this rank's theta, z, w
+                     // pieces) for the all-reduce instead of the log-joint
   std::int64_t docs_per_block, nb_doc;
 };
 
@@ -2097,6 +2099,14 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
     for (int k = threadIdx.x; k < a.K; k += blockDim.x) s[3] += __ldcg(&a.phi_term[k]);
     block_sum_n<4>(s, scratch);
     const double s0 = s[0], s1 = s[1], s2 = s[2], f = s[3];
+    if (a.red_only) {
+      if (threadIdx.x == 0) {
+        a.red[0] = s0;
+        a.red[1] = s1;
+        a.red[2] = s2;
+      }
+      return;
+    }
     if (threadIdx.x == 0) {
       const double lj = ((f + s0) + s1) + s2;
       const std::int64_t it = *o.iter;
@@ -2977,9 +2987,11 @@ class Lda final : public Model {
     }
     const unsigned nbw = static_cast<unsigned>(nbw_);
     if (comm_.active()) {
-      wterm_kernel<false><<<nbw, 256, 0, st>>>(a, out, 0);
+      // this rank's pieces by the last wterm block, then the all-reduce and the finish
+      LdaArgs ar = a;
+      ar.red_only = 1;
+      launch_pdl(wterm_kernel<true>, dim3(nbw), dim3(256), 0, st, ar, out, 0);
       mark(st, "wterm");
-      reduce_kernel<false><<<1, 1024, 0, st>>>(a);
       BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
       finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
       mark(st, "reduce_finalize");
