@@ -265,7 +265,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         b, e = g.partition(np.arange(docs + 1, dtype=np.int64) * L, world, rank)
         sites_local = (e - b) * L
         # phi_gamma2, phi_colsum2, theta2, z-step screen, z-step fallback, wterm<FINAL>
-        per_sweep_kernels = 6
+        # (sharded: + finalize after the log-joint all-reduce; NCCL's own kernels not counted)
+        per_sweep_kernels = 6 + (1 if world > 1 else 0)
         dominant = "zstep"
         # SURVEY 8(d), per token: phi row 8K (fp64) + w 4 + z 4 + topic-word count 4 +
         # doc-topic count 4, theta row 8K per work unit (a document, <= 2048 tokens)
