@@ -145,6 +145,15 @@ int bnmc_gpu_sweep(bnmc_gpu_ctx* ctx, int64_t iter, double* log_joint, int* mh_a
  * unspecified. */
 int bnmc_gpu_sweep_store(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store, int64_t iter, double* log_joint,
                          int* mh_accepted);
+/* Page-locks the arrays of `store` (cudaHostRegister) for this context's copies, and
+ * releases ranges registered earlier that the view no longer holds (a new or
+ * reallocated store).  The reference's ParamStore is pageable std::vector memory; an
+ * Engine that keeps borrowing the same store registers it once at binding.  The arrays
+ * must stay allocated until bnmc_gpu_unregister_host / bnmc_gpu_destroy (or the next
+ * register call with a different view).  Ranges already page-locked by their owner are
+ * used as they are and never released here. */
+int bnmc_gpu_register_host(bnmc_gpu_ctx* ctx, const bnmc_gpu_store* store);
+int bnmc_gpu_unregister_host(bnmc_gpu_ctx* ctx);
 /* Host <-> device bytes moved by the last bnmc_gpu_sweep_store call (LDA: z up; z,
  * theta, phi and the log-joint / accept ring entry down).  Models other than LDA
  * report only the ring entry. */

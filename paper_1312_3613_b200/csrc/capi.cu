@@ -60,6 +60,8 @@ struct bnmc_gpu_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::string last_error;
+  // host ranges this context page-locked (bnmc_gpu_register_host): the caller's store
+  std::vector<std::pair<void*, std::size_t>> registered;
 };
 
 namespace {
@@ -275,6 +277,7 @@ void bnmc_gpu_destroy(bnmc_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& r : c->registered) cudaHostUnregister(r.first);
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
   c->model.reset();
@@ -410,6 +413,55 @@ int bnmc_gpu_sweep_store(bnmc_gpu_ctx* c, const bnmc_gpu_store* s, std::int64_t 
     m->d2h_bytes += static_cast<std::int64_t>(sizeof(double) + sizeof(int));  // the ring entry
     m->spec_epoch = m->epoch;
   });
+}
+
+int bnmc_gpu_register_host(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
+  if (!c || !s) return fail(c, BNMC_GPU_ERR_ARG, "null argument");
+  // Host-side only: the device state is untouched, so no epoch bump (a following
+  // bnmc_gpu_sweep_store may still start speculatively).
+  try {
+    BNMC_CUDA(cudaSetDevice(c->device));
+    require(s->len != nullptr && s->real != nullptr && s->ival != nullptr, BNMC_GPU_ERR_ARG,
+            "store view is incomplete");
+    std::vector<std::pair<void*, std::size_t>> want;
+    for (int i = 0; i < s->n_vars; ++i) {
+      void* p = s->real[i] ? static_cast<void*>(s->real[i]) : static_cast<void*>(s->ival[i]);
+      if (p && s->len[i] > 0) want.emplace_back(p, static_cast<std::size_t>(s->len[i]) * 8);
+    }
+    std::vector<std::pair<void*, std::size_t>> keep;
+    for (auto& r : c->registered) {
+      if (std::find(want.begin(), want.end(), r) != want.end()) {
+        keep.push_back(r);
+      } else {
+        cudaHostUnregister(r.first);  // a range of a store no longer bound (or reallocated)
+        cudaGetLastError();
+      }
+    }
+    c->registered = keep;
+    for (auto& r : want) {
+      if (std::find(c->registered.begin(), c->registered.end(), r) != c->registered.end()) continue;
+      const cudaError_t e = cudaHostRegister(r.first, r.second, cudaHostRegisterDefault);
+      if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();  // page-locked by its owner already: not ours to release
+        continue;
+      }
+      BNMC_CUDA(e);
+      c->registered.push_back(r);
+    }
+    return BNMC_GPU_OK;
+  } catch (const Error& e) {
+    return fail(c, e.code, e.what());
+  }
+}
+
+int bnmc_gpu_unregister_host(bnmc_gpu_ctx* c) {
+  if (!c) return fail(c, BNMC_GPU_ERR_ARG, "null context");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& r : c->registered) cudaHostUnregister(r.first);
+  cudaGetLastError();
+  c->registered.clear();
+  return BNMC_GPU_OK;
 }
 
 int bnmc_gpu_transfer_stats(bnmc_gpu_ctx* c, int64_t* h2d_bytes, int64_t* d2h_bytes) {
@@ -574,7 +626,16 @@ struct CkptHeader {
   std::int64_t next_iter;
   std::int32_t rank, world;
   std::uint32_t nbufs, pad;
+  // version 2: the configuration that shapes the chain -- a checkpoint resumes only into
+  // a context with the same flags (exact weights, observed phi, Gibbs / MWG plan), MH
+  // proposal scale and hyperparameters
+  std::uint32_t flags, pad2;
+  double mh_scale;
+  double hyper[8];
 };
+constexpr std::uint32_t kCkptVersion = 2;
+// flags that do not change the chain (launch mode only)
+constexpr std::uint32_t kCkptIgnoredFlags = BNMC_GPU_NO_GRAPH;
 
 struct FileCloser {
   std::FILE* f;
@@ -586,7 +647,7 @@ struct FileCloser {
 CkptHeader ckpt_header(const bnmc_gpu_ctx* c, std::uint32_t nbufs) {
   CkptHeader h{};
   std::memcpy(h.magic, "BNMCCKPT", 8);
-  h.version = 1;
+  h.version = kCkptVersion;
   h.kind = c->desc.kind;
   h.K = c->desc.K;
   h.V = c->desc.V;
@@ -597,6 +658,9 @@ CkptHeader ckpt_header(const bnmc_gpu_ctx* c, std::uint32_t nbufs) {
   h.rank = c->comm.rank;
   h.world = c->comm.world;
   h.nbufs = nbufs;
+  h.flags = c->desc.flags & ~kCkptIgnoredFlags;
+  h.mh_scale = c->desc.mh_scale;
+  for (int i = 0; i < 8; ++i) h.hyper[i] = c->desc.hyper[i];
   return h;
 }
 }  // namespace
@@ -633,14 +697,19 @@ int bnmc_gpu_load_checkpoint(bnmc_gpu_ctx* c, const char* path) {
     require(f != nullptr, BNMC_GPU_ERR_RUNTIME, std::string("cannot read ") + path);
     FileCloser fc{f};
     CkptHeader h{};
-    require(std::fread(&h, sizeof(h), 1, f) == 1 && std::memcmp(h.magic, "BNMCCKPT", 8) == 0 && h.version == 1,
-            BNMC_GPU_ERR_RUNTIME, "not a bnmc checkpoint");
+    require(std::fread(&h, sizeof(h), 1, f) == 1 && std::memcmp(h.magic, "BNMCCKPT", 8) == 0 && h.version == kCkptVersion,
+            BNMC_GPU_ERR_RUNTIME, "not a bnmc checkpoint (or written by an older version)");
     const CkptHeader want = ckpt_header(c, static_cast<std::uint32_t>(bufs.size()));
     require(h.kind == want.kind && h.K == want.K && h.V == want.V && h.M == want.M && h.N == want.N &&
                 h.rank == want.rank && h.world == want.world && h.nbufs == want.nbufs,
             BNMC_GPU_ERR_RUNTIME, "checkpoint was written by a different model / shard");
     require(h.seed == want.seed, BNMC_GPU_ERR_RUNTIME,
             "checkpoint seed differs (the RNG streams are keyed by the seed: the chain would not resume)");
+    bool same_hyper = h.mh_scale == want.mh_scale;
+    for (int i = 0; i < 8; ++i) same_hyper = same_hyper && h.hyper[i] == want.hyper[i];
+    require(h.flags == want.flags && same_hyper, BNMC_GPU_ERR_RUNTIME,
+            "checkpoint was written under a different configuration (flags, mh_scale or hyperparameters): "
+            "the chain would not resume");
     std::vector<unsigned char> host;
     for (const auto& b : bufs) {
       std::uint64_t n = 0;

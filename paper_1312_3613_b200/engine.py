@@ -344,6 +344,15 @@ class Engine:
         unknown = observe - set(spec["vars"])
         if unknown:
             raise BnmcError(f"cannot observe unknown variable '{sorted(unknown)[0]}'")
+        # The device sweeps implement the reference plans of the served models plus one
+        # clamped latent variable: LDA's phi (the lpp protocol, bench.cpp:30-77).  Any
+        # other observe_extra entry would change the plan (plan.cpp drops observed
+        # variables from the blocks) and is refused instead of silently resampled.
+        clampable = set(spec["observed"]) | ({"phi"} if model == "lda" else set())
+        unsupported = observe - clampable
+        if unsupported:
+            raise ValueError(f"observe_extra {sorted(unsupported)} is not supported on the GPU path for '{model}' "
+                             f"(clampable: {sorted(clampable)})")
         if model == "lda" and "phi" in observe:
             flags |= OBSERVE_PHI
         if self.cfg.exact_weights:
@@ -510,8 +519,13 @@ class Engine:
         return [(names[i].decode(), ms[i]) for i in range(n.value)]
 
     def eval_log_joint(self, store: ParamStore | None = None) -> float:
-        if store is not None and self._bound is not store:
-            self.upload(store)
+        """Engine::eval_log_joint(store): the store's current state (re-read every call, as
+        the reference does; without a store: the device state)."""
+        if store is not None:
+            if self._bound is not store:
+                self.upload(store)
+            else:
+                self.upload_state(store)  # the caller may have changed its latent state
         lj = c_double()
         _raise(lib().bnmc_gpu_eval_log_joint(self._h, ctypes.byref(lj)), self._h)
         return lj.value
@@ -523,6 +537,8 @@ class Engine:
         thinned samples are downloaded as they are taken."""
         if self._bound is not store:
             self.upload(store)
+        else:
+            self.upload_state(store)  # the chain starts from the store's current state
         cfg = self.cfg
         if n < 0 or cfg.thin < 1:
             raise BnmcError("run needs n >= 0 and thin >= 1")
@@ -570,14 +586,26 @@ class Engine:
         """Device state + next iteration to a binary file (bnmc_gpu_save_checkpoint)."""
         _raise(lib().bnmc_gpu_save_checkpoint(self._h, os.fsencode(path)), self._h)
 
-    def load_checkpoint(self, path: str) -> int:
-        """Restore a checkpoint of the same model / sizes / seed; returns the iteration the
-        next sweep runs (the chain resumes exactly)."""
+    def load_checkpoint(self, path: str, store: ParamStore | None = None) -> int:
+        """Restore a checkpoint of the same model / sizes / seed / configuration; returns
+        the iteration the next sweep runs.  The chain resumes exactly from the device
+        state (sweep_device / run_device), or -- given `store`, whose observed data must
+        be the checkpointed run's -- the restored latent state is written into `store`,
+        which becomes the bound store, so sweep(store, it) / run(store) resume too."""
         _raise(lib().bnmc_gpu_load_checkpoint(self._h, os.fsencode(path)), self._h)
         it = c_int64()
         _raise(lib().bnmc_gpu_checkpoint_iter(self._h, ctypes.byref(it)), self._h)
         self._bound = None
+        if store is not None:
+            self.download(store)
+            self.upload(store)  # binds the observed data; the latent state round-trips unchanged
         return it.value
+
+    def rebind(self, store: ParamStore):
+        """Re-upload everything, observed data included.  The observed arrays of a bound
+        store are uploaded once per binding (the engine never writes them); a caller who
+        edits observed data in place between calls rebinds, or passes a new store."""
+        self.upload(store)
 
     def lda_load_corpus(self, path: str):
         """Stream a binary corpus (write_corpus) into device memory (bnmc_gpu_lda_load_corpus)."""

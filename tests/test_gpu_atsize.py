@@ -1,0 +1,171 @@
+"""At-size parity: every BASELINE.json config the reference can run, on the GPU against
+the LIVE compiled reference (oracle/_ref, the unmodified sampler) on the same inputs.
+
+  GMM    gen_gmm(1e5, {-5,-1,1,5}, {1,0.1,2,1}) + prior_init, 100 sweeps   (sampler.cpp:114-130,222-265)
+  LDA    NIPS gen_lda(1500, 12419, 100, 1267) + prior_init, 3 sweeps,
+         product-form (default) and log-space (EXACT_WEIGHTS) modes       (sampler.cpp:52-265)
+  LDA    the 1B shape K=1000, V=1e5 on an 8 x 10k-token slice, 1 sweep,
+         and the device prior_init of that slice                          (batch.cpp:45-83)
+  MH     regression.bn on gen_regression(1e5, 64), 10 steps               (sampler.cpp:284-340)
+
+Contract: z / counts / accept decisions bit-exact on every sweep (0
+mismatches); phi, theta, pi <= 1e-12 relative; GMM mu, sigma2 <= 1e-10; log-joint <= 1e-10.
+The reference chain runs in a child process (tests/refrun.py: multi-threaded where its
+pool survives, retried, else single-threaded).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from refrun import run_chain
+
+pytestmark = pytest.mark.gpu
+
+RTOL_PARAM = 1e-12
+RTOL_MU = 1e-10
+RTOL_LJ = 1e-10
+THREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_1312_3613_b200 as g
+
+    g.lib()
+    return g
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _needs_reference():
+    from oracle import REFERENCE_SO
+
+    if not os.path.exists(REFERENCE_SO):
+        pytest.skip("oracle/_ref/libbnmc_ref.so not built")
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if a.size else 0.0
+
+
+def _lj_ok(a, b):
+    return abs(a - b) <= RTOL_LJ * abs(b)
+
+
+# ----------------------------------------------------------------------------------------
+# GMM, N = 1e5, the paper's 4-centre set, 100 sweeps
+# ----------------------------------------------------------------------------------------
+def test_gmm_1e5_100_sweeps(g):
+    N, K, seed, n = 100000, 4, 2024, 100
+    ref = run_chain({"model": "gmm", "hyper": {"N": N, "K": K}, "method": "gibbs", "seed": seed, "threads": 1,
+                     "gen": ["gmm", [N, [-5.0, -1.0, 1.0, 5.0], [1.0, 0.1, 2.0, 1.0], seed]],
+                     "observed": ["x"], "init": "prior", "sweeps": n,
+                     "record": ["z", "pi", "mu", "sigma2"]})
+    e = g.Engine("gmm", {"N": N, "K": K}, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["x"] = ref["x"]
+    e.prior_init(s, seed)                  # the device prior_init must equal the reference's
+    assert np.array_equal(s["z"], ref["z_init"])
+    for v, tol in (("pi", RTOL_PARAM), ("mu", RTOL_PARAM), ("sigma2", RTOL_PARAM)):
+        assert rel(s[v], ref[v + "_init"]) < tol, v
+    s["z"], s["pi"], s["mu"], s["sigma2"] = ref["z_init"], ref["pi_init"], ref["mu_init"], ref["sigma2_init"]
+    worst = {"pi": 0.0, "mu": 0.0, "sigma2": 0.0}
+    for it in range(n):
+        lj = e.sweep(s, it)
+        mism = int((s["z"] != ref["z"][it]).sum())
+        assert mism == 0, f"sweep {it}: {mism} z mismatches of {N}"
+        for v in worst:
+            worst[v] = max(worst[v], rel(s[v], ref[v][it]))
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+    assert worst["pi"] < RTOL_PARAM and worst["mu"] < RTOL_MU and worst["sigma2"] < RTOL_MU, worst
+    e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# LDA, NIPS-shaped, 3 consecutive sweeps, both weight modes
+# ----------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def nips_ref():
+    M, V, K, L, seed = 1500, 12419, 100, 1267, 42
+    return run_chain({"model": "lda", "hyper": {"K": K, "V": V, "M": M, "N": [L] * M}, "method": "gibbs",
+                      "seed": seed, "threads": THREADS, "gen": ["lda", [M, V, K, L, seed]], "observed": ["w"],
+                      "init": "prior", "sweeps": 3, "record": ["z", "phi", "theta"]}, timeout=1800)
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["product-form", "log-space"])
+def test_lda_nips_3_sweeps(g, nips_ref, exact):
+    M, V, K, L, seed = 1500, 12419, 100, 1267, 42
+    ref = nips_ref
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed, exact_weights=exact))
+    s = e.allocate()
+    s["w"] = ref["w"]
+    e.prior_init(s, seed)
+    assert np.array_equal(s["z"], ref["z_init"])
+    assert rel(s["phi"], ref["phi_init"]) < RTOL_PARAM and rel(s["theta"], ref["theta_init"]) < RTOL_PARAM
+    assert _lj_ok(e.eval_log_joint(s), float(ref["lj_init"]))
+    for it in range(3):
+        lj = e.sweep(s, it)
+        mism = int((s["z"] != ref["z"][it]).sum())
+        assert mism == 0, f"sweep {it}: {mism} z mismatches of {M * L}"
+        assert rel(s["phi"], ref["phi"][it]) < RTOL_PARAM, it
+        assert rel(s["theta"], ref["theta"][it]) < RTOL_PARAM, it
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+    # the topic-word counts of the final z (the next sweep's phi block input)
+    nkw, nmk = e.lda_counts()
+    want = np.zeros((K, V), dtype=np.int64)
+    np.add.at(want, (ref["z"][-1], ref["w"]), 1)
+    assert np.array_equal(nkw, want)
+    e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# LDA at the 1B shape (K = 1000, V = 1e5): an 8-document x 10k-token slice, one sweep
+# ----------------------------------------------------------------------------------------
+def test_lda_k1000_v1e5_slice(g):
+    M, V, K, L, seed = 8, 100000, 1000, 10000, 7
+    ref = run_chain({"model": "lda", "hyper": {"K": K, "V": V, "M": M, "N": [L] * M}, "method": "gibbs",
+                     "seed": seed, "threads": THREADS, "gen": ["lda", [M, V, K, L, seed]], "observed": ["w"],
+                     "init": "prior", "sweeps": 1, "record": ["z", "phi", "theta"]}, timeout=1800)
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["w"] = ref["w"]
+    e.prior_init(s, seed)
+    assert np.array_equal(s["z"], ref["z_init"])
+    assert rel(s["phi"], ref["phi_init"]) < RTOL_PARAM and rel(s["theta"], ref["theta_init"]) < RTOL_PARAM
+    lj = e.sweep(s, 0)
+    mism = int((s["z"] != ref["z"][0]).sum())
+    assert mism == 0, f"{mism} z mismatches of {M * L}"
+    assert rel(s["phi"], ref["phi"][0]) < RTOL_PARAM
+    assert rel(s["theta"], ref["theta"][0]) < RTOL_PARAM
+    assert _lj_ok(lj, ref["lj"][0]), (lj, ref["lj"][0])
+    e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# Metropolis-Hastings, regression.bn, N = 1e5 rows x 64 features, 10 steps
+# ----------------------------------------------------------------------------------------
+def test_mh_linreg_1e5x64_10_steps(g):
+    N, K, seed, n = 100000, 64, 11, 10
+    # the reference's pool crashes on this model when multi-threaded: 1 thread
+    ref = run_chain({"model": "regression", "hyper": {"N": N, "K": K, "l": -1.0, "u": 1.0}, "method": "mh",
+                     "seed": seed, "threads": 1, "mh_scale": 0.5, "gen": ["regression", [N, K, 0.1, seed]],
+                     "observed": ["x", "y"], "init": "prior", "sweeps": n, "record": ["w", "b", "tau"]},
+                    timeout=1800)
+    assert 0 < ref["acc"].sum() < n  # both branches of the accept test are exercised
+    e = g.Engine("regression", {"N": N, "K": K, "l": -1.0, "u": 1.0}, g.RunConfig(seed=seed, mh_scale=0.5))
+    s = e.allocate()
+    s["x"], s["y"] = ref["x"], ref["y"]
+    e.prior_init(s, seed)
+    for v in ("w", "b", "tau"):
+        assert rel(s[v], ref[v + "_init"]) < RTOL_PARAM, v
+    s["w"], s["b"], s["tau"] = ref["w_init"], ref["b_init"], ref["tau_init"]
+    assert _lj_ok(e.eval_log_joint(s), float(ref["lj_init"]))
+    for it in range(n):
+        acc = []
+        lj = e.sweep(s, it, acc)
+        assert acc[0] == bool(ref["acc"][it]), f"accept decision differs at step {it}"
+        for v in ("w", "b", "tau"):
+            assert rel(s[v], ref[v][it]) < RTOL_PARAM, (it, v)
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+    e.close()
