@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define BNMC_GPU_ABI_VERSION 1
+#define BNMC_GPU_ABI_VERSION 2
 
 typedef enum {
   BNMC_GPU_LDA = 1,       /* proj/models/lda.bn, Gibbs: blocks phi, theta, z */
@@ -74,6 +74,11 @@ typedef enum {
 
 /* Model description: what the reference Engine derives from (CheckedModel,
  * HyperValues, RunConfig).  Sizes are GLOBAL (all ranks). */
+/* A peer group: W contexts of ONE process (one host thread per rank; one GPU per rank,
+ * or several ranks sharing a GPU) whose collectives run as libbnmc_gpu's own all-reduce
+ * kernel over peer memory instead of NCCL (see bnmc_gpu_group_create). */
+typedef struct bnmc_gpu_group bnmc_gpu_group;
+
 typedef struct bnmc_gpu_desc {
   int32_t abi_version;  /* = BNMC_GPU_ABI_VERSION */
   int32_t kind;         /* bnmc_gpu_kind */
@@ -95,8 +100,10 @@ typedef struct bnmc_gpu_desc {
   double mh_scale;      /* RunConfig::mh_scale (PlanConfig, plan.hpp:31-33) */
   int32_t rank;         /* this process's shard (documents / rows) */
   int32_t world_size;   /* number of GPUs sharing the model; 1 = unsharded */
-  const void* nccl_id;  /* 128-byte ncclUniqueId, required when world_size > 1 */
+  const void* nccl_id;  /* 128-byte ncclUniqueId: world_size > 1 over NCCL (one process per GPU) */
   void* stream;         /* cudaStream_t to enqueue on; NULL = context-owned stream */
+  bnmc_gpu_group* group;/* world_size > 1 inside one process: the ranks' shared group (instead
+                           of nccl_id); such contexts launch without CUDA graphs */
 } bnmc_gpu_desc;
 
 /* A view of the reference ParamStore (store.hpp:74-83): flat arrays indexed by
@@ -112,6 +119,13 @@ typedef struct bnmc_gpu_store {
 typedef struct bnmc_gpu_ctx bnmc_gpu_ctx;
 
 int bnmc_gpu_abi_version(void);
+/* Peer groups (single-process sharding, e.g. one host thread per GPU of a node, or the
+ * ranks of a sharded run emulated on one GPU).  Every collective of the W member
+ * contexts is a rendezvous of their host threads: each rank must issue its calls from its
+ * own thread, in the same order as the others (as with NCCL).  The group must outlive its
+ * contexts.  Ranks on different GPUs need peer access (NVLink / NVSwitch). */
+int bnmc_gpu_group_create(int32_t world_size, bnmc_gpu_group** out);
+void bnmc_gpu_group_destroy(bnmc_gpu_group* group);
 /* Thread-local message of the last failure (ctx may be NULL). */
 const char* bnmc_gpu_last_error(const bnmc_gpu_ctx* ctx);
 

@@ -6,5 +6,5 @@ sm_100a.  This package holds its sources (csrc/), the in-tree build
 """
 from .engine import (BnmcError, CudaError, DomainError, Engine, ParamStore, RunConfig,  # noqa: F401
                      dirichlet_batch, layout_lengths, lib, log_predictive_probability, map_estimate,
-                     nccl_unique_id, partition, probe_gamma, probe_log_weights, probe_rng, read_bandwidth,
+                     nccl_unique_id, partition, PeerGroup, probe_gamma, probe_log_weights, probe_rng, read_bandwidth,
                      sample, write_corpus, lpp_curve)

@@ -207,6 +207,7 @@ int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
     c->desc = *desc;
     c->desc.doc_offsets = nullptr;  // not retained
     c->desc.nccl_id = nullptr;
+    c->desc.group = nullptr;
     if (desc->device >= 0) {
       c->device = desc->device;
     } else {
@@ -230,7 +231,13 @@ int bnmc_gpu_create(const bnmc_gpu_desc* desc, bnmc_gpu_ctx** out) {
     const bool force = fn && std::string(fn) == "1" && c->comm.world == 1 &&
                        (desc->kind == BNMC_GPU_LDA || desc->kind == BNMC_GPU_MH_LINREG ||
                         desc->kind == BNMC_GPU_MH_LOGREG || desc->kind == BNMC_GPU_MH_POLYREG);
-    if (c->comm.world > 1 || force) {
+    if (desc->group) {  // single-process ranks: our peer-memory all-reduce (comm.cu)
+      require(c->comm.world > 1, BNMC_GPU_ERR_ARG, "a peer group needs world_size > 1");
+      require(desc->nccl_id == nullptr, BNMC_GPU_ERR_ARG, "give either an ncclUniqueId or a peer group");
+      c->comm.group = group_of(desc->group);
+      peer_group_join(c->comm.group, c->comm.rank, c->comm.world, c->device);
+      c->desc.flags |= BNMC_GPU_NO_GRAPH;  // cross-context event waits cannot be captured
+    } else if (c->comm.world > 1 || force) {
       ncclUniqueId id;
       if (c->comm.world > 1) {
         require(desc->nccl_id != nullptr, BNMC_GPU_ERR_ARG, "world_size > 1 needs an ncclUniqueId");
@@ -282,6 +289,7 @@ void bnmc_gpu_destroy(bnmc_gpu_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   c->model.reset();
   if (c->comm.comm) ncclCommDestroy(c->comm.comm);
+  if (c->comm.group) peer_group_leave(c->comm.group, c->comm.rank);
   if (c->host_iter) cudaFreeHost(c->host_iter);
   if (c->host_err) cudaFreeHost(c->host_err);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -194,13 +194,32 @@ struct Model {
   }
 };
 
+// Collectives of a sharded model, over one of two transports:
+//  * NCCL: one process per GPU (an ncclUniqueId in the desc); or a 1-rank communicator
+//    forced with BNMC_FORCE_NCCL=1 (the sharded code path on one GPU);
+//  * a peer group (bnmc_gpu_group, comm.cu): the ranks are contexts of ONE process, one
+//    host thread each, on one GPU or several; the all-reduce is our own kernel over peer
+//    memory (rank r reduces chunk r of every rank's buffer and stores the result into
+//    every rank's buffer: P2P loads / stores over NVLink, plain loads when the ranks share
+//    a GPU), ordered against the ranks' streams by events and a host rendezvous.
+enum class RedType { I32, F64 };
+enum class RedOp { Sum, Min, Max };
+struct PeerGroup;
+
 struct Comm {
   ncclComm_t comm = nullptr;
+  PeerGroup* group = nullptr;
   int rank = 0, world = 1;
-  // the NCCL code paths run whenever a communicator exists: world > 1, or a 1-rank
-  // communicator forced with BNMC_FORCE_NCCL=1 (exercises the sharded path on one GPU)
-  bool active() const { return comm != nullptr; }
+  // the sharded code paths run whenever a transport exists (world > 1 or forced NCCL)
+  bool active() const { return comm != nullptr || group != nullptr; }
+  // in-place all-reduce of n elements on stream st (collective: every rank calls it)
+  void all_reduce(void* buf, std::size_t n, RedType t, RedOp op, cudaStream_t st) const;
 };
+
+// Peer groups (comm.cu): join at context creation, leave at destruction.
+PeerGroup* group_of(bnmc_gpu_group* g);
+void peer_group_join(PeerGroup* g, int rank, int world, int device);
+void peer_group_leave(PeerGroup* g, int rank);
 
 std::unique_ptr<Model> make_lda(const bnmc_gpu_desc& d, const Comm& c, Outputs o);
 std::unique_ptr<Model> make_gmm(const bnmc_gpu_desc& d, const Comm& c, Outputs o);

@@ -2797,7 +2797,7 @@ class Lda final : public Model {
     if (comm_.active()) {
       *spec_flag_host_ = ok ? 1 : 0;
       BNMC_CUDA(cudaMemcpyAsync(spec_flag_.p, spec_flag_host_, sizeof(int), cudaMemcpyHostToDevice, st));
-      BNMC_NCCL(ncclAllReduce(spec_flag_.p, spec_flag_.p, 1, ncclInt32, ncclMin, comm_.comm, st));
+      comm_.all_reduce(spec_flag_.p, 1, RedType::I32, RedOp::Min, st);
       BNMC_CUDA(cudaMemcpyAsync(spec_flag_host_, spec_flag_.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       BNMC_CUDA(cudaStreamSynchronize(st));
       ok = *spec_flag_host_ == 1;
@@ -2815,7 +2815,7 @@ class Lda final : public Model {
   void spec_verify(cudaStream_t st) override {
     BNMC_CUDA(cudaStreamWaitEvent(st, ev_up_, 0));
     spec_check_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 8), 256, 0, st>>>(up64_.p, zprev_.p, Nl_, spec_flag_.p);
-    if (comm_.active()) BNMC_NCCL(ncclAllReduce(spec_flag_.p, spec_flag_.p, 1, ncclInt32, ncclMax, comm_.comm, st));
+    if (comm_.active()) comm_.all_reduce(spec_flag_.p, 1, RedType::I32, RedOp::Max, st);
     BNMC_CUDA(cudaMemcpyAsync(spec_flag_host_, spec_flag_.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   }
 
@@ -2932,7 +2932,7 @@ class Lda final : public Model {
     }
     if (!observe_phi_) {
       if (comm_.active()) {
-        BNMC_NCCL(ncclAllReduce(nkw_.p, nkw_.p, nkw_.n, ncclInt32, ncclSum, comm_.comm, st));
+        comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
         mark(st, "allreduce_counts");
       }
       if (phi_v1_) {
@@ -2992,7 +2992,7 @@ class Lda final : public Model {
       ar.red_only = 1;
       launch_pdl(wterm_kernel<true>, dim3(nbw), dim3(256), 0, st, ar, out, 0);
       mark(st, "wterm");
-      BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
+      comm_.all_reduce(red_.p, 3, RedType::F64, RedOp::Sum, st);
       finalize_kernel<<<1, 256, 0, st>>>(a, out, 1);
       mark(st, "reduce_finalize");
     } else {
@@ -3009,7 +3009,7 @@ class Lda final : public Model {
     if (Ml_ > 0) doc_eval_kernel<<<grid_docs(), 256, 0, st>>>(a, out.err);
     reduce_kernel<true><<<1, 1024, 0, st>>>(a);
     if (comm_.active())
-      BNMC_NCCL(ncclAllReduce(red_.p, red_.p, 3, ncclFloat64, ncclSum, comm_.comm, st));
+      comm_.all_reduce(red_.p, 3, RedType::F64, RedOp::Sum, st);
     finalize_kernel<<<1, 256, 0, st>>>(a, out, 0);
     BNMC_CUDA(cudaGetLastError());
   }
@@ -3101,7 +3101,7 @@ class Lda final : public Model {
       a.nkw = tmp.p;
       if (Nl_ > 0) count_kernel<<<std::min<unsigned>(blocks_for(Nl_, 256), 148 * 16), 256, 0, st>>>(a, out.err);
       if (comm_.active())
-        BNMC_NCCL(ncclAllReduce(tmp.p, tmp.p, tmp.n, ncclInt32, ncclSum, comm_.comm, st));
+        comm_.all_reduce(tmp.p, tmp.n, RedType::I32, RedOp::Sum, st);
       std::vector<int> h(tmp.n);
       BNMC_CUDA(cudaMemcpyAsync(h.data(), tmp.p, tmp.bytes(), cudaMemcpyDeviceToHost, st));
       BNMC_CUDA(cudaStreamSynchronize(st));

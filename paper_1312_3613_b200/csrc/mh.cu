@@ -624,7 +624,7 @@ class Mh final : public Model {
     const double* tot = nullptr;
     if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
-      BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      comm_.all_reduce(tot_.p, 1, RedType::F64, RedOp::Sum, st);
       tot = tot_.p;
       mark(st, "allreduce_lik");
     }
@@ -669,7 +669,7 @@ class Mh final : public Model {
     const double* tot = nullptr;
     if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p);
-      BNMC_NCCL(ncclAllReduce(tot_.p, tot_.p, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      comm_.all_reduce(tot_.p, 1, RedType::F64, RedOp::Sum, st);
       tot = tot_.p;
     }
     accept_kernel<<<1, 256, 0, st>>>(a, out, 0, tot);
@@ -683,7 +683,7 @@ class Mh final : public Model {
     const double* tot = nullptr;
     if (comm_.active()) {
       sum_to_kernel<<<1, 256, 0, st>>>(part_.p, kBlocks, tot_.p + 1);
-      BNMC_NCCL(ncclAllReduce(tot_.p + 1, tot_.p + 1, 1, ncclFloat64, ncclSum, comm_.comm, st));
+      comm_.all_reduce(tot_.p + 1, 1, RedType::F64, RedOp::Sum, st);
       tot = tot_.p + 1;
     }
     fx_finalize_kernel<<<1, 256, 0, st>>>(a, tot);

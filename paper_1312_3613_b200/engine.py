@@ -25,7 +25,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BNMC_GPU_LIB") or os.path.join(HERE, "libbnmc_gpu.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 LDA, GMM, MH_LINREG, MH_LOGREG, CATMIX, NAIVEBAYES, HMM, MH_POLYREG = 1, 2, 3, 4, 5, 6, 7, 8
 OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH, GIBBS, MWG = 1, 2, 4, 8, 16
@@ -48,7 +48,7 @@ class _Desc(ctypes.Structure):
                 ("flags", c_uint32), ("K", c_int64), ("V", c_int64), ("M", c_int64), ("N", c_int64),
                 ("doc_offsets", POINTER(c_int64)), ("hyper", c_double * 8), ("var_ids", c_int32 * 8),
                 ("mh_scale", c_double), ("rank", c_int32), ("world_size", c_int32),
-                ("nccl_id", c_void_p), ("stream", c_void_p)]
+                ("nccl_id", c_void_p), ("stream", c_void_p), ("group", c_void_p)]
 
 
 class _Store(ctypes.Structure):
@@ -87,6 +87,10 @@ def lib():
     L.bnmc_gpu_sweep_phases.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_char_p), c_int,
                                         POINTER(c_int)]
     L.bnmc_gpu_nccl_unique_id.argtypes = [c_void_p]
+    L.bnmc_gpu_group_create.argtypes = [c_int32, POINTER(c_void_p)]
+    L.bnmc_gpu_group_destroy.argtypes = [c_void_p]
+    L.bnmc_gpu_register_host.argtypes = [c_void_p, POINTER(_Store)]
+    L.bnmc_gpu_unregister_host.argtypes = [c_void_p]
     L.bnmc_gpu_download.argtypes = [c_void_p, POINTER(_Store)]
     L.bnmc_gpu_sweep.argtypes = [c_void_p, c_int64, POINTER(c_double), POINTER(c_int)]
     L.bnmc_gpu_run.argtypes = [c_void_p, c_int64, c_int64, POINTER(c_double), POINTER(c_int)]
@@ -307,6 +311,29 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class PeerGroup:
+    """A single-process peer group (bnmc_gpu_group): `world` Engines created with
+    group=this share collectives over our own peer-memory all-reduce instead of NCCL --
+    one host thread per rank (each rank's calls from its own thread), the ranks on one
+    GPU or one GPU each.  Keep the group alive while its engines live."""
+
+    def __init__(self, world: int):
+        h = c_void_p()
+        _raise(lib().bnmc_gpu_group_create(int(world), ctypes.byref(h)))
+        self._h, self.world = h, int(world)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bnmc_gpu_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def partition(doc_offsets, world: int, rank: int):
     """Documents [begin, end) owned by `rank` (bnmc_gpu_partition)."""
     off = np.ascontiguousarray(doc_offsets, dtype=np.int64)
@@ -319,7 +346,8 @@ class Engine:
     """GPU twin of bnmc::Engine (sampler.hpp:45-86) for LDA / GMM Gibbs and MH regression."""
 
     def __init__(self, model: str, hyper: dict, cfg: RunConfig | None = None, *, rank: int = 0,
-                 world_size: int = 1, nccl_id: bytes | None = None, stream: int | None = None):
+                 world_size: int = 1, nccl_id: bytes | None = None, stream: int | None = None,
+                 group: PeerGroup | None = None):
         if model not in MODELS:
             raise ValueError(f"model '{model}' has no GPU path (supported: {sorted(MODELS)})")
         self.model, self.hyper = model, dict(hyper)
@@ -404,9 +432,14 @@ class Engine:
         d.rank, d.world_size = rank, world_size
         self._rank, self._world = rank, world_size
         self._nccl = None
-        if world_size > 1:
+        self._group = group
+        if group is not None:
+            if group.world != world_size:
+                raise ValueError("the peer group's world size differs from world_size")
+            d.group = group._h
+        elif world_size > 1:
             if nccl_id is None or len(nccl_id) != 128:
-                raise ValueError("world_size > 1 needs a 128-byte ncclUniqueId")
+                raise ValueError("world_size > 1 needs a 128-byte ncclUniqueId or a PeerGroup")
             self._nccl = ctypes.create_string_buffer(bytes(nccl_id), 128)
             d.nccl_id = ctypes.cast(self._nccl, c_void_p)
         d.stream = stream

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert len(syms) >= 20
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/bnmc_gpu.h but not exported"
-    assert L.bnmc_gpu_abi_version() == 1
+    assert L.bnmc_gpu_abi_version() == g.engine.ABI_VERSION == 2
     out = subprocess.run(["nm", "-D", "--defined-only", g.engine.LIB_PATH], capture_output=True, text=True).stdout
     for s in syms:
         assert re.search(rf"\bT {s}$", out, re.M), s
