@@ -103,7 +103,9 @@ struct LdaArgs {
   double* red;       // [4]
   double alpha, beta;
   int pow_alpha, pow_beta;  // 1/alpha, 1/beta when exactly an integer in [2, 64] (boost by squaring), else 0
-  int phi_pf;               // phi_gamma2: count prefetch distance in blocks (0: off)
+  int trow_blocks;          // phi_colsum2: y-blocks finishing the pool's theta rows
+  int pool_phi;             // phi_pool: the pool draws the phi cells too (0: phi clamped)
+  int phi_pf;               // phi_gamma2: count prefetch distance in blocks; phi_pool: in grid-widths of groups (0: off)
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
@@ -203,6 +205,10 @@ __global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::in
 // the exp(log) form below ~40 ulp) instead of a log and an exp per zero-count cell.
 __device__ __forceinline__ double boost_factor(double u, int e, double inv) {
   if (e == 0) return exp(inv * log(u));
+  if (e == 10) {  // lda.bn's alpha = beta = 0.1: the loop below unrolled (same products)
+    const double u2 = u * u, u4 = u2 * u2;
+    return u2 * (u4 * u4);
+  }
   double r = 1.0, b = u;
   for (; e; e >>= 1) {
     if (e & 1) r *= b;
@@ -315,6 +321,193 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
   a.lpart[vb * a.K + k] = sl;
 }
 
+// phi block, v3 ("warp pool"): a persistent grid (one resident wave) in which warp w
+// owns the contiguous cell range [w C / W, (w+1) C / W) of the C = V K cells (k
+// fastest, the phiT row order), so every warp has the same number of cells.  The 32
+// lanes draw the range as one pool, <= kPoolCells cells (one shared-memory chunk of
+// counts) at a time: every iteration each lane makes one Marsaglia-Tsang attempt on
+// its current cell, and the lanes whose attempt was accepted take the next undrawn
+// cells (ballot + prefix rank).  A warp iterates ~(cells x 1.06) / 32 times with all
+// lanes busy until the chunk's last attempts -- the v2 kernel's lanes each ran their
+// own cells' rejection sequences and waited for the slowest lane of the warp (ncu
+// r01: ~930 thread instructions per cell, 20.7 of 32 lanes active per instruction)
+// and its 1.64-wave grid left a tail.
+// * No column partials and no per-cell log here: phi_colsum2<true> sums the columns of
+//   phiT directly (sum g, and sum log g as the log of a frexp-renormalised product),
+//   and the log-joint's w-factor takes log g of the counted cells (wterm_kernel).
+// * Streams keyed(seed, 4, var_phi, iter).derive(k, v), consumed in the reference's
+//   order (gaussian until 1 + c x > 0, uniform, [boost uniform]; dist.cpp:136-155):
+//   the draws are the reference's whichever lane draws a cell.
+constexpr int kPoolCells = 1024;
+constexpr int kPoolWarps = 8;
+
+// cell c of the flat [V][K] order -> (v, k); double reciprocal + one correction step
+__device__ __forceinline__ void cell_vk(std::int64_t c, int K, double invK, int& v, int& k) {
+  std::int64_t q = static_cast<std::int64_t>(static_cast<double>(c) * invK);
+  std::int64_t r = c - q * K;
+  if (r < 0) {
+    --q;
+    r += K;
+  } else if (r >= K) {
+    ++q;
+    r -= K;
+  }
+  v = static_cast<int>(q);
+  k = static_cast<int>(r);
+}
+
+template <bool KTAB>
+__global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int64_t* iter_p) {
+  __shared__ double tab_d[2][kGammaTab], tab_c[2][kGammaTab], tab_inv[2][kGammaTab];
+  __shared__ std::uint64_t kkey_s[KTAB ? kPoolCells : 1];
+  __shared__ int col32_s[KTAB ? kPoolCells : 1];
+  __shared__ int cnt_s[kPoolWarps][kPoolCells];
+  const std::int64_t iter = *iter_p;
+  for (int i = threadIdx.x; i < 2 * kGammaTab; i += blockDim.x) {
+    const int kind = i / kGammaTab, n = i - kind * kGammaTab;  // 0: phi (beta), 1: theta (alpha)
+    const double shape = (kind ? a.alpha : a.beta) + static_cast<double>(n);
+    const bool boost = shape < 1.0;
+    const double aa = boost ? shape + 1.0 : shape;
+    const double d = aa - 1.0 / 3.0;
+    tab_d[kind][n] = d;
+    tab_c[kind][n] = 1.0 / sqrt(9.0 * d);
+    tab_inv[kind][n] = boost ? 1.0 / shape : 0.0;
+  }
+  const std::uint64_t base = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
+                                   static_cast<std::uint64_t>(iter));
+  const std::uint64_t tbase = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
+                                    static_cast<std::uint64_t>(iter));
+  if constexpr (KTAB) {
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+      kkey_s[k] = fold(base, static_cast<std::uint64_t>(k));
+      col32_s[k] = a.phiT32 ? phys32(k, a.R32, a.G32, a.CW32) : 0;
+    }
+  }
+  __syncthreads();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  int* cnt = cnt_s[threadIdx.x >> 5];
+  const unsigned lt = (1u << lane) - 1u;
+  const double invK = 1.0 / static_cast<double>(a.K);
+  // cells [0, cphi): phi (v, k) in phiT row order; [cphi, cphi + Ml K): theta (m, k)
+  const std::int64_t cphi = a.pool_phi ? static_cast<std::int64_t>(a.V) * a.K : 0;
+  const std::int64_t ncells = cphi + a.Ml * a.K;
+  const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const std::int64_t c_end = ncells * (gw + 1) / nw;
+  auto count_at = [&](std::int64_t c) -> int* {
+    if (c >= cphi) return a.nmk + (c - cphi);
+    int v, k;
+    cell_vk(c, a.K, invK, v, k);
+    return a.nkw + static_cast<std::size_t>(v) * a.Kp + k;
+  };
+  for (std::int64_t c0 = ncells * gw / nw; c0 < c_end; c0 += kPoolCells) {
+    const int n = static_cast<int>(c_end - c0 < kPoolCells ? c_end - c0 : kPoolCells);
+    // the chunk's counts into shared memory (consumed: the z-step accumulates the next
+    // sweep's counts here), 8 loads in flight per lane before the zeroing stores (the
+    // stores may alias the next loads: a load-store loop would serialise one HBM round
+    // trip per 32 cells); the next chunk's counts into L2 meanwhile
+    for (int j0 = 0; j0 < n; j0 += 8 * 32) {
+      int val[8];
+      int* at[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = j0 + 32 * i + lane;
+        val[i] = 0;
+        at[i] = nullptr;
+        if (j < n) {
+          at[i] = count_at(c0 + j);
+          val[i] = __ldcg(at[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (at[i]) {
+          cnt[j0 + 32 * i + lane] = val[i];
+          *at[i] = 0;
+        }
+      }
+    }
+    if (c0 + kPoolCells + 32 * lane < c_end)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(count_at(c0 + kPoolCells + 32 * lane)));
+    __syncwarp();
+    int j = lane, next = 32;
+    bool fresh = true;
+    std::uint64_t pos = 0;
+    double d = 1.0, c = 1.0, inv = 0.0;
+    double* outp = nullptr;
+    float* out32 = nullptr;
+    int pw = 0;
+    while (__any_sync(0xffffffffu, j < n)) {
+      bool accepted = false;
+      if (j < n) {
+        if (fresh) {
+          const std::int64_t cell = c0 + j;
+          const int cn = cnt[j];
+          const int kind = cell >= cphi;
+          int v, k;
+          if (!kind) {  // phi cell (v, k): Stream(derive(base, k, v))
+            cell_vk(cell, a.K, invK, v, k);
+            pos = fold(KTAB ? kkey_s[k] : fold(base, static_cast<std::uint64_t>(k)), static_cast<std::uint64_t>(v));
+            outp = a.phiT + static_cast<std::size_t>(v) * a.Kp + k;
+            out32 = a.phiT32 ? a.phiT32 + static_cast<std::size_t>(v) * a.Kp32 +
+                                   (KTAB ? col32_s[k] : phys32(k, a.R32, a.G32, a.CW32))
+                             : nullptr;
+            pw = a.pow_beta;
+          } else {  // theta cell (m, k): Stream(derive(tbase, doc_base + m, k)), g unnormalised
+            cell_vk(cell - cphi, a.K, invK, v, k);
+            pos = fold(fold(tbase, static_cast<std::uint64_t>(a.doc_base + v)), static_cast<std::uint64_t>(k));
+            outp = a.theta + (cell - cphi);
+            out32 = nullptr;
+            pw = a.pow_alpha;
+          }
+          if (cn < kGammaTab) {
+            d = tab_d[kind][cn];
+            c = tab_c[kind][cn];
+            inv = tab_inv[kind][cn];
+          } else {
+            const double shape = (kind ? a.alpha : a.beta) + static_cast<double>(cn);  // >= 64: no boost
+            d = shape - 1.0 / 3.0;
+            c = 1.0 / sqrt(9.0 * d);
+            inv = 0.0;
+          }
+          fresh = false;
+        }
+        pos += kGolden;
+        const double u1 = (static_cast<double>(mix(pos) >> 11) + 0.5) * 0x1p-53;
+        pos += kGolden;
+        const double u2 = (static_cast<double>(mix(pos) >> 11) + 0.5) * 0x1p-53;
+        const double x = sqrt(-2.0 * log(u1)) * cos(6.28318530717958647692529 * u2);
+        double vv = 1.0 + c * x;
+        if (vv > 0.0) {
+          vv = vv * vv * vv;
+          pos += kGolden;
+          const double u = (static_cast<double>(mix(pos) >> 11) + 0.5) * 0x1p-53;
+          bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
+          if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
+          if (acc) {
+            double g = d * vv;
+            if (inv != 0.0) {
+              pos += kGolden;
+              g = g * boost_factor((static_cast<double>(mix(pos) >> 11) + 0.5) * 0x1p-53, pw, inv);
+            }
+            *outp = g;
+            if (out32) *out32 = static_cast<float>(g);
+            accepted = true;
+          }
+        }
+      }
+      const unsigned am = __ballot_sync(0xffffffffu, accepted);
+      if (accepted) {
+        j = next + __popc(am & lt);
+        fresh = true;
+      }
+      next += __popc(am);
+    }
+    __syncwarp();
+  }
+}
+
 // Per topic: S[k] = sum over vb of gpart and the phi factor
 // (beta-1) (sum log g - V log S) - sum lgamma(beta) + lgamma(sum beta)
 // (dist.cpp:115-130).  Grid (ceil(K/32), kColStripes): block (kb, s) sums stripe s of
@@ -322,13 +515,65 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
 // spart[s][k]; the last stripe block of kb to finish (atomic ticket) adds the
 // stripes in stripe order.  The ticket decides who adds, never the order, so the
 // result is deterministic.
-constexpr int kColStripes = 64;
+constexpr int kColStripes = 128;
 
 __device__ void h16_rows(const LdaArgs& a, std::int64_t w0, std::int64_t nw);
 
 // Blocks with blockIdx.y >= col_stripes convert the new phi rows to fp16 for the
 // level-1 screen (h16_rows) -- the conversion needs the rows, not S, so it runs beside
 // the column sums instead of after them.
+// FROM_G (warp-pool phi block): the stripes sum the columns of phiT itself (rows v,
+// stride Kp): sum g, and sum log g as log(mantissa product) + exponent sum
+// (frexp-renormalised after every factor: one log per thread and column instead of one
+// per cell).  Otherwise the v2 kernel's row-block partials gpart / lpart.
+struct LogProd {
+  double mant = 1.0;
+  int ex = 0;
+  bool zero = false;
+  __device__ __forceinline__ void mul(double g) {
+    if (g > 0.0) {
+      int e1, e2;
+      mant = frexp(mant * frexp(g, &e1), &e2);
+      ex += e1 + e2;
+    } else {
+      zero = true;
+    }
+  }
+  __device__ __forceinline__ double log_value() const {
+    return zero ? -INFINITY : log(mant) + static_cast<double>(ex) * 0.69314718055994530942;
+  }
+};
+
+// Theta row m of the warp-pool block (one warp): the pool left the gamma draws g in
+// theta; S = sum g, sum log g (log of the frexp product), theta = g / S and the
+// row's Dirichlet log-pdf piece (dist.cpp:115-130: (alpha-1)(sum log g - K log S)
+// - sum lgamma(alpha) + lgamma(sum alpha); sum theta = 1 by construction).  Lane sums
+// in k order, lanes combined by a fixed shfl_down tree: deterministic.
+__device__ __forceinline__ void theta_row_finish(const LdaArgs& a, std::int64_t m) {
+  const int lane = threadIdx.x & 31;
+  double* row = a.theta + m * a.K;
+  double s = 0.0;
+  LogProd lp;
+  for (int k = lane; k < a.K; k += 32) {
+    const double g = row[k];
+    s += g;
+    lp.mul(g);
+  }
+  double l = lp.log_value();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    l += __shfl_down_sync(0xffffffffu, l, o);
+  }
+  const double S = __shfl_sync(0xffffffffu, s, 0);
+  for (int k = lane; k < a.K; k += 32) row[k] = row[k] / S;
+  if (lane == 0) {
+    const double lpdf = (a.alpha - 1.0) * (l - static_cast<double>(a.K) * log(S));
+    a.tpart[m] = (!(S > 0.0) || !isfinite(S)) ? -INFINITY : lpdf - a.theta_norm + a.theta_lgasum;
+  }
+}
+
+template <bool FROM_G>
 __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __shared__ double sg_s[8][33], sl_s[8][33];
   __shared__ bool last;
@@ -339,43 +584,71 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
     if (a.q2_len) *a.q2_len = 0;
   }
   const int stripes = a.col_stripes;
-  if (static_cast<int>(blockIdx.y) >= stripes) {
-    const std::int64_t hb = static_cast<std::int64_t>(blockIdx.y - stripes) * gridDim.x + blockIdx.x;
-    const std::int64_t nhb = static_cast<std::int64_t>(gridDim.y - stripes) * gridDim.x;
+  if (static_cast<int>(blockIdx.y) >= stripes + a.trow_blocks) {
+    const std::int64_t hb = static_cast<std::int64_t>(blockIdx.y - stripes - a.trow_blocks) * gridDim.x + blockIdx.x;
+    const std::int64_t nhb = static_cast<std::int64_t>(gridDim.y - stripes - a.trow_blocks) * gridDim.x;
     h16_rows(a, hb * 8 + (threadIdx.x >> 5), nhb * 8);
+    return;
+  }
+  if (static_cast<int>(blockIdx.y) >= stripes) {  // theta rows of the warp-pool block
+    const std::int64_t w0 = (static_cast<std::int64_t>(blockIdx.y - stripes) * gridDim.x + blockIdx.x) * 8 + (threadIdx.x >> 5);
+    const std::int64_t nwr = static_cast<std::int64_t>(a.trow_blocks) * gridDim.x * 8;
+    for (std::int64_t m = w0; m < a.Ml; m += nwr) theta_row_finish(a, m);
     return;
   }
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
-  const std::int64_t chunk = (a.nvb + stripes - 1) / stripes;
-  const std::int64_t b0 = blockIdx.y * chunk, b1 = min(a.nvb, b0 + chunk);
+  const std::int64_t rows = FROM_G ? a.V : a.nvb;
+  const std::int64_t chunk = (rows + stripes - 1) / stripes;
+  const std::int64_t b0 = blockIdx.y * chunk, b1 = min(rows, b0 + chunk);
   double sg = 0.0, sl = 0.0;
   if (k < a.K) {
-    std::int64_t b = b0 + ty;
-    for (; b + 56 < b1; b += 64) {  // 8 independent loads in flight per operand
+    if constexpr (FROM_G) {
+      LogProd lp;
+      std::int64_t b = b0 + ty;
+      for (; b < b1; b += 64) {  // 8 loads in flight
+        double g8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const std::int64_t bj = b + 8 * j;
+          g8[j] = bj < b1 ? a.phiT[bj * a.Kp + k] : 1.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (b + 8 * j < b1) {
+            sg += g8[j];
+            lp.mul(g8[j]);
+          }
+        }
+      }
+      sl = lp.log_value();
+    } else {
+      std::int64_t b = b0 + ty;
+      for (; b + 56 < b1; b += 64) {  // 8 independent loads in flight per operand
+        double g8[8], l8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          g8[j] = a.gpart[(b + 8 * j) * a.K + k];
+          l8[j] = a.lpart[(b + 8 * j) * a.K + k];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          sg += g8[j];
+          sl += l8[j];
+        }
+      }
       double g8[8], l8[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        g8[j] = a.gpart[(b + 8 * j) * a.K + k];
-        l8[j] = a.lpart[(b + 8 * j) * a.K + k];
+      for (int j = 0; j < 8; ++j) {  // the remaining < 8 rows of this thread, loads issued together
+        const std::int64_t bj = b + 8 * j;
+        g8[j] = bj < b1 ? a.gpart[bj * a.K + k] : 0.0;
+        l8[j] = bj < b1 ? a.lpart[bj * a.K + k] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         sg += g8[j];
         sl += l8[j];
       }
-    }
-    double g8[8], l8[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {  // the remaining < 8 rows of this thread, loads issued together
-      const std::int64_t bj = b + 8 * j;
-      g8[j] = bj < b1 ? a.gpart[bj * a.K + k] : 0.0;
-      l8[j] = bj < b1 ? a.lpart[bj * a.K + k] : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      sg += g8[j];
-      sl += l8[j];
     }
   }
   sg_s[ty][tx] = sg;
@@ -400,21 +673,23 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // stripes s = ty, ty + 8, ... per warp (all loads in flight: stripes <= 64), then the
-  // 8 warp sums in order: fixed order, one L2 round trip
+  // stripes s = ty, ty + 8, ... per warp (8 loads in flight: one L2 round trip per 64
+  // stripes), then the 8 warp sums in order: fixed order
   sg = sl = 0.0;
   if (k < a.K) {
-    double g8[8], l8[8];
+    for (int s0 = 0; s0 < stripes; s0 += 64) {
+      double g8[8], l8[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int st = ty + 8 * j;
-      g8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2]) : 0.0;
-      l8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2 + 1]) : 0.0;
-    }
+      for (int j = 0; j < 8; ++j) {
+        const int st = s0 + ty + 8 * j;
+        g8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2]) : 0.0;
+        l8[j] = st < stripes ? __ldcg(&a.spart[(static_cast<std::size_t>(st) * a.K + k) * 2 + 1]) : 0.0;
+      }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      sg += g8[j];
-      sl += l8[j];
+      for (int j = 0; j < 8; ++j) {
+        sg += g8[j];
+        sl += l8[j];
+      }
     }
   }
   __syncthreads();
@@ -2136,7 +2411,10 @@ __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int
     const std::int64_t nvec = static_cast<std::int64_t>(a.V) * a.Kp / 4;
     const bool narrow = nvec < (std::int64_t{1} << 29);  // 4 * nvec fits 31 bits
     const int4* n4 = reinterpret_cast<const int4*>(a.nkw);
-    const double2* l2 = reinterpret_cast<const double2*>(a.logg);
+    // log g stored per cell (v2 phi block), or taken here from g = phiT for the
+    // counted cells only (warp-pool phi block: a.logg == nullptr)
+    const bool take_log = a.logg == nullptr;
+    const double2* l2 = reinterpret_cast<const double2*>(take_log ? a.phiT : a.logg);
     for (std::int64_t c0 = g0; c0 < nvec; c0 += kWU * stride) {
       int4 n[kWU];
       double2 la[kWU], lb[kWU];
@@ -2156,10 +2434,11 @@ __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int
         if (c >= nvec || (n[j].x | n[j].y | n[j].z | n[j].w) == 0) continue;
         const int k0 = narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
                               : static_cast<int>((4 * c) % a.Kp);
-        if (n[j].x) accw += static_cast<double>(n[j].x) * (la[j].x - __ldg(&a.logS[k0]));
-        if (n[j].y) accw += static_cast<double>(n[j].y) * (la[j].y - __ldg(&a.logS[k0 + 1]));
-        if (n[j].z) accw += static_cast<double>(n[j].z) * (lb[j].x - __ldg(&a.logS[k0 + 2]));
-        if (n[j].w) accw += static_cast<double>(n[j].w) * (lb[j].y - __ldg(&a.logS[k0 + 3]));
+        auto lg = [take_log](double x) { return take_log ? log(x) : x; };  // log(0) = -inf
+        if (n[j].x) accw += static_cast<double>(n[j].x) * (lg(la[j].x) - __ldg(&a.logS[k0]));
+        if (n[j].y) accw += static_cast<double>(n[j].y) * (lg(la[j].y) - __ldg(&a.logS[k0 + 1]));
+        if (n[j].z) accw += static_cast<double>(n[j].z) * (lg(lb[j].x) - __ldg(&a.logS[k0 + 2]));
+        if (n[j].w) accw += static_cast<double>(n[j].w) * (lg(lb[j].y) - __ldg(&a.logS[k0 + 3]));
       }
     }
   } else {
@@ -2628,48 +2907,60 @@ class Lda final : public Model {
     wpart_.alloc(nbw_);
     ttpart_.alloc(nbw_);
     colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
-    // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
-    // vs 42 at 1): enough threads to fill the GPU while the per-thread rejection loop
-    // still amortises over several cells; 2 when 4 leaves the GPU under one wave
-    phi_rows_ = 4;
     {
-      // a grid below one resident wave at 4 rows (KOS: 337 blocks for 740 slots) draws
-      // 2 rows per thread instead: twice the threads in flight (r01, KOS phi 35.3 -> 32.2 us)
       int dev = 0, sms = 148, per_sm = 1;
       BNMC_CUDA(cudaGetDevice(&dev));
       BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0));
-      const std::int64_t blocks4 = ((V_ + 3) / 4 * K_ + 255) / 256;
-      if (blocks4 < static_cast<std::int64_t>(sms) * std::max(per_sm, 1)) phi_rows_ = 2;
-    }
-    if (const char* e = std::getenv("BNMC_PHI_ROWS")) {
-      const int r = std::atoi(e);
-      if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
+      const char* pe = std::getenv("BNMC_PHI_POOL");
+      const char* pv1 = std::getenv("BNMC_PHI_V1");
+      const char* tv1 = std::getenv("BNMC_THETA_V1");
+      pool_ = !(pe && std::string(pe) == "0") && !(pv1 && std::string(pv1) == "1") &&
+              !(tv1 && std::string(tv1) == "1");
+      if (pool_) {
+        // warp-pool phi block: a persistent grid (one resident wave), equal cell ranges
+        // per warp; the column sums read phiT rows (nvb_ = V rows for phi_colsum2<true>)
+        if (K_ <= kPoolCells)
+          BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<true>, 256, 0));
+        else
+          BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<false>, 256, 0));
+        pool_blocks_ = sms * std::max(per_sm, 1);
+        phi_rows_ = 1;
+      } else {
+        // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
+        // vs 42 at 1); 2 when 4 leaves the GPU under one wave (KOS phi 35.3 -> 32.2 us)
+        phi_rows_ = 4;
+        BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0));
+        const std::int64_t blocks4 = ((V_ + 3) / 4 * K_ + 255) / 256;
+        if (blocks4 < static_cast<std::int64_t>(sms) * std::max(per_sm, 1)) phi_rows_ = 2;
+        if (const char* e = std::getenv("BNMC_PHI_ROWS")) {
+          const int r = std::atoi(e);
+          if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
+        }
+        switch (phi_rows_) {
+          case 1: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<1>, 256, 0)); break;
+          case 2: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<2>, 256, 0)); break;
+          case 4: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0)); break;
+          default: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<8>, 256, 0)); break;
+        }
+        phi_pf_ = static_cast<int>(0.7 * sms * std::max(per_sm, 1));  // measured: 0.55-0.8 of a wave best
+        if (const char* e = std::getenv("BNMC_PHI_PREFETCH")) phi_pf_ = std::max(0, std::atoi(e));
+      }
     }
     nvb_ = (V_ + phi_rows_ - 1) / phi_rows_;
+    col_stripes_ = static_cast<int>(std::min<std::int64_t>(pool_ ? kColStripes : 64, std::max<std::int64_t>(4, nvb_ / (pool_ ? 48 : 96))));
     {
-      int dev = 0, sms = 148, per_sm = 1;
-      BNMC_CUDA(cudaGetDevice(&dev));
-      BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      switch (phi_rows_) {
-        case 1: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<1>, 256, 0)); break;
-        case 2: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<2>, 256, 0)); break;
-        case 4: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0)); break;
-        default: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<8>, 256, 0)); break;
-      }
-      phi_pf_ = static_cast<int>(0.7 * sms * std::max(per_sm, 1));  // measured: 0.55-0.8 of a wave best
-      if (const char* e = std::getenv("BNMC_PHI_PREFETCH")) phi_pf_ = std::max(0, std::atoi(e));
+      const std::int64_t gx = (K_ + 31) / 32, wblocks = (Ml_ + 7) / 8;
+      trow_blocks_ = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((wblocks + gx - 1) / gx, 16384)));
     }
-    col_stripes_ = static_cast<int>(std::min<std::int64_t>(kColStripes, std::max<std::int64_t>(4, nvb_ / 96)));
     if (const char* e = std::getenv("BNMC_COL_STRIPES")) col_stripes_ = std::min(kColStripes, std::max(1, std::atoi(e)));
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
     ticket_.alloc((K_ + 31) / 32 + 1);
     ticket_.zero(nullptr);
-    gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
-    logg_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    if (!pool_) gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
+    if (!pool_) logg_.alloc(static_cast<std::size_t>(V_) * Kp_);  // the pool kernel keeps no per-cell log
     logS_.alloc(Kp_);
     logS_.zero(nullptr);  // padding columns stay 0 (wterm_kernel reads 4-cell vectors)
-    lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
+    if (!pool_) lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
     phi_term_.alloc(K_);
@@ -2918,63 +3209,106 @@ class Lda final : public Model {
 
   void enqueue_sweep(cudaStream_t st) override {
     LdaArgs a = args();
-    a.logg_valid = (!observe_phi_ && !phi_v1_) ? 1 : 0;  // this sweep's phi block writes logg/logS
+    // this sweep's phi block leaves g (unnormalised) + logS: the w-factor takes
+    // log g - log S (the exact mode normalises phiT in place, S = 1: the phi/S path)
+    a.logg_valid = (!observe_phi_ && !phi_v1_ && !(pool_ && exact_)) ? 1 : 0;
     const bool timed = marks != nullptr;  // phase timing: everything on one stream
     mark(st, "begin");
-    // The theta block depends only on the doc-topic counts: it runs on a side stream
-    // concurrently with the phi block (fork/join events; captured into the graph).
-    if (Ml_ > 0 && !timed) {
-      BNMC_CUDA(cudaEventRecord(ev_fork_, st));
-      BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-      launch_theta(a, side_);
-      record_external(ev_theta_ready_, side_);
-      BNMC_CUDA(cudaEventRecord(ev_join_, side_));
-    }
-    if (!observe_phi_) {
-      if (comm_.active()) {
+    if (pool_) {
+      // warp-pool conjugate block: phi and theta cells in one balanced kernel, then the
+      // phi column sums (phi_colsum2<true> stripes) and the theta rows (extra y-blocks)
+      if (!observe_phi_ && comm_.active()) {
         comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
         mark(st, "allreduce_counts");
       }
-      if (phi_v1_) {
-        phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
-        mark(st, "phi_gamma");
-        phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
-        if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
-      } else {
-        const unsigned nbg = blocks_for(nvb_ * K_, 256);
-        switch (phi_rows_) {
-          case 1: phi_gamma2_kernel<1><<<nbg, 256, 0, st>>>(a, out.iter); break;
-          case 2: phi_gamma2_kernel<2><<<nbg, 256, 0, st>>>(a, out.iter); break;
-          case 4: phi_gamma2_kernel<4><<<nbg, 256, 0, st>>>(a, out.iter); break;
-          default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
-        }
-        mark(st, "phi_gamma");
-        // (+ h16_blocks_ y-blocks converting the rows for the level-1 screen)
-        launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, col_stripes_ + (h16_ ? h16_blocks_ : 0)), dim3(256), 0, st, a);
+      if (observe_phi_) nkw_.zero(st);  // phi clamped: the z-step's counts feed only the w-factor
+      a.pool_phi = observe_phi_ ? 0 : 1;
+      a.trow_blocks = Ml_ > 0 ? trow_blocks_ : 0;
+      a.col_stripes = observe_phi_ ? 0 : col_stripes_;
+      if (a.pool_phi || Ml_ > 0) {
+        if (K_ <= kPoolCells)
+          phi_pool_kernel<true><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+        else
+          phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+        mark(st, "conj_pool");
+        launch_pdl(phi_colsum2_kernel<true>, dim3((K_ + 31) / 32, a.col_stripes + a.trow_blocks + (h16_ ? h16_blocks_ : 0)),
+                   dim3(256), 0, st, a);
         fq_reset_ = true;
+        mark(st, "colsum_rows");
       }
-      mark(st, "phi_colsum");
-      if (exact_) {
+      if (!observe_phi_ && exact_) {
         // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
         phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
         fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
         mark(st, "phi_norm");
       }
-      // phi (phiT, S) is final from here: an overlapped download may start (external
-      // event node in the captured graph)
-      if (!timed) record_external(ev_phi_ready_, st);
+      if (!timed) {  // phi, theta final: overlapped downloads may start (external event nodes)
+        if (!observe_phi_) record_external(ev_phi_ready_, st);
+        if (Ml_ > 0) record_external(ev_theta_ready_, st);
+      }
     } else {
-      // phi clamped: no phi block consumes the counts; the z-step's counts of this
-      // sweep feed only the w-factor.
-      nkw_.zero(st);
+      // The theta block depends only on the doc-topic counts: it runs on a side stream
+      // concurrently with the phi block (fork/join events; captured into the graph).
+      if (Ml_ > 0 && !timed) {
+        BNMC_CUDA(cudaEventRecord(ev_fork_, st));
+        BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        launch_theta(a, side_);
+        record_external(ev_theta_ready_, side_);
+        BNMC_CUDA(cudaEventRecord(ev_join_, side_));
+      }
+      if (!observe_phi_) {
+        if (comm_.active()) {
+          comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
+          mark(st, "allreduce_counts");
+        }
+        if (phi_v1_) {
+          phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
+          mark(st, "phi_gamma");
+          phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
+          if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
+        } else {
+          const unsigned nbg = blocks_for(nvb_ * K_, 256);
+          if (pool_) {
+            if (K_ <= kPoolCells)
+              phi_pool_kernel<true><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+            else
+              phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+          } else switch (phi_rows_) {
+            case 1: phi_gamma2_kernel<1><<<nbg, 256, 0, st>>>(a, out.iter); break;
+            case 2: phi_gamma2_kernel<2><<<nbg, 256, 0, st>>>(a, out.iter); break;
+            case 4: phi_gamma2_kernel<4><<<nbg, 256, 0, st>>>(a, out.iter); break;
+            default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
+          }
+          mark(st, "phi_gamma");
+          // (+ h16_blocks_ y-blocks converting the rows for the level-1 screen)
+          launch_pdl(pool_ ? phi_colsum2_kernel<true> : phi_colsum2_kernel<false>, dim3((K_ + 31) / 32, col_stripes_ + (h16_ ? h16_blocks_ : 0)), dim3(256), 0, st, a);
+          fq_reset_ = true;
+        }
+        mark(st, "phi_colsum");
+        if (exact_) {
+          // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
+          phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
+          fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
+          mark(st, "phi_norm");
+        }
+        // phi (phiT, S) is final from here: an overlapped download may start (external
+        // event node in the captured graph)
+        if (!timed) record_external(ev_phi_ready_, st);
+      } else {
+        // phi clamped: no phi block consumes the counts; the z-step's counts of this
+        // sweep feed only the w-factor.
+        nkw_.zero(st);
+      }
+      if (Ml_ > 0) {
+        if (timed) {
+          launch_theta(a, st);
+          mark(st, "theta");
+        } else {
+          BNMC_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+        }
+      }
     }
     if (Ml_ > 0) {
-      if (timed) {
-        launch_theta(a, st);
-        mark(st, "theta");
-      } else {
-        BNMC_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
-      }
       launch_zstep(a, st);
       mark(st, "zstep");
       if (timed && std::getenv("BNMC_SCREEN_STATS")) {  // diagnostics: queue lengths of this sweep
@@ -3626,6 +3960,9 @@ class Lda final : public Model {
   std::int64_t nvb_ = 1;
   int phi_rows_ = kPhiRowsMax;
   bool boost_pow_ = std::getenv("BNMC_BOOST_POW") == nullptr || std::string(std::getenv("BNMC_BOOST_POW")) != "0";
+  bool pool_ = true;     // phi block: warp-pool kernel (BNMC_PHI_POOL=0: v2)
+  int pool_blocks_ = 148;
+  int trow_blocks_ = 1;   // phi_colsum2 y-blocks for the pool's theta rows
   int phi_pf_ = 0;     // phi_gamma2 count prefetch distance (blocks)
   DevBuf<double> gpart_, lpart_, spart_, logg_, logS_, ttpart_;
   DevBuf<int> ticket_;
