@@ -11,16 +11,28 @@ theta block, z block, log-joint), exactly Engine::sweep (sampler.cpp:390-405).
 
 Prints ONE JSON line (rank 0).  Fields beyond the base contract:
   roofline     the dominant kernel (zstep: the z block) against the measured HBM copy
-               bandwidth; achieved = algorithmic bytes per launch (phi row
-               8K + 16 B of token state per site + the theta row per 512-token unit) /
-               its CUDA-event duration
-  cpu_baseline the compiled reference (oracle/_ref) timed on this host's cores on a
-               bounded sample of the same workload
+               bandwidth (MEASURED_PEAKS.json).  achieved = the kernel's compulsory DRAM
+               bytes per launch / its CUDA-event duration: at NIPS/KOS the working set
+               (w, z, the fp32 screen rows, theta, counts) lives in the 126 MB L2, so the
+               HBM fraction is small and `binding` names the unit that bounds the kernel
+               (ncu: the L1TEX data pipe); `l2` relates the operand bytes the kernel
+               actually streams to the L2 -> SM read bandwidth measured in this run.
+  roofline_1b  (default NIPS run, N=1) a short pass over the 1B-token config, where the
+               z-step IS HBM-bound (410 MB of screen rows, no word reuse): its DRAM
+               fraction with its own clocks
+  cpu_baseline the compiled reference (oracle/_ref) timed on one host core on half of
+               the same corpus (identical documents)
   e2e          the same metric through the public API with HOST buffers: every step
                uploads what the sweep reads from the caller's store (LDA: z; its phi and
                theta blocks redraw phi and theta first), sweeps, and downloads the whole
-               latent state + log-joint (Engine::sweep borrow semantics), pinned memory
-Multi-GPU (torchrun): documents sharded across ranks (weak scaling: each rank holds a
+               latent state + log-joint (Engine::sweep borrow semantics).  The store is
+               plain numpy memory the engine page-locks once per binding (as the
+               reference-side adapter does for its std::vector store); `e2e_pageable`
+               is the same loop with pin_host=False.
+Both arms run on identical inputs: the corpus is drawn by gen_lda_corpus (seeded) and
+the reference arm reads it from a binary corpus file (oracle/ref_bench lda-file).
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run) when not already
+under torchrun; documents sharded across ranks (weak scaling: each rank holds a
 NIPS-shaped shard), one NCCL all-reduce of the K x V counts per sweep inside the graph.
 """
 from __future__ import annotations
@@ -161,15 +173,19 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(key: str):
-    """dram bytes per launch of the kernel `workload:kernel` from the committed ncu summaries
-    (profiles/ncu_traffic.json; one `ncu --set full` capture per workload), if any."""
+def ncu_profile(key: str):
+    """The committed `ncu --set full` summary of kernel `workload:kernel`
+    (profiles/ncu_traffic.json): {"dram_bytes": per launch, "l1tex_pct", "lts_pct",
+    "source"}; None when that capture does not exist."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(key)
+            v = json.load(f).get(key)
     except Exception:
         return None
+    if isinstance(v, (int, float)):
+        return {"dram_bytes": float(v)}
+    return v
 
 
 # ----------------------------------------------------------------------------------------
@@ -217,6 +233,55 @@ def pinned_like(arr):
     return a, t
 
 
+L2_NOTE = ("GPU arm: 256 MiB written before every timed sweep (L2 flushed; NIPS/KOS fit the "
+           "126 MB L2 within a sweep); CPU arm: not applicable")
+
+
+def write_corpus_file(path, offsets, w, V):
+    """The binary corpus format of bnmc_gpu_lda_load_corpus (include/bnmc_gpu.h), read by
+    oracle/ref_bench lda-file (kept here so the reference arm imports nothing of ours)."""
+    with open(path, "wb") as f:
+        f.write(b"BNMCCORP")
+        f.write(np.array([1, 0], dtype=np.uint32).tobytes())
+        f.write(np.array([len(offsets) - 1, len(w), V], dtype=np.int64).tobytes())
+        f.write(np.ascontiguousarray(offsets, dtype=np.int64).tobytes())
+        f.write(np.ascontiguousarray(w, dtype=np.int32).tobytes())
+
+
+def gmm_points(n, seed):
+    """gen_gmm's process (gen.cpp:90-107): centres -5, -1, 1, 5 with sd 1, 0.1, 2, 1."""
+    rs = np.random.default_rng(seed)
+    c, sd = np.array([-5.0, -1.0, 1.0, 5.0]), np.array([1.0, 0.1, 2.0, 1.0])
+    zt = rs.integers(0, 4, n)
+    return c[zt] + sd[zt] * rs.normal(size=n)
+
+
+def shared_config(args, world):
+    """The `config` both arms print (identical dicts: same workload, same inputs)."""
+    wl = WORKLOADS[args.workload]
+    if wl["model"] == "lda":
+        docs = wl["docs"] * (world if wl["scaling"] == "weak" else 1)
+        cfg = {"workload": f"lda-{args.workload}", "model": "lda (proj/models/lda.bn)", "docs": docs,
+               "vocab": wl["vocab"], "topics": wl["topics"], "doc_len": wl["doc_len"],
+               "tokens": docs * wl["doc_len"], "seed": args.seed,
+               "init": "prior_init(seed) (sampler.cpp:542-555)", "l2": L2_NOTE}
+        if args.workload == "1b":
+            cfg["corpus"] = ("GPU arm: device generator (gen_lda's process, gen_tokens_kernel); "
+                             "CPU arm: reference gen_lda on a sample (the host cannot hold 1e9 tokens)")
+        else:
+            cfg["corpus"] = ("gen_lda_corpus (numpy, seeded; gen_lda's process gen.cpp:21-60: phi_k ~ "
+                             "Dir(0.05), theta_d ~ Dir(0.3)); identical documents in both arms")
+        return cfg
+    if wl["model"] == "gmm":
+        return {"workload": "gmm-100k", "model": "gmm (proj/models/gmm.bn)", "points": wl["points"],
+                "components": wl["topics"], "seed": args.seed, "init": "prior_init(seed)",
+                "data": "gmm_points (numpy, seeded; gen_gmm's process); identical points in both arms",
+                "l2": L2_NOTE}
+    return {"workload": "logreg-mh-10m", "model": "logistic regression MH", "rows": wl["rows"] * world,
+            "features": wl["features"], "seed": args.seed, "l2": L2_NOTE,
+            "data": "GPU arm: logistic rows; CPU arm: regression.bn (the reference has no logistic model)"}
+
+
 # ----------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------
@@ -237,6 +302,63 @@ def run_ours(args, rank, world, local_rank):
         return _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream)
 
 
+def gpu_index_of(local_rank):
+    gi = local_rank
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            gi = int(vis.split(",")[local_rank])
+        except (ValueError, IndexError):
+            pass
+    return gi
+
+
+def time_sweeps(eng, torch, stream, flush, it, steps, gpu_index, dist=None):
+    """`steps` sweeps, each bracketed by CUDA events on the engine's stream after an L2
+    flush; clocks sampled during the timed region.  Returns (mean ms, clocks, wall s)."""
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(gpu_index) as clk:
+        w0 = time.perf_counter()
+        for i in range(steps):
+            flush.zero_()                      # > 126 MB L2: every sweep starts cold
+            starts[i].record(stream)
+            eng.enqueue(it + i, 1)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    ms = float(np.mean([s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]))
+    return ms, clk.summary(), wall
+
+
+def phase_times(eng, torch, flush, it, n):
+    """The same sweep launched kernel by kernel with events (bnmc_gpu_sweep_phases)."""
+    phase_ms = {}
+    for i in range(n):
+        flush.zero_()
+        torch.cuda.synchronize()
+        for name, t in eng.sweep_phases(it + i):
+            phase_ms.setdefault(name, []).append(t)
+    return {k: float(np.mean(v)) for k, v in phase_ms.items()}
+
+
+def lda_zstep_bytes(docs, V, K, L):
+    """Per z-step launch: (compulsory DRAM bytes of its working set, operand bytes it
+    streams).  Working set: w, z (4 + 4 B per token), the fp32 screen rows (V x Kp32),
+    theta/S (M x K), both count arrays written (V x Kp, M x K int32).  Operands: per
+    token its fp32 row (4 Kp32 B) + w, z, 2 count updates (16 B), per document its
+    theta row (8 K B)."""
+    N = docs * L
+    kp32 = -(-K // 32) * 32
+    kp = -(-K // 4) * 4
+    compulsory = 8 * N + 4 * V * kp32 + 8 * docs * K + 4 * V * kp + 4 * docs * K
+    operand = N * (4 * kp32 + 16) + 8 * docs * K
+    return compulsory, operand
+
+
 def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     nccl_id = None
     if world > 1:
@@ -245,9 +367,11 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         nccl_id = obj[0]
 
     model = wl["model"]
+    config = shared_config(args, world)
     t_setup = time.perf_counter()
+    extra = {}
     if model == "lda":
-        docs = wl["docs"] * (world if wl["scaling"] == "weak" else 1)
+        docs = config["docs"]
         V, K, L = wl["vocab"], wl["topics"], wl["doc_len"]
         hyper = {"K": K, "V": V, "M": docs, "N": [L] * docs}
         cfg = g.RunConfig(seed=args.seed, device=local_rank)
@@ -264,38 +388,26 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             store = None
         b, e = g.partition(np.arange(docs + 1, dtype=np.int64) * L, world, rank)
         sites_local = (e - b) * L
-        # phi_gamma2, phi_colsum2, theta2, z-step screen, z-step fallback, wterm<FINAL>
+        # conj_pool, colsum_rows, z-step screen, z-step fallback, wterm<FINAL>
         # (sharded: + finalize after the log-joint all-reduce; NCCL's own kernels not counted)
-        per_sweep_kernels = 6 + (1 if world > 1 else 0)
+        per_sweep_kernels = 5 + (1 if world > 1 else 0)
         dominant = "zstep"
-        # SURVEY 8(d), per token: phi row 8K (fp64) + w 4 + z 4 + topic-word count 4 +
-        # doc-topic count 4, theta row 8K per work unit (a document, <= 2048 tokens)
-        bytes_per_site_dom = 8 * K + 16 + 8 * K / min(L, 2048)
-        # what the implementation moves per token: the fp32 screen row (4K) + the same 16
-        impl_bytes_per_site = 4 * K + 16
-        bytes_per_site_sweep = 8 * K + 16 * K / L + 16 + 20 * K * V / (docs * L)
-        config = {"workload": f"lda-{args.workload}", "model": "lda (proj/models/lda.bn)", "docs": docs,
-                  "vocab": V, "topics": K, "doc_len": L, "tokens": sites_total, "seed": args.seed,
-                  "weights": "product theta*phi (fp64)", "parallelism": f"docs sharded x{world} (NCCL allreduce K x V counts)"}
+        compulsory, operand = lda_zstep_bytes(e - b, V, K, L)
+        extra["weights"] = "product theta*phi (fp64; fp32 screen + fp64 fallback, z bit-exact)"
     elif model == "gmm":
         N, K = wl["points"], wl["topics"]
-        rs = np.random.default_rng(args.seed)
-        c, sd = np.array([-5.0, -1.0, 1.0, 5.0]), np.array([1.0, 0.1, 2.0, 1.0])
-        zt = rs.integers(0, 4, N)
         hyper = {"N": N, "K": K}
         eng = g.Engine("gmm", hyper, g.RunConfig(seed=args.seed, device=local_rank), stream=stream.cuda_stream)
         store = eng.allocate()
-        store["x"] = c[zt] + sd[zt] * rs.normal(size=N)
+        store["x"] = gmm_points(N, args.seed)
         eng.prior_init(store, args.seed)
-        sites_total = sites_local = N * world  # replicas
-        sites_local = N
+        sites_total, sites_local = N * world, N  # replicas
         # K <= 8: the fused sweep -- draw_params, z (+ next-sweep statistics), finalize
         fused = K <= 8 and os.environ.get("BNMC_GMM_FUSED", "1") != "0"
         per_sweep_kernels, dominant = (3, "z_stats") if fused else (6, "z")
-        bytes_per_site_dom = bytes_per_site_sweep = impl_bytes_per_site = 16
+        compulsory = operand = 16 * N
         host_corpus = True
-        config = {"workload": "gmm-100k", "model": "gmm (proj/models/gmm.bn)", "points": N, "components": K,
-                  "seed": args.seed, "parallelism": f"replicas x{world}"}
+        extra["parallelism"] = f"replicas x{world}"
     else:
         N, Kf = wl["rows"], wl["features"]
         Nt = N * world
@@ -312,10 +424,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         eng.upload(store)
         sites_total, sites_local = Nt, Nt // world
         per_sweep_kernels, dominant = 3, "lik"
-        bytes_per_site_dom = bytes_per_site_sweep = impl_bytes_per_site = 8 * Kf + 8
+        compulsory = operand = sites_local * (8 * Kf + 8)
         host_corpus = True
-        config = {"workload": "logreg-mh-10m", "model": "logistic regression MH", "rows": Nt, "features": Kf,
-                  "seed": args.seed, "parallelism": f"rows sharded x{world}"}
     setup_s = time.perf_counter() - t_setup
 
     # --- device-resident timing (value): per-sweep CUDA events, L2 flushed in between ---
@@ -324,31 +434,10 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     eng.enqueue(it, args.warmup)
     it += args.warmup
     eng.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    gpu_index = env_int("LOCAL_RANK", 0)
-    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    if vis:
-        try:
-            gpu_index = int(vis.split(",")[local_rank])
-        except (ValueError, IndexError):
-            pass
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(gpu_index) as clk:
-        w0 = time.perf_counter()
-        for i in range(args.steps):
-            flush.zero_()                      # > 126 MB L2: every sweep starts cold
-            starts[i].record(stream)
-            eng.enqueue(it + i, 1)
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - w0
+    gpu_index = gpu_index_of(local_rank)
+    ms_step, clocks, wall = time_sweeps(eng, torch, stream, flush, it, args.steps, gpu_index, dist)
     lj_last, _ = eng.synchronize()
     it += args.steps
-    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    ms_step = float(np.mean(ms))
     if dist:
         t = torch.tensor([ms_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -357,96 +446,144 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     value = sites_total / (ms_step / 1e3)
 
     # --- per-kernel pass (same sweep, launched phase by phase with events) ---
-    phase_ms = {}
-    for i in range(max(3, min(args.steps, 20))):
-        flush.zero_()
-        torch.cuda.synchronize()
-        for name, t in eng.sweep_phases(it):
-            phase_ms.setdefault(name, []).append(t)
-        it += 1
-    phases = {k: float(np.mean(v)) for k, v in phase_ms.items()}
+    nph = max(3, min(args.steps, 20))
+    phases = phase_times(eng, torch, flush, it, nph)
+    it += nph
     dom_ms = phases.get(dominant)
     peak, peak_src = measured_peak_hbm()
-    roofline = roofline_l2 = None
+    roofline = None
     if dom_ms:
-        achieved = sites_local * bytes_per_site_dom / (dom_ms / 1e3) / 1e9
-        traffic = ncu_traffic(f"{args.workload}:{dominant}")
+        prof = ncu_profile(f"{args.workload}:{dominant}") or {}
+        achieved = compulsory / (dom_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1), "peak": peak,
                     "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                    "traffic": traffic, "algorithmic_bytes_per_site": round(bytes_per_site_dom, 2),
-                    "kernel_ms": round(dom_ms, 5), "share_of_sweep": round(dom_ms / sum(phases.values()), 3),
-                    "sweep_effective_frac": round(value / world * bytes_per_site_sweep / 1e9 / peak, 4),
-                    "sweep_bytes_per_site": round(bytes_per_site_sweep, 2),
-                    "note": "KOS/NIPS working sets fit the 126 MB L2 within a sweep (L2 is flushed before every "
-                            "timed sweep, so reads start in HBM): frac > 1 means the kernel is fed from L2 -- "
-                            "see roofline_l2"}
-        # Secondary roofline: the bytes the implementation moves / the kernel time against
-        # the device's L2 -> SM read bandwidth, measured here (bnmc_gpu_probe_read_bandwidth
-        # over a 48 MB buffer); the HBM read bandwidth is measured the same way for context.
-        try:
-            l2_bw = g.read_bandwidth(48 << 20, 50)
-            hbm_bw = g.read_bandwidth(4 << 30, 5)
-            ach_impl = sites_local * impl_bytes_per_site / (dom_ms / 1e3) / 1e9
-            roofline_l2 = {"bound": "l2", "kernel": dominant, "achieved": round(ach_impl, 1),
-                           "peak": round(l2_bw, 1), "unit": "GB/s", "frac": round(ach_impl / l2_bw, 4),
-                           "implementation_bytes_per_site": impl_bytes_per_site,
-                           "peak_source": "measured in this run: 256-bit read stream over a 48 MB buffer",
-                           "hbm_read_measured": round(hbm_bw, 1)}
-        except Exception as ex:  # reported, never fatal
-            roofline_l2 = {"error": str(ex)}
+                    "traffic": prof.get("dram_bytes"), "algorithmic_bytes_per_launch": compulsory,
+                    "kernel_ms": round(dom_ms, 5), "share_of_sweep": round(dom_ms / sum(phases.values()), 3)}
+        if model == "lda":
+            roofline["algorithmic_bytes_note"] = (
+                "compulsory DRAM bytes of the z-step's working set (w, z, fp32 screen rows, theta, "
+                "both count arrays); the rows are re-read per token from L2, not HBM")
+            if prof.get("l1tex_pct") is not None:
+                roofline["binding"] = {"unit": "l1tex data pipe", "pct_of_peak": prof.get("l1tex_pct"),
+                                       "lts_pct_of_peak": prof.get("lts_pct"),
+                                       "source": prof.get("source")}
+            # the operand bytes the kernel streams (fp32 row per token) against the L2 -> SM
+            # read bandwidth measured in this run by one long launch over 24 MB
+            try:
+                l2_bw = g.read_bandwidth(24 << 20, 200)
+                hbm_bw = g.read_bandwidth(4 << 30, 3)
+                ach_l2 = operand / (dom_ms / 1e3) / 1e9
+                roofline["l2"] = {"achieved": round(ach_l2, 1), "peak": round(l2_bw, 1), "unit": "GB/s",
+                                  "frac": round(ach_l2 / l2_bw, 4), "operand_bytes_per_launch": operand,
+                                  "peak_source": "measured in this run: one persistent launch re-reading a 24 MB "
+                                                 "buffer 200 times (256-bit loads)",
+                                  "hbm_read_measured": round(hbm_bw, 1)}
+            except Exception as ex:  # reported, never fatal
+                roofline["l2"] = {"error": str(ex)}
 
     # --- e2e through the public API with host buffers ---
     e2e = None
+    e2e_pageable = None
     if host_corpus and store is not None:
-        for name in store.names:
-            if not store.observed[name]:
-                arr, t = pinned_like(store.arrays[name])
-                store.arrays[name] = arr
-                store.__dict__.setdefault("_pins", []).append(t)
         # bytes per step, counted by the library (bnmc_gpu_transfer_stats) on the call after
         # the bind: LDA this rank's z slice up (the sweep reads only z of the latent state),
         # z and theta slices + the global phi + lj down; MH w, b up and down; GMM z, pi,
         # mu, sigma2 up and down
-        eng.sweep(store, it)  # bind (uploads the observed data once, outside the timed region)
-        it += 1
-        eng.sweep(store, it)
-        it += 1
-        up, down = eng.transfer_stats()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            eng.sweep(store, it + i)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        it += args.steps
-        if dist:
-            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        def e2e_loop(e_, s_, it_):
+            e_.sweep(s_, it_)  # bind (page-locks the store, uploads the observed data once)
+            e_.sweep(s_, it_ + 1)
+            up, down = e_.transfer_stats()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                e_.sweep(s_, it_ + 2 + i)
+            torch.cuda.synchronize()
+            sec = (time.perf_counter() - t0) / args.steps
+            if dist:
+                t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                sec = float(t.item())
+            return sec, up, down, it_ + 2 + args.steps
+
+        e2e_s, up, down, it = e2e_loop(eng, store, it)
         e2e = {"value": sites_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(up),
                "d2h_bytes_per_step": int(down), "ms_per_step": e2e_s * 1e3,
-               "path": "Engine.sweep(store, iter) with pinned host arrays: bnmc_gpu_sweep_store (upload of "
-                       "what the sweep reads, sweep, write-back)" + E2E_NOTES.get(model, "")}
+               "path": "Engine.sweep(store, iter) on the caller's numpy store, page-locked once at binding "
+                       "(RunConfig.pin_host): bnmc_gpu_sweep_store (upload of what the sweep reads, sweep, "
+                       "write-back)" + E2E_NOTES.get(model, "")}
+        if model in ("lda", "gmm") and world == 1:
+            # the same loop with the store left pageable (pin_host=False): a fresh engine on
+            # the same stream, the store's state as the pinned loop left it
+            eng.close()
+            eng = g.Engine(model, hyper, g.RunConfig(seed=args.seed, device=local_rank, pin_host=False),
+                           stream=stream.cuda_stream)
+            sp, up2, down2, it = e2e_loop(eng, store, it)
+            e2e_pageable = {"value": sites_total / sp, "unit": UNIT, "ms_per_step": sp * 1e3,
+                            "h2d_bytes_per_step": int(up2), "d2h_bytes_per_step": int(down2)}
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "1B corpus is generated and kept on the device (host cannot hold it)"}
+    eng.close()
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (gen_lda process, numpy; device prior_init)" if model == "lda" else "synthetic",
-           "config": {**config, "l2": "flushed before every timed sweep (256 MiB write)"},
-           "roofline": roofline, "roofline_l2": roofline_l2, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
-           "e2e": e2e, "gpu_launches": per_sweep_kernels * args.steps,
-           "clocks": clk.summary(), "wall_s_timed": wall, "setup_s": setup_s, "last_log_joint": lj_last}
+           "config": config, "execution": {**extra, "parallelism": extra.get(
+               "parallelism", f"{'documents' if model == 'lda' else 'rows'} sharded x{world}")},
+           "roofline": roofline, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
+           "e2e": e2e, "e2e_pageable": e2e_pageable, "gpu_launches": per_sweep_kernels * args.steps,
+           "clocks": clocks, "wall_s_timed": wall, "setup_s": setup_s, "last_log_joint": lj_last}
+    if rank == 0 and world == 1 and args.workload == "nips" and not args.no_1b:
+        out["roofline_1b"] = roofline_1b(args, g, torch, stream, flush, gpu_index)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
-    eng.close()
     if dist:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def roofline_1b(args, g, torch, stream, flush, gpu_index):
+    """A short pass over the 1B-token config (K=1000, V=1e5, 1e6 documents x 1000 tokens;
+    device generator + device prior_init): 3 warm + 3 timed sweeps, the z-step's time from
+    the phase pass, its DRAM fraction from the committed ncu capture's bytes per launch."""
+    try:
+        wl = WORKLOADS["1b"]
+        docs, V, K, L = wl["docs"], wl["vocab"], wl["topics"], wl["doc_len"]
+        t0 = time.perf_counter()
+        eng = g.Engine("lda", {"K": K, "V": V, "M": docs, "N": [L] * docs},
+                       g.RunConfig(seed=args.seed, device=torch.cuda.current_device()), stream=stream.cuda_stream)
+        eng.lda_generate(args.seed)
+        eng.enqueue(0, 3)
+        eng.synchronize()
+        setup = time.perf_counter() - t0
+        ms, clocks, _ = time_sweeps(eng, torch, stream, flush, 3, 3, gpu_index)
+        phases = phase_times(eng, torch, flush, 6, 2)
+        eng.close()
+        zms = phases["zstep"]
+        N = docs * L
+        peak, peak_src = measured_peak_hbm()
+        compulsory, operand = lda_zstep_bytes(docs, V, K, L)
+        # no word reuse within documents or blocks of documents in this corpus (SURVEY 8d,
+        # DESIGN 3): the algorithmic DRAM bytes are the operand bytes, 4 Kp32 + 16 per token
+        ach = operand / (zms / 1e3) / 1e9
+        prof = ncu_profile("1b:zstep") or {}
+        dram = prof.get("dram_bytes")
+        out = {"bound": "hbm", "kernel": "zstep", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+               "frac": round(ach / peak, 4), "peak_source": peak_src, "algorithmic_bytes_per_launch": operand,
+               "traffic": dram, "kernel_ms": round(zms, 3), "sweep_ms": round(ms, 3),
+               "sites_per_s": N / (ms / 1e3), "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+               "clocks": clocks, "setup_s": round(setup, 2),
+               "config": {"workload": "lda-1b", "docs": docs, "vocab": V, "topics": K, "doc_len": L, "tokens": N}}
+        if dram:
+            out["dram_frac"] = round(dram / (zms / 1e3) / 1e9 / peak, 4)
+            out["dram_note"] = ("ncu DRAM bytes per launch (profiles/) over this run's kernel time: the "
+                                "operand rows come ~85 % from DRAM, the rest from L2 hits")
+        return out
+    except Exception as ex:  # reported, never fatal for the NIPS line
+        return {"error": str(ex)}
 
 
 # ----------------------------------------------------------------------------------------
@@ -469,79 +606,130 @@ def ref_bench(argv, timeout, retries=3):
     raise RuntimeError(last)
 
 
-def cpu_baseline(args):
+def shared_inputs(args, world, tmp):
+    """The arm-independent input file for the reference (`lda-file` / `gmm-file`), written
+    from the same seeded generators the GPU arm uses; None for the workloads whose
+    reference run draws its own sample (1b, logreg)."""
     wl = WORKLOADS[args.workload]
-    if wl["model"] != "lda" or args.workload == "1b":
-        docs = None
+    if wl["model"] == "lda" and args.workload != "1b":
+        cfg = shared_config(args, world)
+        docs, L = cfg["docs"], wl["doc_len"]
+        path = os.path.join(tmp, "corpus.bnc")
+        write_corpus_file(path, np.arange(docs + 1, dtype=np.int64) * L,
+                          gen_lda_corpus(docs, wl["vocab"], wl["topics"], L, args.seed), wl["vocab"])
+        return path
+    if wl["model"] == "gmm":
+        path = os.path.join(tmp, "points.f64")
+        gmm_points(wl["points"], args.seed).tofile(path)
+        return path
+    return None
+
+
+def cpu_baseline(args):
+    """The reference on ONE host core on half of the same corpus (the first 750 of the
+    1500 NIPS documents), 2 timed sweeps (~25 s)."""
+    import tempfile
+
+    wl = WORKLOADS[args.workload]
     try:
-        if wl["model"] == "lda":
-            docs = 150 if args.workload == "nips" else (600 if args.workload == "kos" else 8)
-            L = wl["doc_len"] if args.workload != "1b" else 10_000
-            res, retries = ref_bench(["lda", docs, wl["vocab"], wl["topics"], L, args.seed, 1, 1, 2], timeout=300)
-            sample = (f"{docs} documents x {L} tokens ({docs * L} sites) of the {args.workload} shape "
-                      f"(V={wl['vocab']}, K={wl['topics']}), reference gen_lda + prior_init, 1 warm + 2 timed "
-                      f"sweeps, Engine::sweep incl. log-joint")
-        elif wl["model"] == "gmm":
-            res, retries = ref_bench(["gmm", wl["points"], args.seed, 1, 1, 5], timeout=300)
-            sample = f"{wl['points']} points, 1 warm + 5 timed sweeps"
-        else:
-            n = 20_000
-            res, retries = ref_bench(["regression", n, wl["features"], args.seed, 1, 1, 3, 0.01], timeout=300)
-            sample = (f"regression.bn MH (linear twin; no logistic reference), {n} rows x {wl['features']} "
-                      f"features, 1 warm + 3 timed steps")
-        s = float(np.mean(res["ms"])) / 1e3
-        return {"value": res["sites"] / s, "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": sample, "s_per_sweep": s, "retries": retries}
+        with tempfile.TemporaryDirectory() as tmp:
+            path = shared_inputs(args, 1, tmp)
+            if wl["model"] == "lda" and path:
+                docs = wl["docs"] // 2
+                res, retries = ref_bench(["lda-file", path, wl["topics"], args.seed, 1, 0, 2, docs], timeout=300)
+                sample = (f"the first {docs} of the {wl['docs']} documents of this run's corpus "
+                          f"({docs * wl['doc_len']} sites), reference prior_init, 2 timed sweeps, "
+                          f"Engine::sweep incl. log-joint")
+            elif wl["model"] == "lda":
+                res, retries = ref_bench(["lda", 8, wl["vocab"], wl["topics"], 10_000, args.seed, 1, 1, 2], timeout=300)
+                sample = "8 documents x 10000 tokens of the 1b shape (reference gen_lda), 1 warm + 2 timed sweeps"
+            elif wl["model"] == "gmm":
+                res, retries = ref_bench(["gmm-file", path, args.seed, 1, 1, 5], timeout=300)
+                sample = f"this run's {wl['points']} points, 1 warm + 5 timed sweeps"
+            else:
+                n = 20_000
+                res, retries = ref_bench(["regression", n, wl["features"], args.seed, 1, 1, 3, 0.01], timeout=300)
+                sample = (f"regression.bn MH (linear twin; no logistic reference), {n} rows x {wl['features']} "
+                          f"features, 1 warm + 3 timed steps")
+        s_ = float(np.mean(res["ms"])) / 1e3
+        return {"value": res["sites"] / s_, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": sample, "s_per_sweep": s_, "retries": retries}
     except Exception as e:  # reported, never fatal for the GPU line
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": None, "error": str(e)}
 
 
 def run_reference(args, world):
+    import tempfile
+
     wl = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     budget_s = 150.0
     steps, warm = args.steps, args.warmup
-    if wl["model"] == "lda":
-        K, L = wl["topics"], wl["doc_len"] if args.workload != "1b" else 10_000
-        full_docs = wl["docs"] * (world if wl["scaling"] == "weak" else 1) if args.workload != "1b" else 8
-        # ~252 ns per token-candidate single-threaded, ~60 % parallel efficiency
-        per_doc_s = L * K * 252e-9 / max(1.0, 0.6 * threads)
-        fixed_s = 1.5 * K * wl["vocab"] / 1.24e6 / max(1.0, 0.6 * threads)
-        docs = int(max(1, min(full_docs, (budget_s / (steps + warm) - fixed_s) / per_doc_s)))
-        argv = ["lda", docs, wl["vocab"], K, L, args.seed]
-        sample = (f"{docs} of {full_docs} documents x {L} tokens, V={wl['vocab']}, K={K}; reference gen_lda + "
-                  f"prior_init; Engine::sweep incl. log-joint")
-        tail = [warm, steps]
-        est = (steps + warm) * (fixed_s + docs * per_doc_s)
-    elif wl["model"] == "gmm":
-        argv, tail = ["gmm", wl["points"], args.seed], [warm, steps]
-        sample, est = f"{wl['points']} points (full workload)", (steps + warm) * 0.1
-    else:
-        n = int(min(wl["rows"], max(10_000, 1e8 / (steps + warm))))
-        argv, tail = ["regression", n, wl["features"], args.seed], [warm, steps]
-        sample, est = f"regression.bn MH (linear twin), {n} rows x {wl['features']}", (steps + warm) * n * 1.6e-5
-    res, retries, used = None, 0, threads
-    for t in (threads, max(1, threads // 2), 1):
-        try:
-            a = argv + [t] + tail + ([0.01] if wl["model"] == "logreg" else [])
-            res, retries = ref_bench(a, timeout=int(60 + 4 * est * max(1, threads / t)))
-            used = t
-            break
-        except Exception as e:
-            last = str(e)
-            continue
+    cfg = shared_config(args, world)
+    with tempfile.TemporaryDirectory() as tmp:
+        path = shared_inputs(args, world, tmp)
+        if wl["model"] == "lda":
+            K = wl["topics"]
+            L = wl["doc_len"] if args.workload != "1b" else 10_000
+            full_docs = cfg["docs"] if args.workload != "1b" else 8
+            # ~252 ns per token-candidate single-threaded (SURVEY.md section 6), ~60 % parallel efficiency
+            per_doc_s = L * K * 252e-9 / max(1.0, 0.6 * threads)
+            fixed_s = 1.5 * K * wl["vocab"] / 1.24e6 / max(1.0, 0.6 * threads)
+            docs = int(max(1, min(full_docs, (budget_s / (steps + warm) - fixed_s) / per_doc_s)))
+            if path:
+                argv, tail = ["lda-file", path, K, args.seed], [warm, steps, docs]
+                sample = (f"{docs} of {full_docs} documents x {L} tokens of this run's corpus (the GPU arm's "
+                          f"documents), V={wl['vocab']}, K={K}; reference prior_init; Engine::sweep incl. log-joint")
+            else:
+                argv, tail = ["lda", docs, wl["vocab"], K, L, args.seed], [warm, steps]
+                sample = (f"{docs} documents x {L} tokens of the 1b shape, reference gen_lda + prior_init; "
+                          f"Engine::sweep incl. log-joint")
+            est = (steps + warm) * (fixed_s + docs * per_doc_s)
+        elif wl["model"] == "gmm":
+            argv, tail = ["gmm-file", path, args.seed], [warm, steps]
+            sample, est = f"this run's {wl['points']} points (full workload)", (steps + warm) * 0.1
+        else:
+            n = int(min(wl["rows"], max(10_000, 1e8 / (steps + warm))))
+            argv, tail = ["regression", n, wl["features"], args.seed], [warm, steps]
+            sample, est = f"regression.bn MH (linear twin), {n} rows x {wl['features']}", (steps + warm) * n * 1.6e-5
+        res, retries, used, last = None, 0, threads, None
+        for t in (threads, max(1, threads // 2), 1):
+            try:
+                if wl["model"] == "lda" and path:
+                    a = argv + [t] + tail
+                else:
+                    a = argv + [t] + tail + ([0.01] if wl["model"] == "logreg" else [])
+                res, retries = ref_bench(a, timeout=int(60 + 4 * est * max(1, threads / t)))
+                used = t
+                break
+            except Exception as e:
+                last = str(e)
+                continue
     if res is None:
         return {"impl": "reference", "unavailable": f"reference sampler failed on this host: {last}"}
-    s = float(np.mean(res["ms"])) / 1e3
-    value = res["sites"] / s
+    s_ = float(np.mean(res["ms"])) / 1e3
+    value = res["sites"] / s_
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": steps, "warmup": warm, "ms_per_step": s * 1e3, "higher_is_better": True,
+            "steps": steps, "warmup": warm, "ms_per_step": s_ * 1e3, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generators)",
-            "config": {"workload": f"{wl['model']}-{args.workload}", "sample": sample, "threads": used},
+            "data": "synthetic (gen_lda process, numpy; device prior_init)" if wl["model"] == "lda" else "synthetic",
+            "config": cfg, "execution": {"sample": sample, "threads": used},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "reference", "sample": sample,
                              "retries": retries},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def spawn_ranks(n):
+    """`--gpus N` outside torchrun: launch this script under torch.distributed.run with N
+    ranks (one per GPU), rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -553,11 +741,12 @@ def main():
     ap.add_argument("--workload", default="nips", choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-1b", action="store_true", help="skip the 1B-token roofline pass of the NIPS run")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    if args.gpus > 1 and world == 1:
-        sys.exit("bench.py --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args, world)), flush=True)

@@ -239,8 +239,9 @@ int bnmc_gpu_lpp(const double* phi, const double* theta, int64_t K, int64_t V, c
 /* sample_dirichlet_batch with per-row concentrations (batch.cpp:45-83) on the device. */
 int bnmc_gpu_dirichlet_batch(int64_t rows, int64_t cols, const double* alpha, uint64_t key,
                              double* out);
-/* Device read bandwidth (GB/s) over a `bytes` buffer, `reps` timed passes: inside the
- * 126 MB L2 it measures L2 -> SM bandwidth (bench.py's secondary roofline). */
+/* Device read bandwidth (GB/s) over a `bytes` buffer read `reps` times by ONE persistent
+ * launch: inside the 126 MB L2 it measures L2 -> SM bandwidth (bench.py's secondary
+ * roofline), a multi-GB buffer HBM read bandwidth. */
 int bnmc_gpu_probe_read_bandwidth(int64_t bytes, int32_t reps, double* gbps);
 /* Primitive probes for known-answer parity (device RNG and draws). */
 int bnmc_gpu_probe_rng(const uint64_t* keys, int64_t n, int64_t per_key, uint64_t* u64,

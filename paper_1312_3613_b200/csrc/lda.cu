@@ -1,27 +1,23 @@
 // csrc/lda.cu -- LDA uncollapsed Gibbs sweep on sm_100a (proj/models/lda.bn).
 //
 // One reference sweep (Engine::sweep, proj/src/sampler.cpp:390-405; plan order
-// phi, theta, z per tests/golden/describe_lda.txt) becomes, per GPU:
+// phi, theta, z per tests/golden/describe_lda.txt) becomes, per GPU, one CUDA graph:
 //
 //   [allreduce nkw]      NCCL int32 sum of the topic-word counts (world > 1 only)
-//   phi_gamma_kernel     phi block draw: per cell Gamma(beta + n[k,v]) from stream
-//                        keyed(seed,4,var_phi,iter).derive(k,v) (batch.cpp:38-41);
-//                        consumes the counts (zeroes them for this sweep's z-step)
-//   colsum_kernel        row sums of the gamma matrix (fixed-order, deterministic)
-//   phi_norm_kernel      phi = g / sum (batch.cpp:58-61) + Dirichlet log-pdf pieces
-//   phi_terms_kernel     per-topic Dirichlet log-pdf (dist.cpp:115-130)
-//   theta_kernel         theta block: per document Dirichlet(alpha + n[d,.]) from the
-//                        doc-topic counts the previous z-step left (sampler.cpp:61-181),
-//                        stream keyed(seed,4,var_theta,iter).derive(d,k); theta log-pdf
-//   zstep_kernel         z block (sampler.cpp:222-265, draw_from_log_weights
-//                        dist.cpp:202-215) over token chunks: new z, the NEXT sweep's
-//                        topic-word and doc-topic counts (integer atomics), and the
-//                        z-factor of the log-joint (sum log theta[d, z])
-//   wterm_kernel         w-factor of the log-joint from the counts:
-//                        sum_t log phi[z_t, w_t] = sum_{k,v} n[k,v] log phi[k,v]
-//   reduce_kernel        fixed-order sums of the theta / z / w pieces
-//   [allreduce 3 doubles]
-//   finalize_kernel      log-joint = ((F_phi + F_theta) + F_z) + F_w (eval.cpp:393-422)
+//   phi_pool_kernel      phi AND theta blocks: every cell's Gamma(prior + count) draw
+//                        (batch.cpp:38-41 streams, dist.cpp:136-155 Marsaglia-Tsang) by
+//                        a persistent warp pool; consumes the counts (zeroes them for
+//                        this sweep's z-step)
+//   phi_colsum2_kernel   phi column sums S[k] and the phi factor of the log-joint;
+//                        theta rows: normalise, theta factor (extra y-blocks)
+//   zscreen_t_kernel     z block (sampler.cpp:222-265, draw_from_log_weights
+//   / zscreen_kernel     dist.cpp:202-215): fp32 screen of the product-form draw, new z,
+//                        the NEXT sweep's counts (integer atomics); ambiguous tokens
+//                        queued for
+//   zfallback_kernel     the fp64 product-form draw (one warp per queued token)
+//   wterm_kernel<FINAL>  w- and z-factors of the log-joint from the counts, the fixed-
+//                        order final sum (eval.cpp:393-422); sharded: this rank's
+//                        pieces -> [allreduce 3 doubles] -> finalize_kernel
 //
 // Device layout (HBM): w, z int32 [N_local]; phiT fp64 [V][Kp] (word-major, so
 // the K weights of a token are one contiguous row; Kp = K rounded up to the
@@ -74,25 +70,19 @@ struct LdaArgs {
   double* phiT;
   float* phiT32;     // fp32 copy of phiT [V][Kp32], columns permuted by phys32 (screen only)
   int Kp32, G32, R32, CW32; // screen layout: Kp32 = CW32 * G32 * R32
-  unsigned short* phiT16;    // fp16 row-scaled copy [V][Kp16], columns permuted by phys16 (level-1 screen)
-  int Kp16, RH;              // Kp16 = 64 RH
-  float* thS32;              // [Ml][K8] theta/S in fp32 (level-1 units -> level 2)
-  int2* q2;                  // level-2 queue (t, m)
-  int* q2_len;
-  int col_stripes;           // phi_colsum2 stripe blocks (extra y-blocks convert phiT16 rows)
+  int col_stripes;           // phi_colsum2 column-stripe blocks
   double* logphiT;   // exact mode only
   double* theta;
   int* nkw;          // [V][Kp]
   int* nmk;          // [Ml][K]
-  double* colpart;   // [nb_phi][K]
-  double* colpart2;  // [nb_phi][K][2]
+  double* colpart2;  // [nb_phi][K][2] (phi_norm_kernel: eval / exact-mode normalisation)
   double* S;         // [K]
   double* phi_term;  // [K]
   double* tpart;     // [Ml] theta-factor pieces
   double* zpart;     // [nbw] z-factor pieces (sum n[d,k] log theta[d,k]) per wterm block
-  double* logg;      // [V][Kp] log of this sweep's gamma draws (phi block v2)
   double* logS;      // [K] log of the gamma row sums
-  int logg_valid;    // logg/logS belong to the current phi (set inside a v2 sweep)
+  int logg_valid;    // phiT holds this sweep's gamma draws g and logS their log row sums
+                     // (inside a sweep): the w-factor is n (log g - log S)
   float screen_margin;  // kScreenMargin (BNMC_SCREEN_MARGIN overrides: tests force the fallback)
   int2* fq;          // screen fallback queue: (local token, local document) [Nl]
   int* fq_len;
@@ -105,15 +95,11 @@ struct LdaArgs {
   int pow_alpha, pow_beta;  // 1/alpha, 1/beta when exactly an integer in [2, 64] (boost by squaring), else 0
   int trow_blocks;          // phi_colsum2: y-blocks finishing the pool's theta rows
   int pool_phi;             // phi_pool: the pool draws the phi cells too (0: phi clamped)
-  int phi_pf;               // phi_gamma2: count prefetch distance in blocks; phi_pool: in grid-widths of groups (0: off)
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
   int var_phi, var_theta, var_z;
   int rows_per_block, nb_phi;
-  double* gpart;     // [nvb][K] phi block v2 partials: sum g, sum log g
-  double* lpart;
-  std::int64_t nvb;
   double* spart;     // [kColStripes][K][2]
   int* ticket;       // [ceil(K/32)] last-block tickets of phi_colsum2
   int* ticket2;      // last-block ticket of wterm_kernel<true>
@@ -125,80 +111,6 @@ struct LdaArgs {
 // ---------------------------------------------------------------------------------
 // phi block
 // ---------------------------------------------------------------------------------
-// Block b owns vocabulary rows [b*R, b*R + R); its threads sweep the R x K cells
-// (k fastest: coalesced phiT rows), then threads k < K sum their column over the
-// block's rows in fixed order -> colpart[b][k].
-__global__ void __launch_bounds__(256) phi_gamma_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  const std::int64_t iter = *iter_p;
-  const std::uint64_t key = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
-                                  static_cast<std::uint64_t>(iter));
-  const int b = blockIdx.x;
-  const int v0 = b * a.rows_per_block;
-  const int v1 = min(a.V, v0 + a.rows_per_block);
-  const int cells = (v1 - v0) * a.K;
-  // The counts come from HBM at the start of a sweep: issue the thread's count loads
-  // up front (<= 4 cells per thread at the configured rows per block) before the
-  // latency-bound gamma draws.
-  int n[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = threadIdx.x + j * blockDim.x;
-    n[j] = 0;
-    if (c < cells) {
-      const std::size_t i = static_cast<std::size_t>(v0 + c / a.K) * a.Kp + c % a.K;
-      n[j] = a.nkw[i];
-      a.nkw[i] = 0;
-    }
-  }
-  for (int c = threadIdx.x, j = 0; c < cells; c += blockDim.x, ++j) {
-    const int v = v0 + c / a.K, k = c % a.K;
-    const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
-    int cnt;
-    if (j < 4) {
-      cnt = n[0];
-      if (j == 1) cnt = n[1];
-      if (j == 2) cnt = n[2];
-      if (j == 3) cnt = n[3];
-    } else {
-      cnt = a.nkw[i];
-      a.nkw[i] = 0;
-    }
-    Stream r(derive(key, static_cast<std::uint64_t>(k), static_cast<std::uint64_t>(v)));
-    const double g = draw_gamma(r, a.beta + static_cast<double>(cnt));
-    a.phiT[i] = g;
-    if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(g);
-  }
-  __syncthreads();
-  // Column partials of the block's rows, fixed order: sum g (the Dirichlet row sum,
-  // batch.cpp:55-58) and sum log g (the phi factor of the log-joint without a
-  // normalisation pass: sum log(g/S) = sum log g - V log S).
-  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-    double sg = 0.0, sl = 0.0;
-    for (int v = v0; v < v1; ++v) {
-      const double g = a.phiT[static_cast<std::size_t>(v) * a.Kp + k];
-      sg += g;
-      sl += g > 0.0 ? log(g) : -INFINITY;
-    }
-    a.colpart[static_cast<std::size_t>(b) * a.K + k] = sg;
-    a.colpart2[(static_cast<std::size_t>(b) * a.K + k) * 2] = sl;
-  }
-}
-
-// phi block, v2: thread (k, vb) draws the cells (v, k), v in [vb*L, vb*L + L), of one
-// topic column in order and keeps fixed-order partials of sum g and sum log g.
-// * Rejection sampling without warp-level waste: the Marsaglia-Tsang loop runs one
-//   attempt per iteration and a thread whose attempt is accepted moves straight on
-//   to its next cell, so a warp iterates ~(1 + reject rate) * L times instead of
-//   L * (max attempts over the warp) (ncu r01 v6: the per-cell loop executed
-//   ~1290 thread instructions per cell, ~2.5x the straight-line count).
-// * Per-count constants d = a - 1/3, c = 1/sqrt(9d), 1/shape for counts < 64 come
-//   from a shared table computed with the reference's expressions (dist.cpp:136-155;
-//   bit-identical), saving a sqrt and two divisions per cell.
-// * log g is stored per cell (logg): the w-factor of the log-joint then needs no
-//   transcendental after the z-step.
-// The stream of every cell is keyed(seed, 4, var_phi, iter).derive(k, v) and is
-// consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
-// uniform]), so the draws are the reference's.
 // The shape < 1 boost g * u^(1/shape) (dist.cpp:139-140) when 1/shape is exactly an
 // integer e (lda.bn's alpha = beta = 0.1: e = 10): u^e by binary powering (4 multiplies
 // for e = 10, <= ~4 ulp from the correctly rounded power -- pow's own error is <= 1 ulp,
@@ -218,110 +130,8 @@ __device__ __forceinline__ double boost_factor(double u, int e, double inv) {
 }
 
 constexpr int kGammaTab = 64;
-constexpr int kPhiRowsMax = 8;  // L: cells per thread (8, or fewer for small K x V)
 
-template <int kPhiRows>
-__global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  __shared__ double tab_d[kGammaTab], tab_c[kGammaTab], tab_inv[kGammaTab];
-  __shared__ int cnt_s[kPhiRows][256];  // the thread's counts, loaded up front
-  const std::int64_t iter = *iter_p;
-  for (int i = threadIdx.x; i < kGammaTab; i += blockDim.x) {
-    const double shape = a.beta + static_cast<double>(i);
-    const bool boost = shape < 1.0;
-    const double aa = boost ? shape + 1.0 : shape;
-    const double d = aa - 1.0 / 3.0;
-    tab_d[i] = d;
-    tab_c[i] = 1.0 / sqrt(9.0 * d);
-    tab_inv[i] = boost ? 1.0 / shape : 0.0;
-  }
-  __syncthreads();
-  const std::int64_t idx = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int k = static_cast<int>(idx % a.K);
-  const std::int64_t vb = idx / a.K;
-  if (vb >= a.nvb) return;
-  const int v0 = static_cast<int>(vb * kPhiRows), v1 = min(a.V, v0 + kPhiRows);
-#pragma unroll
-  for (int j = 0; j < kPhiRows; ++j) {
-    if (v0 + j < v1) {
-      const std::size_t i = static_cast<std::size_t>(v0 + j) * a.Kp + k;
-      cnt_s[j][threadIdx.x] = a.nkw[i];
-      a.nkw[i] = 0;  // consumed: the z-step accumulates the next sweep's counts here
-    }
-  }
-  // The counts of the block ~0.7 resident waves later (a.phi_pf blocks on), into L2 while
-  // this block draws: the next wave then starts from L2 instead of HBM (the bench flushes
-  // L2 before every sweep; r01: phi 73 -> 66 us on NIPS).
-  if (a.phi_pf > 0) {
-    const std::int64_t idx2 = idx + static_cast<std::int64_t>(a.phi_pf) * blockDim.x;
-    const std::int64_t vb2 = idx2 / a.K;
-    if (vb2 < a.nvb) {
-      const int k2 = static_cast<int>(idx2 % a.K);
-#pragma unroll
-      for (int j = 0; j < kPhiRows; ++j) {
-        const std::int64_t v2 = vb2 * kPhiRows + j;
-        if (v2 < a.V) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.nkw + static_cast<std::size_t>(v2) * a.Kp + k2));
-      }
-    }
-  }
-  const int col32 = a.phiT32 ? phys32(k, a.R32, a.G32, a.CW32) : 0;
-  pdl_trigger();
-  const std::uint64_t kkey = fold(keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_phi),
-                                        static_cast<std::uint64_t>(iter)),
-                                  static_cast<std::uint64_t>(k));
-  double sg = 0.0, sl = 0.0;
-  int v = v0;
-  bool fresh = true;
-  Stream r(0);
-  double d = 1.0, c = 1.0, inv = 0.0;
-  while (v < v1) {
-    if (fresh) {
-      const int n = cnt_s[v - v0][threadIdx.x];
-      r = Stream(fold(kkey, static_cast<std::uint64_t>(v)));
-      if (n < kGammaTab) {
-        d = tab_d[n];
-        c = tab_c[n];
-        inv = tab_inv[n];
-      } else {
-        const double shape = a.beta + static_cast<double>(n);  // >= 64: no boost
-        d = shape - 1.0 / 3.0;
-        c = 1.0 / sqrt(9.0 * d);
-        inv = 0.0;
-      }
-      fresh = false;
-    }
-    const double x = r.next_gaussian();
-    double vv = 1.0 + c * x;
-    if (vv > 0.0) {
-      vv = vv * vv * vv;
-      const double u = r.next_unit();
-      bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
-      if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
-      if (acc) {
-        double g = d * vv;
-        // the reference's boost g * pow(u, 1/shape) (dist.cpp:139-140) as exp(log(u) / shape):
-        // |log u / shape| <= 37 / shape, so the relative difference from a correctly
-        // rounded pow is <= ~2^-53 * 37 / shape (4e-14 at shape 0.1), far inside the 1e-12
-        // contract, and exp + log cost half of pow's double-double path (r01 v33: phi
-        // block 83 -> 77 us on NIPS)
-        if (inv != 0.0) g = g * boost_factor(r.next_unit(), a.pow_beta, inv);
-        const std::size_t i = static_cast<std::size_t>(v) * a.Kp + k;
-        a.phiT[i] = g;
-        if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + col32] = static_cast<float>(g);
-        sg += g;
-        // log g: the phi prior term here, the w-factor after the z-step (wterm_kernel)
-        const double lg = g > 0.0 ? log(g) : -INFINITY;
-        a.logg[i] = lg;
-        sl += lg;
-        ++v;
-        fresh = true;
-      }
-    }
-  }
-  a.gpart[vb * a.K + k] = sg;
-  a.lpart[vb * a.K + k] = sl;
-}
-
-// phi block, v3 ("warp pool"): a persistent grid (one resident wave) in which warp w
+// phi + theta block ("warp pool"): a persistent grid (one resident wave) in which warp w
 // owns the contiguous cell range [w C / W, (w+1) C / W) of the C = V K cells (k
 // fastest, the phiT row order), so every warp has the same number of cells.  The 32
 // lanes draw the range as one pool, <= kPoolCells cells (one shared-memory chunk of
@@ -338,7 +148,7 @@ __global__ void __launch_bounds__(256) phi_gamma2_kernel(LdaArgs a, const std::i
 // * Streams keyed(seed, 4, var_phi, iter).derive(k, v), consumed in the reference's
 //   order (gaussian until 1 + c x > 0, uniform, [boost uniform]; dist.cpp:136-155):
 //   the draws are the reference's whichever lane draws a cell.
-constexpr int kPoolCells = 1024;
+constexpr int kPoolCells = 512;
 constexpr int kPoolWarps = 8;
 
 // cell c of the flat [V][K] order -> (v, k); double reciprocal + one correction step
@@ -356,8 +166,30 @@ __device__ __forceinline__ void cell_vk(std::int64_t c, int K, double invK, int&
   k = static_cast<int>(r);
 }
 
+// Marsaglia-Tsang's second acceptance test, log(u) < 0.5 x^2 + d (1 - v + log(v))
+// (dist.cpp:146-149), with the two logs first taken in fp32 (MUFU.LG2): when the fp32
+// sides are further apart than a bound 40x the fp32 log error (1e-5 (1 + |log|) per log,
+// lg2.approx is within 2^-21 (1 + |log2|)), that decides the comparison exactly as the
+// double expression would; otherwise (~1e-4 of the calls) the double logs decide.  The
+// squeeze fails for ~3 % of the attempts, so the double path used to run in most warp
+// iterations for one or two lanes (ncu r02: ~19 % of the pool's instructions).
+__device__ __forceinline__ bool mt_log_test(double u, double x, double v, double d) {
+  if (v > 1e-30 && v < 1e30) {
+    const double lu = static_cast<double>(__log2f(static_cast<float>(u))) * 0.69314718055994530942;
+    const double lv = static_cast<double>(__log2f(static_cast<float>(v))) * 0.69314718055994530942;
+    const double rhs = 0.5 * x * x + d * (1.0 - v + lv);
+    const double err = 1e-5 * (1.0 + fabs(lu)) + d * 1e-5 * (1.0 + fabs(lv)) + 1e-12 * (1.0 + fabs(rhs));
+    if (lu + err < rhs) return true;
+    if (lu - err > rhs) return false;
+  }
+  return log(u) < 0.5 * x * x + d * (1.0 - v + log(v));
+}
+
+#ifndef BNMC_POOL_MINB
+#define BNMC_POOL_MINB 1
+#endif
 template <bool KTAB>
-__global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int64_t* iter_p) {
+__global__ void __launch_bounds__(256, BNMC_POOL_MINB) phi_pool_kernel(LdaArgs a, const std::int64_t* iter_p) {
   __shared__ double tab_d[2][kGammaTab], tab_c[2][kGammaTab], tab_inv[2][kGammaTab];
   __shared__ std::uint64_t kkey_s[KTAB ? kPoolCells : 1];
   __shared__ int col32_s[KTAB ? kPoolCells : 1];
@@ -395,18 +227,33 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
   const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const std::int64_t c_end = ncells * (gw + 1) / nw;
-  auto count_at = [&](std::int64_t c) -> int* {
-    if (c >= cphi) return a.nmk + (c - cphi);
-    int v, k;
-    cell_vk(c, a.K, invK, v, k);
-    return a.nkw + static_cast<std::size_t>(v) * a.Kp + k;
-  };
+  const float invKf = 1.0f / static_cast<float>(a.K);
   for (std::int64_t c0 = ncells * gw / nw; c0 < c_end; c0 += kPoolCells) {
     const int n = static_cast<int>(c_end - c0 < kPoolCells ? c_end - c0 : kPoolCells);
+    // chunk bases: cells j < jt are phi cells (v, k) = (pv0, pk0) + j, cells j >= jt theta
+    // cells (m, k) = (tm0, tk0) + (j - jt) in row-major order; within the chunk, row and
+    // column come from a 32-bit offset r < K + 1024 by one float reciprocal (exact: the
+    // quotient's fractional part stays >= 0.5 / K away from an integer)
+    const int jt = static_cast<int>(cphi - c0 <= 0 ? 0 : (cphi - c0 >= n ? n : cphi - c0));
+    int pv0 = 0, pk0 = 0, tm0 = 0, tk0 = 0;
+    if (jt > 0) cell_vk(c0, a.K, invK, pv0, pk0);
+    if (jt < n) cell_vk(c0 + jt - cphi, a.K, invK, tm0, tk0);
+    auto vk_of = [&](int j, int& v, int& k) {  // (v or m, k) of chunk cell j
+      const int r = j < jt ? pk0 + j : tk0 + (j - jt);
+      const int q = __float2int_rz((static_cast<float>(r) + 0.5f) * invKf);
+      v = (j < jt ? pv0 : tm0) + q;
+      k = r - q * a.K;
+    };
+    auto count_at = [&](int j) -> int* {
+      int v, k;
+      vk_of(j, v, k);
+      return j < jt ? a.nkw + static_cast<std::size_t>(v) * a.Kp + k
+                    : a.nmk + static_cast<std::size_t>(v) * a.K + k;
+    };
     // the chunk's counts into shared memory (consumed: the z-step accumulates the next
     // sweep's counts here), 8 loads in flight per lane before the zeroing stores (the
     // stores may alias the next loads: a load-store loop would serialise one HBM round
-    // trip per 32 cells); the next chunk's counts into L2 meanwhile
+    // trip per 32 cells)
     for (int j0 = 0; j0 < n; j0 += 8 * 32) {
       int val[8];
       int* at[8];
@@ -416,7 +263,7 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
         val[i] = 0;
         at[i] = nullptr;
         if (j < n) {
-          at[i] = count_at(c0 + j);
+          at[i] = count_at(j);
           val[i] = __ldcg(at[i]);
         }
       }
@@ -428,8 +275,16 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
         }
       }
     }
-    if (c0 + kPoolCells + 32 * lane < c_end)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(count_at(c0 + kPoolCells + 32 * lane)));
+    // the next chunk's counts into L2 meanwhile (one line per 32 cells)
+    {
+      const std::int64_t cn = c0 + kPoolCells + 32 * lane;
+      if (cn < c_end) {
+        int v, k;
+        cell_vk(cn < cphi ? cn : cn - cphi, a.K, invK, v, k);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(cn < cphi ? a.nkw + static_cast<std::size_t>(v) * a.Kp + k
+                                                                : a.nmk + static_cast<std::size_t>(v) * a.K + k));
+      }
+    }
     __syncwarp();
     int j = lane, next = 32;
     bool fresh = true;
@@ -442,12 +297,11 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
       bool accepted = false;
       if (j < n) {
         if (fresh) {
-          const std::int64_t cell = c0 + j;
           const int cn = cnt[j];
-          const int kind = cell >= cphi;
+          const int kind = j >= jt;
           int v, k;
+          vk_of(j, v, k);
           if (!kind) {  // phi cell (v, k): Stream(derive(base, k, v))
-            cell_vk(cell, a.K, invK, v, k);
             pos = fold(KTAB ? kkey_s[k] : fold(base, static_cast<std::uint64_t>(k)), static_cast<std::uint64_t>(v));
             outp = a.phiT + static_cast<std::size_t>(v) * a.Kp + k;
             out32 = a.phiT32 ? a.phiT32 + static_cast<std::size_t>(v) * a.Kp32 +
@@ -455,9 +309,8 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
                              : nullptr;
             pw = a.pow_beta;
           } else {  // theta cell (m, k): Stream(derive(tbase, doc_base + m, k)), g unnormalised
-            cell_vk(cell - cphi, a.K, invK, v, k);
             pos = fold(fold(tbase, static_cast<std::uint64_t>(a.doc_base + v)), static_cast<std::uint64_t>(k));
-            outp = a.theta + (cell - cphi);
+            outp = a.theta + static_cast<std::size_t>(v) * a.K + k;
             out32 = nullptr;
             pw = a.pow_alpha;
           }
@@ -484,7 +337,7 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
           pos += kGolden;
           const double u = (static_cast<double>(mix(pos) >> 11) + 0.5) * 0x1p-53;
           bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
-          if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
+          if (!acc) acc = mt_log_test(u, x, vv, d);
           if (acc) {
             double g = d * vv;
             if (inv != 0.0) {
@@ -508,32 +361,35 @@ __global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int
   }
 }
 
-// Per topic: S[k] = sum over vb of gpart and the phi factor
-// (beta-1) (sum log g - V log S) - sum lgamma(beta) + lgamma(sum beta)
-// (dist.cpp:115-130).  Grid (ceil(K/32), kColStripes): block (kb, s) sums stripe s of
-// the row blocks for 32 topics (threads 32 x 8, fixed-order smem reduction) into
-// spart[s][k]; the last stripe block of kb to finish (atomic ticket) adds the
-// stripes in stripe order.  The ticket decides who adds, never the order, so the
-// result is deterministic.
 constexpr int kColStripes = 128;
 
-__device__ void h16_rows(const LdaArgs& a, std::int64_t w0, std::int64_t nw);
-
-// Blocks with blockIdx.y >= col_stripes convert the new phi rows to fp16 for the
-// level-1 screen (h16_rows) -- the conversion needs the rows, not S, so it runs beside
-// the column sums instead of after them.
-// FROM_G (warp-pool phi block): the stripes sum the columns of phiT itself (rows v,
-// stride Kp): sum g, and sum log g as log(mantissa product) + exponent sum
-// (frexp-renormalised after every factor: one log per thread and column instead of one
-// per cell).  Otherwise the v2 kernel's row-block partials gpart / lpart.
+// Per topic k: S[k] = sum_v g[v][k] (the Dirichlet row sum, batch.cpp:55-58) and the phi
+// factor (beta-1)(sum log g - V log S) - sum lgamma(beta) + lgamma(sum beta)
+// (dist.cpp:115-130; sum phi = sum g / S = 1 by construction), from phiT itself.
+// Grid (ceil(K/32), col_stripes + trow_blocks): block (kb, s < col_stripes) sums stripe s
+// of the rows for 32 topics (threads 32 x 8: sum g, and sum log g as log(mantissa
+// product) + exponent sum, frexp-renormalised after every factor -- one log per thread
+// and column instead of one per cell; fixed-order smem reduction) into spart[s][k]; the
+// last stripe block of kb to finish (atomic ticket) adds the stripes in stripe order.
+// The ticket decides who adds, never the order: deterministic.  Blocks with
+// blockIdx.y >= col_stripes finish the pool's theta rows (theta_row_finish).
 struct LogProd {
   double mant = 1.0;
   int ex = 0;
   bool zero = false;
+  // frexp by bit operations for normal positive doubles (the gamma draws here are
+  // >= ~1e-175: normal); frexp's own special-case branches for the rest
+  static __device__ __forceinline__ double split(double x, int& e) {
+    const long long b = __double_as_longlong(x);
+    const int be = static_cast<int>((b >> 52) & 0x7ff);
+    if (be == 0 || be == 0x7ff) return frexp(x, &e);
+    e = be - 1022;
+    return __longlong_as_double((b & 0x000fffffffffffffll) | 0x3fe0000000000000ll);
+  }
   __device__ __forceinline__ void mul(double g) {
     if (g > 0.0) {
       int e1, e2;
-      mant = frexp(mant * frexp(g, &e1), &e2);
+      mant = split(mant * split(g, e1), e2);
       ex += e1 + e2;
     } else {
       zero = true;
@@ -573,7 +429,6 @@ __device__ __forceinline__ void theta_row_finish(const LdaArgs& a, std::int64_t 
   }
 }
 
-template <bool FROM_G>
 __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   __shared__ double sg_s[8][33], sl_s[8][33];
   __shared__ bool last;
@@ -581,15 +436,8 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   pdl_trigger();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {  // this sweep's redraw queues
     if (a.fq_len) *a.fq_len = 0;
-    if (a.q2_len) *a.q2_len = 0;
   }
   const int stripes = a.col_stripes;
-  if (static_cast<int>(blockIdx.y) >= stripes + a.trow_blocks) {
-    const std::int64_t hb = static_cast<std::int64_t>(blockIdx.y - stripes - a.trow_blocks) * gridDim.x + blockIdx.x;
-    const std::int64_t nhb = static_cast<std::int64_t>(gridDim.y - stripes - a.trow_blocks) * gridDim.x;
-    h16_rows(a, hb * 8 + (threadIdx.x >> 5), nhb * 8);
-    return;
-  }
   if (static_cast<int>(blockIdx.y) >= stripes) {  // theta rows of the warp-pool block
     const std::int64_t w0 = (static_cast<std::int64_t>(blockIdx.y - stripes) * gridDim.x + blockIdx.x) * 8 + (threadIdx.x >> 5);
     const std::int64_t nwr = static_cast<std::int64_t>(a.trow_blocks) * gridDim.x * 8;
@@ -598,58 +446,28 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   }
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
-  const std::int64_t rows = FROM_G ? a.V : a.nvb;
+  const std::int64_t rows = a.V;
   const std::int64_t chunk = (rows + stripes - 1) / stripes;
   const std::int64_t b0 = blockIdx.y * chunk, b1 = min(rows, b0 + chunk);
   double sg = 0.0, sl = 0.0;
   if (k < a.K) {
-    if constexpr (FROM_G) {
-      LogProd lp;
-      std::int64_t b = b0 + ty;
-      for (; b < b1; b += 64) {  // 8 loads in flight
-        double g8[8];
+    LogProd lp;
+    for (std::int64_t b = b0 + ty; b < b1; b += 64) {  // 8 loads in flight
+      double g8[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const std::int64_t bj = b + 8 * j;
-          g8[j] = bj < b1 ? a.phiT[bj * a.Kp + k] : 1.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (b + 8 * j < b1) {
-            sg += g8[j];
-            lp.mul(g8[j]);
-          }
-        }
-      }
-      sl = lp.log_value();
-    } else {
-      std::int64_t b = b0 + ty;
-      for (; b + 56 < b1; b += 64) {  // 8 independent loads in flight per operand
-        double g8[8], l8[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          g8[j] = a.gpart[(b + 8 * j) * a.K + k];
-          l8[j] = a.lpart[(b + 8 * j) * a.K + k];
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sg += g8[j];
-          sl += l8[j];
-        }
-      }
-      double g8[8], l8[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {  // the remaining < 8 rows of this thread, loads issued together
+      for (int j = 0; j < 8; ++j) {
         const std::int64_t bj = b + 8 * j;
-        g8[j] = bj < b1 ? a.gpart[bj * a.K + k] : 0.0;
-        l8[j] = bj < b1 ? a.lpart[bj * a.K + k] : 0.0;
+        g8[j] = bj < b1 ? a.phiT[bj * a.Kp + k] : 1.0;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        sg += g8[j];
-        sl += l8[j];
+        if (b + 8 * j < b1) {
+          sg += g8[j];
+          lp.mul(g8[j]);
+        }
       }
     }
+    sl = lp.log_value();
   }
   sg_s[ty][tx] = sg;
   sl_s[ty][tx] = sl;
@@ -709,26 +527,6 @@ __global__ void __launch_bounds__(256) phi_colsum2_kernel(LdaArgs a) {
   a.phi_term[k] = (!(g > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
 }
 
-// Per topic: S[k] = sum_b colpart (the gamma row sum) and the phi factor
-// lp - sum lgamma(beta) + lgamma(sum beta) with lp = (beta-1) (sum log g - V log S)
-// (dist.cpp:115-130; sum phi = sum g / S = 1 by construction).
-__global__ void phi_colsum_terms_kernel(LdaArgs a) {
-  __shared__ double scratch[32];
-  const int k = blockIdx.x;
-  double sg = 0.0, sl = 0.0;
-  for (int b = threadIdx.x; b < a.nb_phi; b += blockDim.x) {
-    sg += a.colpart[static_cast<std::size_t>(b) * a.K + k];
-    sl += a.colpart2[(static_cast<std::size_t>(b) * a.K + k) * 2];
-  }
-  sg = block_sum(sg, scratch);
-  sl = block_sum(sl, scratch);
-  if (threadIdx.x == 0) {
-    a.S[k] = sg;
-    const double lp = (a.beta - 1.0) * (sl - static_cast<double>(a.V) * log(sg));
-    a.phi_term[k] = (!(sg > 0.0) || !(a.beta > 0.0)) ? -INFINITY : lp - a.phi_norm + a.phi_lgasum;
-  }
-}
-
 // fp32 screen copy of phi's numerator: phiT32 = (float)(phiT / S) (S = 1 outside a sweep).
 __global__ void phi_f32_kernel(LdaArgs a) {
   const std::int64_t n = static_cast<std::int64_t>(a.V) * a.K;
@@ -783,157 +581,6 @@ __global__ void phi_terms_kernel(LdaArgs a) {
   if (threadIdx.x == 0) {
     a.phi_term[k] = (fabs(sx - 1.0) > 1e-9 || !(a.beta > 0.0)) ? -INFINITY
                                                                 : lp - a.phi_norm + a.phi_lgasum;
-  }
-}
-
-// ---------------------------------------------------------------------------------
-// theta block: one CTA per document row
-// ---------------------------------------------------------------------------------
-__global__ void theta_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* g = reinterpret_cast<double*>(smem_raw);  // [K]
-  __shared__ double scratch[32];
-  const std::int64_t iter = *iter_p;
-  const std::uint64_t tkey = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
-                                   static_cast<std::uint64_t>(iter));
-  for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
-    const std::uint64_t mg = static_cast<std::uint64_t>(a.doc_base + m);
-    int* cnt = a.nmk + m * a.K;
-    double part = 0.0;
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-      const int n = cnt[k];
-      cnt[k] = 0;  // consumed: the z-step accumulates the next sweep's counts here
-      Stream r(derive(tkey, mg, static_cast<std::uint64_t>(k)));
-      const double x = draw_gamma(r, a.alpha + static_cast<double>(n));
-      g[k] = x;
-      part += x;
-    }
-    const double S = block_sum(part, scratch);
-    double lp = 0.0, sx = 0.0;
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-      const double x = g[k] / S;
-      a.theta[m * a.K + k] = x;
-      lp += (a.alpha - 1.0) * (x > 0.0 ? log(x) : -INFINITY);
-      sx += x;
-    }
-    lp = block_sum(lp, scratch);
-    sx = block_sum(sx, scratch);
-    if (threadIdx.x == 0)
-      a.tpart[m] = fabs(sx - 1.0) > 1e-9 ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
-    __syncthreads();
-  }
-}
-
-// theta block, v2: the phi_gamma2 scheme on document rows.  A block holds `dpb`
-// documents; each document row is split into runs of TL consecutive topics, one
-// run per thread (persistent rejection loop, counts prefetched to shared memory,
-// shared per-count constants).  Per document: S = sum g (fixed order: thread runs
-// in order), theta = g / S, and the Dirichlet log-pdf via
-// sum log theta = sum log g - K log S with sum log g from renormalised products.
-// Streams keyed(seed, 4, var_theta, iter).derive(d, k) as the reference (batch.cpp:38-41).
-constexpr int kThetaRun = 4;
-
-__global__ void __launch_bounds__(256) theta2_kernel(LdaArgs a, const std::int64_t* iter_p, int tpd, int dpb) {
-  __shared__ double tab_d[kGammaTab], tab_c[kGammaTab], tab_inv[kGammaTab];
-  __shared__ int cnt_s[kThetaRun][256];
-  __shared__ double g_s[kThetaRun][256];
-  __shared__ double ps[256], pl[256], dS[256];
-  const std::int64_t iter = *iter_p;
-  for (int i = threadIdx.x; i < kGammaTab; i += blockDim.x) {
-    const double shape = a.alpha + static_cast<double>(i);
-    const bool boost = shape < 1.0;
-    const double aa = boost ? shape + 1.0 : shape;
-    const double d = aa - 1.0 / 3.0;
-    tab_d[i] = d;
-    tab_c[i] = 1.0 / sqrt(9.0 * d);
-    tab_inv[i] = boost ? 1.0 / shape : 0.0;
-  }
-  const std::uint64_t tkey = keyed(a.seed, kConjugate, static_cast<std::uint64_t>(a.var_theta),
-                                   static_cast<std::uint64_t>(iter));
-  const int j = threadIdx.x / tpd, t = threadIdx.x - (threadIdx.x / tpd) * tpd;
-  const std::int64_t m = static_cast<std::int64_t>(blockIdx.x) * dpb + j;
-  const bool active = j < dpb && m < a.Ml;
-  const int k0 = t * kThetaRun, k1 = active ? min(a.K, k0 + kThetaRun) : k0;
-#pragma unroll
-  for (int i = 0; i < kThetaRun; ++i) {
-    if (k0 + i < k1) {
-      int* c = a.nmk + m * a.K + k0 + i;
-      cnt_s[i][threadIdx.x] = *c;
-      *c = 0;  // consumed: the z-step accumulates the next sweep's counts here
-    }
-  }
-  __syncthreads();
-  const std::uint64_t mkey = fold(tkey, static_cast<std::uint64_t>(a.doc_base + m));
-  double sg = 0.0, mant = 1.0;
-  int ex = 0;
-  bool zero = false;
-  int k = k0;
-  bool fresh = true;
-  Stream r(0);
-  double d = 1.0, c = 1.0, inv = 0.0;
-  while (k < k1) {
-    if (fresh) {
-      const int n = cnt_s[k - k0][threadIdx.x];
-      r = Stream(fold(mkey, static_cast<std::uint64_t>(k)));
-      if (n < kGammaTab) {
-        d = tab_d[n];
-        c = tab_c[n];
-        inv = tab_inv[n];
-      } else {
-        const double shape = a.alpha + static_cast<double>(n);
-        d = shape - 1.0 / 3.0;
-        c = 1.0 / sqrt(9.0 * d);
-        inv = 0.0;
-      }
-      fresh = false;
-    }
-    const double x = r.next_gaussian();
-    double vv = 1.0 + c * x;
-    if (vv > 0.0) {
-      vv = vv * vv * vv;
-      const double u = r.next_unit();
-      bool acc = u < 1.0 - 0.0331 * (x * x) * (x * x);
-      if (!acc) acc = log(u) < 0.5 * x * x + d * (1.0 - vv + log(vv));
-      if (acc) {
-        double g = d * vv;
-        // the reference's boost g * pow(u, 1/shape) (dist.cpp:139-140) as exp(log(u) / shape):
-        // |log u / shape| <= 37 / shape, so the relative difference from a correctly
-        // rounded pow is <= ~2^-53 * 37 / shape (4e-14 at shape 0.1), far inside the 1e-12
-        // contract, and exp + log cost half of pow's double-double path (r01 v33: phi
-        // block 83 -> 77 us on NIPS)
-        if (inv != 0.0) g = g * boost_factor(r.next_unit(), a.pow_alpha, inv);
-        g_s[k - k0][threadIdx.x] = g;
-        sg += g;
-        if (g > 0.0) {
-          int e1, e2;
-          mant = frexp(mant * frexp(g, &e1), &e2);
-          ex += e1 + e2;
-        } else {
-          zero = true;
-        }
-        ++k;
-        fresh = true;
-      }
-    }
-  }
-  ps[threadIdx.x] = sg;
-  pl[threadIdx.x] = zero ? -INFINITY : log(mant) + static_cast<double>(ex) * 0.69314718055994530942;
-  __syncthreads();
-  if (active && t == 0) {  // document row sums, runs in topic order
-    double S = 0.0, L = 0.0;
-    for (int q = 0; q < tpd; ++q) {
-      S += ps[threadIdx.x + q];
-      L += pl[threadIdx.x + q];
-    }
-    dS[j] = S;
-    // sum log theta = sum log g - K log S;  sum theta = 1 by construction
-    const double lp = (a.alpha - 1.0) * (L - static_cast<double>(a.K) * log(S));
-    a.tpart[m] = (!(S > 0.0) || !isfinite(S)) ? -INFINITY : lp - a.theta_norm + a.theta_lgasum;
-  }
-  __syncthreads();
-  if (active) {
-    const double S = dS[j];
-    for (int kk = k0; kk < k1; ++kk) a.theta[m * a.K + kk] = g_s[kk - k0][threadIdx.x] / S;
   }
 }
 
@@ -1577,602 +1224,6 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
   }
 }
 
-// ---------------------------------------------------------------------------------
-// z block, two-level screen (experimental, BNMC_ZSCREEN_H=1): fp16 rows, then fp32, then fp64
-// ---------------------------------------------------------------------------------
-// The z-step moves one phi row per token from L2 (ncu r01: at the L2 read bandwidth),
-// so the row bytes set its time.  Level 1 reads the rows in fp16 (phiT16: 2 bytes per
-// candidate, half of phiT32) with theta/S in fp16 and FHFMA (fp16 x fp16 products,
-// exact in fp32, fp32 accumulation):
-//  * per-row scale c_v and per-document scale a_d (powers of two) put each row's and
-//    document's maximum in [2^14, 2^15) -- the draw does not depend on them (both
-//    scale every weight of the token alike);
-//  * error of every level-1 prefix / total / u * total against the exact scaled value:
-//    quantisation of both factors 2^-11 + 2^-11 relative (normal range) or 2^-25
-//    absolute per factor (fp16 subnormals), fp32 rounding <= 24 * 2^-24 relative, so
-//    <= 2^-9.9 * value + A with A = 2^-24 (32768 K + Theta_d), Theta_d = sum of the
-//    document's fp16 theta values (every fp16 value <= 2^15);
-//  * a token is decided when u * total lies >= mg1 = 2^-8.5 * uf + 4 A inside its
-//    candidate's interval (covers both boundaries' and uf's errors);
-//    otherwise it is queued for level 2 (q2).
-// Level 2 (zscreen_q_kernel) redraws the queued tokens with the fp32 transposed screen
-// (phiT32 rows, theta/S rows the level-1 units left in thS32) and queues what is still
-// ambiguous for the fp64 draw (zfallback_kernel).  The pick is the fp64 product-form
-// draw in every case.
-__host__ __device__ __forceinline__ int phys16(int k, int RH) {
-  const int c = k >> 4, j = k & 15, gl = c / RH, r = c - gl * RH;
-  return ((r << 2) + gl) * 16 + j;
-}
-
-__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
-  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
-  return c;
-}
-
-struct Oct16 {
-  unsigned v[8];  // 16 halves
-};
-
-__device__ __forceinline__ Oct16 ldg256h(const unsigned short* p) {
-  Oct16 o;
-  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=r"(o.v[0]), "=r"(o.v[1]), "=r"(o.v[2]), "=r"(o.v[3]), "=r"(o.v[4]), "=r"(o.v[5]), "=r"(o.v[6]),
-        "=r"(o.v[7])
-      : "l"(p));
-  return o;
-}
-
-// fp16 rows of the current phi numerator (phiT32 -> phiT16, row-scaled); warps w0,
-// w0 + nw, ... of the caller each take one row at a time.  K <= 128.
-__device__ void h16_rows(const LdaArgs& a, std::int64_t w0, std::int64_t nw) {
-  // lane L holds phiT32 physical columns 4L .. 4L + 3 (one coalesced 16-byte load per
-  // row; Kp32 <= 128); two rows per warp iteration
-  const int lane = threadIdx.x & 31;
-  const int p0 = 4 * lane;
-  int kl[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {  // logical candidate of physical column p0 + j (phys32 inverse)
-    const int p = p0 + j, c = p / a.CW32, jj = p - c * a.CW32, r = c / a.G32, gl = c - r * a.G32;
-    kl[j] = (gl * a.R32 + r) * a.CW32 + jj;
-  }
-  const bool mine = p0 < a.Kp32;
-  for (std::int64_t v0 = w0; v0 < a.V; v0 += 2 * nw) {
-    float4 x[2];
-    float mx[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const std::int64_t v = v0 + i * nw;
-      x[i] = (mine && v < a.V) ? *reinterpret_cast<const float4*>(a.phiT32 + static_cast<std::size_t>(v) * a.Kp32 + p0)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {  // (padding columns hold 0)
-      mx[i] = fmaxf(fmaxf(x[i].x, x[i].y), fmaxf(x[i].z, x[i].w));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const std::int64_t v = v0 + i * nw;
-      if (!mine || v >= a.V) continue;
-      const int e = mx[i] > 0.0f ? min(127, max(-126, 14 - ilogbf(mx[i]))) : 0;
-      const float sc = ldexpf(1.0f, e);
-      unsigned short* out = a.phiT16 + static_cast<std::size_t>(v) * a.Kp16;
-      const float xv[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (kl[j] < a.K) out[phys16(kl[j], a.RH)] = __half_as_ushort(__float2half_rn(xv[j] * sc));
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) phi_h16_kernel(LdaArgs a) {
-  const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
-  h16_rows(a, static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5), nw);
-}
-
-// max / sum over a unit's team (a warp for warp units, the CTA otherwise)
-template <bool WU>
-__device__ __forceinline__ float team_max(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if constexpr (WU) return v;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  v = lane < nw ? red[lane] : 0.0f;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-template <bool WU>
-__device__ __forceinline__ float team_sum(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if constexpr (WU) return v;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  v = lane < nw ? red[lane] : 0.0f;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-constexpr float kL1Rel = 0.0027622f;  // level-1 margin relative to u * total (>= 2^-8.5)
-
-// Level 1.  RH: 16-candidate rounds per lane (K <= 64 * RH); units as zscreen_t_kernel.
-// Shared memory per team: thh [4][16 RH + 8] halves (fp16 theta/S * a_d), csum
-// [warps][32][16] floats, cnt [K] ints, red [32] floats.
-template <int RH, bool WU>
-__global__ void __launch_bounds__(kZThreads, 3) zscreen_h_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  constexpr int G = 4, KLH = 16 * RH, KLHP = KLH + 8, C = G * RH;
-  static_assert(C <= 16, "csum rows hold 16 chunk sums");
-  const int kWarps = blockDim.x >> 5;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G;
-  const int warp = threadIdx.x >> 5;
-  const int kpad = (a.K + 3) & ~3;
-  // team area: [thh G*KLHP halves][csum][cnt kpad][red 32]
-  const std::size_t team_floats = G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16) + kpad + 32;
-  float* base = reinterpret_cast<float*>(smem_raw) + (WU ? warp * team_floats : 0);
-  unsigned short* thh = reinterpret_cast<unsigned short*>(base);
-  float* csum = base + G * KLHP / 2 + (WU ? 0 : warp * 32 * 16);
-  int* cnt_s = reinterpret_cast<int*>(base + G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16));
-  float* red = base + G * KLHP / 2 + (WU ? 32 * 16 : kWarps * 32 * 16) + kpad;
-  pdl_wait();
-  pdl_trigger();
-  const std::int64_t iter = *iter_p;
-  const int rl = min(RH, max(0, (a.K - gl * KLH + 15) / 16));
-  const int tid_u = WU ? lane : static_cast<int>(threadIdx.x);
-  const int nthr_u = WU ? 32 : static_cast<int>(blockDim.x);
-  const std::int64_t nunits = WU ? a.n_wunits : a.n_units;
-  const std::int64_t* units = WU ? a.wunits : a.units;
-  const std::int64_t ustart = WU ? static_cast<std::int64_t>(blockIdx.x) * kWarps + warp : blockIdx.x;
-  const std::int64_t ustride = WU ? static_cast<std::int64_t>(gridDim.x) * kWarps : gridDim.x;
-  const int K8 = (a.K + 7) & ~7;
-
-  for (std::int64_t unit = ustart; unit < nunits; unit += ustride) {
-    const std::int64_t m = units[unit * 3], t0 = units[unit * 3 + 1], t1 = units[unit * 3 + 2];
-    const double* thg = a.theta + m * a.K;
-    float* ths = a.thS32 + m * K8;  // theta/S in fp32 for level 2 (natural order, zero-padded)
-    // theta/S (fp32) and its maximum; the document scale a_d; fp16 operands and Theta_d
-    float mx = 0.0f;
-    for (int k = tid_u; k < G * KLH; k += nthr_u) {
-      const float x = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
-      if (k < K8) ths[k] = x;
-      mx = fmaxf(mx, x);
-      if (k < a.K) cnt_s[k] = 0;
-    }
-    mx = team_max<WU>(mx, red);
-    const float ad = ldexpf(1.0f, mx > 0.0f ? min(127, max(-126, 14 - ilogbf(mx))) : 0);
-    float th_sum = 0.0f;
-    for (int k = tid_u; k < G * KLH; k += nthr_u) {
-      const float x = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
-      const __half h = __float2half_rn(x * ad);
-      thh[(k / KLH) * KLHP + k % KLH] = __half_as_ushort(h);
-      th_sum += __half2float(h);
-    }
-    th_sum = team_sum<WU>(th_sum, red);
-    const float A = 0x1p-24f * (32768.0f * static_cast<float>(a.K) + th_sum);
-    if constexpr (WU) __syncwarp();
-    else __syncthreads();
-    unsigned tw[KLH / 2];
-#pragma unroll
-    for (int i = 0; i < KLH / 2; i += 4) {
-      const uint4 t = *reinterpret_cast<const uint4*>(thh + gl * KLHP + 2 * i);
-      tw[i] = t.x, tw[i + 1] = t.y, tw[i + 2] = t.z, tw[i + 3] = t.w;
-    }
-    const std::int64_t bstep = WU ? 32 : kWarps * 32;
-    std::int64_t b0 = t0 + (WU ? 0 : warp * 32);
-    int wl_next = b0 + lane < t1 ? __ldg(a.w + b0 + lane) : 0;
-    for (; b0 < t1; b0 += bstep) {
-      const std::int64_t t = b0 + lane;
-      const bool valid = t < t1;
-      const int wl = wl_next;
-      wl_next = b0 + bstep + lane < t1 ? __ldg(a.w + b0 + bstep + lane) : 0;  // next batch, in flight
-      // (1) level-1 chunk sums: 4 lanes per token, 16 candidates per round; the rows of
-      // sub-batch s + 1 are in flight while sub-batch s is summed
-      const std::int64_t left = (t1 - b0 + 7) / 8;
-      const int nsub = left < 4 ? static_cast<int>(left) : 4;  // warp-uniform
-      Oct16 cur[RH], nxt[RH];
-      auto fetch = [&](int s2, Oct16 (&ph)[RH]) {
-        const int wv = __shfl_sync(0xffffffffu, wl, s2 * 8 + gid);
-        const unsigned short* row = a.phiT16 + static_cast<std::size_t>(wv) * a.Kp16;
-#pragma unroll
-        for (int r = 0; r < RH; ++r) {
-          if (r < rl) ph[r] = ldg256h(row + 16 * (r * G + gl));
-          else ph[r] = Oct16{};
-        }
-      };
-      fetch(0, cur);
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        if (s >= nsub) break;  // warp-uniform
-        if (s + 1 < nsub) fetch(s + 1, nxt);
-        const int src = s * 8 + gid;
-#pragma unroll
-        for (int r = 0; r < RH; ++r) {
-          float sr = 0.0f;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            sr = fhfma(static_cast<unsigned short>(tw[8 * r + j] & 0xffffu), static_cast<unsigned short>(cur[r].v[j] & 0xffffu), sr);
-            sr = fhfma(static_cast<unsigned short>(tw[8 * r + j] >> 16), static_cast<unsigned short>(cur[r].v[j] >> 16), sr);
-          }
-          csum[cs_idx(src, gl * RH + r)] = sr;
-        }
-#pragma unroll
-        for (int r = 0; r < RH; ++r) cur[r] = nxt[r];
-      }
-      __syncwarp();
-      // (2) search: lane = token
-      if (valid) {
-        Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
-                        static_cast<std::uint64_t>(iter)));
-        const float u01 = static_cast<float>(rng.next_unit());
-        float P[C];
-        float run = 0.0f;
-#pragma unroll
-        for (int c = 0; c < C; c += 4) {
-          const float4 y = *reinterpret_cast<const float4*>(csum + cs_idx(lane, c));
-          run += y.x;
-          P[c] = run;
-          run += y.y;
-          P[c + 1] = run;
-          run += y.z;
-          P[c + 2] = run;
-          run += y.w;
-          P[c + 3] = run;
-        }
-        const float total = run;
-        const float uf = u01 * total;
-        const float mg = kL1Rel * uf + 4.0f * A;
-        int k = -1;
-        if (uf < total && total < 0x1p100f) {
-          int cs = C - 1;
-          float lo = 0.0f;
-#pragma unroll
-          for (int c = C - 1; c >= 0; --c)
-            if (uf < P[c]) cs = c;
-#pragma unroll
-          for (int c = 0; c < C - 1; ++c)
-            if (c < cs) lo = P[c];
-          const int og = cs / RH, orr = cs - og * RH;
-          const Oct16 p = ldg256h(a.phiT16 + static_cast<std::size_t>(wl) * a.Kp16 + 16 * (orr * G + og));
-          const uint4 y0 = *reinterpret_cast<const uint4*>(thh + og * KLHP + 16 * orr);
-          const uint4 y1 = *reinterpret_cast<const uint4*>(thh + og * KLHP + 16 * orr + 8);
-          const unsigned tv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-          float acc = lo, prev = lo;
-          int j = -1;
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const unsigned ta = tv[jj >> 1], pa = p.v[jj >> 1];
-            const float nx = fhfma(static_cast<unsigned short>((jj & 1) ? ta >> 16 : ta & 0xffffu),
-                                   static_cast<unsigned short>((jj & 1) ? pa >> 16 : pa & 0xffffu), acc);
-            if (j < 0) {
-              if (uf < nx) {
-                j = jj;
-                prev = acc;
-              }
-              acc = nx;
-            }
-          }
-          const int kk = 16 * cs + j;
-          if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
-        }
-        if (k >= 0) {
-          a.z[t] = k;
-          atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
-          atomicAdd(&cnt_s[k], 1);
-        } else {
-          const int slot = atomicAdd(a.q2_len, 1);  // level 2 (zscreen_q_kernel)
-          a.q2[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
-        }
-      }
-      __syncwarp();
-    }
-    if constexpr (WU) __syncwarp();
-    else __syncthreads();
-    for (int k = tid_u; k < a.K; k += nthr_u) {
-      const int n = cnt_s[k];
-      if (n) atomicAdd(&a.nmk[m * a.K + k], n);
-    }
-  }
-}
-
-// Level 2: the fp32 transposed screen (zscreen_t_kernel's arithmetic and margin) over
-// the level-1 queue.  Each token brings its own document: the theta/S operands come
-// from thS32 (written by the level-1 unit), counts go straight to nmk.  R: rounds of
-// the phiT32 layout (G = 4 x CW = 8).
-template <int R>
-__global__ void __launch_bounds__(256) zscreen_q_kernel(LdaArgs a, const std::int64_t* iter_p) {
-  constexpr int G = 4, CW = 8, C = G * R;
-  __shared__ __align__(16) float csum_all[8][32 * 16];
-  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gid = lane / G, warp = threadIdx.x >> 5;
-  float* csum = csum_all[warp];
-  pdl_wait();
-  pdl_trigger();
-  const std::int64_t iter = *iter_p;
-  const int n = *a.q2_len;
-  const int K8 = (a.K + 7) & ~7;
-  const int rl = min(R, max(0, (a.K - gl * CW * R + CW - 1) / CW));
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  for (int b0 = (blockIdx.x * (blockDim.x >> 5) + warp) * 32; b0 < n; b0 += nwarps * 32) {
-    const int i = b0 + lane;
-    const bool valid = i < n;
-    const int2 q = valid ? a.q2[i] : make_int2(0, 0);
-    const int wl = valid ? __ldg(a.w + q.x) : 0;
-#pragma unroll 1
-    for (int s = 0; s < 4; ++s) {
-      if (b0 + s * 8 >= n) break;  // warp-uniform
-      const int src = s * 8 + gid;
-      const int wv = __shfl_sync(0xffffffffu, wl, src);
-      const int mv = __shfl_sync(0xffffffffu, q.y, src);
-      const float* row = a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
-      const float* th = a.thS32 + static_cast<std::size_t>(mv) * K8;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float sr = 0.0f;
-        if (r < rl) {
-          const Oct p = ldg256f(row + CW * (r * G + gl));
-          const int k0 = CW * (gl * R + r);  // logical candidates of this chunk
-          const float4 x0 = *reinterpret_cast<const float4*>(th + k0);
-          const float4 x1 = *reinterpret_cast<const float4*>(th + k0 + 4);
-          const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-          sr = x[0] * p.v[0];
-#pragma unroll
-          for (int j = 1; j < CW; ++j) sr = __fmaf_rn(x[j], p.v[j], sr);
-        }
-        csum[cs_idx(src, gl * R + r)] = sr;
-      }
-    }
-    __syncwarp();
-    if (valid) {
-      const std::int64_t t = q.x, m = q.y;
-      Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
-                      static_cast<std::uint64_t>(iter)));
-      const float u01 = static_cast<float>(rng.next_unit());
-      float P[C];
-      float run = 0.0f;
-#pragma unroll
-      for (int c = 0; c < C; c += 4) {
-        const float4 y = *reinterpret_cast<const float4*>(csum + cs_idx(lane, c));
-        run += y.x;
-        P[c] = run;
-        run += y.y;
-        P[c + 1] = run;
-        run += y.z;
-        P[c + 2] = run;
-        run += y.w;
-        P[c + 3] = run;
-      }
-      const float total = run;
-      const float uf = u01 * total;
-      const float mg = a.screen_margin * total;
-      int k = -1;
-      if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
-        int cs = C - 1;
-        float lo = 0.0f;
-#pragma unroll
-        for (int c = C - 1; c >= 0; --c)
-          if (uf < P[c]) cs = c;
-#pragma unroll
-        for (int c = 0; c < C - 1; ++c)
-          if (c < cs) lo = P[c];
-        const int og = cs / R, orr = cs - og * R;
-        const Oct p = ldg256f(a.phiT32 + static_cast<std::size_t>(wl) * a.Kp32 + CW * (orr * G + og));
-        const float* th = a.thS32 + static_cast<std::size_t>(m) * K8 + CW * cs;
-        const float4 y0 = *reinterpret_cast<const float4*>(th);
-        const float4 y1 = *reinterpret_cast<const float4*>(th + 4);
-        const float tv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-        float acc = lo, prev = lo;
-        int j = -1;
-#pragma unroll
-        for (int jj = 0; jj < CW; ++jj) {
-          const float nx = __fmaf_rn(tv[jj], p.v[jj], acc);
-          if (j < 0) {
-            if (uf < nx) {
-              j = jj;
-              prev = acc;
-            }
-            acc = nx;
-          }
-        }
-        const int kk = CW * cs + j;
-        if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
-      }
-      if (k >= 0) {
-        a.z[t] = k;
-        atomicAdd(&a.nkw[static_cast<std::size_t>(wl) * a.Kp + k], 1);
-        atomicAdd(&a.nmk[m * a.K + k], 1);
-      } else {
-        const int slot = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
-        a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// ---------------------------------------------------------------------------------
-// z block, TMA-staged screen (experimental, BNMC_ZSTAGE=1; slower, see choose_screen)
-// ---------------------------------------------------------------------------------
-// ncu r01 v15 (zscreen_t): every warp serialised ~5 L2 round trips per 32-token batch
-// (4 sub-batch row fetches + the rescan re-fetch, which missed L1) and register
-// double-buffering could not hold enough rows in flight.  Here the phi rows go
-// global -> shared by the bulk-copy engine (cp.async.bulk, completion on an
-// mbarrier), NS batches ahead per warp, with no register cost:
-//  * work = batches of <= 32 consecutive tokens of one document; warp g of the
-//    persistent grid owns a contiguous range of batches;
-//  * lane j issues the 16*KQ-byte bulk copy of token j's phiT32 row (natural topic
-//    order, fp32) into the warp's slot; lane 0 arms the slot's mbarrier with the
-//    batch's byte count;
-//  * compute is lane-per-token from shared memory: K products theta/S * g in
-//    16-byte granules, running prefix in registers, u * total, the crossing granule,
-//    the in-granule scan (all from shared memory: no re-fetch), the margin check,
-//    z and the count atomics -- no shuffles;
-//  * theta/S of the warp's current document sits in shared memory (fp32), reloaded
-//    when the batch's document changes.
-// Same screen / fp64-fallback contract as zscreen_kernel.
-struct ZBatch {
-  std::int64_t t0;
-  int m, n;
-};
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "ZW_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra ZW_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int KQ>
-__global__ void __launch_bounds__(256) zstage_kernel(LdaArgs a, const std::int64_t* iter_p, const ZBatch* batches,
-                                                     std::int64_t nbatch, int ns, int stride16) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const unsigned row_bytes = 16u * KQ;
-  const std::size_t slot_bytes = static_cast<std::size_t>(32) * stride16 * 16;
-  // CTA area: S (fp64, K).  Warp area: bars[ns], w[ns][32], theta/S[4KQ], rows[ns].
-  double* Ssm = reinterpret_cast<double*>(smem_raw);
-  const std::size_t cta_bytes = (static_cast<std::size_t>(a.K) * 8 + 127) / 128 * 128;
-  const std::size_t warp_hdr = (static_cast<std::size_t>(ns) * (16 + 128) + 16 * KQ + 127) / 128 * 128;
-  unsigned char* wbase = smem_raw + cta_bytes + warp * (warp_hdr + ns * slot_bytes);
-  std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(wbase);
-  int* wsm = reinterpret_cast<int*>(wbase + 16 * ns);
-  float* th = reinterpret_cast<float*>(wbase + 16 * ns + 128 * ns);
-  unsigned char* rows = wbase + warp_hdr;
-
-  for (int k = threadIdx.x; k < a.K; k += blockDim.x) Ssm[k] = a.S[k];
-  if (lane == 0)
-    for (int i = 0; i < ns; ++i) mbar_init(bar + i, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-
-  const std::int64_t iter = *iter_p;
-  const std::int64_t tw = static_cast<std::int64_t>(gridDim.x) * nw;
-  const std::int64_t g = static_cast<std::int64_t>(blockIdx.x) * nw + warp;
-  const std::int64_t b_first = nbatch * g / tw, b_last = nbatch * (g + 1) / tw;
-  const std::int64_t count = b_last - b_first;
-
-  auto issue = [&](std::int64_t c, int slot) {
-    const ZBatch zb = batches[b_first + c];
-    const int wv = lane < zb.n ? __ldg(a.w + zb.t0 + lane) : 0;
-    wsm[slot * 32 + lane] = wv;
-    if (lane == 0) mbar_expect_tx(bar + slot, row_bytes * static_cast<unsigned>(zb.n));
-    __syncwarp();
-    if (lane < zb.n)
-      bulk_g2s(rows + slot * slot_bytes + static_cast<std::size_t>(lane) * stride16 * 16,
-               a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32, row_bytes, bar + slot);
-  };
-  for (std::int64_t c = 0; c < count && c < ns; ++c) issue(c, static_cast<int>(c));
-
-  int curm = -1;
-  for (std::int64_t c = 0; c < count; ++c) {
-    const int slot = static_cast<int>(c % ns);
-    const unsigned parity = static_cast<unsigned>((c / ns) & 1);
-    const ZBatch zb = batches[b_first + c];
-    if (zb.m != curm) {
-      __syncwarp();
-      const double* thg = a.theta + static_cast<std::int64_t>(zb.m) * a.K;
-      for (int k = lane; k < 4 * KQ; k += 32) th[k] = k < a.K ? static_cast<float>(thg[k] / Ssm[k]) : 0.0f;
-      curm = zb.m;
-      __syncwarp();
-    }
-    mbar_wait(bar + slot, parity);
-    if (lane < zb.n) {
-      const std::int64_t t = zb.t0 + lane;
-      const int wv = wsm[slot * 32 + lane];
-      const float* row = reinterpret_cast<const float*>(rows + slot * slot_bytes + static_cast<std::size_t>(lane) * stride16 * 16);
-      Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)), static_cast<std::uint64_t>(iter)));
-      const float u01 = static_cast<float>(rng.next_unit());
-      float P[KQ];
-      float run = 0.0f;
-#pragma unroll
-      for (int q = 0; q < KQ; ++q) {
-        const float4 f = *reinterpret_cast<const float4*>(row + 4 * q);
-        const float4 x = *reinterpret_cast<const float4*>(th + 4 * q);
-        float sq = x.x * f.x;
-        sq = __fmaf_rn(x.y, f.y, sq);
-        sq = __fmaf_rn(x.z, f.z, sq);
-        sq = __fmaf_rn(x.w, f.w, sq);
-        run += sq;
-        P[q] = run;
-      }
-      const float total = run;
-      const float uf = u01 * total;
-      const float mg = a.screen_margin * total;
-      int k = -1;
-      if (uf < total && total > 0x1p-90f && total < 0x1p100f) {
-        int cs = KQ - 1;
-        float lo = 0.0f;
-#pragma unroll
-        for (int q = KQ - 1; q >= 0; --q)
-          if (uf < P[q]) cs = q;
-#pragma unroll
-        for (int q = 0; q < KQ - 1; ++q)
-          if (q < cs) lo = P[q];
-        const float4 f = *reinterpret_cast<const float4*>(row + 4 * cs);
-        const float4 x = *reinterpret_cast<const float4*>(th + 4 * cs);
-        const float fv[4] = {f.x, f.y, f.z, f.w};
-        const float xv[4] = {x.x, x.y, x.z, x.w};
-        float acc = lo, prev = lo;
-        int j = -1;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const float nx = __fmaf_rn(xv[jj], fv[jj], acc);
-          if (j < 0) {
-            if (uf < nx) {
-              j = jj;
-              prev = acc;
-            }
-            acc = nx;
-          }
-        }
-        const int kk = 4 * cs + j;
-        if (j >= 0 && kk < a.K && uf - prev >= mg && acc - uf >= mg) k = kk;
-      }
-      if (k >= 0) {
-        a.z[t] = k;
-        atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
-        atomicAdd(&a.nmk[static_cast<std::int64_t>(zb.m) * a.K + k], 1);
-      } else {
-        const int slotq = atomicAdd(a.fq_len, 1);  // fp64 redraw (zfallback_kernel)
-        a.fq[slotq] = make_int2(static_cast<int>(t), zb.m);
-      }
-    }
-    __syncwarp();
-    // the slot's generic reads are done: order them before the next bulk write into it
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (c + ns < count) issue(c + ns, slot);
-  }
-}
-
 // fp64 product-form draw for the tokens the screen could not decide (~2K * 2^-16
 // of them): one warp per queued token.  Lane l owns the contiguous candidates
 // [l*c, (l+1)*c), c = ceil(K/32); warp scan of the lane sums, the owner rescans
@@ -2396,50 +1447,86 @@ __device__ __forceinline__ void loglik_finish(const LdaArgs& a, const Outputs& o
 // kernel is bound by its launch and last-block tail, not its loads)
 constexpr int kWU = 2;
 
+// Counted-cell terms n (log x - s) of one warp iteration: each lane holds S slots
+// (n = 0: nothing to add); the nonzero slots are compacted through a per-warp shared
+// buffer (warp prefix scan of the lanes' counts) and the logs then run at full warp
+// width -- ~40 % of the NIPS cells are counted, and per-slot `if (n) log(...)` blocks
+// ran every log pass for ~10 of 32 lanes (ncu r02: 60 % of wterm's instructions).
+// Item order depends only on the data: the sum is deterministic.
+template <int S>
+__device__ __forceinline__ double counted_log_terms(const int (&nn)[S], const double (&xx)[S], const double (&ss)[S],
+                                                    int* bn, double* bx, double* bs) {
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) cnt += nn[i] != 0;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int p = incl - cnt;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    if (nn[i]) {
+      bn[p] = nn[i];
+      bx[p] = xx[i];
+      bs[p] = ss[i];
+      ++p;
+    }
+  }
+  __syncwarp();
+  double acc = 0.0;
+  for (int i = lane; i < total; i += 32) acc += static_cast<double>(bn[i]) * (log(bx[i]) - bs[i]);  // log(0) = -inf
+  __syncwarp();
+  return acc;
+}
+
 template <bool FINAL>
 __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int advance) {
   __shared__ double scratch[4 * 32];
+  __shared__ int cb_n[8][32 * 4 * kWU];
+  __shared__ double cb_x[8][32 * 4 * kWU], cb_s[8][32 * 4 * kWU];
   pdl_wait();
+  const int wib = threadIdx.x >> 5;
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   const std::int64_t g0 = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   // w-factor over the topic-word cells, static cell -> thread assignment (deterministic).
   // The padded [V][Kp] arrays are read as 4-cell vectors (Kp % 4 == 0: a vector never
   // crosses a row; padding cells have n = 0 and logS is zero-padded to Kp), two vectors
-  // per thread in flight; no per-cell index arithmetic beyond one modulo per vector.
+  // per thread in flight; the counted cells' logs compacted per warp.
   double accw = 0.0;
   if (a.logg_valid) {
     const std::int64_t nvec = static_cast<std::int64_t>(a.V) * a.Kp / 4;
     const bool narrow = nvec < (std::int64_t{1} << 29);  // 4 * nvec fits 31 bits
     const int4* n4 = reinterpret_cast<const int4*>(a.nkw);
-    // log g stored per cell (v2 phi block), or taken here from g = phiT for the
-    // counted cells only (warp-pool phi block: a.logg == nullptr)
-    const bool take_log = a.logg == nullptr;
-    const double2* l2 = reinterpret_cast<const double2*>(take_log ? a.phiT : a.logg);
-    for (std::int64_t c0 = g0; c0 < nvec; c0 += kWU * stride) {
-      int4 n[kWU];
-      double2 la[kWU], lb[kWU];
+    const double2* l2 = reinterpret_cast<const double2*>(a.phiT);  // g (the pool stores g, not log g)
+    for (std::int64_t c0 = g0; __any_sync(0xffffffffu, c0 < nvec); c0 += kWU * stride) {
+      int nn[4 * kWU];
+      double xx[4 * kWU], ss[4 * kWU];
 #pragma unroll
       for (int j = 0; j < kWU; ++j) {
         const std::int64_t c = c0 + j * stride;
-        n[j] = make_int4(0, 0, 0, 0);
+        int4 n = make_int4(0, 0, 0, 0);
+        double2 la = make_double2(1.0, 1.0), lb = make_double2(1.0, 1.0);
         if (c < nvec) {
-          n[j] = n4[c];
-          la[j] = l2[2 * c];
-          lb[j] = l2[2 * c + 1];
+          n = n4[c];
+          la = l2[2 * c];
+          lb = l2[2 * c + 1];
         }
-      }
+        const int k0 = c >= nvec ? 0
+                       : narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
+                                : static_cast<int>((4 * c) % a.Kp);
+        nn[4 * j] = n.x, nn[4 * j + 1] = n.y, nn[4 * j + 2] = n.z, nn[4 * j + 3] = n.w;
+        xx[4 * j] = la.x, xx[4 * j + 1] = la.y, xx[4 * j + 2] = lb.x, xx[4 * j + 3] = lb.y;
+        // (logS loaded unconditionally -- padded to Kp -- so its load issues with n's
+        // instead of after it)
 #pragma unroll
-      for (int j = 0; j < kWU; ++j) {  // log phi = log g - log S
-        const std::int64_t c = c0 + j * stride;
-        if (c >= nvec || (n[j].x | n[j].y | n[j].z | n[j].w) == 0) continue;
-        const int k0 = narrow ? static_cast<int>(static_cast<unsigned>(4 * c) % static_cast<unsigned>(a.Kp))
-                              : static_cast<int>((4 * c) % a.Kp);
-        auto lg = [take_log](double x) { return take_log ? log(x) : x; };  // log(0) = -inf
-        if (n[j].x) accw += static_cast<double>(n[j].x) * (lg(la[j].x) - __ldg(&a.logS[k0]));
-        if (n[j].y) accw += static_cast<double>(n[j].y) * (lg(la[j].y) - __ldg(&a.logS[k0 + 1]));
-        if (n[j].z) accw += static_cast<double>(n[j].z) * (lg(lb[j].x) - __ldg(&a.logS[k0 + 2]));
-        if (n[j].w) accw += static_cast<double>(n[j].w) * (lg(lb[j].y) - __ldg(&a.logS[k0 + 3]));
+        for (int q = 0; q < 4; ++q) ss[4 * j + q] = __ldg(&a.logS[k0 + q]);
       }
+      accw += counted_log_terms<4 * kWU>(nn, xx, ss, cb_n[wib], cb_x[wib], cb_s[wib]);  // log phi = log g - log S
     }
   } else {
     for (std::int64_t c = g0; c < static_cast<std::int64_t>(a.V) * a.K; c += stride) {
@@ -2454,23 +1541,28 @@ __global__ void __launch_bounds__(256, 4) wterm_kernel(LdaArgs a, Outputs o, int
     }
   }
   // z-factor over the doc-topic cells: the flat [Ml][K] arrays as 4-cell vectors
-  // (cudaMalloc bases are 256-byte aligned), the ragged tail scalar
+  // (cudaMalloc bases are 256-byte aligned), counted cells compacted as above, the
+  // ragged tail scalar
   double accz = 0.0;
   const std::int64_t ncz = a.Ml * a.K, nvz = ncz / 4;
   const int4* m4 = reinterpret_cast<const int4*>(a.nmk);
   const double2* t2 = reinterpret_cast<const double2*>(a.theta);
-  auto zterm = [](int n, double x) {
-    return n ? static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY) : 0.0;
-  };
-  for (std::int64_t c = g0; c < nvz; c += stride) {
-    const int4 n = m4[c];
-    const double2 x = t2[2 * c], y = t2[2 * c + 1];
-    accz += zterm(n.x, x.x);
-    accz += zterm(n.y, x.y);
-    accz += zterm(n.z, y.x);
-    accz += zterm(n.w, y.y);
+  for (std::int64_t c = g0; __any_sync(0xffffffffu, c < nvz); c += stride) {
+    int nn[4] = {0, 0, 0, 0};
+    double xx[4] = {1.0, 1.0, 1.0, 1.0}, ss[4] = {0.0, 0.0, 0.0, 0.0};
+    if (c < nvz) {
+      const int4 n = m4[c];
+      const double2 x = t2[2 * c], y = t2[2 * c + 1];
+      nn[0] = n.x, nn[1] = n.y, nn[2] = n.z, nn[3] = n.w;
+      xx[0] = x.x, xx[1] = x.y, xx[2] = y.x, xx[3] = y.y;
+    }
+    accz += counted_log_terms<4>(nn, xx, ss, cb_n[wib], cb_x[wib], cb_s[wib]);
   }
-  if (g0 < ncz - 4 * nvz) accz += zterm(a.nmk[4 * nvz + g0], a.theta[4 * nvz + g0]);
+  if (g0 < ncz - 4 * nvz) {
+    const int n = a.nmk[4 * nvz + g0];
+    const double x = a.theta[4 * nvz + g0];
+    if (n) accz += static_cast<double>(n) * (x > 0.0 ? log(x) : -INFINITY);
+  }
   // the theta factor's per-document pieces, spread over the grid (single-rank path:
   // the last block then reads nbw partials instead of Ml)
   double acct = 0.0;
@@ -2816,7 +1908,6 @@ class Lda final : public Model {
     const std::int64_t target_blocks = 148 * 16;
     rows_per_block_ = static_cast<int>(std::max<std::int64_t>(1, (V_ + target_blocks - 1) / target_blocks));
     nb_phi_ = (V_ + rows_per_block_ - 1) / rows_per_block_;
-    theta_threads_ = std::min(256, ((K_ + 31) / 32) * 32);
 
     // z-step work units: chunks of <= kChunk tokens of one document (whole documents
     // up to kChunk: one theta setup per document).  The transposed z-step's CTA has
@@ -2862,35 +1953,7 @@ class Lda final : public Model {
     screen_ = !exact_ && !(sc && std::string(sc) == "0");
     choose_screen();
     Kp32_ = CW32_ * G32_ * RS_;
-    if (stage_ && screen_) {
-      std::vector<ZBatch> hb;
-      for (std::int64_t m = 0; m < Ml_; ++m)
-        for (std::int64_t t = off_host_[m]; t < off_host_[m + 1]; t += 32)
-          hb.push_back(ZBatch{t, static_cast<int>(m), static_cast<int>(std::min<std::int64_t>(32, off_host_[m + 1] - t))});
-      nbatch_ = static_cast<std::int64_t>(hb.size());
-      batches_.alloc(std::max<std::size_t>(hb.size(), 1));
-      if (!hb.empty())
-        BNMC_CUDA(cudaMemcpy(batches_.p, hb.data(), sizeof(ZBatch) * hb.size(), cudaMemcpyHostToDevice));
-      plan_stage();
-    }
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
-    // two-level screen (fp16 rows, then fp32): experimental, BNMC_ZSCREEN_H=1.  Measured
-    // slower (r01, NIPS): level 1 takes 79 us against the fp32 screen's 85 us -- half the
-    // row bytes, but the kernel is bound by its per-batch latency chain, not bytes --
-    // and level 2 (4.6 % of the tokens, one latency chain per scattered batch) plus
-    // the row conversion add ~24 us.
-    const char* zh = std::getenv("BNMC_ZSCREEN_H");
-    h16_ = screen_ && transposed_ && !stage_ && K_ <= 128 && zh && std::string(zh) == "1";
-    if (h16_) {
-      RH_ = (K_ + 63) / 64;
-      Kp16_ = 64 * RH_;
-      phiT16_.alloc(static_cast<std::size_t>(V_) * Kp16_);
-      thS32_.alloc(static_cast<std::size_t>(std::max<std::int64_t>(Ml_, 1)) * ((K_ + 7) & ~7));
-      q2_.alloc(std::max<std::int64_t>(Nl_, 1));
-      q2_len_.alloc(1);
-      const int gx = (K_ + 31) / 32;
-      h16_blocks_ = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((V_ + 8 * gx - 1) / (8 * gx), 296 / gx)));
-    }
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
@@ -2906,48 +1969,20 @@ class Lda final : public Model {
     fq_len_.alloc(1);
     wpart_.alloc(nbw_);
     ttpart_.alloc(nbw_);
-    colpart_.alloc(static_cast<std::size_t>(nb_phi_) * K_);
     {
+      // warp-pool conjugate block: a persistent grid (one resident wave), equal cell
+      // ranges per warp
       int dev = 0, sms = 148, per_sm = 1;
       BNMC_CUDA(cudaGetDevice(&dev));
       BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const char* pe = std::getenv("BNMC_PHI_POOL");
-      const char* pv1 = std::getenv("BNMC_PHI_V1");
-      const char* tv1 = std::getenv("BNMC_THETA_V1");
-      pool_ = !(pe && std::string(pe) == "0") && !(pv1 && std::string(pv1) == "1") &&
-              !(tv1 && std::string(tv1) == "1");
-      if (pool_) {
-        // warp-pool phi block: a persistent grid (one resident wave), equal cell ranges
-        // per warp; the column sums read phiT rows (nvb_ = V rows for phi_colsum2<true>)
-        if (K_ <= kPoolCells)
-          BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<true>, 256, 0));
-        else
-          BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<false>, 256, 0));
-        pool_blocks_ = sms * std::max(per_sm, 1);
-        phi_rows_ = 1;
-      } else {
-        // rows per thread L = 4 (measured r01 v29: NIPS 82 us at L=4 vs 92 at 8; KOS 38 us
-        // vs 42 at 1); 2 when 4 leaves the GPU under one wave (KOS phi 35.3 -> 32.2 us)
-        phi_rows_ = 4;
-        BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0));
-        const std::int64_t blocks4 = ((V_ + 3) / 4 * K_ + 255) / 256;
-        if (blocks4 < static_cast<std::int64_t>(sms) * std::max(per_sm, 1)) phi_rows_ = 2;
-        if (const char* e = std::getenv("BNMC_PHI_ROWS")) {
-          const int r = std::atoi(e);
-          if (r == 1 || r == 2 || r == 4 || r == 8) phi_rows_ = r;
-        }
-        switch (phi_rows_) {
-          case 1: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<1>, 256, 0)); break;
-          case 2: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<2>, 256, 0)); break;
-          case 4: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<4>, 256, 0)); break;
-          default: BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_gamma2_kernel<8>, 256, 0)); break;
-        }
-        phi_pf_ = static_cast<int>(0.7 * sms * std::max(per_sm, 1));  // measured: 0.55-0.8 of a wave best
-        if (const char* e = std::getenv("BNMC_PHI_PREFETCH")) phi_pf_ = std::max(0, std::atoi(e));
-      }
+      if (K_ <= kPoolCells)
+        BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<true>, 256, 0));
+      else
+        BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<false>, 256, 0));
+      pool_blocks_ = sms * std::max(per_sm, 1);
     }
-    nvb_ = (V_ + phi_rows_ - 1) / phi_rows_;
-    col_stripes_ = static_cast<int>(std::min<std::int64_t>(pool_ ? kColStripes : 64, std::max<std::int64_t>(4, nvb_ / (pool_ ? 48 : 96))));
+    // column-sum stripes of ~48 rows (<= 128), theta-row blocks of 8 warps (one row each)
+    col_stripes_ = static_cast<int>(std::min<std::int64_t>(kColStripes, std::max<std::int64_t>(4, V_ / 48)));
     {
       const std::int64_t gx = (K_ + 31) / 32, wblocks = (Ml_ + 7) / 8;
       trow_blocks_ = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((wblocks + gx - 1) / gx, 16384)));
@@ -2956,11 +1991,8 @@ class Lda final : public Model {
     spart_.alloc(static_cast<std::size_t>(kColStripes) * K_ * 2);
     ticket_.alloc((K_ + 31) / 32 + 1);
     ticket_.zero(nullptr);
-    if (!pool_) gpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
-    if (!pool_) logg_.alloc(static_cast<std::size_t>(V_) * Kp_);  // the pool kernel keeps no per-cell log
     logS_.alloc(Kp_);
     logS_.zero(nullptr);  // padding columns stay 0 (wterm_kernel reads 4-cell vectors)
-    if (!pool_) lpart_.alloc(static_cast<std::size_t>(nvb_) * K_);
     colpart2_.alloc(static_cast<std::size_t>(nb_phi_) * K_ * 2);
     S_.alloc(K_);
     phi_term_.alloc(K_);
@@ -2977,8 +2009,6 @@ class Lda final : public Model {
     wpart_.zero(s0);
     phiT_.zero(s0);
     phiT32_.zero(s0);
-    phiT16_.zero(s0);
-    q2_len_.zero(s0);
     nkw_.zero(s0);
     w_.zero(s0);
     z_.zero(s0);
@@ -3002,20 +2032,13 @@ class Lda final : public Model {
     // or registers (BNMC_ZSTEP_THETA=regs: 128 registers; measured 20 % slower on NIPS).
     const char* tr = std::getenv("BNMC_ZSTEP_THETA");
     theta_regs_ = tr && std::string(tr) == "regs";
-    const char* pv = std::getenv("BNMC_PHI_V1");
-    phi_v1_ = pv && std::string(pv) == "1";
     if (const char* e = std::getenv("BNMC_SCREEN_MARGIN")) screen_margin_ = static_cast<float>(std::atof(e));
     if (const char* e = std::getenv("BNMC_PDL")) pdl_ = std::string(e) != "0";
-    const char* tv = std::getenv("BNMC_THETA_V1");
-    theta_v1_ = tv && std::string(tv) == "1";
     configure_kernels();
-    BNMC_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
     BNMC_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_phi_ready_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_theta_ready_, cudaEventDisableTiming));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_copy_done_, cudaEventDisableTiming));
-    BNMC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-    BNMC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     BNMC_CUDA(cudaStreamCreateWithFlags(&up_, cudaStreamNonBlocking));
     BNMC_CUDA(cudaEventCreateWithFlags(&ev_up_, cudaEventDisableTiming));
     BNMC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&spec_flag_host_), sizeof(int)));
@@ -3024,13 +2047,10 @@ class Lda final : public Model {
   }
 
   ~Lda() override {
-    if (side_) cudaStreamDestroy(side_);
     if (copy_) cudaStreamDestroy(copy_);
     if (ev_phi_ready_) cudaEventDestroy(ev_phi_ready_);
     if (ev_theta_ready_) cudaEventDestroy(ev_theta_ready_);
     if (ev_copy_done_) cudaEventDestroy(ev_copy_done_);
-    if (ev_fork_) cudaEventDestroy(ev_fork_);
-    if (ev_join_) cudaEventDestroy(ev_join_);
     if (up_) cudaStreamDestroy(up_);
     if (ev_up_) cudaEventDestroy(ev_up_);
     if (spec_flag_host_) cudaFreeHost(spec_flag_host_);
@@ -3211,112 +2231,47 @@ class Lda final : public Model {
     LdaArgs a = args();
     // this sweep's phi block leaves g (unnormalised) + logS: the w-factor takes
     // log g - log S (the exact mode normalises phiT in place, S = 1: the phi/S path)
-    a.logg_valid = (!observe_phi_ && !phi_v1_ && !(pool_ && exact_)) ? 1 : 0;
+    a.logg_valid = (!observe_phi_ && !exact_) ? 1 : 0;
     const bool timed = marks != nullptr;  // phase timing: everything on one stream
     mark(st, "begin");
-    if (pool_) {
-      // warp-pool conjugate block: phi and theta cells in one balanced kernel, then the
-      // phi column sums (phi_colsum2<true> stripes) and the theta rows (extra y-blocks)
-      if (!observe_phi_ && comm_.active()) {
-        comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
-        mark(st, "allreduce_counts");
-      }
-      if (observe_phi_) nkw_.zero(st);  // phi clamped: the z-step's counts feed only the w-factor
-      a.pool_phi = observe_phi_ ? 0 : 1;
-      a.trow_blocks = Ml_ > 0 ? trow_blocks_ : 0;
-      a.col_stripes = observe_phi_ ? 0 : col_stripes_;
-      if (a.pool_phi || Ml_ > 0) {
-        if (K_ <= kPoolCells)
-          phi_pool_kernel<true><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
-        else
-          phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
-        mark(st, "conj_pool");
-        launch_pdl(phi_colsum2_kernel<true>, dim3((K_ + 31) / 32, a.col_stripes + a.trow_blocks + (h16_ ? h16_blocks_ : 0)),
-                   dim3(256), 0, st, a);
-        fq_reset_ = true;
-        mark(st, "colsum_rows");
-      }
-      if (!observe_phi_ && exact_) {
-        // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
-        phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
-        fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
-        mark(st, "phi_norm");
-      }
-      if (!timed) {  // phi, theta final: overlapped downloads may start (external event nodes)
-        if (!observe_phi_) record_external(ev_phi_ready_, st);
-        if (Ml_ > 0) record_external(ev_theta_ready_, st);
-      }
-    } else {
-      // The theta block depends only on the doc-topic counts: it runs on a side stream
-      // concurrently with the phi block (fork/join events; captured into the graph).
-      if (Ml_ > 0 && !timed) {
-        BNMC_CUDA(cudaEventRecord(ev_fork_, st));
-        BNMC_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-        launch_theta(a, side_);
-        record_external(ev_theta_ready_, side_);
-        BNMC_CUDA(cudaEventRecord(ev_join_, side_));
-      }
-      if (!observe_phi_) {
-        if (comm_.active()) {
-          comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
-          mark(st, "allreduce_counts");
-        }
-        if (phi_v1_) {
-          phi_gamma_kernel<<<nb_phi_, 256, 0, st>>>(a, out.iter);
-          mark(st, "phi_gamma");
-          phi_colsum_terms_kernel<<<K_, 128, 0, st>>>(a);
-          if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
-        } else {
-          const unsigned nbg = blocks_for(nvb_ * K_, 256);
-          if (pool_) {
-            if (K_ <= kPoolCells)
-              phi_pool_kernel<true><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
-            else
-              phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
-          } else switch (phi_rows_) {
-            case 1: phi_gamma2_kernel<1><<<nbg, 256, 0, st>>>(a, out.iter); break;
-            case 2: phi_gamma2_kernel<2><<<nbg, 256, 0, st>>>(a, out.iter); break;
-            case 4: phi_gamma2_kernel<4><<<nbg, 256, 0, st>>>(a, out.iter); break;
-            default: phi_gamma2_kernel<8><<<nbg, 256, 0, st>>>(a, out.iter); break;
-          }
-          mark(st, "phi_gamma");
-          // (+ h16_blocks_ y-blocks converting the rows for the level-1 screen)
-          launch_pdl(pool_ ? phi_colsum2_kernel<true> : phi_colsum2_kernel<false>, dim3((K_ + 31) / 32, col_stripes_ + (h16_ ? h16_blocks_ : 0)), dim3(256), 0, st, a);
-          fq_reset_ = true;
-        }
-        mark(st, "phi_colsum");
-        if (exact_) {
-          // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
-          phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
-          fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
-          mark(st, "phi_norm");
-        }
-        // phi (phiT, S) is final from here: an overlapped download may start (external
-        // event node in the captured graph)
-        if (!timed) record_external(ev_phi_ready_, st);
-      } else {
-        // phi clamped: no phi block consumes the counts; the z-step's counts of this
-        // sweep feed only the w-factor.
-        nkw_.zero(st);
-      }
-      if (Ml_ > 0) {
-        if (timed) {
-          launch_theta(a, st);
-          mark(st, "theta");
-        } else {
-          BNMC_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
-        }
-      }
+    // warp-pool conjugate block: phi and theta cells in one balanced kernel, then the
+    // phi column sums (phi_colsum2 stripes) and the theta rows (extra y-blocks)
+    if (!observe_phi_ && comm_.active()) {
+      comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
+      mark(st, "allreduce_counts");
+    }
+    if (observe_phi_) nkw_.zero(st);  // phi clamped: the z-step's counts feed only the w-factor
+    a.pool_phi = observe_phi_ ? 0 : 1;
+    a.trow_blocks = Ml_ > 0 ? trow_blocks_ : 0;
+    a.col_stripes = observe_phi_ ? 0 : col_stripes_;
+    if (a.pool_phi || Ml_ > 0) {
+      if (K_ <= kPoolCells)
+        phi_pool_kernel<true><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+      else
+        phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
+      mark(st, "conj_pool");
+      launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, a.col_stripes + a.trow_blocks), dim3(256), 0, st, a);
+      fq_reset_ = true;
+      mark(st, "colsum_rows");
+    }
+    if (!observe_phi_ && exact_) {
+      // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
+      phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
+      fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
+      mark(st, "phi_norm");
+    }
+    if (!timed) {  // phi, theta final: overlapped downloads may start (external event nodes)
+      if (!observe_phi_) record_external(ev_phi_ready_, st);
+      if (Ml_ > 0) record_external(ev_theta_ready_, st);
     }
     if (Ml_ > 0) {
       launch_zstep(a, st);
       mark(st, "zstep");
       if (timed && std::getenv("BNMC_SCREEN_STATS")) {  // diagnostics: queue lengths of this sweep
-        int n2 = -1, n3 = -1;
+        int n3 = -1;
         BNMC_CUDA(cudaStreamSynchronize(st));
-        if (h16_) BNMC_CUDA(cudaMemcpy(&n2, q2_len_.p, sizeof(int), cudaMemcpyDeviceToHost));
         BNMC_CUDA(cudaMemcpy(&n3, fq_len_.p, sizeof(int), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[bnmc] z-step queues: level2 %d fp64 %d of %lld tokens\n", n2, n3, static_cast<long long>(Nl_));
+        std::fprintf(stderr, "[bnmc] z-step fp64 queue: %d of %lld tokens\n", n3, static_cast<long long>(Nl_));
       }
     }
     const unsigned nbw = static_cast<unsigned>(nbw_);
@@ -3494,19 +2449,8 @@ class Lda final : public Model {
     phi_norm_kernel<false><<<nb_phi_, phi_threads_, 0, st>>>(a);
     phi_terms_kernel<<<K_, 128, 0, st>>>(a);
     if (screen_) phi_f32_kernel<<<148 * 8, 256, 0, st>>>(a);
-    if (h16_) phi_h16_kernel<<<148 * 4, 256, 0, st>>>(a);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
-  }
-
-  void launch_theta(const LdaArgs& a, cudaStream_t st) {
-    if (theta_v1_ || K_ > 256 * kThetaRun) {
-      theta_kernel<<<grid_docs(), theta_threads_, sizeof(double) * K_, st>>>(a, out.iter);
-      return;
-    }
-    const int tpd = (K_ + kThetaRun - 1) / kThetaRun;
-    const int dpb = std::max(1, 256 / tpd);
-    theta2_kernel<<<static_cast<unsigned>((Ml_ + dpb - 1) / dpb), 256, 0, st>>>(a, out.iter, tpd, dpb);
   }
 
   unsigned grid_docs() const { return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(Ml_, 1 << 20))); }
@@ -3522,9 +2466,6 @@ class Lda final : public Model {
   }
 
   void configure_kernels() {
-    if (sizeof(double) * K_ > 48 * 1024)
-      BNMC_CUDA(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sizeof(double) * K_)));
     if (zstep_smem() <= 48 * 1024) return;
     dispatch_zstep([&](auto g, auto r, auto e) { zstep_attr<decltype(g)::value, decltype(r)::value, decltype(e)::value>(); });
   }
@@ -3560,23 +2501,6 @@ class Lda final : public Model {
   // shared memory doubled the L1 register-writeback traffic, the limiter); K > 512:
   // G = 32 x CW = 8, theta in shared memory.  BNMC_ZSCREEN=g<G>w<CW>[s|r] overrides.
   void choose_screen() {
-    // Off by default: measured slower on NIPS (160 us vs 107 us; r01 v19) -- 32 bulk
-    // copies of 400 B per batch, the bulk-copy issue rate bounds it.  BNMC_ZSTAGE=1.
-    stage_ = false;
-    if (const char* e = std::getenv("BNMC_ZSTAGE")) stage_ = std::string(e) == "1" && K_ <= 128;
-    if (stage_) {
-      kq_ = 0;
-      for (int q : kStageKQ)
-        if (q * 4 >= K_) {
-          kq_ = q;
-          break;
-        }
-      G32_ = 1;
-      CW32_ = 8;
-      RS_ = (kq_ + 1) / 2;  // Kp32 = 8 RS >= 4 KQ: the bulk copy never leaves the row
-      transposed_ = false;
-      return;
-    }
     transposed_ = K_ <= 128;
     G32_ = 32;
     CW32_ = 8;
@@ -3664,101 +2588,9 @@ class Lda final : public Model {
     }
   }
 
-  template <int RH, bool WU>
-  void zscreen_h_launch(const LdaArgs& a, cudaStream_t st) {
-    const int kpad = (K_ + 3) & ~3;
-    const std::size_t hw = 4 * (16 * RH + 8) / 2;  // thh, in floats
-    if (WU) {
-      const std::size_t sm = sizeof(float) * 8 * (hw + 32 * 16 + kpad + 32);
-      const unsigned gw = static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((n_wunits_ + 7) / 8, 148 * 3)));
-      launch_pdl(zscreen_h_kernel<RH, true>, dim3(gw), dim3(256), sm, st, a, static_cast<const std::int64_t*>(out.iter));
-      return;
-    }
-    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
-    const std::size_t sm = sizeof(float) * (hw + zt_warps_ * 32 * 16 + kpad + 32);
-    launch_pdl(zscreen_h_kernel<RH, false>, dim3(g), dim3(32 * zt_warps_), sm, st, a, static_cast<const std::int64_t*>(out.iter));
-  }
-
-  template <int R>
-  void zscreen_q_launch(const LdaArgs& a, cudaStream_t st) {
-    // one wave of warps covers ~200 k queued tokens (NIPS: ~87 k): the kernel is one
-    // latency chain per batch, so warps, not blocks per SM, set its time
-    launch_pdl(zscreen_q_kernel<R>, dim3(148 * 6), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter));
-  }
-
-  // Level 1 (fp16 rows) then level 2 (fp32 rows, the level-1 queue).
-  void launch_zscreen_h(const LdaArgs& a, cudaStream_t st) {
-    if (RH_ == 1) {
-      if (zt_wu_) zscreen_h_launch<1, true>(a, st);
-      else zscreen_h_launch<1, false>(a, st);
-    } else {
-      if (zt_wu_) zscreen_h_launch<2, true>(a, st);
-      else zscreen_h_launch<2, false>(a, st);
-    }
-    switch (RS_) {
-      case 1: zscreen_q_launch<1>(a, st); break;
-      case 2: zscreen_q_launch<2>(a, st); break;
-      case 3: zscreen_q_launch<3>(a, st); break;
-      default: zscreen_q_launch<4>(a, st); break;
-    }
-  }
-
-  template <int KQ>
-  void zstage_launch(const LdaArgs& a, cudaStream_t st) {
-    if (!stage_attr_) {
-      BNMC_CUDA(cudaFuncSetAttribute(zstage_kernel<KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(stage_smem_)));
-      stage_attr_ = true;
-    }
-    zstage_kernel<KQ><<<stage_grid_, 32 * stage_warps_, stage_smem_, st>>>(
-        a, out.iter, batches_.p, nbatch_, stage_slots_, stage_stride16_);
-  }
-
-  template <int... Q>
-  void zstage_dispatch(const LdaArgs& a, cudaStream_t st, std::integer_sequence<int, Q...>) {
-    bool done = false;
-    ((!done && Q == kq_ ? (zstage_launch<Q>(a, st), done = true) : false), ...);
-  }
-
-  // Shared-memory plan of zstage_kernel: W warps x NS slots of 32 rows.
-  void plan_stage() {
-    stage_stride16_ = kq_ | 1;  // odd 16-byte row stride: conflict-free lane-per-row reads
-    const std::size_t slot = static_cast<std::size_t>(32) * stage_stride16_ * 16;
-    const std::size_t cta = (static_cast<std::size_t>(K_) * 8 + 127) / 128 * 128;
-    int dev = 0, smem_max = 0, sms = 148;
-    BNMC_CUDA(cudaGetDevice(&dev));
-    BNMC_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    stage_warps_ = 8;
-    if (const char* e = std::getenv("BNMC_ZSTAGE_WARPS")) stage_warps_ = std::min(8, std::max(1, std::atoi(e)));
-    auto hdr = [&](int ns) { return (static_cast<std::size_t>(ns) * (16 + 128) + 16 * kq_ + 127) / 128 * 128; };
-    auto need = [&](int w, int ns) { return cta + w * (hdr(ns) + ns * slot); };
-    stage_slots_ = 2;
-    while (stage_slots_ < 8 && need(stage_warps_, stage_slots_ + 1) <= static_cast<std::size_t>(smem_max))
-      ++stage_slots_;
-    if (const char* e = std::getenv("BNMC_ZSTAGE_SLOTS")) stage_slots_ = std::min(16, std::max(1, std::atoi(e)));
-    while (stage_warps_ > 1 && need(stage_warps_, stage_slots_) > static_cast<std::size_t>(smem_max)) --stage_warps_;
-    stage_smem_ = need(stage_warps_, stage_slots_);
-    require(stage_smem_ <= static_cast<std::size_t>(smem_max), BNMC_GPU_ERR_ARG, "z-step staging does not fit shared memory");
-    stage_grid_ = static_cast<unsigned>(sms);
-  }
-
   void launch_zscreen(const LdaArgs& a, cudaStream_t st) {
-    if (!fq_reset_) {
-      BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
-      if (h16_) BNMC_CUDA(cudaMemsetAsync(q2_len_.p, 0, sizeof(int), st));
-    }
+    if (!fq_reset_) BNMC_CUDA(cudaMemsetAsync(fq_len_.p, 0, sizeof(int), st));
     fq_reset_ = false;
-    if (h16_) {
-      launch_zscreen_h(a, st);
-      launch_pdl(zfallback_kernel, dim3(148 * 8), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter), out.err);
-      return;
-    }
-    if (stage_) {
-      zstage_dispatch(a, st, std::integer_sequence<int, 1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32>{});
-      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
-      return;
-    }
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
@@ -3827,17 +2659,10 @@ class Lda final : public Model {
     a.G32 = G32_;
     a.R32 = RS_;
     a.CW32 = CW32_;
-    a.phiT16 = h16_ ? phiT16_.p : nullptr;
-    a.Kp16 = Kp16_;
-    a.RH = RH_;
-    a.thS32 = h16_ ? thS32_.p : nullptr;
-    a.q2 = h16_ ? q2_.p : nullptr;
-    a.q2_len = h16_ ? q2_len_.p : nullptr;
     a.col_stripes = col_stripes_;
     a.logphiT = exact_ ? logphiT_.p : nullptr;
     a.theta = theta_.p;
     a.nkw = nkw_.p;
-    a.colpart = colpart_.p;
     a.colpart2 = colpart2_.p;
     a.S = S_.p;
     a.phi_term = phi_term_.p;
@@ -3856,7 +2681,6 @@ class Lda final : public Model {
     a.beta = beta_;
     a.pow_alpha = boost_pow_ ? exact_int_inverse(alpha_) : 0;
     a.pow_beta = boost_pow_ ? exact_int_inverse(beta_) : 0;
-    a.phi_pf = phi_pf_;
     a.phi_norm = phi_norm_;
     a.phi_lgasum = phi_lgasum_;
     a.theta_norm = theta_norm_;
@@ -3867,10 +2691,6 @@ class Lda final : public Model {
     a.var_theta = var_theta_;
     a.var_z = var_z_;
     a.rows_per_block = rows_per_block_;
-    a.gpart = gpart_.p;
-    a.lpart = lpart_.p;
-    a.nvb = nvb_;
-    a.logg = logg_.p;
     a.logS = logS_.p;
     a.logg_valid = 0;
     a.spart = spart_.p;
@@ -3892,24 +2712,9 @@ class Lda final : public Model {
   std::vector<std::int64_t> off_host_;
   bool exact_ = false, observe_phi_ = false, theta_regs_ = false, screen_ = false;
   int Kp32_ = 0, RS_ = 1, G32_ = 8, CW32_ = 4;
-  bool tfr_ = true, transposed_ = false, phi_v1_ = false, theta_v1_ = false;
-  // TMA-staged z-step (zstage_kernel)
-  static constexpr int kStageKQ[] = {1, 2, 4, 6, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24, 25, 26, 28, 30, 32};
-  bool stage_ = false, stage_attr_ = false;
-  int kq_ = 0, stage_stride16_ = 1, stage_warps_ = 8, stage_slots_ = 2;
-  std::size_t stage_smem_ = 0;
-  unsigned stage_grid_ = 148;
-  DevBuf<ZBatch> batches_;
-  std::int64_t nbatch_ = 0;
+  bool tfr_ = true, transposed_ = false;
   DevBuf<float> phiT32_;
-  // two-level screen (zscreen_h_kernel + zscreen_q_kernel), K <= 128
-  bool h16_ = false;
-  int RH_ = 1, Kp16_ = 64, h16_blocks_ = 1;
-  DevBuf<unsigned short> phiT16_;
-  DevBuf<float> thS32_;
-  DevBuf<int2> q2_;
-  DevBuf<int> q2_len_;
-  cudaStream_t side_ = nullptr, copy_ = nullptr;
+  cudaStream_t copy_ = nullptr;
   // speculative sweep_store
   cudaStream_t up_ = nullptr;
   cudaEvent_t ev_up_ = nullptr;
@@ -3918,11 +2723,10 @@ class Lda final : public Model {
   int* spec_flag_host_ = nullptr;
   bool zprev_valid_ = false, speculate_ = true;
   cudaEvent_t ev_phi_ready_ = nullptr, ev_theta_ready_ = nullptr, ev_copy_done_ = nullptr;
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   double alpha_ = 0.1, beta_ = 0.1, phi_norm_ = 0, phi_lgasum_ = 0, theta_norm_ = 0, theta_lgasum_ = 0;
   std::uint64_t seed_ = 0;
   int var_phi_ = 0, var_theta_ = 1, var_z_ = 2, var_w_ = 3;
-  int phi_threads_ = 128, theta_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
+  int phi_threads_ = 128, rows_per_block_ = 1, nb_phi_ = 1;
   std::vector<std::int64_t> units_host_;
   std::int64_t n_units_ = 0, docs_per_block_ = 1, nb_doc_ = 0, n_wunits_ = 0;
   DevBuf<std::int64_t> wunits_;
@@ -3957,16 +2761,12 @@ class Lda final : public Model {
   DevBuf<int> w_, z_, nkw_, nmk_;
   DevBuf<std::int64_t> units_;
   DevBuf<std::int64_t> off_;
-  std::int64_t nvb_ = 1;
-  int phi_rows_ = kPhiRowsMax;
   bool boost_pow_ = std::getenv("BNMC_BOOST_POW") == nullptr || std::string(std::getenv("BNMC_BOOST_POW")) != "0";
-  bool pool_ = true;     // phi block: warp-pool kernel (BNMC_PHI_POOL=0: v2)
   int pool_blocks_ = 148;
   int trow_blocks_ = 1;   // phi_colsum2 y-blocks for the pool's theta rows
-  int phi_pf_ = 0;     // phi_gamma2 count prefetch distance (blocks)
-  DevBuf<double> gpart_, lpart_, spart_, logg_, logS_, ttpart_;
+  DevBuf<double> spart_, logS_, ttpart_;
   DevBuf<int> ticket_;
-  DevBuf<double> phiT_, logphiT_, theta_, colpart_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
+  DevBuf<double> phiT_, logphiT_, theta_, colpart2_, S_, phi_term_, doc_part_, red_, tpart_,
       zpart_, wpart_;
 };
 

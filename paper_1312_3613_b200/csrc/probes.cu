@@ -216,34 +216,41 @@ double lpp(const double* phi, const double* theta, std::int64_t K, std::int64_t 
   return total;
 }
 
-// Read-bandwidth probe (bench.py's secondary roofline): every thread streams 256-bit
-// loads over a `bytes` buffer, `reps` passes, fixed grid (148 x 8 x 256 threads).
-// A buffer well inside the 126 MB L2 measures L2 -> SM read bandwidth; a multi-GB
-// buffer measures HBM.  Returns GB/s of the timed passes (after one warm pass).
-__global__ void __launch_bounds__(256) read_bw_kernel(const double4* p, std::size_t n, double* sink) {
-  // 4 independent 256-bit loads in flight per thread per iteration
+// Read-bandwidth probe (bench.py's secondary roofline): ONE launch of a persistent grid
+// (148 x 8 CTAs x 256 threads) in which every thread streams 256-bit loads over its
+// slice of a `bytes` buffer `passes` times (4 loads in flight per thread; ld.global.cg:
+// cached in L2 only -- each SM's slice of a 24 MB buffer would otherwise fit its L1
+// and the re-reads would measure L1), so launch
+// and tail costs are amortised over the whole read (r01's probe launched ~6 us kernels
+// back to back).  A buffer well inside the 126 MB L2 (16-32 MB) measures the L2 -> SM
+// read bandwidth; a multi-GB buffer measures HBM.  Returns GB/s of the timed launch
+// (after one warm single-pass launch).
+__global__ void __launch_bounds__(256) read_bw_kernel(const double4* p, std::size_t n, int passes, double* sink) {
   double acc = 0.0;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
-  std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    double4 v[4];
+  const std::size_t i0 = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  for (int pass = 0; pass < passes; ++pass) {
+    std::size_t i = i0;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+      double4 v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-                   : "=d"(v[j].x), "=d"(v[j].y), "=d"(v[j].z), "=d"(v[j].w)
-                   : "l"(p + i + j * stride));
+      for (int j = 0; j < 4; ++j)
+        asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(v[j].x), "=d"(v[j].y), "=d"(v[j].z), "=d"(v[j].w)
+                     : "l"(p + i + j * stride));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-  }
-  for (; i < n; i += stride) {
-    double4 v;
-    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p + i));
-    acc += (v.x + v.y) + (v.z + v.w);
+      for (int j = 0; j < 4; ++j) acc += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    }
+    for (; i < n; i += stride) {
+      double4 v;
+      asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p + i));
+      acc += (v.x + v.y) + (v.z + v.w);
+    }
   }
   if (acc == 12345.678) *sink = acc;  // keeps the loads alive
 }
 
-double probe_read_bandwidth(std::size_t bytes, int reps) {
+double probe_read_bandwidth(std::size_t bytes, int passes) {
   const std::size_t n = std::max<std::size_t>(bytes / sizeof(double4), 1);
   DevBuf<double4> buf;
   DevBuf<double> sink;
@@ -253,16 +260,16 @@ double probe_read_bandwidth(std::size_t bytes, int reps) {
   cudaEvent_t e0, e1;
   BNMC_CUDA(cudaEventCreate(&e0));
   BNMC_CUDA(cudaEventCreate(&e1));
-  read_bw_kernel<<<148 * 16, 256>>>(buf.p, n, sink.p);
+  read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, 1, sink.p);
   BNMC_CUDA(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) read_bw_kernel<<<148 * 16, 256>>>(buf.p, n, sink.p);
+  read_bw_kernel<<<148 * 8, 256>>>(buf.p, n, std::max(passes, 1), sink.p);
   BNMC_CUDA(cudaEventRecord(e1));
   BNMC_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   BNMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  return static_cast<double>(n) * sizeof(double4) * reps / (ms * 1e-3) / 1e9;
+  return static_cast<double>(n) * sizeof(double4) * std::max(passes, 1) / (ms * 1e-3) / 1e9;
 }
 
 }  // namespace bnmc_gpu

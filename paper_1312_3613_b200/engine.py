@@ -175,6 +175,10 @@ class RunConfig:
     exact_weights: bool = False   # LDA: reference log-space weights instead of theta*phi
     device: int = -1
     use_graph: bool = True
+    # page-lock the bound store's arrays once per binding (bnmc_gpu_register_host), as
+    # the reference-side adapter does for its std::vector store (integration/): the
+    # per-call copies then run at pinned-memory speed from the caller's own arrays
+    pin_host: bool = True
 
 
 def layout_lengths(model: str, hyper: dict) -> dict:
@@ -447,10 +451,14 @@ class Engine:
         _raise(L.bnmc_gpu_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
         self._bound = None  # the ParamStore whose state is on the device
+        self._registered = None  # the store view whose arrays are page-locked
+        self._registered_arrays = None
 
     # -- lifetime -----------------------------------------------------------------------
     def close(self):
         if getattr(self, "_h", None):
+            lib().bnmc_gpu_unregister_host(self._h)
+            self._registered = self._registered_arrays = None
             lib().bnmc_gpu_destroy(self._h)
             self._h = None
 
@@ -474,8 +482,19 @@ class Engine:
             s.observed[n] = True
         return s
 
+    def _register(self, store: ParamStore, st):
+        # once per view (the view is cached per array identity: a replaced array builds a
+        # new view, which re-registers; ranges no longer bound are released by the C side).
+        # The registered arrays are kept alive until then: numpy must not free page-locked
+        # memory under the driver.
+        if self.cfg.pin_host and self._registered is not st:
+            _raise(lib().bnmc_gpu_register_host(self._h, ctypes.byref(st)), self._h)
+            self._registered = st
+            self._registered_arrays = tuple(store.arrays.values())
+
     def upload(self, store: ParamStore):
         st = store._view()
+        self._register(store, st)
         _raise(lib().bnmc_gpu_upload(self._h, ctypes.byref(st)), self._h)
         self._bound = store
 
@@ -510,6 +529,7 @@ class Engine:
             # upload what the sweep reads, sweep, write back (phi / theta copies overlap
             # the z-step): bnmc_gpu_sweep_store
             st = store._view()
+            self._register(store, st)
             _raise(lib().bnmc_gpu_sweep_store(self._h, ctypes.byref(st), it, ctypes.byref(lj), ctypes.byref(acc)),
                    self._h)
         if mh_accepted is not None:

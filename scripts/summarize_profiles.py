@@ -3,9 +3,12 @@
 
     python scripts/summarize_profiles.py launches <launches.csv> <out.txt> [--title T]
     python scripts/summarize_profiles.py full <kernel.ncu-rep> <out.txt> [--traffic-key NAME]
+    python scripts/summarize_profiles.py csv <raw.csv> <sass.csv> <out.txt> [--traffic-key NAME]
 
 `launches`: the `ncu --metrics gpu__time_duration.sum --clock-control none` launch list
 -> per-kernel count / mean / share of the per-sweep kernel time.
+`csv`: the same from the `--page raw --csv` / `--page source --csv --print-source sass`
+exports of a capture (scripts/gpu_round_profile.sh reduces reports to these on the box).
 `full`: one `ncu --set full` capture -> the metrics the roofline and DESIGN.md cite
 (duration, dram bytes, L2/L1 throughput, occupancy, issue, stall reasons, top SASS
 opcodes); with --traffic-key, dram read+write bytes per launch are also written to
@@ -67,8 +70,9 @@ def to_bytes(v, unit):
     return float(v) * f if f else None
 
 
-def full(rep, dst, key):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def full(rep, dst, key, raw=None, src=None, source_name=None):
+    if raw is None:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u = rows[0], rows[1]
     out = []
@@ -88,11 +92,22 @@ def full(rep, dst, key):
         rb = to_bytes(m.get("dram__bytes_read.sum", 0), un.get("dram__bytes_read.sum"))
         wb = to_bytes(m.get("dram__bytes_write.sum", 0), un.get("dram__bytes_write.sum"))
         if rb is not None and wb is not None:
-            traffic.append(rb + wb)
+            def pct(k):
+                try:
+                    return round(float(m[k]), 2)
+                except (KeyError, ValueError):
+                    return None
+            traffic.append({"dram_bytes": rb + wb,
+                            "l1tex_pct": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                            "lts_pct": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                            "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                            "kernel_us_ncu": pct("gpu__time_duration.sum"),
+                            "source": os.path.relpath(dst, ROOT)})
             out.append(f"  dram read+write bytes per launch: {rb + wb:.4g}")
     # SASS opcode mix (instructions executed)
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    if src is None:
+        src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
     if len(srows) > 2 and "Source" in srows[1]:
         sh = srows[1]
@@ -122,7 +137,10 @@ def full(rep, dst, key):
 
 if __name__ == "__main__":
     mode = sys.argv[1]
-    if mode == "launches":
+    if mode == "csv":
+        key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
+        full(None, sys.argv[4], key, raw=open(sys.argv[2]).read(), src=open(sys.argv[3]).read())
+    elif mode == "launches":
         title = sys.argv[sys.argv.index("--title") + 1] if "--title" in sys.argv else "ncu launch list"
         launches(sys.argv[2], sys.argv[3], title)
     else:

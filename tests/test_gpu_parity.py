@@ -332,9 +332,8 @@ def _gen_lda(restatement, reference, M, V, K, L, seed):
     return w, off, phi, theta, z
 
 
-@pytest.mark.parametrize("cfg,env", [(("kos", 3430, 6906, 50, 136), {}), (("nips", 1500, 12419, 100, 1267), {}),
-                                     (("nips", 1500, 12419, 100, 1267), {"BNMC_ZSCREEN_H": "1"})],
-                         ids=["kos", "nips", "nips-two-level-screen"])
+@pytest.mark.parametrize("cfg,env", [(("kos", 3430, 6906, 50, 136), {}), (("nips", 1500, 12419, 100, 1267), {})],
+                         ids=["kos", "nips"])
 def test_lda_full_size_one_sweep(g, restatement, reference, monkeypatch, cfg, env):
     """KOS / NIPS-shaped corpora: one sweep from the reference's prior_init
     state; z and the counts must be bit-exact (0 mismatches), floats within tolerance."""
@@ -471,20 +470,32 @@ LAYOUTS = [
     (100, {"BNMC_ZSCREEN": "g16w4s"}), (100, {"BNMC_ZSCREEN": "g32w4r"}),
     (100, {"BNMC_ZSTEP_THETA": "smem"}),
     (100, {"BNMC_ZT_WU": "1"}), (33, {"BNMC_ZT_WU": "1", "BNMC_ZSTEP_THETA": "smem"}), (64, {"BNMC_ZT_WU": "0"}),
-    # TMA bulk-copy staged screen (experimental layout)
-    (64, {"BNMC_ZSTAGE": "1"}), (100, {"BNMC_ZSTAGE": "1"}), (7, {"BNMC_ZSTAGE": "1", "BNMC_ZSTAGE_SLOTS": "3"}),
     # every token through the fp64 fallback queue
     (100, {"BNMC_SCREEN_MARGIN": "1.0"}), (1000, {"BNMC_SCREEN_MARGIN": "1.0"}),
     # screen off: the grouped fp64 kernel
     (100, {"BNMC_ZSTEP_SCREEN": "0"}), (1000, {"BNMC_ZSTEP_SCREEN": "0"}),
-    # phi / theta block v1 kernels
-    (100, {"BNMC_PHI_V1": "1", "BNMC_THETA_V1": "1"}),
-    # two-level screen: fp16 rows (level 1), fp32 queue (level 2), fp64 queue
-    (5, {"BNMC_ZSCREEN_H": "1"}), (33, {"BNMC_ZSCREEN_H": "1"}), (64, {"BNMC_ZSCREEN_H": "1"}),
-    (100, {"BNMC_ZSCREEN_H": "1"}), (128, {"BNMC_ZSCREEN_H": "1"}),
-    (100, {"BNMC_ZSCREEN_H": "1", "BNMC_ZT_WU": "1"}), (50, {"BNMC_ZSCREEN_H": "1", "BNMC_ZT_WU": "0"}),
-    (100, {"BNMC_ZSCREEN_H": "1", "BNMC_PHI_V1": "1"}),
 ]
+
+
+@pytest.mark.parametrize("K,V", [(600, 9000), (40, 140000)], ids=["K600-V9000", "K40-V140000"])
+def test_lda_pool_multichunk_vs_restatement(g, restatement, K, V):
+    """The warp-pool conjugate block with more than one shared-memory count chunk per
+    warp (K V > 1024 cells per resident warp: 5.4 M / 5.6 M cells) -- chunk boundaries,
+    the next-chunk prefetch, phi and theta cells in one range -- two sweeps bit-exact in z
+    against the restatement."""
+    M, seed = 30, 77
+    off, w, phi, theta, z = _ragged_corpus(restatement, K, V, M, seed)
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": np.diff(off).tolist()}, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["w"], s["z"], s["phi"], s["theta"] = w, z, phi, theta
+    for it in range(2):
+        lj = e.sweep(s, it)
+        lj2 = restatement.lda_sweep(K, V, off, w, z, phi, theta, seed, it)
+        assert int((s["z"] != z).sum()) == 0
+        assert rel(s["phi"], phi) < RTOL_PARAM
+        assert rel(s["theta"], theta) < RTOL_PARAM
+        assert abs(lj - lj2) <= RTOL_LJ * abs(lj2)
+    e.close()
 
 
 @pytest.mark.parametrize("K,env", LAYOUTS, ids=[f"K{k}-" + "-".join(f"{a}={b}" for a, b in e.items()) for k, e in LAYOUTS])

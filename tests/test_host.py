@@ -137,3 +137,46 @@ def test_store_view_cache_follows_the_arrays():
     assert v3 is not v2 and ctypes.addressof(v3.real[4].contents) == s["x"].ctypes.data
     s.observed["z"] = True
     assert s._view() is not v3
+
+
+def test_bench_corpus_file_matches_engine_format(tmp_path):
+    """bench.write_corpus_file (the reference arm's input) writes the bytes of
+    engine.write_corpus (the library's .bnc format)."""
+    import bench
+    from paper_1312_3613_b200.engine import write_corpus
+
+    w = bench.gen_lda_corpus(7, 50, 4, 9, 5)
+    off = np.arange(8, dtype=np.int64) * 9
+    bench.write_corpus_file(str(tmp_path / "a.bnc"), off, w, 50)
+    write_corpus(str(tmp_path / "b.bnc"), off, w, 50)
+    assert (tmp_path / "a.bnc").read_bytes() == (tmp_path / "b.bnc").read_bytes()
+
+
+def test_bench_arms_share_config():
+    """Both arms print shared_config(args, world): identical dicts per workload."""
+    import argparse
+
+    import bench
+
+    for wl in bench.WORKLOADS:
+        a = argparse.Namespace(workload=wl, seed=7)
+        assert bench.shared_config(a, 1) == bench.shared_config(a, 1)
+        assert "l2" in bench.shared_config(a, 2)
+
+
+def test_reference_reads_the_bench_corpus(tmp_path):
+    """oracle/_ref/ref_bench lda-file runs the reference on the corpus the GPU arm uses
+    (first DOCS documents) and counts its sites."""
+    import bench
+    from oracle import REF_BENCH
+
+    if not os.path.exists(REF_BENCH):
+        pytest.skip("reference not built")
+    w = bench.gen_lda_corpus(12, 200, 6, 30, 2)
+    bench.write_corpus_file(str(tmp_path / "c.bnc"), np.arange(13, dtype=np.int64) * 30, w, 200)
+    res, _ = bench.ref_bench(["lda-file", str(tmp_path / "c.bnc"), 6, 2, 1, 0, 2, 5], timeout=120)
+    assert res["sites"] == 5 * 30 and len(res["ms"]) == 2
+    x = bench.gmm_points(500, 3)
+    x.tofile(str(tmp_path / "x.f64"))
+    res, _ = bench.ref_bench(["gmm-file", str(tmp_path / "x.f64"), 3, 1, 0, 2], timeout=120)
+    assert res["sites"] == 500
