@@ -536,6 +536,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
            "roofline": roofline, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
            "e2e": e2e, "e2e_pageable": e2e_pageable, "gpu_launches": per_sweep_kernels * args.steps,
            "clocks": clocks, "wall_s_timed": wall, "setup_s": setup_s, "last_log_joint": lj_last}
+    if rank == 0 and world == 1 and model == "lda" and host_corpus:
+        out["e2e_reference_engine"] = e2e_reference_engine(args, config, store["w"])
     if rank == 0 and world == 1 and args.workload == "nips" and not args.no_1b:
         out["roofline_1b"] = roofline_1b(args, g, torch, stream, flush, gpu_index)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -543,6 +545,36 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     if dist:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def e2e_reference_engine(args, config, w):
+    """The reference's OWN bnmc::Engine::sweep with RunConfig::device = B200
+    (integration/: reference_b200.patch + gpu_backend.cpp, linked to libbnmc_gpu.so) on
+    its std::vector ParamStore -- pageable memory the backend page-locks once at binding --
+    timed per call in C++ (b2r_sweeps_timed) on this run's corpus: what a caller of the
+    unchanged reference API sees."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "integration"))
+        import b200ref
+
+        R = b200ref.B200Ref()
+        hyper = {"K": config["topics"], "V": config["vocab"], "M": config["docs"],
+                 "N": [config["doc_len"]] * config["docs"]}
+        e = R.open("lda", hyper, "gibbs", args.seed, device="b200")
+        if not e.on_device:
+            return {"error": "the reference Engine did not select the B200 backend"}
+        e.set("w", w)
+        e.prior_init(args.seed)
+        e.sweeps_timed(0, 3)  # bind (page-lock, observed data up) + warm calls
+        lj, ms = e.sweeps_timed(3, args.steps)
+        e.close()
+        mean = float(np.mean(ms))
+        return {"value": config["tokens"] / (mean / 1e3), "unit": UNIT, "ms_per_step": mean,
+                "ms_min": float(np.min(ms)), "last_log_joint": float(lj[-1]),
+                "path": "bnmc::Engine::sweep of the patched reference (RunConfig::device = B200) on its own "
+                        "std::vector ParamStore, C++ steady_clock per call (integration/b200_driver.cpp)"}
+    except Exception as ex:  # reported, never fatal
+        return {"error": str(ex)}
 
 
 def roofline_1b(args, g, torch, stream, flush, gpu_index):
