@@ -59,8 +59,12 @@ typedef enum {
   BNMC_GPU_GIBBS = 1u << 3,          /* regression / polyreg: Method::Gibbs plan -- one MH
                                         block per non-conjugate variable (w, b), conjugate
                                         tau (plan.cpp:139-164) -- instead of one MH block */
-  BNMC_GPU_MWG = 1u << 4             /* regression / polyreg: Method::MWG plan -- single-site
+  BNMC_GPU_MWG = 1u << 4,            /* regression / polyreg: Method::MWG plan -- single-site
                                         blocks per element (run_mwg_block, sampler.cpp:342-388) */
+  BNMC_GPU_TAU_PRECISION = 1u << 5   /* regression: tau is the noise PRECISION with a Gamma(shape,
+                                        scale) prior, y ~ N(mean, pow(tau, -1)) -- the
+                                        GammaPrecision conjugate kind (rewrite.cpp:538-549,
+                                        sampler.cpp:205-207); hyper[4], hyper[5] = shape, scale */
 } bnmc_gpu_flag;
 
 typedef enum {

@@ -22,7 +22,7 @@ _ip, _dp = POINTER(c_int64), POINTER(c_double)
 VARS = {"lda": ["phi", "theta", "z", "w"], "gmm": ["pi", "mu", "sigma2", "z", "x"],
         "regression": ["w", "b", "tau", "x", "y"], "catmix": ["theta", "phi", "z", "x"],
         "naivebayes": ["pC", "c", "pF", "f"], "hmm": ["T", "bias", "s", "flips"],
-        "polyreg": ["w", "bias", "x", "y"]}
+        "polyreg": ["w", "bias", "x", "y"], "regprec": ["w", "b", "tau", "x", "y"]}
 
 
 class RefError(RuntimeError):

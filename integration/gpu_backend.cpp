@@ -97,6 +97,7 @@ struct ZooEntry {
   const char* name;
   int kind;
   const char* methods;  // plans the device kernels implement
+  unsigned flags = 0;   // extra bnmc_gpu_flag bits of the model
 };
 constexpr ZooEntry kZoo[] = {
     {"lda", BNMC_GPU_LDA, "gibbs"},
@@ -106,6 +107,8 @@ constexpr ZooEntry kZoo[] = {
     {"naivebayes", BNMC_GPU_NAIVEBAYES, "gibbs"},
     {"hmm", BNMC_GPU_HMM, "gibbs"},
     {"polyreg", BNMC_GPU_MH_POLYREG, "mh gibbs mwg"},
+    // regression with a Gamma noise precision (oracle/models/regprec.bn): the GammaPrecision kind
+    {"regprec", BNMC_GPU_MH_LINREG, "mh gibbs mwg", BNMC_GPU_TAU_PRECISION},
 };
 
 int var_id(const CheckedModel& m, const char* name) {
@@ -189,6 +192,7 @@ std::shared_ptr<GpuBackend> GpuBackend::create(const CheckedModel& model, const 
   if (cfg.method == Method::Gibbs && (hit->kind == BNMC_GPU_MH_LINREG || hit->kind == BNMC_GPU_MH_POLYREG))
     d.flags |= BNMC_GPU_GIBBS;
   if (cfg.method == Method::MWG) d.flags |= BNMC_GPU_MWG;
+  d.flags |= hit->flags;
   for (std::size_t i = 0; i < model.vars.size() && i < 8; ++i) d.var_ids[i] = static_cast<int32_t>(i);
   std::vector<int64_t> offsets;
   auto lay = [&](const char* n) -> const VarLayout& { return L[static_cast<std::size_t>(var_id(model, n))]; };
@@ -218,6 +222,7 @@ std::shared_ptr<GpuBackend> GpuBackend::create(const CheckedModel& model, const 
       d.hyper[4] = 1.0;
       break;
     case BNMC_GPU_MH_LINREG:  // regression.bn: w, b ~ Gaussian(0, 10), tau ~ InvGamma(3, 1), x ~ U(l, u)
+                              // (regprec.bn: tau ~ Gamma(3, 1), a precision)
       d.K = lay("w").total;
       d.N = lay("y").total;
       d.hyper[0] = hyper_real(model, bind, "l");

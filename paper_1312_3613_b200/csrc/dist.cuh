@@ -51,6 +51,13 @@ __device__ __forceinline__ double log_pdf_gaussian(double x, double mean, double
   return -0.5 * (d * d / var + log(var) + kLog2Pi);
 }
 
+// log_pdf_gamma (dist.cpp:85-90); shape / scale parameterisation.
+__device__ __forceinline__ double log_pdf_gamma(double x, double shape, double scale) {
+  if (!(shape > 0.0) || !(scale > 0.0)) return -INFINITY;
+  if (!(x > 0.0)) return -INFINITY;
+  return (shape - 1.0) * log(x) - x / scale - shape * log(scale) - lgamma(shape);
+}
+
 // log_pdf_inverse_gamma (dist.cpp:92-97).
 __device__ __forceinline__ double log_pdf_inverse_gamma(double x, double shape, double scale) {
   if (!(shape > 0.0) || !(scale > 0.0)) return -INFINITY;

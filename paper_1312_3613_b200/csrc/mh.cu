@@ -1,7 +1,9 @@
 // csrc/mh.cu -- random-walk Metropolis-Hastings over i.i.d. rows
 // (Engine::run_mh_block, proj/src/sampler.cpp:284-340).
 //
-// Models: proj/models/regression.bn (y ~ N(w.x + b, tau), method MH) and its
+// Models: proj/models/regression.bn (y ~ N(w.x + b, tau), method MH; with
+// BNMC_GPU_TAU_PRECISION the precision variant y ~ N(w.x + b, pow(tau, -1)), tau ~ Gamma,
+// oracle/models/regprec.bn -- the GammaPrecision conjugate kind) and its
 // logistic twin (y ~ Bernoulli(sigmoid(w.x + b)); no reference model exists, the
 // MH machinery is shared).  The reference evaluates the blanket before, the
 // blanket after, and the full log-joint: three passes over the N x K data.  Here
@@ -42,6 +44,7 @@ struct MhArgs {
   int var_w, var_b, var_tau;
   int logistic;
   int notau;        // logistic or polyreg: no tau variable (polyreg: y ~ N(mean, 1.0))
+  int prec;         // tau is a precision: y ~ N(mean, pow(tau, -1)), tau ~ Gamma(tau_a, tau_b)
   const double* xr; // fx factor input: raw x (polyreg: N scalars) or the feature matrix
   std::int64_t nfx; // its length
 };
@@ -81,8 +84,17 @@ __device__ __forceinline__ void ldg256(const double* p, double& a, double& b, do
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
-__device__ __forceinline__ double row_loglik(const MhArgs& a, double s, double yi, double tau) {
-  return a.logistic ? yi * s - softplus(s) : log_pdf_gaussian(yi, s, tau);
+// y's variance from the tau variable: tau itself (regression.bn), or pow(tau, -1) for a
+// precision (the reference evaluates std::pow(tau, -1.0), correctly rounded like 1 / tau)
+__device__ __forceinline__ double tau_variance(const MhArgs& a, double tau) { return a.prec ? 1.0 / tau : tau; }
+
+__device__ __forceinline__ double row_loglik(const MhArgs& a, double s, double yi, double var) {
+  return a.logistic ? yi * s - softplus(s) : log_pdf_gaussian(yi, s, var);
+}
+
+// log p(tau): InverseGamma(shape, scale) variance or Gamma(shape, scale) precision
+__device__ __forceinline__ double tau_prior(const MhArgs& a, double tau) {
+  return a.prec ? log_pdf_gamma(tau, a.tau_a, a.tau_b) : log_pdf_inverse_gamma(tau, a.tau_a, a.tau_b);
 }
 
 template <bool VEC, int CPL = 1>  // CPL: 4-feature chunks per lane (vector path)
@@ -91,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) lik_kernel(MhArgs a, const double* p
   __shared__ double scratch[32];
   for (int j = threadIdx.x; j < a.K + 2; j += blockDim.x) wsh[j] = p[j];
   __syncthreads();
-  const double b = wsh[a.K], tau = wsh[a.K + 1];
+  const double b = wsh[a.K], tau = tau_variance(a, wsh[a.K + 1]);
   double acc = 0.0;
   if constexpr (VEC) {
     const int gl = threadIdx.x & (kRowGroup - 1);
@@ -180,7 +192,7 @@ __device__ double priors(const MhArgs& a, const double* p, double* fw, double* f
   for (int j = 0; j < a.K; ++j) s += log_pdf_gaussian(p[j], 0.0, a.w_var);
   *fw = s;
   *fb = log_pdf_gaussian(p[a.K], 0.0, a.b_var);
-  *ftau = a.notau ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
+  *ftau = a.notau ? 0.0 : tau_prior(a, p[a.K + 1]);
   return a.notau ? (*fw + *fb) : ((*fw + *fb) + *ftau);
 }
 
@@ -204,7 +216,7 @@ __device__ double priors_block(const MhArgs& a, const double* p, double* fw, dou
     for (int j = 0; j < a.K; ++j) s += terms[j];
     *fw = s;
     *fb = log_pdf_gaussian(p[a.K], 0.0, a.b_var);
-    *ftau = a.notau ? 0.0 : log_pdf_inverse_gamma(p[a.K + 1], a.tau_a, a.tau_b);
+    *ftau = a.notau ? 0.0 : tau_prior(a, p[a.K + 1]);
     r = a.notau ? (*fw + *fb) : ((*fw + *fb) + *ftau);
   }
   return r;
@@ -284,7 +296,8 @@ __global__ void prior_kernel(MhArgs a, std::uint64_t seed) {
         a.w[t] = a.logistic ? 0.0 : 1.0;  // polyreg: the fixed unit variance of y
       } else {
         Stream r(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_tau), 0));
-        a.w[t] = a.tau_b / draw_gamma(r, a.tau_a);
+        // InverseGamma: scale / gamma (dist.cpp:175-177); Gamma: scale * gamma (:157-159)
+        a.w[t] = a.prec ? a.tau_b * draw_gamma(r, a.tau_a) : a.tau_b / draw_gamma(r, a.tau_a);
       }
     }
   }
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(kThreads) mwg_lik_kernel(MhArgs a, const std::
     dlt = RSS ? 0.0 : mwg_proposal(a, e, *iter_p, r) - a.w[e];
   }
   __syncthreads();
-  const double b = a.w[a.K], tau = a.w[a.K + 1], d = dlt;
+  const double b = a.w[a.K], tau = tau_variance(a, a.w[a.K + 1]), d = dlt;
   const int lane = threadIdx.x & 31;
   double acc0 = 0.0, acc1 = 0.0;
   const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -388,7 +401,9 @@ __global__ void mwg_accept_kernel(MhArgs a, const std::int64_t* iter_p, int e, c
   }
 }
 
-// tau ~ InverseGamma(tau_a + n/2, tau_b + rss/2), stream keyed(seed,4,var_tau,iter).derive(0)
+// tau ~ InverseGamma(tau_a + n/2, tau_b + rss/2) (InverseGammaVariance), or for a precision
+// tau ~ Gamma(tau_a + n/2, scale 1 / (1/tau_b + rss/2)) (GammaPrecision, sampler.cpp:205-207);
+// stream keyed(seed,4,var_tau,iter).derive(0)
 __global__ void mwg_tau_kernel(MhArgs a, const std::int64_t* iter_p, const double* part) {
   __shared__ double scratch[32];
   double rss = 0.0;
@@ -399,7 +414,8 @@ __global__ void mwg_tau_kernel(MhArgs a, const std::int64_t* iter_p, const doubl
                                     static_cast<std::uint64_t>(*iter_p));
     Stream r(derive(key, 0));
     const double n = static_cast<double>(a.N);
-    a.w[a.K + 1] = (a.tau_b + 0.5 * rss) / draw_gamma(r, a.tau_a + 0.5 * n);
+    a.w[a.K + 1] = a.prec ? (1.0 / (1.0 / a.tau_b + 0.5 * rss)) * draw_gamma(r, a.tau_a + 0.5 * n)
+                          : (a.tau_b + 0.5 * rss) / draw_gamma(r, a.tau_a + 0.5 * n);
   }
 }
 
@@ -465,6 +481,9 @@ class Mh final : public Model {
     poly_ = d.kind == BNMC_GPU_MH_POLYREG;
     gibbs_ = (d.flags & BNMC_GPU_GIBBS) != 0;
     mwg_ = (d.flags & BNMC_GPU_MWG) != 0;
+    prec_ = (d.flags & BNMC_GPU_TAU_PRECISION) != 0;
+    require(!prec_ || d.kind == BNMC_GPU_MH_LINREG, BNMC_GPU_ERR_ARG,
+            "BNMC_GPU_TAU_PRECISION applies to the linear-regression kind only");
     require(!(gibbs_ || mwg_) || (!logistic_ && c.world == 1), BNMC_GPU_ERR_ARG,
             "the Gibbs / MWG plans serve regression.bn / polyreg.bn on one GPU");
     require(d.K >= 1 && d.N >= 0, BNMC_GPU_ERR_ARG, "MH needs K >= 1 features");
@@ -714,6 +733,7 @@ class Mh final : public Model {
     a.var_tau = (logistic_ || poly_) ? -1 : var_[2];
     a.logistic = logistic_ ? 1 : 0;
     a.notau = (logistic_ || poly_) ? 1 : 0;
+    a.prec = prec_ ? 1 : 0;
     a.xr = poly_ ? xraw_.p : x_.p;
     a.nfx = poly_ ? Nl_ : Nl_ * K_;
     return a;
@@ -721,7 +741,7 @@ class Mh final : public Model {
 
   Comm comm_;
   bool data_ = false;
-  bool logistic_ = false, poly_ = false, gibbs_ = false, mwg_ = false;
+  bool logistic_ = false, poly_ = false, gibbs_ = false, mwg_ = false, prec_ = false;
   int K_ = 0;
   std::int64_t N_ = 0, r0_ = 0, r1_ = 0, Nl_ = 0;
   double lo_, hi_, w_var_, b_var_, tau_a_, tau_b_, mh_scale_;

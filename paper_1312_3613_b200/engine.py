@@ -28,7 +28,7 @@ LIB_PATH = os.environ.get("BNMC_GPU_LIB") or os.path.join(HERE, "libbnmc_gpu.so"
 ABI_VERSION = 2
 
 LDA, GMM, MH_LINREG, MH_LOGREG, CATMIX, NAIVEBAYES, HMM, MH_POLYREG = 1, 2, 3, 4, 5, 6, 7, 8
-OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH, GIBBS, MWG = 1, 2, 4, 8, 16
+OBSERVE_PHI, EXACT_WEIGHTS, NO_GRAPH, GIBBS, MWG, TAU_PRECISION = 1, 2, 4, 8, 16, 32
 
 
 class BnmcError(RuntimeError):
@@ -149,6 +149,10 @@ MODELS = {
                 observed={"x"}),
     "regression": dict(kind=MH_LINREG, method="mh", vars=["w", "b", "tau", "x", "y"], ints=set(),
                        observed={"x", "y"}),
+    # regression with a Gamma-distributed noise PRECISION, y ~ N(mean, pow(tau, -1))
+    # (oracle/models/regprec.bn): the GammaPrecision conjugate kind
+    "regprec": dict(kind=MH_LINREG, method="mh", vars=["w", "b", "tau", "x", "y"], ints=set(),
+                    observed={"x", "y"}, flags=TAU_PRECISION),
     "logreg": dict(kind=MH_LOGREG, method="mh", vars=["w", "b", "x", "y"], ints=set(), observed={"x", "y"}),
     # the rest of the reference zoo
     "catmix": dict(kind=CATMIX, method="gibbs", vars=["theta", "phi", "z", "x"], ints={"z", "x"},
@@ -202,10 +206,10 @@ def layout_lengths(model: str, hyper: dict) -> dict:
     if model == "polyreg":
         N, M = int(hyper["N"]), int(hyper["M"])
         return {"w": M, "bias": 1, "x": N, "y": N}
-    if model in ("regression", "logreg"):
+    if model in ("regression", "regprec", "logreg"):
         N, K = int(hyper["N"]), int(hyper["K"])
         d = {"w": K, "b": 1, "x": N * K, "y": N}
-        if model == "regression":
+        if model in ("regression", "regprec"):
             d["tau"] = 1
         return d
     raise ValueError(f"model '{model}' has no GPU path")
@@ -360,7 +364,7 @@ class Engine:
         method = self.cfg.method or spec["method"]
         # regression.bn / polyreg.bn also run their Gibbs plan (an MH block per variable,
         # conjugate tau) and their MWG plan (single-site blocks): BNMC_GPU_GIBBS / _MWG
-        methods = {spec["method"], "gibbs", "mwg"} if model in ("regression", "polyreg") else {spec["method"]}
+        methods = {spec["method"], "gibbs", "mwg"} if model in ("regression", "regprec", "polyreg") else {spec["method"]}
         if method not in methods:
             raise ValueError(f"the GPU path runs {model} with method {sorted(methods)}, not '{method}'")
         self.method = method
@@ -395,6 +399,7 @@ class Engine:
             flags |= GIBBS
         if method == "mwg":
             flags |= MWG
+        flags |= spec.get("flags", 0)
         d.flags = flags
         self._offsets = None
         if model == "lda":

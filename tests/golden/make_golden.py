@@ -181,6 +181,20 @@ def zoo(F: Reference):
                 {"x": xr.ravel(), "y": yr}, seed=61, sweeps=4, method="mwg", mh_scale=0.1)
 
 
+def regprec(F: Reference):
+    """The GammaPrecision conjugate kind (rewrite.cpp:538-549, sampler.cpp:205-207) through our
+    test model oracle/models/regprec.bn (regression with y ~ N(mean, pow(tau, -1)), tau ~
+    Gamma(3, 1)) under its MH, Gibbs (conjugate Gamma tau) and MWG plans."""
+    rs = np.random.default_rng(101)
+    xr = rs.uniform(-1.0, 1.0, (700, 5))
+    yr = xr @ np.array([0.5, -1.0, 0.3, 0.0, 2.0]) + 0.2 + 0.3 * rs.normal(size=700)
+    hyper = {"K": 5, "N": 700, "l": -1.0, "u": 1.0}
+    data = {"x": xr.ravel(), "y": yr}
+    zoo_fixture(F, "regprec_mh", "regprec", hyper, data, seed=67, sweeps=12, method="mh", mh_scale=0.1)
+    zoo_fixture(F, "regprec_gibbs", "regprec", hyper, data, seed=71, sweeps=6, method="gibbs", mh_scale=0.1)
+    zoo_fixture(F, "regprec_mwg", "regprec", hyper, data, seed=73, sweeps=4, method="mwg", mh_scale=0.1)
+
+
 def describe(F: Reference):
     # Block order of the LDA plan (phi, theta, z) as the reference reports it.
     with open(os.path.join(HERE, "describe_lda.txt"), "w") as f:
@@ -196,6 +210,7 @@ if __name__ == "__main__":
     gmm_fixture(F, "gmm_small", N=3000, seed=17, sweeps=5)
     mh_fixture(F, "mh_linreg", N=1500, K=16, seed=23, steps=12)
     zoo(F)
+    regprec(F)
     describe(F)
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

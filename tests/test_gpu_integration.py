@@ -162,6 +162,10 @@ ZOO = [
     ("hmm", "hmm_small", None, "gibbs", None, 0.5, RTOL),
     ("polyreg", "polyreg_small", None, "mh", None, 0.05, RTOL),
     ("polyreg", "polyreg_small", None, "gibbs", None, 0.05, RTOL),
+    # the GammaPrecision kind through our test model oracle/models/regprec.bn
+    ("regprec", "regprec_mh", None, "mh", None, 0.1, RTOL),
+    ("regprec", "regprec_gibbs", None, "gibbs", None, 0.1, RTOL),
+    ("regprec", "regprec_mwg", None, "mwg", None, 0.1, RTOL),
 ]
 
 

@@ -591,7 +591,9 @@ def test_run_trace_matches_stepwise(g, model):
 # ----------------------------------------------------------------------------------------
 ZOO = [("catmix_small", "catmix"), ("naivebayes_small", "naivebayes"), ("hmm_small", "hmm"),
        ("polyreg_small", "polyreg"), ("polyreg_gibbs", "polyreg"), ("regression_gibbs", "regression"),
-       ("polyreg_mwg", "polyreg"), ("regression_mwg", "regression")]
+       ("polyreg_mwg", "polyreg"), ("regression_mwg", "regression"),
+       # the GammaPrecision conjugate kind (oracle/models/regprec.bn) under MH, Gibbs, MWG
+       ("regprec_mh", "regprec"), ("regprec_gibbs", "regprec"), ("regprec_mwg", "regprec")]
 
 
 def _zoo_engine(g, fx, model):
@@ -631,7 +633,7 @@ def test_zoo_sweeps_vs_reference(g, name, model):
     for it in range(len(fx["lj"])):
         acc = []
         lj = e.sweep(s, it, acc)
-        if model in ("polyreg", "regression"):  # the (last) MH block's decision
+        if model in ("polyreg", "regression", "regprec"):  # the (last) MH block's decision
             assert acc[0] == bool(fx["accepted"][it]), f"accept decision differs at step {it}"
         for n in latent:
             if s[n].dtype == np.int64:

@@ -7,11 +7,12 @@ Everything here is bit-exact: the restatement follows the reference's
 arithmetic expression for expression on the same libm.
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import ROOT, golden
 
 
 class _R(ctypes.Structure):
@@ -194,7 +195,10 @@ def test_observed_phi_protocol(restatement, reference):
                                                ("polyreg_gibbs", "polyreg", "gibbs"),
                                                ("regression_gibbs", "regression", "gibbs"),
                                                ("polyreg_mwg", "polyreg", "mwg"),
-                                               ("regression_mwg", "regression", "mwg")])
+                                               ("regression_mwg", "regression", "mwg"),
+                                               ("regprec_mh", "regprec", "mh"),
+                                               ("regprec_gibbs", "regprec", "gibbs"),
+                                               ("regprec_mwg", "regprec", "mwg")])
 def test_zoo_goldens_vs_live_reference(reference, name, model, method):
     """The zoo fixtures (tests/golden/make_golden.py) are outputs of the compiled
     reference: re-run its prior_init and two sweeps and compare bitwise."""
@@ -217,3 +221,17 @@ def test_zoo_goldens_vs_live_reference(reference, name, model, method):
         assert lj == fx["lj"][it] and acc == bool(fx["accepted"][it])
         for n in latent:
             assert np.array_equal(e.get(n), fx[n][it]), (n, it)
+
+
+def test_regprec_plans_tau_as_gamma_precision():
+    """oracle/models/regprec.bn exercises the reference's GammaPrecision conjugate kind
+    (rewrite.cpp:538-549): the reference CLI's `describe` of its Gibbs plan draws tau ~
+    Gamma(3 + n/2, 1/(1/1 + rss/2))."""
+    import subprocess
+
+    cli = os.path.join(ROOT, "integration", "_build", "bnmc")
+    if not os.path.exists(cli):
+        pytest.skip("reference CLI not built (make -C integration)")
+    d = subprocess.run([cli, "describe", "--model", os.path.join(ROOT, "oracle", "models", "regprec.bn"),
+                        "--method", "gibbs"], capture_output=True, text=True, timeout=60).stdout
+    assert "conjugate draw tau ~ Gamma(3 + n/2, 1/(1/(1) + rss/2))" in d, d
