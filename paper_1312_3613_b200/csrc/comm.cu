@@ -34,6 +34,29 @@ struct PeerPtrs {
   void* p[kMaxPeers];
 };
 
+// Reduce-scatter over peer memory: rank r sums chunk r of all W buffers (rank order) into
+// its OWN buffer only; every other rank reads its own chunk of r's buffer, never r's chunk.
+template <class T>
+__global__ void peer_reduce_scatter_kernel(PeerPtrs b, int world, int r, std::size_t begin, std::size_t end) {
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  for (std::size_t i = begin + blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < end; i += stride) {
+    T acc = static_cast<const T*>(b.p[0])[i];
+    for (int s = 1; s < world; ++s) acc = acc + static_cast<const T*>(b.p[s])[i];
+    static_cast<T*>(b.p[r])[i] = acc;
+  }
+}
+
+// All-gather over peer memory: rank r writes its chunk r into every other rank's buffer.
+template <class T>
+__global__ void peer_all_gather_kernel(PeerPtrs b, int world, int r, std::size_t begin, std::size_t end) {
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  for (std::size_t i = begin + blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < end; i += stride) {
+    const T v = static_cast<const T*>(b.p[r])[i];
+    for (int s = 0; s < world; ++s)
+      if (s != r) static_cast<T*>(b.p[s])[i] = v;
+  }
+}
+
 template <class T, int OP>
 __global__ void peer_allreduce_kernel(PeerPtrs b, int world, std::size_t begin, std::size_t end) {
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
@@ -115,14 +138,18 @@ void launch_reduce(const PeerPtrs& b, int world, std::size_t lo, std::size_t hi,
   }
 }
 
-void group_all_reduce(PeerGroup* g, int r, void* buf, std::size_t n, RedType t, RedOp op, cudaStream_t st) {
+enum class Coll { AllReduce = 0, ReduceScatter = 8, AllGather = 16 };
+
+// n: the whole buffer's elements (W chunks of n / W for the scatter / gather kinds)
+void group_collective(PeerGroup* g, int r, Coll kind, void* buf, std::size_t n, RedType t, RedOp op,
+                      cudaStream_t st) {
   const int W = g->world;
   auto& me = g->slot[static_cast<std::size_t>(r)];
   BNMC_CUDA(cudaEventRecord(me.ev_in, st));
   me.buf = buf;
   me.n = n;
   me.type = static_cast<int>(t);
-  me.op = static_cast<int>(op);
+  me.op = static_cast<int>(op) + static_cast<int>(kind);  // the collective must match, too
   g->rendezvous();  // every rank published its buffer and input event
   PeerPtrs b{};
   for (int s = 0; s < W; ++s) {
@@ -146,8 +173,19 @@ void group_all_reduce(PeerGroup* g, int r, void* buf, std::size_t n, RedType t, 
   for (int s = 0; s < W; ++s) BNMC_CUDA(cudaStreamWaitEvent(st, g->slot[static_cast<std::size_t>(s)].ev_in, 0));
   const std::size_t lo = n * static_cast<std::size_t>(r) / static_cast<std::size_t>(W);
   const std::size_t hi = n * static_cast<std::size_t>(r + 1) / static_cast<std::size_t>(W);
-  if (t == RedType::I32) launch_reduce<int>(b, W, lo, hi, me.op, st);
-  else launch_reduce<double>(b, W, lo, hi, me.op, st);
+  if (kind == Coll::AllReduce) {
+    if (t == RedType::I32) launch_reduce<int>(b, W, lo, hi, static_cast<int>(op), st);
+    else launch_reduce<double>(b, W, lo, hi, static_cast<int>(op), st);
+  } else if (hi > lo) {
+    const unsigned grid = std::min<unsigned>(blocks_for(static_cast<std::int64_t>(hi - lo), 256), 148 * 4);
+    if (kind == Coll::ReduceScatter) {
+      if (t == RedType::I32) peer_reduce_scatter_kernel<int><<<grid, 256, 0, st>>>(b, W, r, lo, hi);
+      else peer_reduce_scatter_kernel<double><<<grid, 256, 0, st>>>(b, W, r, lo, hi);
+    } else {
+      if (t == RedType::I32) peer_all_gather_kernel<int><<<grid, 256, 0, st>>>(b, W, r, lo, hi);
+      else peer_all_gather_kernel<double><<<grid, 256, 0, st>>>(b, W, r, lo, hi);
+    }
+  }
   BNMC_CUDA(cudaGetLastError());
   BNMC_CUDA(cudaEventRecord(me.ev_out, st));
   g->rendezvous();  // every rank's chunk kernel is enqueued
@@ -165,7 +203,31 @@ void Comm::all_reduce(void* buf, std::size_t n, RedType t, RedOp op, cudaStream_
   if (comm) {
     BNMC_NCCL(ncclAllReduce(buf, buf, n, nccl_type(t), nccl_op(op), comm, st));
   } else if (group) {
-    group_all_reduce(group, rank, buf, n, t, op, st);
+    group_collective(group, rank, Coll::AllReduce, buf, n, t, op, st);
+  }
+}
+
+// In place: buf holds world chunks of `chunk` elements; rank r ends with the rank-order sum
+// of chunk r in its chunk r (NCCL's in-place form: recvbuff = sendbuff + rank * recvcount).
+void Comm::reduce_scatter(void* buf, std::size_t chunk, RedType t, cudaStream_t st) const {
+  const std::size_t es = t == RedType::I32 ? sizeof(int) : sizeof(double);
+  if (comm) {
+    BNMC_NCCL(ncclReduceScatter(buf, static_cast<char*>(buf) + es * chunk * static_cast<std::size_t>(rank), chunk,
+                                nccl_type(t), ncclSum, comm, st));
+  } else if (group) {
+    group_collective(group, rank, Coll::ReduceScatter, buf, chunk * static_cast<std::size_t>(world), t, RedOp::Sum, st);
+  }
+}
+
+// In place: every rank's chunk r of buf is replaced by rank r's (NCCL's in-place form:
+// sendbuff = recvbuff + rank * sendcount).
+void Comm::all_gather(void* buf, std::size_t chunk, RedType t, cudaStream_t st) const {
+  const std::size_t es = t == RedType::I32 ? sizeof(int) : sizeof(double);
+  if (comm) {
+    BNMC_NCCL(ncclAllGather(static_cast<char*>(buf) + es * chunk * static_cast<std::size_t>(rank), buf, chunk,
+                            nccl_type(t), comm, st));
+  } else if (group) {
+    group_collective(group, rank, Coll::AllGather, buf, chunk * static_cast<std::size_t>(world), t, RedOp::Sum, st);
   }
 }
 

@@ -214,6 +214,10 @@ struct Comm {
   bool active() const { return comm != nullptr || group != nullptr; }
   // in-place all-reduce of n elements on stream st (collective: every rank calls it)
   void all_reduce(void* buf, std::size_t n, RedType t, RedOp op, cudaStream_t st) const;
+  // in place over world chunks of `chunk` elements: rank r keeps the sum of chunk r /
+  // every rank receives each rank's own chunk (collective: every rank calls it)
+  void reduce_scatter(void* buf, std::size_t chunk, RedType t, cudaStream_t st) const;
+  void all_gather(void* buf, std::size_t chunk, RedType t, cudaStream_t st) const;
 };
 
 // Peer groups (comm.cu): join at context creation, leave at destruction.

@@ -95,6 +95,7 @@ struct LdaArgs {
   int pow_alpha, pow_beta;  // 1/alpha, 1/beta when exactly an integer in [2, 64] (boost by squaring), else 0
   int trow_blocks;          // phi_colsum2: y-blocks finishing the pool's theta rows
   int pool_phi;             // phi_pool: the pool draws the phi cells too (0: phi clamped)
+  int pool_v0, pool_v1;     // phi_pool: the phi rows it draws (sharded: this rank's row slice)
   double phi_norm, phi_lgasum, theta_norm, theta_lgasum;
   std::uint64_t seed;
   std::uint64_t zkey_prefix;  // fold(fold(fold(1, seed), kDiscrete), var_z)
@@ -221,8 +222,9 @@ __global__ void __launch_bounds__(256, BNMC_POOL_MINB) phi_pool_kernel(LdaArgs a
   int* cnt = cnt_s[threadIdx.x >> 5];
   const unsigned lt = (1u << lane) - 1u;
   const double invK = 1.0 / static_cast<double>(a.K);
-  // cells [0, cphi): phi (v, k) in phiT row order; [cphi, cphi + Ml K): theta (m, k)
-  const std::int64_t cphi = a.pool_phi ? static_cast<std::int64_t>(a.V) * a.K : 0;
+  // cells [0, cphi): phi (v, k) of rows [pool_v0, pool_v1) in phiT row order;
+  // [cphi, cphi + Ml K): theta (m, k)
+  const std::int64_t cphi = a.pool_phi ? static_cast<std::int64_t>(a.pool_v1 - a.pool_v0) * a.K : 0;
   const std::int64_t ncells = cphi + a.Ml * a.K;
   const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -236,7 +238,10 @@ __global__ void __launch_bounds__(256, BNMC_POOL_MINB) phi_pool_kernel(LdaArgs a
     // quotient's fractional part stays >= 0.5 / K away from an integer)
     const int jt = static_cast<int>(cphi - c0 <= 0 ? 0 : (cphi - c0 >= n ? n : cphi - c0));
     int pv0 = 0, pk0 = 0, tm0 = 0, tk0 = 0;
-    if (jt > 0) cell_vk(c0, a.K, invK, pv0, pk0);
+    if (jt > 0) {
+      cell_vk(c0, a.K, invK, pv0, pk0);
+      pv0 += a.pool_v0;
+    }
     if (jt < n) cell_vk(c0 + jt - cphi, a.K, invK, tm0, tk0);
     auto vk_of = [&](int j, int& v, int& k) {  // (v or m, k) of chunk cell j
       const int r = j < jt ? pk0 + j : tk0 + (j - jt);
@@ -281,6 +286,7 @@ __global__ void __launch_bounds__(256, BNMC_POOL_MINB) phi_pool_kernel(LdaArgs a
       if (cn < c_end) {
         int v, k;
         cell_vk(cn < cphi ? cn : cn - cphi, a.K, invK, v, k);
+        if (cn < cphi) v += a.pool_v0;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(cn < cphi ? a.nkw + static_cast<std::size_t>(v) * a.Kp + k
                                                                 : a.nmk + static_cast<std::size_t>(v) * a.K + k));
       }
@@ -1946,16 +1952,25 @@ class Lda final : public Model {
     w_.alloc(std::max<std::int64_t>(Nl_, 1));
     z_.alloc(std::max<std::int64_t>(Nl_, 1));
     off_.alloc(Ml_ + 1);
-    phiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    // phi row slices of the sharded phi block: ceil(V / world) rows per rank (arrays padded
+    // to world slices: the collectives move equal chunks)
+    {
+      const int world = comm_.active() ? comm_.world : 1, rank = comm_.active() ? comm_.rank : 0;
+      slice_ = (V_ + world - 1) / world;
+      Vpad_ = static_cast<std::int64_t>(slice_) * world;
+      pv0_ = std::min(V_, rank * slice_);
+      pv1_ = std::min(V_, pv0_ + slice_);
+    }
+    phiT_.alloc(static_cast<std::size_t>(Vpad_) * Kp_);
     if (exact_) logphiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
     // fp32-screened z-step (product weights only); BNMC_ZSTEP_SCREEN=0 disables it.
     const char* sc = std::getenv("BNMC_ZSTEP_SCREEN");
     screen_ = !exact_ && !(sc && std::string(sc) == "0");
     choose_screen();
     Kp32_ = CW32_ * G32_ * RS_;
-    if (screen_) phiT32_.alloc(static_cast<std::size_t>(V_) * Kp32_);
+    if (screen_) phiT32_.alloc(static_cast<std::size_t>(Vpad_) * Kp32_);
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
-    nkw_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    nkw_.alloc(static_cast<std::size_t>(Vpad_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     units_.alloc(std::max<std::size_t>(units_host_.size(), 3));
     tpart_.alloc(std::max<std::int64_t>(Ml_, 1));
@@ -2236,12 +2251,24 @@ class Lda final : public Model {
     mark(st, "begin");
     // warp-pool conjugate block: phi and theta cells in one balanced kernel, then the
     // phi column sums (phi_colsum2 stripes) and the theta rows (extra y-blocks)
-    if (!observe_phi_ && comm_.active()) {
-      comm_.all_reduce(nkw_.p, nkw_.n, RedType::I32, RedOp::Sum, st);
-      mark(st, "allreduce_counts");
+    // Sharded: each rank draws the phi rows of its slice only -- a reduce-scatter gives it
+    // the global counts of those rows (the other rows' local counts are then zeroed for
+    // this sweep's z-step), and an all-gather of the drawn rows follows the pool.  The
+    // draws are keyed by (k, v), so phi is bitwise the unsharded one for every world size.
+    const bool sliced = !observe_phi_ && comm_.active();
+    if (sliced) {
+      comm_.reduce_scatter(nkw_.p, static_cast<std::size_t>(slice_) * Kp_, RedType::I32, st);
+      const std::size_t row = static_cast<std::size_t>(Kp_) * sizeof(int);
+      if (pv0_ > 0) BNMC_CUDA(cudaMemsetAsync(nkw_.p, 0, row * pv0_, st));
+      const std::int64_t after = static_cast<std::int64_t>(pv0_) + slice_;
+      if (Vpad_ > after)
+        BNMC_CUDA(cudaMemsetAsync(nkw_.p + after * Kp_, 0, row * static_cast<std::size_t>(Vpad_ - after), st));
+      mark(st, "reduce_scatter_counts");
     }
     if (observe_phi_) nkw_.zero(st);  // phi clamped: the z-step's counts feed only the w-factor
     a.pool_phi = observe_phi_ ? 0 : 1;
+    a.pool_v0 = pv0_;
+    a.pool_v1 = pv1_;
     a.trow_blocks = Ml_ > 0 ? trow_blocks_ : 0;
     a.col_stripes = observe_phi_ ? 0 : col_stripes_;
     if (a.pool_phi || Ml_ > 0) {
@@ -2250,6 +2277,11 @@ class Lda final : public Model {
       else
         phi_pool_kernel<false><<<pool_blocks_, 256, 0, st>>>(a, out.iter);
       mark(st, "conj_pool");
+      if (sliced) {  // the drawn rows: fp64 g, and their fp32 screen copy (4-byte words)
+        comm_.all_gather(phiT_.p, static_cast<std::size_t>(slice_) * Kp_, RedType::F64, st);
+        if (screen_) comm_.all_gather(phiT32_.p, static_cast<std::size_t>(slice_) * Kp32_, RedType::I32, st);
+        mark(st, "all_gather_phi");
+      }
       launch_pdl(phi_colsum2_kernel, dim3((K_ + 31) / 32, a.col_stripes + a.trow_blocks), dim3(256), 0, st, a);
       fq_reset_ = true;
       mark(st, "colsum_rows");
@@ -2763,6 +2795,8 @@ class Lda final : public Model {
   DevBuf<std::int64_t> off_;
   bool boost_pow_ = std::getenv("BNMC_BOOST_POW") == nullptr || std::string(std::getenv("BNMC_BOOST_POW")) != "0";
   int pool_blocks_ = 148;
+  int slice_ = 1, pv0_ = 0, pv1_ = 1;  // phi rows per rank, this rank's rows [pv0_, pv1_)
+  std::int64_t Vpad_ = 1;
   int trow_blocks_ = 1;   // phi_colsum2 y-blocks for the pool's theta rows
   DevBuf<double> spart_, logS_, ttpart_;
   DevBuf<int> ticket_;
