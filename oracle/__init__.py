@@ -155,6 +155,14 @@ class Restatement:
         self._check(self.lib.bo_lda_draw_phi(ctypes.byref(m), _i(nkw), c_uint64(seed), c_int64(it), _d(phi)))
         return phi
 
+    def lda_phi_gammas(self, K, V, offsets, w, nkw, seed, it, v0, v1):
+        """Unnormalised phi cells of vocabulary columns [v0, v1) (zeros elsewhere)."""
+        m = self._lda(K, V, offsets, w)
+        g = np.zeros(K * V)
+        self._check(self.lib.bo_lda_phi_gammas(ctypes.byref(m), _i(nkw), c_uint64(seed), c_int64(it),
+                                               c_int64(v0), c_int64(v1), _d(g)))
+        return g
+
     def lda_theta_z(self, K, V, offsets, w, z, phi, theta, seed, it, d0, d1):
         m = self._lda(K, V, offsets, w)
         self._check(self.lib.bo_lda_theta_z(ctypes.byref(m), _i(z), _d(phi), _d(theta), c_uint64(seed),

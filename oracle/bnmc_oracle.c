@@ -235,6 +235,21 @@ int bo_lda_draw_phi(const bo_lda* m, const int64_t* nkw, uint64_t seed, int64_t 
   return rc;
 }
 
+int bo_lda_phi_gammas(const bo_lda* m, const int64_t* nkw, uint64_t seed, int64_t iter, int64_t v0,
+                      int64_t v1, double* g) {
+  /* The unnormalised cells g[k][v], v in [v0,v1), of the phi block's Dirichlet batch:
+   * the per-cell streams keyed(seed,4,var_phi,iter).derive(k,v) and Gamma(beta + count)
+   * draws of bo_dirichlet_batch (batch.cpp:38-41, 45-83) -- the vocabulary slice a rank
+   * of the sharded sweep draws before the all-gather and the row normalisation. */
+  const uint64_t key = bo_keyed(seed, P_CONJUGATE, (uint64_t)m->var_phi, (uint64_t)iter, 0);
+  for (int64_t k = 0; k < m->K; ++k)
+    for (int64_t v = v0; v < v1; ++v) {
+      bo_rng r = stream(bo_derive(key, (uint64_t)k, (uint64_t)v));
+      g[k * m->V + v] = bo_draw_gamma(&r, m->beta + (double)nkw[k * m->V + v]);
+    }
+  return 0;
+}
+
 int bo_lda_theta_z(const bo_lda* m, int64_t* z, const double* phi, double* theta, uint64_t seed,
                    int64_t iter, int64_t d0, int64_t d1) {
   const int64_t K = m->K, V = m->V;

@@ -74,6 +74,9 @@ int bo_lda_count_phi(const bo_lda* m, const int64_t* z, int64_t d0, int64_t d1, 
 /* phi block draw from counts (sampler.cpp:138-181 + batch.cpp). */
 int bo_lda_draw_phi(const bo_lda* m, const int64_t* nkw, uint64_t seed, int64_t iter,
                     double* phi);
+/* The phi block's unnormalised gamma cells g[k*V+v] for v in [v0,v1) (batch.cpp:38-41). */
+int bo_lda_phi_gammas(const bo_lda* m, const int64_t* nkw, uint64_t seed, int64_t iter, int64_t v0,
+                      int64_t v1, double* g);
 /* theta block (counts + draw) then z block for documents [d0,d1) (sampler.cpp:222-265). */
 int bo_lda_theta_z(const bo_lda* m, int64_t* z, const double* phi, double* theta, uint64_t seed,
                    int64_t iter, int64_t d0, int64_t d1);

@@ -1,12 +1,15 @@
 """CPU, world_size 2 over gloo: the document-sharded sweep decomposition is exact.
 
-The multi-GPU LDA sweep (csrc/lda.cu) runs per rank: local topic-word counts ->
-all-reduce (NCCL) -> identical phi draw on every rank (counter RNG keyed by (k, v,
-iter), no broadcast) -> theta + z blocks on the rank's own documents (keys use
-GLOBAL document / token indices) -> all-reduce of the log-joint pieces.  Here the
-same decomposition runs on the oracle restatement with torch.distributed/gloo as
-the collective and the C-ABI's own partition (bnmc_gpu_partition); the gathered
-state must equal the unsharded reference sweep bit for bit.
+The multi-GPU LDA sweep (csrc/lda.cu) runs per rank: local
+topic-word counts -> reduce-scatter by vocabulary slices of ceil(V / W) columns -> the
+rank draws the phi cells of ITS slice only (counter RNG keyed by (k, v, iter)) ->
+all-gather of the drawn cells -> the Dirichlet row normalisation over the gathered cells
+(identical on every rank) -> theta + z blocks on the rank's own documents (keys use
+GLOBAL document / token indices) -> all-reduce of the log-joint pieces.  Here the same
+decomposition runs on the oracle restatement with torch.distributed/gloo as the
+collective (reduce-scatter = all-reduce + own slice) and the C-ABI's own partition
+(bnmc_gpu_partition); the gathered state must equal the unsharded reference sweep bit
+for bit.  The CUDA path itself runs W ranks on one GPU in tests/test_gpu_shard.py.
 """
 import os
 import socket
@@ -45,8 +48,17 @@ def _worker(rank, world, port, name, sweeps, out_dir):
     for it in range(sweeps):
         nkw = R.lda_count_phi(K, V, off, w, z, b, e)              # local counts
         t = torch.from_numpy(nkw)
-        dist.all_reduce(t)                                        # the per-sweep exchange
-        phi = R.lda_draw_phi(K, V, off, w, t.numpy(), seed, it)   # identical on every rank
+        dist.all_reduce(t)                                        # reduce-scatter: this rank
+        sl = -(-V // world)                                       # uses its slice's columns
+        v0, v1 = min(V, rank * sl), min(V, rank * sl + sl)
+        gam = R.lda_phi_gammas(K, V, off, w, t.numpy(), seed, it, v0, v1)
+        parts = [None] * world                                    # all-gather of the slices
+        dist.all_gather_object(parts, (v0, v1, gam.reshape(K, V)[:, v0:v1].copy()))
+        g = np.zeros((K, V))
+        for p0, p1, pg in parts:
+            g[:, p0:p1] = pg
+        S = np.cumsum(g, axis=1)[:, -1:]                          # left-to-right row sums and
+        phi = (g / S).ravel()                                     # normalisation (batch.cpp:55-61)
         R.lda_theta_z(K, V, off, w, z, phi, theta, seed, it, b, e)
         # local pieces of the log-joint, summed over ranks
         zt = sum(np.log(theta[d * K + z[off[d]:off[d + 1]]]).sum() for d in range(b, e))
