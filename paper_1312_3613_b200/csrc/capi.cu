@@ -448,6 +448,9 @@ int bnmc_gpu_register_host(bnmc_gpu_ctx* c, const bnmc_gpu_store* s) {
     c->registered = keep;
     for (auto& r : want) {
       if (std::find(c->registered.begin(), c->registered.end(), r) != c->registered.end()) continue;
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, r.first) == cudaSuccess && pa.type == cudaMemoryTypeHost) continue;
+      cudaGetLastError();  // (pageable memory: "not a CUDA pointer" on older drivers)
       const cudaError_t e = cudaHostRegister(r.first, r.second, cudaHostRegisterDefault);
       if (e == cudaErrorHostMemoryAlreadyRegistered) {
         cudaGetLastError();  // page-locked by its owner already: not ours to release

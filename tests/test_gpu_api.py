@@ -123,3 +123,25 @@ def test_observed_edit_needs_rebind(g):
     assert np.array_equal(s["z"], t["z"])
     e.close()
     f.close()
+
+
+@pytest.mark.gpu
+def test_store_already_page_locked_by_its_owner(g):
+    """A store whose arrays are already pinned (torch pin_memory / cudaHostAlloc) binds: the
+    engine's one-time page-locking skips them instead of failing."""
+    import torch
+
+    fx = golden("lda_desk")
+    e, s = _lda(g, fx)
+    for n in s.names:
+        if not s.observed[n]:
+            t = torch.empty(s.arrays[n].size, dtype=torch.from_numpy(s.arrays[n][:0]).dtype, pin_memory=True)
+            a = t.numpy()
+            a[:] = s.arrays[n]
+            s.arrays[n] = a
+    f, t2 = _lda(g, fx)
+    for it in range(2):
+        assert e.sweep(s, it) == f.sweep(t2, it)
+        assert np.array_equal(s["z"], t2["z"])
+    e.close()
+    f.close()
