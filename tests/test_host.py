@@ -3,6 +3,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -180,3 +181,24 @@ def test_reference_reads_the_bench_corpus(tmp_path):
     x.tofile(str(tmp_path / "x.f64"))
     res, _ = bench.ref_bench(["gmm-file", str(tmp_path / "x.f64"), 3, 1, 0, 2], timeout=120)
     assert res["sites"] == 500
+
+
+def test_bench_self_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself
+    (torch.distributed.run, 127.0.0.1); with --impl reference rank 0 alone prints the
+    line and rank 1 exits 0 without work -- the driver's reference-arm contract, here on
+    the CPU with the GMM workload (its reference run takes ~1 s)."""
+    import json
+
+    from oracle import REF_BENCH
+
+    if not os.path.exists(REF_BENCH):
+        pytest.skip("reference not built")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--workload", "gmm", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
