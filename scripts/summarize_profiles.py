@@ -66,7 +66,7 @@ WANT = [
 
 
 def to_bytes(v, unit):
-    f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit)
+    f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit)
     return float(v) * f if f else None
 
 
