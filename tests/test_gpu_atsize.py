@@ -169,3 +169,34 @@ def test_mh_linreg_1e5x64_10_steps(g):
             assert rel(s[v], ref[v][it]) < RTOL_PARAM, (it, v)
         assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
     e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# A long LDA chain: 300 sweeps from the reference's prior_init, posterior summaries
+# ----------------------------------------------------------------------------------------
+def test_lda_long_chain_posterior_vs_reference(g):
+    """north_star (b): posterior summaries over many sweeps.  A 300-sweep chain on a
+    gen_lda corpus (200 documents x 60 tokens, V = 500, K = 10): z equal to the live
+    reference's on EVERY sweep (the whole chain, not one step), the log-joint trajectory
+    within 1e-10, and the posterior means of phi and theta over the last 150 sweeps within
+    1e-10 relative."""
+    M, V, K, L, seed, n = 200, 500, 10, 60, 11, 300
+    ref = run_chain({"model": "lda", "hyper": {"K": K, "V": V, "M": M, "N": [L] * M}, "method": "gibbs",
+                     "seed": seed, "threads": 1, "gen": ["lda", [M, V, K, L, seed]], "observed": ["w"],
+                     "init": "prior", "sweeps": n, "record": ["z", "phi", "theta"]}, timeout=1800)
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed))
+    s = e.allocate()
+    s["w"] = ref["w"]
+    e.prior_init(s, seed)
+    assert np.array_equal(s["z"], ref["z_init"])
+    phis, thetas = [], []
+    for it in range(n):
+        lj = e.sweep(s, it)
+        assert np.array_equal(s["z"], ref["z"][it]), f"z differs at sweep {it}"
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+        if it >= n // 2:
+            phis.append(s["phi"].copy())
+            thetas.append(s["theta"].copy())
+    assert rel(np.mean(phis, axis=0), ref["phi"][n // 2:].mean(axis=0)) < 1e-10
+    assert rel(np.mean(thetas, axis=0), ref["theta"][n // 2:].mean(axis=0)) < 1e-10
+    e.close()
