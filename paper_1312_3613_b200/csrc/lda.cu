@@ -133,22 +133,25 @@ __device__ __forceinline__ double boost_factor(double u, int e, double inv) {
 constexpr int kGammaTab = 64;
 
 // phi + theta block ("warp pool"): a persistent grid (one resident wave) in which warp w
-// owns the contiguous cell range [w C / W, (w+1) C / W) of the C = V K cells (k
-// fastest, the phiT row order), so every warp has the same number of cells.  The 32
-// lanes draw the range as one pool, <= kPoolCells cells (one shared-memory chunk of
-// counts) at a time: every iteration each lane makes one Marsaglia-Tsang attempt on
-// its current cell, and the lanes whose attempt was accepted take the next undrawn
-// cells (ballot + prefix rank).  A warp iterates ~(cells x 1.06) / 32 times with all
-// lanes busy until the chunk's last attempts -- the v2 kernel's lanes each ran their
-// own cells' rejection sequences and waited for the slowest lane of the warp (ncu
-// r01: ~930 thread instructions per cell, 20.7 of 32 lanes active per instruction)
-// and its 1.64-wave grid left a tail.
-// * No column partials and no per-cell log here: phi_colsum2<true> sums the columns of
-//   phiT directly (sum g, and sum log g as the log of a frexp-renormalised product),
-//   and the log-joint's w-factor takes log g of the counted cells (wterm_kernel).
-// * Streams keyed(seed, 4, var_phi, iter).derive(k, v), consumed in the reference's
-//   order (gaussian until 1 + c x > 0, uniform, [boost uniform]; dist.cpp:136-155):
-//   the draws are the reference's whichever lane draws a cell.
+// owns the contiguous range [w C / W, (w+1) C / W) of the C cells of the sweep's conjugate
+// draws -- the phi cells (v, k) of rows [pool_v0, pool_v1) in phiT row order (all V rows
+// on one GPU, the rank's row slice when sharded), then the theta cells (m, k) of the
+// rank's documents -- so every warp has the same number of cells.  The 32 lanes draw the
+// range as one pool, <= kPoolCells cells (one shared-memory chunk of counts) at a time:
+// every iteration each lane makes one Marsaglia-Tsang attempt on its current cell, and the
+// lanes whose attempt was accepted take the next undrawn cells (ballot + prefix rank).  A
+// warp iterates ~(cells x 1.06) / 32 times with all lanes busy until the chunk's last
+// attempts -- the r01 kernels' lanes each ran their own cells' rejection sequences and
+// waited for the slowest lane of the warp (ncu: ~930 thread instructions per cell, 20.7 of
+// 32 lanes active per instruction), the phi grid left a 1.64-wave tail and theta ran on a
+// side stream.
+// * No column partials and no per-cell log here: phi_colsum2_kernel sums the columns of
+//   phiT directly (sum g, and sum log g as the log of a frexp-renormalised product) and
+//   finishes the theta rows; the log-joint's w-factor takes log g of the counted cells
+//   (wterm_kernel).
+// * Streams keyed(seed, 4, var, iter).derive(k, v) (phi) / .derive(doc, k) (theta),
+//   consumed in the reference's order (gaussian until 1 + c x > 0, uniform, [boost
+//   uniform]; dist.cpp:136-155): the draws are the reference's whichever lane draws a cell.
 constexpr int kPoolCells = 512;
 constexpr int kPoolWarps = 8;
 
@@ -186,11 +189,8 @@ __device__ __forceinline__ bool mt_log_test(double u, double x, double v, double
   return log(u) < 0.5 * x * x + d * (1.0 - v + log(v));
 }
 
-#ifndef BNMC_POOL_MINB
-#define BNMC_POOL_MINB 1
-#endif
 template <bool KTAB>
-__global__ void __launch_bounds__(256, BNMC_POOL_MINB) phi_pool_kernel(LdaArgs a, const std::int64_t* iter_p) {
+__global__ void __launch_bounds__(256) phi_pool_kernel(LdaArgs a, const std::int64_t* iter_p) {
   __shared__ double tab_d[2][kGammaTab], tab_c[2][kGammaTab], tab_inv[2][kGammaTab];
   __shared__ std::uint64_t kkey_s[KTAB ? kPoolCells : 1];
   __shared__ int col32_s[KTAB ? kPoolCells : 1];
