@@ -876,3 +876,35 @@ def test_zoo_run_trace_matches_stepwise(g, name, model):
         assert np.array_equal(tr["map_state"][x], map_state[x]), x
     e1.close()
     e2.close()
+
+
+def test_lda_joint_known_answer(g):
+    """The reference's lda_joint_oracle (tests/test_ir.cpp:148-177): the LDA log-joint of a
+    tiny state written against the arrays directly -- Dirichlet(0.1) terms of every phi
+    and theta row plus sum_t log theta[d_t, z_t] + log phi[z_t, w_t] -- against the
+    device's eval_log_joint."""
+    from math import lgamma, log
+
+    K, V, lengths = 2, 3, [3, 4]
+    rs = np.random.default_rng(7)
+    phi = rs.dirichlet(np.ones(V), size=K)
+    theta = rs.dirichlet(np.ones(K), size=len(lengths))
+    N = sum(lengths)
+    z = rs.integers(0, K, N)
+    w = rs.integers(0, V, N)
+
+    def dterm(x, a):
+        return sum((a - 1.0) * log(xi) for xi in x) - len(x) * lgamma(a) + lgamma(a * len(x))
+
+    want = sum(dterm(phi[k], 0.1) for k in range(K)) + sum(dterm(theta[m], 0.1) for m in range(len(lengths)))
+    t = 0
+    for m, L in enumerate(lengths):
+        for _ in range(L):
+            want += log(theta[m, z[t]]) + log(phi[z[t], w[t]])
+            t += 1
+    e = g.Engine("lda", {"K": K, "V": V, "M": len(lengths), "N": lengths}, g.RunConfig(seed=1))
+    s = e.allocate()
+    s["phi"], s["theta"], s["z"], s["w"] = phi.ravel(), theta.ravel(), z, w
+    got = e.eval_log_joint(s)
+    assert abs(got - want) <= 1e-12 * abs(want), (got, want)
+    e.close()
