@@ -1990,11 +1990,15 @@ class Lda final : public Model {
       int dev = 0, sms = 148, per_sm = 1;
       BNMC_CUDA(cudaGetDevice(&dev));
       BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      if (K_ <= kPoolCells)
+      if (K_ <= kPoolCells) {
         BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<true>, 256, 0));
-      else
+        // 3 resident blocks/SM measured ~2 us faster than 4 on NIPS/KOS (more L1 left
+        // beside the tables); 3.5 and 2 are both slower
+        per_sm = std::min(per_sm, 3);
+      } else
         BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phi_pool_kernel<false>, 256, 0));
       pool_blocks_ = sms * std::max(per_sm, 1);
+      if (const char* e = std::getenv("BNMC_POOL_BLOCKS")) pool_blocks_ = std::max(1, std::atoi(e));
     }
     // column-sum stripes of ~48 rows (<= 128), theta-row blocks of 8 warps (one row each)
     col_stripes_ = static_cast<int>(std::min<std::int64_t>(kColStripes, std::max<std::int64_t>(4, V_ / 48)));
