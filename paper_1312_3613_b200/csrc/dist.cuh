@@ -44,6 +44,28 @@ __device__ __forceinline__ double draw_gamma(Stream& rng, double shape) {
   return g;
 }
 
+// The counters draw_gamma(rng, shape) consumes, without its value: the same attempt
+// sequence (the acceptance tests need x, v, u), no d * v and no boost power.
+__device__ __forceinline__ void skip_gamma(Stream& rng, double shape) {
+  if (!(shape > 0.0)) return;
+  const bool boost = shape < 1.0;
+  const double a = boost ? shape + 1.0 : shape;
+  const double d = a - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (;;) {
+    double x, v;
+    do {
+      x = rng.next_gaussian();
+      v = 1.0 + c * x;
+    } while (v <= 0.0);
+    v = v * v * v;
+    const double u = rng.next_unit();
+    if (u < 1.0 - 0.0331 * (x * x) * (x * x)) break;
+    if (log(u) < 0.5 * x * x + d * (1.0 - v + log(v))) break;
+  }
+  if (boost) rng.next_u64();
+}
+
 // log_pdf_gaussian (dist.cpp:61-68); variance parameterisation.
 __device__ __forceinline__ double log_pdf_gaussian(double x, double mean, double var) {
   if (!(var > 0.0)) return -INFINITY;

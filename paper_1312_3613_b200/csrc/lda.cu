@@ -1785,6 +1785,124 @@ __global__ void prior_rows_kernel(double* out, std::int64_t rows, int cols, std:
   for (int c = 0; c < cols; ++c) out[r * ld_row + c * ld_col] /= sum;
 }
 
+// Long Dirichlet rows (phi's V columns per topic) drawn in parallel, same values.
+// A row's gammas come from ONE stream whose counters each gamma consumes in a
+// data-dependent number (Marsaglia-Tsang rejections), so the start of gamma j is
+// known only after gamma j-1. The stream is counter-based (any position can be
+// entered directly), so the row's counter range is cut into segments of kPriorSeg:
+//   walk:  from each of kPriorCand candidate entries s, s+1, .. of every segment,
+//          count the gammas that start inside it and the first start beyond it;
+//   link:  per row, left to right: the true entry of segment i is segment i-1's exit;
+//          it is a candidate (or the second start of one) except after a rare long
+//          rejection run, where this thread walks the segment itself;
+//   draw:  every segment redraws its gammas from its true entry into their columns;
+//   sum:   per row, the left-to-right sum (draw_dirichlet's order), then normalise.
+constexpr int kPriorSeg = 512, kPriorCand = 4;
+
+__global__ void prior_seg_walk_kernel(std::int64_t rows, int nseg, double conc, std::uint64_t seed, int var,
+                                      std::int64_t row_base, int* cnt, std::int64_t* exit_pos,
+                                      std::int64_t* second) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows * nseg * kPriorCand) return;
+  const int cand = static_cast<int>(i % kPriorCand);
+  const std::int64_t rs = i / kPriorCand, r = rs / nseg;
+  const std::int64_t seg = rs % nseg, end = (seg + 1) * kPriorSeg;
+  Stream s(keyed(seed, kInit, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(row_base + r)),
+           static_cast<std::uint64_t>(seg * kPriorSeg + cand));
+  int c = 0;
+  std::int64_t sec = -1;
+  while (static_cast<std::int64_t>(s.counter) < end) {
+    skip_gamma(s, conc);
+    if (++c == 1) sec = static_cast<std::int64_t>(s.counter);
+  }
+  cnt[i] = c;
+  exit_pos[i] = static_cast<std::int64_t>(s.counter);
+  second[i] = sec;
+}
+
+__global__ void prior_seg_link_kernel(std::int64_t rows, int cols, int nseg, double conc, std::uint64_t seed,
+                                      int var, std::int64_t row_base, const int* cnt, const std::int64_t* exit_pos,
+                                      const std::int64_t* second, std::int64_t* entry, int* first_col) {
+  const std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const std::uint64_t key = keyed(seed, kInit, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(row_base + r));
+  std::int64_t t = 0;
+  int col = 0;
+  for (int seg = 0; seg < nseg; ++seg) {
+    const std::int64_t rs = r * nseg + seg;
+    entry[rs] = t;
+    first_col[rs] = col;
+    if (col >= cols || seg == nseg - 1) continue;  // the last segment runs open-ended
+    const std::int64_t s0 = static_cast<std::int64_t>(seg) * kPriorSeg, d = t - s0;
+    const std::int64_t* ex = exit_pos + rs * kPriorCand;
+    const int* cn = cnt + rs * kPriorCand;
+    int hit = -1, skip = 0;
+    if (d < kPriorCand) {
+      hit = static_cast<int>(d);
+    } else {
+      for (int j = 0; j < kPriorCand; ++j)
+        if (second[rs * kPriorCand + j] == t) hit = j, skip = 1;
+    }
+    if (hit >= 0 && cn[hit] > skip) {
+      col += cn[hit] - skip;
+      t = ex[hit];
+    } else {
+      Stream s(key, static_cast<std::uint64_t>(t));
+      while (static_cast<std::int64_t>(s.counter) < s0 + kPriorSeg) {
+        skip_gamma(s, conc);
+        ++col;
+      }
+      t = static_cast<std::int64_t>(s.counter);
+    }
+  }
+}
+
+__global__ void prior_seg_draw_kernel(double* out, std::int64_t rows, int cols, int nseg, std::int64_t ld_row,
+                                      std::int64_t ld_col, double conc, std::uint64_t seed, int var,
+                                      std::int64_t row_base, const std::int64_t* entry, const int* first_col) {
+  const std::int64_t rs = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (rs >= rows * nseg) return;
+  const std::int64_t r = rs / nseg;
+  const int seg = static_cast<int>(rs % nseg);
+  int col = first_col[rs];
+  if (col >= cols) return;
+  const std::int64_t end = seg == nseg - 1 ? INT64_MAX : static_cast<std::int64_t>(seg + 1) * kPriorSeg;
+  Stream s(keyed(seed, kInit, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(row_base + r)),
+           static_cast<std::uint64_t>(entry[rs]));
+  while (col < cols && static_cast<std::int64_t>(s.counter) < end)
+    out[r * ld_row + static_cast<std::int64_t>(col++) * ld_col] = draw_gamma(s, conc);
+}
+
+// draw_dirichlet's sum (left to right) per row, thread per row.
+__global__ void prior_row_sum_kernel(const double* out, std::int64_t rows, int cols, std::int64_t ld_row,
+                                     std::int64_t ld_col, double* sums) {
+  const std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const double* p = out + r * ld_row;
+  double sum = 0.0;
+  int c = 0;
+  for (; c + 8 <= cols; c += 8) {
+    double g[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = p[static_cast<std::int64_t>(c + j) * ld_col];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum += g[j];
+  }
+  for (; c < cols; ++c) sum += p[static_cast<std::int64_t>(c) * ld_col];
+  sums[r] = sum;
+}
+
+__global__ void prior_row_norm_kernel(double* out, std::int64_t rows, int cols, std::int64_t ld_row,
+                                      std::int64_t ld_col, const double* sums) {
+  const std::int64_t n = rows * cols;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    // consecutive threads on consecutive rows when the rows are the inner dimension
+    const std::int64_t r = ld_row == 1 ? i % rows : i / cols, c = ld_row == 1 ? i / rows : i % cols;
+    out[r * ld_row + c * ld_col] /= sums[r];
+  }
+}
+
 // z ~ Categorical(theta[d]) by linear scan (draw_categorical, dist.cpp:183-191).
 __global__ void prior_z_kernel(LdaArgs a, std::uint64_t seed) {
   for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
@@ -1859,6 +1977,44 @@ double seq_sum_const(double x, std::int64_t n) {  // sum of n copies, left to ri
   double s = 0.0;
   for (std::int64_t i = 0; i < n; ++i) s += x;
   return s;
+}
+
+// prior_init's Dirichlet rows: thread per row for short rows (theta), the segmented
+// walk above for long ones (phi's V columns); BNMC_PRIOR_SERIAL=1 forces thread per row.
+// Returns after the rows are written (the walk's scratch is freed here).
+void dirichlet_rows(double* out, std::int64_t rows, int cols, std::int64_t ld_row, std::int64_t ld_col, double conc,
+                    std::uint64_t seed, int var, std::int64_t row_base, cudaStream_t st) {
+  const char* e = std::getenv("BNMC_PRIOR_SERIAL");
+  const bool serial = (e && std::string(e) != "0") || cols < 4 * kPriorSeg || rows > 148 * 64 || !(conc > 0.0);
+  if (serial) {
+    prior_rows_kernel<<<blocks_for(rows, 64), 64, 0, st>>>(out, rows, cols, ld_row, ld_col, conc, seed, var, row_base);
+    BNMC_CUDA(cudaGetLastError());
+    return;
+  }
+  // counters per gamma: 3 per attempt (+2 per v <= 0 retry), +1 for the shape < 1 boost;
+  // over-estimated (a short estimate only lengthens the open-ended last segment)
+  const double per = conc < 1.0 ? 4.4 : 3.4;
+  const int nseg = static_cast<int>((per * cols + 256) / kPriorSeg) + 1;
+  const std::int64_t ns = rows * nseg;
+  DevBuf<int> cnt, first_col;
+  DevBuf<std::int64_t> exit_pos, second, entry;
+  DevBuf<double> sums;
+  cnt.alloc(ns * kPriorCand);
+  exit_pos.alloc(ns * kPriorCand);
+  second.alloc(ns * kPriorCand);
+  entry.alloc(ns);
+  first_col.alloc(ns);
+  sums.alloc(rows);
+  prior_seg_walk_kernel<<<blocks_for(ns * kPriorCand, 128), 128, 0, st>>>(rows, nseg, conc, seed, var, row_base,
+                                                                          cnt.p, exit_pos.p, second.p);
+  prior_seg_link_kernel<<<blocks_for(rows, 32), 32, 0, st>>>(rows, cols, nseg, conc, seed, var, row_base, cnt.p,
+                                                              exit_pos.p, second.p, entry.p, first_col.p);
+  prior_seg_draw_kernel<<<blocks_for(ns, 128), 128, 0, st>>>(out, rows, cols, nseg, ld_row, ld_col, conc, seed, var,
+                                                              row_base, entry.p, first_col.p);
+  prior_row_sum_kernel<<<blocks_for(rows, 32), 32, 0, st>>>(out, rows, cols, ld_row, ld_col, sums.p);
+  prior_row_norm_kernel<<<148 * 8, 256, 0, st>>>(out, rows, cols, ld_row, ld_col, sums.p);
+  BNMC_CUDA(cudaGetLastError());
+  BNMC_CUDA(cudaStreamSynchronize(st));
 }
 
 class Lda final : public Model {
@@ -2342,10 +2498,9 @@ class Lda final : public Model {
   void prior_init(std::uint64_t seed, cudaStream_t st) override {
     LdaArgs a = args();
     if (!observe_phi_)
-      prior_rows_kernel<<<blocks_for(K_, 32), 32, 0, st>>>(phiT_.p, K_, V_, 1, Kp_, beta_, seed, var_phi_, 0);
+      dirichlet_rows(phiT_.p, K_, V_, 1, Kp_, beta_, seed, var_phi_, 0, st);
     if (Ml_ > 0) {
-      prior_rows_kernel<<<blocks_for(Ml_, 64), 64, 0, st>>>(theta_.p, Ml_, K_, K_, 1, alpha_, seed,
-                                                           var_theta_, d0_);
+      dirichlet_rows(theta_.p, Ml_, K_, K_, 1, alpha_, seed, var_theta_, d0_, st);
       prior_z_kernel<<<grid_docs(), 256, 0, st>>>(a, seed);
     }
     BNMC_CUDA(cudaGetLastError());
@@ -2450,11 +2605,10 @@ class Lda final : public Model {
     DevBuf<double> cum, th;
     cum.alloc(static_cast<std::size_t>(K_) * V_);
     th.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
-    prior_rows_kernel<<<blocks_for(K_, 32), 32, 0, st>>>(cum.p, K_, V_, V_, 1, phi_conc, seed ^ 0xDA7Aull, 0, 0);
+    dirichlet_rows(cum.p, K_, V_, V_, 1, phi_conc, seed ^ 0xDA7Aull, 0, 0, st);
     row_cumsum_kernel<<<blocks_for(K_, 32), 32, 0, st>>>(cum.p, K_, V_);
     if (Ml_ > 0) {
-      prior_rows_kernel<<<blocks_for(Ml_, 64), 64, 0, st>>>(th.p, Ml_, K_, K_, 1, theta_conc,
-                                                           seed ^ 0xDA7Aull, 1, d0_);
+      dirichlet_rows(th.p, Ml_, K_, K_, 1, theta_conc, seed ^ 0xDA7Aull, 1, d0_, st);
       LdaArgs a = args();
       gen_tokens_kernel<<<grid_docs(), 256, 0, st>>>(a, cum.p, th.p, seed);
     }

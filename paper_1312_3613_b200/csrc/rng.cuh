@@ -42,6 +42,9 @@ struct Stream {
   std::uint64_t pos;  // key + kGolden * counter (mod 2^64), advanced by addition
 
   __device__ __forceinline__ explicit Stream(std::uint64_t k) : key(k), counter(0), pos(k) {}
+  // the stream after `at` draws (counter-based: no draws replayed)
+  __device__ __forceinline__ Stream(std::uint64_t k, std::uint64_t at)
+      : key(k), counter(at), pos(k + kGolden * at) {}
 
   // mix(key + kGolden * ++counter) (rng.hpp:40); the product is carried incrementally
   // (one 64-bit add instead of a 64-bit multiply per draw; identical modulo 2^64).

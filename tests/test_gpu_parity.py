@@ -369,6 +369,50 @@ def test_lda_device_prior_init_matches_reference(g, restatement):
     assert np.array_equal(s["z"], fx["z0"])
 
 
+@pytest.mark.parametrize("V,K", [(12419, 100), (100000, 4), (2048, 3)], ids=["nips", "v1e5", "v2048"])
+def test_lda_prior_init_long_rows(g, restatement, monkeypatch, V, K):
+    """prior_init's phi rows (V gammas from one stream each, dist.cpp:193-200) drawn by the
+    segmented walk (lda.cu dirichlet_rows): bitwise the thread-per-row draw, and the
+    restatement (pinned to the reference) within tolerance; z exact."""
+    M, L, seed = 24, 40, 11
+    w = np.random.default_rng(seed).integers(0, V, M * L).astype(np.int64)
+    off = np.arange(M + 1, dtype=np.int64) * L
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+    got = {}
+    for serial in ("1", "0"):
+        monkeypatch.setenv("BNMC_PRIOR_SERIAL", serial)
+        e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+        s = e.allocate()
+        s["w"] = w
+        e.prior_init(s, seed)
+        got[serial] = (s["phi"].copy(), s["theta"].copy(), s["z"].copy())
+        e.close()
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
+    phi, theta, z = restatement.lda_prior_init(K, V, off, w, seed)
+    assert rel(got["0"][0], phi) < RTOL_PARAM
+    assert rel(got["0"][1], theta) < RTOL_PARAM
+    assert np.array_equal(got["0"][2], z)
+
+
+def test_lda_generate_long_rows(g, monkeypatch):
+    """lda_generate's true-phi rows (concentration 0.05, gen.cpp:26-31) through the
+    segmented walk: the corpus and the prior state equal the thread-per-row draw's."""
+    K, V, M, L, seed = 6, 100000, 16, 64, 5
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+    got = {}
+    for serial in ("1", "0"):
+        monkeypatch.setenv("BNMC_PRIOR_SERIAL", serial)
+        e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+        e.lda_generate(seed)
+        s = e.allocate()
+        e.download(s)
+        got[serial] = (e.lda_counts()[0].copy(), s["phi"].copy(), s["z"].copy())
+        e.close()
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
+
+
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
