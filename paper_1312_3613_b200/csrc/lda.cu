@@ -1873,23 +1873,39 @@ __global__ void prior_seg_draw_kernel(double* out, std::int64_t rows, int cols, 
     out[r * ld_row + static_cast<std::int64_t>(col++) * ld_col] = draw_gamma(s, conc);
 }
 
-// draw_dirichlet's sum (left to right) per row, thread per row.
-__global__ void prior_row_sum_kernel(const double* out, std::int64_t rows, int cols, std::int64_t ld_row,
-                                     std::int64_t ld_col, double* sums) {
-  const std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+// Left-to-right row sums (draw_dirichlet's order) or running sums (kCum, in place), one
+// warp per row: the warp stages 256-column tiles through shared memory, lane 0 adds them
+// in order (the roundings of a sequential loop), the warp writes running sums back.
+constexpr int kScanTile = 256, kScanWarps = 4;
+
+template <bool kCum>
+__global__ void __launch_bounds__(32 * kScanWarps) row_scan_kernel(double* x, std::int64_t rows, int cols,
+                                                                     std::int64_t ld_row, std::int64_t ld_col,
+                                                                     double* sums) {
+  __shared__ double tile[kScanWarps][kScanTile];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const std::int64_t r = blockIdx.x * static_cast<std::int64_t>(kScanWarps) + wi;
   if (r >= rows) return;
-  const double* p = out + r * ld_row;
-  double sum = 0.0;
-  int c = 0;
-  for (; c + 8 <= cols; c += 8) {
-    double g[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) g[j] = p[static_cast<std::int64_t>(c + j) * ld_col];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sum += g[j];
+  double* row = x + r * ld_row;
+  double* tl = tile[wi];
+  double acc = 0.0;
+  for (int c0 = 0; c0 < cols; c0 += kScanTile) {
+    const int n = min(kScanTile, cols - c0);
+    for (int j = lane; j < n; j += 32) tl[j] = row[static_cast<std::int64_t>(c0 + j) * ld_col];
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll 8
+      for (int j = 0; j < n; ++j) {
+        acc += tl[j];
+        if (kCum) tl[j] = acc;
+      }
+    }
+    __syncwarp();
+    if (kCum)
+      for (int j = lane; j < n; j += 32) row[static_cast<std::int64_t>(c0 + j) * ld_col] = tl[j];
+    __syncwarp();
   }
-  for (; c < cols; ++c) sum += p[static_cast<std::int64_t>(c) * ld_col];
-  sums[r] = sum;
+  if (!kCum && lane == 0) sums[r] = acc;
 }
 
 __global__ void prior_row_norm_kernel(double* out, std::int64_t rows, int cols, std::int64_t ld_row,
@@ -1903,25 +1919,61 @@ __global__ void prior_row_norm_kernel(double* out, std::int64_t rows, int cols, 
   }
 }
 
-// z ~ Categorical(theta[d]) by linear scan (draw_categorical, dist.cpp:183-191).
+// z ~ Categorical(theta[d]) (draw_categorical, dist.cpp:183-191): the reference scans
+// acc += theta[k] until u < acc. The running sums are formed once per document, left to
+// right by one thread (the same roundings), in shared memory; each token then binary-
+// searches the first k with u < acc[k] (acc is non-decreasing: the same pick as the scan,
+// K-1 when u is beyond the last sum). kSmem = false: K too large for shared memory, scan.
+__device__ __forceinline__ void doc_cumsum_smem(const double* th, int K, double* cum) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) cum[k] = th[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      acc += cum[k];
+      cum[k] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int first_above(const double* cum, int n, double u) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (u < cum[mid])
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int scan_pick(const double* th, int K, double u) {
+  double acc = 0.0;
+  for (int k = 0; k < K; ++k) {
+    acc += th[k];
+    if (u < acc) return k;
+  }
+  return K - 1;
+}
+
+constexpr int kDocCumMax = 2048;  // doubles of running sums in shared memory (the z-step's K limit)
+
+template <bool kSmem>
 __global__ void prior_z_kernel(LdaArgs a, std::uint64_t seed) {
+  extern __shared__ double cum[];
   for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
     const double* th = a.theta + m * a.K;
+    if (kSmem) doc_cumsum_smem(th, a.K, cum);
     for (std::int64_t t = a.off[m] + threadIdx.x; t < a.off[m + 1]; t += blockDim.x) {
       Stream s(keyed(seed, kInit, static_cast<std::uint64_t>(a.var_z),
                      static_cast<std::uint64_t>(a.tok_base + t)));
       const double u = s.next_unit();
-      double acc = 0.0;
-      int pick = a.K - 1;
-      for (int k = 0; k < a.K; ++k) {
-        acc += th[k];
-        if (u < acc) {
-          pick = k;
-          break;
-        }
-      }
-      a.z[t] = pick;
+      a.z[t] = kSmem ? first_above(cum, a.K, u) : scan_pick(th, a.K, u);
     }
+    if (kSmem) __syncthreads();
   }
 }
 
@@ -1929,46 +1981,25 @@ __global__ void prior_z_kernel(LdaArgs a, std::uint64_t seed) {
 // rows ~ Dir(phi_conc), theta_d ~ Dir(theta_conc), z ~ Cat(theta_d), w ~ Cat(phi_z).
 // Word draws use a per-topic cumulative table + binary search (not the reference's
 // O(V) scan) and counter streams per token (not one serial stream).
+template <bool kSmem>
 __global__ void gen_tokens_kernel(LdaArgs a, const double* cum_phi /*[K][V]*/, const double* theta_true,
                                   std::uint64_t seed) {
+  extern __shared__ double cum[];
   for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
     const double* th = theta_true + m * a.K;
+    if (kSmem) doc_cumsum_smem(th, a.K, cum);
     for (std::int64_t t = a.off[m] + threadIdx.x; t < a.off[m + 1]; t += blockDim.x) {
       Stream s(keyed(seed, 0xDA7A, 1, static_cast<std::uint64_t>(a.tok_base + t)));
       const double u = s.next_unit();
-      double acc = 0.0;
-      int k = a.K - 1;
-      for (int j = 0; j < a.K; ++j) {
-        acc += th[j];
-        if (u < acc) {
-          k = j;
-          break;
-        }
-      }
+      const int k = kSmem ? first_above(cum, a.K, u) : scan_pick(th, a.K, u);
       const double* cp = cum_phi + static_cast<std::size_t>(k) * a.V;
-      const double uw = s.next_unit() * cp[a.V - 1];
-      int lo = 0, hi = a.V - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (uw < cp[mid])
-          hi = mid;
-        else
-          lo = mid + 1;
-      }
-      const_cast<int*>(a.w)[t] = lo;
+      const_cast<int*>(a.w)[t] = first_above(cp, a.V, s.next_unit() * cp[a.V - 1]);
     }
+    if (kSmem) __syncthreads();
   }
 }
 
-__global__ void row_cumsum_kernel(double* x, std::int64_t rows, int cols) {
-  const std::int64_t r = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  if (r >= rows) return;
-  double acc = 0.0;
-  for (int c = 0; c < cols; ++c) {
-    acc += x[r * cols + c];
-    x[r * cols + c] = acc;
-  }
-}
+
 
 // ---------------------------------------------------------------------------------
 // host side
@@ -2011,7 +2042,8 @@ void dirichlet_rows(double* out, std::int64_t rows, int cols, std::int64_t ld_ro
                                                               exit_pos.p, second.p, entry.p, first_col.p);
   prior_seg_draw_kernel<<<blocks_for(ns, 128), 128, 0, st>>>(out, rows, cols, nseg, ld_row, ld_col, conc, seed, var,
                                                               row_base, entry.p, first_col.p);
-  prior_row_sum_kernel<<<blocks_for(rows, 32), 32, 0, st>>>(out, rows, cols, ld_row, ld_col, sums.p);
+  row_scan_kernel<false><<<blocks_for(rows, kScanWarps), 32 * kScanWarps, 0, st>>>(out, rows, cols, ld_row, ld_col,
+                                                                                    sums.p);
   prior_row_norm_kernel<<<148 * 8, 256, 0, st>>>(out, rows, cols, ld_row, ld_col, sums.p);
   BNMC_CUDA(cudaGetLastError());
   BNMC_CUDA(cudaStreamSynchronize(st));
@@ -2501,7 +2533,10 @@ class Lda final : public Model {
       dirichlet_rows(phiT_.p, K_, V_, 1, Kp_, beta_, seed, var_phi_, 0, st);
     if (Ml_ > 0) {
       dirichlet_rows(theta_.p, Ml_, K_, K_, 1, alpha_, seed, var_theta_, d0_, st);
-      prior_z_kernel<<<grid_docs(), 256, 0, st>>>(a, seed);
+      if (doc_cum_smem())
+        prior_z_kernel<true><<<grid_docs(), 256, sizeof(double) * K_, st>>>(a, seed);
+      else
+        prior_z_kernel<false><<<grid_docs(), 256, 0, st>>>(a, seed);
     }
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
@@ -2606,11 +2641,14 @@ class Lda final : public Model {
     cum.alloc(static_cast<std::size_t>(K_) * V_);
     th.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     dirichlet_rows(cum.p, K_, V_, V_, 1, phi_conc, seed ^ 0xDA7Aull, 0, 0, st);
-    row_cumsum_kernel<<<blocks_for(K_, 32), 32, 0, st>>>(cum.p, K_, V_);
+    row_scan_kernel<true><<<blocks_for(K_, kScanWarps), 32 * kScanWarps, 0, st>>>(cum.p, K_, V_, V_, 1, nullptr);
     if (Ml_ > 0) {
       dirichlet_rows(th.p, Ml_, K_, K_, 1, theta_conc, seed ^ 0xDA7Aull, 1, d0_, st);
       LdaArgs a = args();
-      gen_tokens_kernel<<<grid_docs(), 256, 0, st>>>(a, cum.p, th.p, seed);
+      if (doc_cum_smem())
+        gen_tokens_kernel<true><<<grid_docs(), 256, sizeof(double) * K_, st>>>(a, cum.p, th.p, seed);
+      else
+        gen_tokens_kernel<false><<<grid_docs(), 256, 0, st>>>(a, cum.p, th.p, seed);
     }
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
@@ -2641,6 +2679,12 @@ class Lda final : public Model {
     if (screen_) phi_f32_kernel<<<148 * 8, 256, 0, st>>>(a);
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  // running sums per document in shared memory (BNMC_DOC_SCAN=1: the reference's linear scan)
+  bool doc_cum_smem() const {
+    const char* e = std::getenv("BNMC_DOC_SCAN");
+    return K_ <= kDocCumMax && !(e && std::string(e) != "0");
   }
 
   unsigned grid_docs() const { return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(Ml_, 1 << 20))); }

@@ -413,6 +413,26 @@ def test_lda_generate_long_rows(g, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("K", [7, 1000, 2048], ids=["k7", "k1000", "k2048"])
+def test_lda_doc_running_sums_equal_the_scan(g, monkeypatch, K):
+    """prior_init's z and lda_generate's tokens pick topics by a binary search over each
+    document's running sums (formed left to right in shared memory): the same picks as the
+    reference's linear scan (draw_categorical, dist.cpp:183-191), bit for bit."""
+    V, M, L, seed = 300, 12, 333, 8
+    hyper = {"K": K, "V": V, "M": M, "N": [L + (m % 3) for m in range(M)]}
+    got = {}
+    for scan in ("1", "0"):
+        monkeypatch.setenv("BNMC_DOC_SCAN", scan)
+        e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+        e.lda_generate(seed)
+        s = e.allocate()
+        e.download(s)
+        got[scan] = (e.lda_counts()[0].copy(), s["z"].copy(), s["theta"].copy())
+        e.close()
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
+
+
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
