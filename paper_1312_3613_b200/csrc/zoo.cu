@@ -282,33 +282,118 @@ __global__ void hmm_bias_kernel(ZooArgs a, const std::int64_t* iter_p) {
   a.B[m] = draw_beta(r, 1.0 + s, 1.0 + (n - s));
 }
 
-// s[t] | rest, t = 0 .. N-1 in order (one thread: the chain is sequential):
+// s[t] | rest, t = 0 .. N-1 in order: site t sees the NEW s[t-1] (`prev`) and the OLD
+// s[t+1] (read from `zold`):
 // logw[v] = 0 + {log T[0][v]}_{t==0} + {log T[s[t-1]][v]}_{t>=1} + {log T[v][s[t+1]]}_{t+1<N}
 //             + log Bernoulli(flips[t] | bias[v])
+// -1 when every weight is -inf.
+__device__ __forceinline__ int hmm_site(const ZooArgs& a, const int* zold, std::uint64_t zp, std::int64_t iter,
+                                        std::int64_t t, int prev, double* lw) {
+  const int S = a.S;
+  const int next = t + 1 < a.N ? zold[t + 1] : 0;
+  for (int v = 0; v < S; ++v) {
+    double lp = 0.0;
+    if (t == 0) lp += log_prob(a.A[v]);
+    if (t >= 1) lp += (prev >= 0 && prev < S) ? log_prob(a.A[prev * S + v]) : -INFINITY;
+    if (t + 1 < a.N) lp += (next >= 0 && next < S) ? log_prob(a.A[v * S + next]) : -INFINITY;
+    lp += log_pmf_bernoulli(a.x[t], a.B[v]);
+    lw[v] = lp;
+  }
+  Stream r(fold(fold(zp, static_cast<std::uint64_t>(t)), static_cast<std::uint64_t>(iter)));
+  return draw_log_weights(r, lw, S);
+}
+
+__device__ __forceinline__ std::uint64_t hmm_zkey(const ZooArgs& a) {
+  return fold(fold(fold(1, a.seed), kDiscrete), static_cast<std::uint64_t>(a.var[2]));
+}
+
+// The scan site by site on one thread (BNMC_HMM_SERIAL=1; the parity check of the
+// chunked scan below).
 __global__ void hmm_scan_kernel(ZooArgs a, const std::int64_t* iter_p, int* err) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   const std::int64_t iter = *iter_p;
-  const int S = a.S;
-  const std::uint64_t zp = fold(fold(fold(1, a.seed), kDiscrete), static_cast<std::uint64_t>(a.var[2]));
+  const std::uint64_t zp = hmm_zkey(a);
   double lw[64];
   for (std::int64_t t = 0; t < a.N; ++t) {
-    const int prev = t >= 1 ? a.z[t - 1] : 0;
-    const int next = t + 1 < a.N ? a.z[t + 1] : 0;
-    for (int v = 0; v < S; ++v) {
-      double lp = 0.0;
-      if (t == 0) lp += log_prob(a.A[v]);
-      if (t >= 1) lp += (prev >= 0 && prev < S) ? log_prob(a.A[prev * S + v]) : -INFINITY;
-      if (t + 1 < a.N) lp += (next >= 0 && next < S) ? log_prob(a.A[v * S + next]) : -INFINITY;
-      lp += log_pmf_bernoulli(a.x[t], a.B[v]);
-      lw[v] = lp;
-    }
-    Stream r(fold(fold(zp, static_cast<std::uint64_t>(t)), static_cast<std::uint64_t>(iter)));
-    const int k = draw_log_weights(r, lw, S);
+    const int k = hmm_site(a, a.z, zp, iter, t, t >= 1 ? a.z[t - 1] : 0, lw);
     if (k < 0) {
       atomicOr(err, kErrDomain);
       return;
     }
     a.z[t] = k;
+  }
+}
+
+// The same scan in parallel. A site's stream does not depend on the state, so site t is
+// a map prev -> s[t] over the S states, and a chunk of sites is the composition of its
+// sites' maps: (1) every chunk runs from each start state (distinct predecessors drawn
+// once per site; -1 marks a chain that hit an all -inf site); (2) one block composes the
+// chunk maps by a Hillis-Steele scan and reads each chunk's true start (the chain from
+// s[-1] = 0); (3) every chunk redraws its sites from its true start and writes them. The
+// old successors come from the sweep-start snapshot `zold`.
+__global__ void hmm_scan_ends_kernel(ZooArgs a, const int* zold, const std::int64_t* iter_p, std::int64_t chunk,
+                                     std::int64_t nchunks, int* maps) {
+  const std::int64_t c = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  const int S = a.S;
+  const std::int64_t iter = *iter_p;
+  const std::uint64_t zp = hmm_zkey(a);
+  int st[64], memo[64];
+  double lw[64];
+  for (int j = 0; j < S; ++j) st[j] = j;
+  const std::int64_t t1 = min(a.N, (c + 1) * chunk);
+  for (std::int64_t t = c * chunk; t < t1; ++t) {
+    for (int j = 0; j < S; ++j) memo[j] = -2;
+    for (int j = 0; j < S; ++j) {
+      const int p = st[j];
+      if (p < 0) continue;
+      if (memo[p] == -2) memo[p] = hmm_site(a, zold, zp, iter, t, p, lw);
+      st[j] = memo[p];
+    }
+  }
+  for (int j = 0; j < S; ++j) maps[c * S + j] = st[j];
+}
+
+__global__ void __launch_bounds__(1024) hmm_scan_link_kernel(int S, std::int64_t nchunks, int* m0, int* m1,
+                                                             int* starts) {
+  int* cur = m0;
+  int* nxt = m1;
+  const std::int64_t n = nchunks * S;
+  for (std::int64_t off = 1; off < nchunks; off <<= 1) {
+    for (std::int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const std::int64_t c = i / S;
+      if (c < off) {
+        nxt[i] = cur[i];
+      } else {
+        const int p = cur[i - off * S];  // chunks (c-off .. ] composed, then chunk c's map
+        nxt[i] = p < 0 ? -1 : cur[c * S + p];
+      }
+    }
+    __syncthreads();
+    int* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  for (std::int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) starts[c] = c == 0 ? 0 : cur[(c - 1) * S];
+}
+
+__global__ void hmm_scan_chain_kernel(ZooArgs a, const int* zold, const std::int64_t* iter_p, std::int64_t chunk,
+                                      std::int64_t nchunks, const int* starts, int* err) {
+  const std::int64_t c = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  int st = starts[c];
+  if (st < 0) return;  // an earlier site ended the scan
+  const std::int64_t iter = *iter_p;
+  const std::uint64_t zp = hmm_zkey(a);
+  double lw[64];
+  const std::int64_t t1 = min(a.N, (c + 1) * chunk);
+  for (std::int64_t t = c * chunk; t < t1; ++t) {
+    st = hmm_site(a, zold, zp, iter, t, st, lw);
+    if (st < 0) {
+      atomicOr(err, kErrDomain);
+      return;
+    }
+    a.z[t] = st;
   }
 }
 
@@ -376,43 +461,90 @@ __device__ int prior_categorical(Stream& s, const double* p, int n) {
   return n - 1;
 }
 
-__global__ void zoo_prior_kernel(ZooArgs a, std::uint64_t seed) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  auto st = [&](int var, std::int64_t t) {
-    return Stream(keyed(seed, kInit, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(t)));
-  };
-  if (a.kind == BNMC_GPU_CATMIX) {
-    for (int k = 0; k < a.K; ++k) {
-      Stream s = st(a.var[0], k);
-      prior_dirichlet_row(s, a.A + static_cast<std::size_t>(k) * a.V, a.V, a.conc_a);
-    }
-    Stream s = st(a.var[1], 0);
-    prior_dirichlet_row(s, a.B, a.K, a.conc_b);
-    for (std::int64_t i = 0; i < a.N; ++i) {
-      Stream r = st(a.var[2], i);
-      a.z[i] = prior_categorical(r, a.B, a.K);
-    }
-  } else if (a.kind == BNMC_GPU_NAIVEBAYES) {
-    Stream s = st(a.var[0], 0);
-    a.A[0] = draw_beta(s, 0.5, 0.5);
-    for (int m = 0; m < 2 * a.K; ++m) {
-      Stream r = st(a.var[2], m);
-      a.B[m] = draw_beta(r, 0.5, 0.5);
-    }
-  } else {  // hmm
-    for (int k = 0; k < a.S; ++k) {
-      Stream s = st(a.var[0], k);
-      prior_dirichlet_row(s, a.A + static_cast<std::size_t>(k) * a.S, a.S, a.conc_a);
-    }
-    for (int m = 0; m < a.S; ++m) {
-      Stream s = st(a.var[1], m);
-      a.B[m] = draw_beta(s, 1.0, 1.0);
-    }
-    for (std::int64_t t = 0; t < a.N; ++t) {
-      Stream r = st(a.var[2], t);
-      const int prev = t == 0 ? 0 : a.z[t - 1];
-      a.z[t] = prior_categorical(r, a.A + static_cast<std::size_t>(prev) * a.S, a.S);
-    }
+__device__ __forceinline__ Stream prior_stream(std::uint64_t seed, int var, std::int64_t elem) {
+  return Stream(keyed(seed, kInit, static_cast<std::uint64_t>(var), static_cast<std::uint64_t>(elem)));
+}
+
+// Each element has its own stream, so the elements are drawn in parallel: Dirichlet rows
+// thread per row, Beta draws and categorical picks thread per element.
+__global__ void zoo_prior_rows_kernel(double* out, int rows, int cols, double conc, std::uint64_t seed, int var) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows) return;
+  Stream s = prior_stream(seed, var, k);
+  prior_dirichlet_row(s, out + static_cast<std::size_t>(k) * cols, cols, conc);
+}
+
+__global__ void zoo_prior_beta_kernel(double* out, int n, double a, double b, std::uint64_t seed, int var) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  Stream s = prior_stream(seed, var, m);
+  out[m] = draw_beta(s, a, b);
+}
+
+__global__ void zoo_prior_cat_kernel(int* z, std::int64_t N, const double* p, int n, std::uint64_t seed, int var) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    Stream r = prior_stream(seed, var, i);
+    z[i] = prior_categorical(r, p, n);
+  }
+}
+
+// HMM prior chain s[t] ~ Cat(T[s[t-1]]), s[-1] = 0, step t with its own stream: step t is
+// the map prev -> pick(u_t, T[prev]) over S states, so chunks of steps compose in
+// parallel: every chunk runs from each start state (ends), one thread links the chunks
+// (starts), every chunk re-runs from its true start and writes the states.
+constexpr int kHmmPriorMaxS = 16;
+
+__device__ __forceinline__ int pick_row(double u, const double* row, int n) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    acc += row[i];
+    if (u < acc) return i;
+  }
+  return n - 1;
+}
+
+__global__ void hmm_prior_ends_kernel(ZooArgs a, std::uint64_t seed, std::int64_t chunk, std::int64_t nchunks,
+                                      int* ends) {
+  const std::int64_t c = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  int st[kHmmPriorMaxS];
+  for (int j = 0; j < a.S; ++j) st[j] = j;
+  const std::int64_t t1 = min(a.N, (c + 1) * chunk);
+  for (std::int64_t t = c * chunk; t < t1; ++t) {
+    const double u = prior_stream(seed, a.var[2], t).next_unit();
+    for (int j = 0; j < a.S; ++j) st[j] = pick_row(u, a.A + static_cast<std::size_t>(st[j]) * a.S, a.S);
+  }
+  for (int j = 0; j < a.S; ++j) ends[c * a.S + j] = st[j];
+}
+
+__global__ void hmm_prior_link_kernel(int S, std::int64_t nchunks, const int* ends, int* starts) {
+  int st = 0;
+  for (std::int64_t c = 0; c < nchunks; ++c) {
+    starts[c] = st;
+    st = ends[c * S + st];
+  }
+}
+
+__global__ void hmm_prior_chain_kernel(ZooArgs a, std::uint64_t seed, std::int64_t chunk, std::int64_t nchunks,
+                                       const int* starts) {
+  const std::int64_t c = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  int st = starts[c];
+  const std::int64_t t1 = min(a.N, (c + 1) * chunk);
+  for (std::int64_t t = c * chunk; t < t1; ++t) {
+    const double u = prior_stream(seed, a.var[2], t).next_unit();
+    st = pick_row(u, a.A + static_cast<std::size_t>(st) * a.S, a.S);
+    a.z[t] = st;
+  }
+}
+
+// S > kHmmPriorMaxS (or BNMC_PRIOR_SERIAL=1): the chain step by step
+__global__ void hmm_prior_serial_kernel(ZooArgs a, std::uint64_t seed) {
+  for (std::int64_t t = 0; t < a.N; ++t) {
+    Stream r = prior_stream(seed, a.var[2], t);
+    const int prev = t == 0 ? 0 : a.z[t - 1];
+    a.z[t] = prior_categorical(r, a.A + static_cast<std::size_t>(prev) * a.S, a.S);
   }
 }
 
@@ -467,6 +599,17 @@ class Zoo final : public Model {
       nb_ = S_;
       ncnt_ = na_ + 2 * S_;
       conc_a_ = d.hyper[0] > 0 ? d.hyper[0] : 0.1;
+      // chunked s-scan: fewer, longer chunks for more states (the link scan composes
+      // chunks x S entries in one block)
+      const char* e = std::getenv("BNMC_HMM_SERIAL");
+      if (N_ > 1 && !(e && std::string(e) != "0")) {
+        hmm_chunks_ = std::min<std::int64_t>(N_, std::max<std::int64_t>(256, 32768 / S_));
+        hmm_chunk_ = (N_ + hmm_chunks_ - 1) / hmm_chunks_;
+        hmm_chunks_ = (N_ + hmm_chunk_ - 1) / hmm_chunk_;
+        zold_.alloc(N_);
+        maps_.alloc(2 * hmm_chunks_ * S_);
+        starts_.alloc(hmm_chunks_);
+      }
     }
     A_.alloc(na_);
     B_.alloc(nb_);
@@ -527,7 +670,15 @@ class Zoo final : public Model {
       dirichlet_rows_kernel<<<S_, 64, 0, st>>>(A_.p, cnt_.p, S_, S_, conc_a_, seed_, var_[0], out.iter);
       hmm_bias_kernel<<<1, 64, 0, st>>>(a, out.iter);
       mark(st, "T_bias");
-      hmm_scan_kernel<<<1, 32, 0, st>>>(a, out.iter, out.err);
+      if (hmm_chunks_ > 0) {
+        BNMC_CUDA(cudaMemcpyAsync(zold_.p, z_.p, sizeof(int) * N_, cudaMemcpyDeviceToDevice, st));
+        const unsigned g = static_cast<unsigned>((hmm_chunks_ + 127) / 128);
+        hmm_scan_ends_kernel<<<g, 128, 0, st>>>(a, zold_.p, out.iter, hmm_chunk_, hmm_chunks_, maps_.p);
+        hmm_scan_link_kernel<<<1, 1024, 0, st>>>(S_, hmm_chunks_, maps_.p, maps_.p + hmm_chunks_ * S_, starts_.p);
+        hmm_scan_chain_kernel<<<g, 128, 0, st>>>(a, zold_.p, out.iter, hmm_chunk_, hmm_chunks_, starts_.p, out.err);
+      } else {
+        hmm_scan_kernel<<<1, 32, 0, st>>>(a, out.iter, out.err);
+      }
       mark(st, "s_scan");
       hmm_lj_kernel<<<1, 1024, 0, st>>>(a);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 1, 5);
@@ -552,7 +703,35 @@ class Zoo final : public Model {
   }
 
   void prior_init(std::uint64_t seed, cudaStream_t st) override {
-    zoo_prior_kernel<<<1, 1, 0, st>>>(args(), seed);
+    const ZooArgs a = args();
+    if (kind_ == BNMC_GPU_CATMIX) {
+      zoo_prior_rows_kernel<<<(K_ + 63) / 64, 64, 0, st>>>(A_.p, K_, V_, a.conc_a, seed, a.var[0]);
+      zoo_prior_rows_kernel<<<1, 1, 0, st>>>(B_.p, 1, K_, a.conc_b, seed, a.var[1]);
+      zoo_prior_cat_kernel<<<grid_for(N_), kT, 0, st>>>(z_.p, N_, B_.p, K_, seed, a.var[2]);
+    } else if (kind_ == BNMC_GPU_NAIVEBAYES) {
+      zoo_prior_beta_kernel<<<1, 1, 0, st>>>(A_.p, 1, 0.5, 0.5, seed, a.var[0]);
+      zoo_prior_beta_kernel<<<(2 * K_ + 63) / 64, 64, 0, st>>>(B_.p, 2 * K_, 0.5, 0.5, seed, a.var[2]);
+    } else {  // hmm
+      zoo_prior_rows_kernel<<<(S_ + 63) / 64, 64, 0, st>>>(A_.p, S_, S_, a.conc_a, seed, a.var[0]);
+      zoo_prior_beta_kernel<<<(S_ + 63) / 64, 64, 0, st>>>(B_.p, S_, 1.0, 1.0, seed, a.var[1]);
+      const char* e = std::getenv("BNMC_PRIOR_SERIAL");
+      if (N_ > 0 && S_ <= kHmmPriorMaxS && !(e && std::string(e) != "0")) {
+        const std::int64_t nchunks = std::min<std::int64_t>(N_, 148 * 128);
+        const std::int64_t chunk = (N_ + nchunks - 1) / nchunks;
+        DevBuf<int> ends, starts;
+        ends.alloc(nchunks * S_);
+        starts.alloc(nchunks);
+        hmm_prior_ends_kernel<<<static_cast<unsigned>((nchunks + 127) / 128), 128, 0, st>>>(a, seed, chunk, nchunks,
+                                                                                           ends.p);
+        hmm_prior_link_kernel<<<1, 1, 0, st>>>(S_, nchunks, ends.p, starts.p);
+        hmm_prior_chain_kernel<<<static_cast<unsigned>((nchunks + 127) / 128), 128, 0, st>>>(a, seed, chunk, nchunks,
+                                                                                            starts.p);
+        BNMC_CUDA(cudaGetLastError());
+        BNMC_CUDA(cudaStreamSynchronize(st));
+      } else if (N_ > 0) {
+        hmm_prior_serial_kernel<<<1, 1, 0, st>>>(a, seed);
+      }
+    }
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
   }
@@ -647,7 +826,8 @@ class Zoo final : public Model {
   double conc_a_ = 0.5, conc_b_ = 0.5;
   bool data_ = false;
   DevBuf<double> A_, B_, red_;
-  DevBuf<int> z_, x_, f_, cnt_;
+  DevBuf<int> z_, x_, f_, cnt_, zold_, maps_, starts_;
+  std::int64_t hmm_chunks_ = 0, hmm_chunk_ = 0;
   DevBuf<std::int64_t> stage_;
 };
 

@@ -687,6 +687,51 @@ def test_zoo_prior_init_matches_reference(g, name, model):
     e.close()
 
 
+@pytest.mark.parametrize("N,S", [(60000, 3), (40001, 16), (5000, 17)], ids=["s3", "s16", "s17-serial"])
+def test_hmm_prior_chain_chunked(g, monkeypatch, N, S):
+    """The HMM prior chain s[t] ~ Cat(T[s[t-1]]) (sampler.cpp:542-555) drawn as composed
+    chunk maps equals the step-by-step chain (BNMC_PRIOR_SERIAL=1), bit for bit."""
+    flips = np.random.default_rng(1).integers(0, 2, N).astype(np.int64)
+    got = {}
+    for serial in ("1", "0"):
+        monkeypatch.setenv("BNMC_PRIOR_SERIAL", serial)
+        e = g.Engine("hmm", {"N": N, "S": S}, g.RunConfig(seed=13))
+        s = e.allocate()
+        s["flips"] = flips
+        e.prior_init(s, 13)
+        got[serial] = (s["s"].copy(), s["T"].copy(), s["bias"].copy())
+        e.close()
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
+    assert len(np.unique(got["0"][0])) > 1
+
+
+@pytest.mark.parametrize("N,S", [(100000, 3), (30001, 16), (4000, 64)], ids=["s3", "s16", "s64"])
+def test_hmm_chunked_scan_equals_the_sequential_scan(g, monkeypatch, N, S):
+    """The HMM s-scan (each site sees the new s[t-1] and the old s[t+1], sampler.cpp:259-264)
+    run as composed chunk maps equals the site-by-site scan (BNMC_HMM_SERIAL=1) bit for bit,
+    sweep after sweep, with the log-joints."""
+    flips = np.random.default_rng(2).integers(0, 2, N).astype(np.int64)
+    got = {}
+    for serial in ("1", "0"):
+        monkeypatch.setenv("BNMC_HMM_SERIAL", serial)
+        e = g.Engine("hmm", {"N": N, "S": S}, g.RunConfig(seed=21))
+        s = e.allocate()
+        s["flips"] = flips
+        e.prior_init(s, 21)
+        ljs, states = [], []
+        for it in range(4):
+            ljs.append(e.sweep(s, it))
+            states.append(s["s"].copy())
+        got[serial] = (ljs, states, s["T"].copy(), s["bias"].copy())
+        e.close()
+    assert got["1"][0] == got["0"][0]
+    for a, b in zip(got["1"][1], got["0"][1]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(got["1"][2], got["0"][2]) and np.array_equal(got["1"][3], got["0"][3])
+    assert not np.array_equal(got["0"][1][0], got["0"][1][-1])
+
+
 @pytest.mark.parametrize("name,model", ZOO)
 def test_zoo_sweeps_vs_reference(g, name, model):
     fx = golden(name)
