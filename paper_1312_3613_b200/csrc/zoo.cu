@@ -257,7 +257,10 @@ __global__ void nb_lj_kernel(ZooArgs a) {
 // cnt[k*S + v]: transitions (s[0] counted in row 0, sampler plan describe_hmm.txt);
 // cnt[S*S + m] = n_m, cnt[S*S + S + m] = sum of flips with s = m
 __global__ void hmm_count_kernel(ZooArgs a, int* err) {
-  const int S = a.S;
+  extern __shared__ int hist[];  // S*S + 2S block-local counts, added to cnt at the end
+  const int S = a.S, nh = S * S + 2 * S;
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
   for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < a.N;
        t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const int st = a.z[t];
@@ -266,10 +269,13 @@ __global__ void hmm_count_kernel(ZooArgs a, int* err) {
       continue;
     }
     const int prev = t == 0 ? 0 : a.z[t - 1];
-    if (prev >= 0 && prev < S) atomicAdd(&a.cnt[prev * S + st], 1);
-    atomicAdd(&a.cnt[S * S + st], 1);
-    atomicAdd(&a.cnt[S * S + S + st], a.x[t]);
+    if (prev >= 0 && prev < S) atomicAdd(&hist[prev * S + st], 1);
+    atomicAdd(&hist[S * S + st], 1);
+    atomicAdd(&hist[S * S + S + st], a.x[t]);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nh; i += blockDim.x)
+    if (hist[i]) atomicAdd(&a.cnt[i], hist[i]);
 }
 
 __global__ void hmm_bias_kernel(ZooArgs a, const std::int64_t* iter_p) {
@@ -354,14 +360,19 @@ __global__ void hmm_scan_ends_kernel(ZooArgs a, const int* zold, const std::int6
   for (int j = 0; j < S; ++j) maps[c * S + j] = st[j];
 }
 
-__global__ void __launch_bounds__(1024) hmm_scan_link_kernel(int S, std::int64_t nchunks, int* m0, int* m1,
+constexpr int kHmmLinkMax = 24576;  // map entries: two buffers of 96 KB in shared memory
+
+__global__ void __launch_bounds__(1024) hmm_scan_link_kernel(int S, std::int64_t nchunks, const int* maps,
                                                              int* starts) {
-  int* cur = m0;
-  int* nxt = m1;
-  const std::int64_t n = nchunks * S;
-  for (std::int64_t off = 1; off < nchunks; off <<= 1) {
-    for (std::int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const std::int64_t c = i / S;
+  extern __shared__ int m[];
+  int* cur = m;
+  int* nxt = m + kHmmLinkMax;
+  const int n = static_cast<int>(nchunks) * S;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cur[i] = maps[i];
+  __syncthreads();
+  for (int off = 1; off < nchunks; off <<= 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int c = i / S;
       if (c < off) {
         nxt[i] = cur[i];
       } else {
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(1024) hmm_scan_link_kernel(int S, std::int64_t
     cur = nxt;
     nxt = t;
   }
-  for (std::int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) starts[c] = c == 0 ? 0 : cur[(c - 1) * S];
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) starts[c] = c == 0 ? 0 : cur[(c - 1) * S];
 }
 
 __global__ void hmm_scan_chain_kernel(ZooArgs a, const int* zold, const std::int64_t* iter_p, std::int64_t chunk,
@@ -398,28 +409,47 @@ __global__ void hmm_scan_chain_kernel(ZooArgs a, const int* zold, const std::int
 }
 
 // log-joint factors [T, bias, s[0], s[t>=1], flips] (single block)
-__global__ void hmm_lj_kernel(ZooArgs a) {
-  __shared__ double scratch[32];
+constexpr int kHmmLjBlocks = 148 * 2;
+
+// per-block partials of the site factors s[t>=1] and flips (fixed-order block sums)
+__global__ void hmm_lj_part_kernel(ZooArgs a, double* part) {
+  __shared__ double scratch[64];
   const int S = a.S;
-  double fT = 0.0, fb = 0.0, fs = 0.0, ff = 0.0;
-  for (int k = threadIdx.x; k < S; k += blockDim.x) {
-    fT += log_pdf_dirichlet_const(a.A + static_cast<std::size_t>(k) * S, S, a.conc_a);
-    fb += log_pdf_beta(a.B[k], 1.0, 1.0);
-  }
-  for (std::int64_t t = threadIdx.x; t < a.N; t += blockDim.x) {
+  double v[2] = {0.0, 0.0};
+  for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < a.N;
+       t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const int st = a.z[t];
     const bool ok = st >= 0 && st < S;
     if (t >= 1) {
       const int pv = a.z[t - 1];
-      fs += (ok && pv >= 0 && pv < S) ? log_prob(a.A[pv * S + st]) : -INFINITY;
+      v[0] += (ok && pv >= 0 && pv < S) ? log_prob(a.A[pv * S + st]) : -INFINITY;
     }
-    ff += ok ? log_pmf_bernoulli(a.x[t], a.B[st]) : -INFINITY;
+    v[1] += ok ? log_pmf_bernoulli(a.x[t], a.B[st]) : -INFINITY;
+  }
+  block_sum_n<2>(v, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = v[0];
+    part[2 * blockIdx.x + 1] = v[1];
+  }
+}
+
+// log-joint factors [T, bias, s[0], s[t>=1], flips] (single block; the partials in block order)
+__global__ void hmm_lj_kernel(ZooArgs a, const double* part) {
+  __shared__ double scratch[32];
+  const int S = a.S;
+  double fT = 0.0, fb = 0.0;
+  for (int k = threadIdx.x; k < S; k += blockDim.x) {
+    fT += log_pdf_dirichlet_const(a.A + static_cast<std::size_t>(k) * S, S, a.conc_a);
+    fb += log_pdf_beta(a.B[k], 1.0, 1.0);
   }
   fT = block_sum(fT, scratch);
   fb = block_sum(fb, scratch);
-  fs = block_sum(fs, scratch);
-  ff = block_sum(ff, scratch);
   if (threadIdx.x == 0) {
+    double fs = 0.0, ff = 0.0;
+    for (int b = 0; b < kHmmLjBlocks; ++b) {
+      fs += part[2 * b];
+      ff += part[2 * b + 1];
+    }
     const int s0 = a.N > 0 ? a.z[0] : 0;
     a.red[0] = fT;
     a.red[1] = fb;
@@ -599,15 +629,17 @@ class Zoo final : public Model {
       nb_ = S_;
       ncnt_ = na_ + 2 * S_;
       conc_a_ = d.hyper[0] > 0 ? d.hyper[0] : 0.1;
-      // chunked s-scan: fewer, longer chunks for more states (the link scan composes
-      // chunks x S entries in one block)
+      ljpart_.alloc(2 * kHmmLjBlocks);
+      // chunked s-scan: chunks x S map entries fit the link block's shared memory
       const char* e = std::getenv("BNMC_HMM_SERIAL");
       if (N_ > 1 && !(e && std::string(e) != "0")) {
-        hmm_chunks_ = std::min<std::int64_t>(N_, std::max<std::int64_t>(256, 32768 / S_));
+        hmm_chunks_ = std::min<std::int64_t>(N_, kHmmLinkMax / S_);
         hmm_chunk_ = (N_ + hmm_chunks_ - 1) / hmm_chunks_;
         hmm_chunks_ = (N_ + hmm_chunk_ - 1) / hmm_chunk_;
         zold_.alloc(N_);
-        maps_.alloc(2 * hmm_chunks_ * S_);
+        maps_.alloc(hmm_chunks_ * S_);
+        BNMC_CUDA(cudaFuncSetAttribute(hmm_scan_link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(int) * 2 * kHmmLinkMax)));
         starts_.alloc(hmm_chunks_);
       }
     }
@@ -666,7 +698,7 @@ class Zoo final : public Model {
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 1, 4);
     } else {
       cnt_.zero(st);
-      hmm_count_kernel<<<grid_for(N_), kT, 0, st>>>(a, out.err);
+      hmm_count_kernel<<<std::min(grid_for(N_), 148u * 2), kT, sizeof(int) * (S_ * S_ + 2 * S_), st>>>(a, out.err);
       dirichlet_rows_kernel<<<S_, 64, 0, st>>>(A_.p, cnt_.p, S_, S_, conc_a_, seed_, var_[0], out.iter);
       hmm_bias_kernel<<<1, 64, 0, st>>>(a, out.iter);
       mark(st, "T_bias");
@@ -674,13 +706,14 @@ class Zoo final : public Model {
         BNMC_CUDA(cudaMemcpyAsync(zold_.p, z_.p, sizeof(int) * N_, cudaMemcpyDeviceToDevice, st));
         const unsigned g = static_cast<unsigned>((hmm_chunks_ + 127) / 128);
         hmm_scan_ends_kernel<<<g, 128, 0, st>>>(a, zold_.p, out.iter, hmm_chunk_, hmm_chunks_, maps_.p);
-        hmm_scan_link_kernel<<<1, 1024, 0, st>>>(S_, hmm_chunks_, maps_.p, maps_.p + hmm_chunks_ * S_, starts_.p);
+        hmm_scan_link_kernel<<<1, 1024, sizeof(int) * 2 * kHmmLinkMax, st>>>(S_, hmm_chunks_, maps_.p, starts_.p);
         hmm_scan_chain_kernel<<<g, 128, 0, st>>>(a, zold_.p, out.iter, hmm_chunk_, hmm_chunks_, starts_.p, out.err);
       } else {
         hmm_scan_kernel<<<1, 32, 0, st>>>(a, out.iter, out.err);
       }
       mark(st, "s_scan");
-      hmm_lj_kernel<<<1, 1024, 0, st>>>(a);
+      hmm_lj_part_kernel<<<kHmmLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      hmm_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 1, 5);
     }
     mark(st, "log_joint");
@@ -696,7 +729,8 @@ class Zoo final : public Model {
       nb_lj_kernel<<<1, 1024, 0, st>>>(a);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 0, 4);
     } else {
-      hmm_lj_kernel<<<1, 1024, 0, st>>>(a);
+      hmm_lj_part_kernel<<<kHmmLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      hmm_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 0, 5);
     }
     BNMC_CUDA(cudaGetLastError());
@@ -825,7 +859,7 @@ class Zoo final : public Model {
   int var_[4] = {0, 1, 2, 3};
   double conc_a_ = 0.5, conc_b_ = 0.5;
   bool data_ = false;
-  DevBuf<double> A_, B_, red_;
+  DevBuf<double> A_, B_, red_, ljpart_;
   DevBuf<int> z_, x_, f_, cnt_, zold_, maps_, starts_;
   std::int64_t hmm_chunks_ = 0, hmm_chunk_ = 0;
   DevBuf<std::int64_t> stage_;
