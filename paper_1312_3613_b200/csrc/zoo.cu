@@ -71,11 +71,12 @@ __device__ __forceinline__ double log_pmf_bernoulli(long long x, double p) {
 __device__ double log_pdf_dirichlet_const(const double* x, int n, double alpha) {
   double sum = 0.0, lp = 0.0, norm = 0.0, asum = 0.0;
   if (!(alpha > 0.0)) return -INFINITY;
+  const double lga = lgamma(alpha);  // the reference's per-element lgamma(alpha), once
   for (int i = 0; i < n; ++i) {
     if (!(x[i] > 0.0)) return -INFINITY;
     sum += x[i];
     lp += (alpha - 1.0) * log(x[i]);
-    norm += lgamma(alpha);
+    norm += lga;
     asum += alpha;
   }
   if (fabs(sum - 1.0) > 1e-9) return -INFINITY;
@@ -158,26 +159,43 @@ __global__ void catmix_z_kernel(ZooArgs a, const std::int64_t* iter_p, int* err)
 }
 
 // log-joint factors [theta, phi, z, x] (single block)
-__global__ void catmix_lj_kernel(ZooArgs a) {
+constexpr int kZooLjBlocks = 148 * 2;
+
+// per-block partials of the z and x factors (fixed-order block sums)
+__global__ void catmix_lj_part_kernel(ZooArgs a, double* part) {
+  __shared__ double scratch[64];
+  double v[2] = {0.0, 0.0};
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < a.N;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const int k = a.z[i], xi = a.x[i];
+    if (k < 0 || k >= a.K) {
+      v[0] += -INFINITY;
+      v[1] += -INFINITY;
+      continue;
+    }
+    v[0] += log_prob(a.B[k]);
+    v[1] += (xi >= 0 && xi < a.V) ? log_prob(a.A[static_cast<std::size_t>(k) * a.V + xi]) : -INFINITY;
+  }
+  block_sum_n<2>(v, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = v[0];
+    part[2 * blockIdx.x + 1] = v[1];
+  }
+}
+
+// log-joint factors [theta, phi, z, x] (single block; the partials in block order)
+__global__ void catmix_lj_kernel(ZooArgs a, const double* part) {
   __shared__ double scratch[32];
   double ft = 0.0;
   for (int k = threadIdx.x; k < a.K; k += blockDim.x)
     ft += log_pdf_dirichlet_const(a.A + static_cast<std::size_t>(k) * a.V, a.V, a.conc_a);
-  double fz = 0.0, fx = 0.0;
-  for (std::int64_t i = threadIdx.x; i < a.N; i += blockDim.x) {
-    const int k = a.z[i], xi = a.x[i];
-    if (k < 0 || k >= a.K) {
-      fz += -INFINITY;
-      fx += -INFINITY;
-      continue;
-    }
-    fz += log_prob(a.B[k]);
-    fx += (xi >= 0 && xi < a.V) ? log_prob(a.A[static_cast<std::size_t>(k) * a.V + xi]) : -INFINITY;
-  }
   ft = block_sum(ft, scratch);
-  fz = block_sum(fz, scratch);
-  fx = block_sum(fx, scratch);
   if (threadIdx.x == 0) {
+    double fz = 0.0, fx = 0.0;
+    for (int b = 0; b < kZooLjBlocks; ++b) {
+      fz += part[2 * b];
+      fx += part[2 * b + 1];
+    }
     a.red[0] = ft;
     a.red[1] = log_pdf_dirichlet_const(a.B, a.K, a.conc_b);
     a.red[2] = fz;
@@ -409,8 +427,6 @@ __global__ void hmm_scan_chain_kernel(ZooArgs a, const int* zold, const std::int
 }
 
 // log-joint factors [T, bias, s[0], s[t>=1], flips] (single block)
-constexpr int kHmmLjBlocks = 148 * 2;
-
 // per-block partials of the site factors s[t>=1] and flips (fixed-order block sums)
 __global__ void hmm_lj_part_kernel(ZooArgs a, double* part) {
   __shared__ double scratch[64];
@@ -446,7 +462,7 @@ __global__ void hmm_lj_kernel(ZooArgs a, const double* part) {
   fb = block_sum(fb, scratch);
   if (threadIdx.x == 0) {
     double fs = 0.0, ff = 0.0;
-    for (int b = 0; b < kHmmLjBlocks; ++b) {
+    for (int b = 0; b < kZooLjBlocks; ++b) {
       fs += part[2 * b];
       ff += part[2 * b + 1];
     }
@@ -629,7 +645,6 @@ class Zoo final : public Model {
       nb_ = S_;
       ncnt_ = na_ + 2 * S_;
       conc_a_ = d.hyper[0] > 0 ? d.hyper[0] : 0.1;
-      ljpart_.alloc(2 * kHmmLjBlocks);
       // chunked s-scan: chunks x S map entries fit the link block's shared memory
       const char* e = std::getenv("BNMC_HMM_SERIAL");
       if (N_ > 1 && !(e && std::string(e) != "0")) {
@@ -645,6 +660,7 @@ class Zoo final : public Model {
     }
     A_.alloc(na_);
     B_.alloc(nb_);
+    ljpart_.alloc(2 * kZooLjBlocks);
     z_.alloc(std::max<std::int64_t>(N_, 1));
     x_.alloc(std::max<std::int64_t>(N_, 1));
     if (kind_ == BNMC_GPU_NAIVEBAYES) f_.alloc(std::max<std::int64_t>(N_ * K_, 1));
@@ -689,7 +705,8 @@ class Zoo final : public Model {
       mark(st, "theta_phi");
       catmix_z_kernel<<<grid_for(N_), kT, 0, st>>>(a, out.iter, out.err);
       mark(st, "z");
-      catmix_lj_kernel<<<1, 1024, 0, st>>>(a);
+      catmix_lj_part_kernel<<<kZooLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      catmix_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 1, 4);
     } else if (kind_ == BNMC_GPU_NAIVEBAYES) {
       nb_draw_kernel<<<static_cast<unsigned>((2 * K_ + kT) / kT), kT, 0, st>>>(a, out.iter);
@@ -712,7 +729,7 @@ class Zoo final : public Model {
         hmm_scan_kernel<<<1, 32, 0, st>>>(a, out.iter, out.err);
       }
       mark(st, "s_scan");
-      hmm_lj_part_kernel<<<kHmmLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      hmm_lj_part_kernel<<<kZooLjBlocks, 256, 0, st>>>(a, ljpart_.p);
       hmm_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 1, 5);
     }
@@ -723,13 +740,14 @@ class Zoo final : public Model {
   void enqueue_log_joint(cudaStream_t st) override {
     ZooArgs a = args();
     if (kind_ == BNMC_GPU_CATMIX) {
-      catmix_lj_kernel<<<1, 1024, 0, st>>>(a);
+      catmix_lj_part_kernel<<<kZooLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      catmix_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 0, 4);
     } else if (kind_ == BNMC_GPU_NAIVEBAYES) {
       nb_lj_kernel<<<1, 1024, 0, st>>>(a);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 0, 4);
     } else {
-      hmm_lj_part_kernel<<<kHmmLjBlocks, 256, 0, st>>>(a, ljpart_.p);
+      hmm_lj_part_kernel<<<kZooLjBlocks, 256, 0, st>>>(a, ljpart_.p);
       hmm_lj_kernel<<<1, 64, 0, st>>>(a, ljpart_.p);
       zoo_finalize_kernel<<<1, 1, 0, st>>>(a, out, 0, 5);
     }
