@@ -35,6 +35,14 @@
 #include "dist.cuh"
 
 namespace bnmc_gpu {
+
+// wordmajor.cu (CUB): stable pair sort on key bits [0, end_bit) -> which buffer holds
+// the result; runs of equal keys of a sorted array -> their count
+int sort_pairs_u32(std::uint32_t* keys, std::uint32_t* keys_alt, int* vals, int* vals_alt, std::int64_t n,
+                   int end_bit, cudaStream_t st);
+std::int64_t run_length_u32(const std::uint32_t* keys, std::int64_t n, std::uint32_t* uniq, int* counts,
+                            cudaStream_t st);
+
 namespace {
 
 constexpr int kZThreads = 256;
@@ -107,6 +115,13 @@ struct LdaArgs {
   int red_only;      // sharded: the last wterm block writes red[0..2] (this rank's theta, z, w
                      // pieces) for the all-reduce instead of the log-joint
   std::int64_t docs_per_block, nb_doc;
+  // word-major z-step order (build_word_major): units [n][3] = word, i0, i1 over the
+  // sorted token list; tok / doc of sorted position i; th32 = fp32 theta/S rows
+  // [Ml][Kp32] in the phiT32 column order
+  const int* wm_tok;
+  const int* wm_doc;
+  float* th32;
+  unsigned long long* wm_ticket;  // next unit to claim (zeroed before each word-major launch)
 };
 
 // ---------------------------------------------------------------------------------
@@ -855,6 +870,38 @@ __device__ int draw_topic_logspace(const double* lth, const double* row, int K, 
   return __shfl_sync(m, pick, 0, G);
 }
 
+// Word-major z-step operand: theta/S of every local document in fp32, in the phiT32
+// column order (the value the document-major z-step forms per unit in shared memory).
+// Padding columns stay 0 (zeroed at allocation).
+__global__ void th32_kernel(LdaArgs a) {
+  const std::int64_t n = a.Ml * a.K;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t m = i / a.K;
+    const int k = static_cast<int>(i - m * a.K);
+    a.th32[m * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(a.theta[i] / a.S[k]);
+  }
+}
+
+// Word-major order keys: (document block, word) per local token, with its index and
+// document (the sort carries the index; the document is gathered after it).
+__global__ void wm_keys_kernel(LdaArgs a, std::int64_t block_docs, std::uint32_t* keys, int* tok, int* docof) {
+  for (std::int64_t m = blockIdx.x; m < a.Ml; m += gridDim.x) {
+    const std::uint32_t hi = static_cast<std::uint32_t>((m / block_docs) * a.V);
+    for (std::int64_t t = a.off[m] + threadIdx.x; t < a.off[m + 1]; t += blockDim.x) {
+      keys[t] = hi + static_cast<std::uint32_t>(a.w[t]);
+      tok[t] = static_cast<int>(t);
+      docof[t] = static_cast<int>(m);
+    }
+  }
+}
+
+__global__ void wm_gather_kernel(const int* tok, const int* docof, int* doc, std::int64_t n) {
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    doc[i] = docof[tok[i]];
+}
+
 // ---------------------------------------------------------------------------------
 // z block, lean fp32 screen (default): lane-contiguous candidates
 // ---------------------------------------------------------------------------------
@@ -900,7 +947,12 @@ __device__ __forceinline__ FChunk<CW> ldg_chunk(const float* p) {
 // G lanes per token, CW candidates per lane per round (G * CW = 32: one 128-byte
 // line per round), R rounds; TFR keeps the lane's theta operands in registers
 // across the work unit (else they are re-read from shared memory every token).
-template <int G, int CW, int R, bool TFR>
+// WM (word-major order, build_word_major): a unit is one word's tokens of a block of
+// documents; the word's g row is the resident operand (shared memory / registers) and
+// each token streams its document's theta/S row (th32, L2-resident per document block).
+// The products, running sums and decisions are the document-major ones operand for
+// operand (x * y in fp32 commutes), so z is bitwise the same.
+template <int G, int CW, int R, bool TFR, bool WM = false>
 __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std::int64_t* iter_p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // theta/S in fp32: lane gl's KL candidates at thf[gl * KLP ..], the +4 pad keeps the
@@ -918,12 +970,36 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
   // rounds of this lane that hold real candidates (the rest is padding, not fetched)
   const int rl = min(R, max(0, (a.K - gl * KL + CW - 1) / CW));
 
-  for (std::int64_t unit = blockIdx.x; unit < a.n_units; unit += gridDim.x) {
+  // document-major: a CTA per unit (a document's tokens, warps on alternate batches);
+  // word-major: a warp per unit (one word's ~60 tokens of a document block), its own
+  // resident row in shared memory
+  // word-major units are claimed in order from a ticket, so the units in flight stay
+  // within one document block (static striding let warps drift over several blocks)
+  if constexpr (WM) thf += warp * (G * KLP);
+  auto next_unit = [&](std::int64_t cur) -> std::int64_t {
+    if constexpr (WM) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(a.wm_ticket, 1ull);
+      return static_cast<std::int64_t>(__shfl_sync(0xffffffffu, u, 0));
+    } else {
+      return cur < 0 ? blockIdx.x : cur + gridDim.x;
+    }
+  };
+  for (std::int64_t unit = next_unit(-1); unit < a.n_units; unit = next_unit(unit)) {
+    // document-major: m = document, [t0, t1) tokens; word-major: m = word, [t0, t1)
+    // positions in the sorted token list
     const std::int64_t m = a.units[unit * 3], t0 = a.units[unit * 3 + 1], t1 = a.units[unit * 3 + 2];
-    const double* thg = a.theta + m * a.K;
-    for (int k = threadIdx.x; k < G * KL; k += blockDim.x)
-      thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
-    __syncthreads();
+    if constexpr (WM) {
+      const float* gv = a.phiT32 + m * a.Kp32;
+      for (int k = lane; k < G * KL; k += 32)
+        thf[(k / KL) * KLP + k % KL] = k < a.K ? gv[phys32(k, R, G, CW)] : 0.0f;
+      __syncwarp();
+    } else {
+      const double* thg = a.theta + m * a.K;
+      for (int k = threadIdx.x; k < G * KL; k += blockDim.x)
+        thf[(k / KL) * KLP + k % KL] = k < a.K ? static_cast<float>(thg[k] / a.S[k]) : 0.0f;
+      __syncthreads();
+    }
     float tf[TFR ? KL : 1];
     if constexpr (TFR) {
 #pragma unroll
@@ -935,27 +1011,37 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
         tf[i + 3] = t.w;
       }
     }
-    int* cnt = a.nmk + m * a.K;
-    for (std::int64_t b0 = t0 + warp * 32; b0 < t1; b0 += kWarps * 32) {
-      // token b0 + lane: its word and its uniform, keyed(seed, 3, var_z, t, iter)
-      const std::int64_t tl = b0 + lane;
-      const bool lvalid = tl < t1;
-      const int wl = lvalid ? __ldg(a.w + tl) : 0;
+    for (std::int64_t b0 = t0 + (WM ? 0 : warp * 32); b0 < t1; b0 += (WM ? 32 : kWarps * 32)) {
+      // token b0 + lane: its word (word-major: its token index and document) and its
+      // uniform, keyed(seed, 3, var_z, t, iter)
+      const std::int64_t il = b0 + lane;
+      const bool lvalid = il < t1;
+      std::int64_t tl = il;
+      int wl = 0;
+      if constexpr (WM) {
+        tl = lvalid ? __ldg(a.wm_tok + il) : 0;
+        wl = lvalid ? __ldg(a.wm_doc + il) : 0;
+      } else {
+        wl = lvalid ? __ldg(a.w + tl) : 0;
+      }
       float ul = 0.5f;
       if (lvalid) {
         Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + tl)),
                         static_cast<std::uint64_t>(iter)));
         ul = static_cast<float>(rng.next_unit());
       }
+      const int tl32 = static_cast<int>(tl);
 #pragma unroll 1
       for (int s = 0; s < G; ++s) {
         if (b0 + s * (32 / G) >= t1) break;  // warp-uniform: no token left in this sub-batch
         const int src = s * (32 / G) + gid;  // lane holding this group's token
-        const std::int64_t t = b0 + src;
-        const bool valid = t < t1;
+        const bool valid = b0 + src < t1;
+        // document-major: wv = word, t = token; word-major: wv = document, t shuffled
+        const std::int64_t t = WM ? static_cast<std::int64_t>(__shfl_sync(0xffffffffu, tl32, src)) : b0 + src;
         const int wv = __shfl_sync(0xffffffffu, wl, src);
         const float u01 = __shfl_sync(0xffffffffu, ul, src);
-        const float* row = a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
+        const float* row = WM ? a.th32 + static_cast<std::size_t>(wv) * a.Kp32
+                              : a.phiT32 + static_cast<std::size_t>(wv) * a.Kp32;
         // all rounds' loads first (memory-level parallelism), then the fma chains
         FChunk<CW> ph[R];
 #pragma unroll
@@ -1032,19 +1118,21 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
         }
         const bool decided = ((__ballot_sync(0xffffffffu, k >= 0) >> gshift) & gbits) != 0;
         if (valid) {
+          const std::int64_t word = WM ? m : wv, doc = WM ? wv : m;
           if (k >= 0) {
             a.z[t] = k;
-            atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + k], 1);
-            atomicAdd(&cnt[k], 1);
+            atomicAdd(&a.nkw[static_cast<std::size_t>(word) * a.Kp + k], 1);
+            atomicAdd(&a.nmk[doc * a.K + k], 1);
           } else if (!decided && gl == 0) {
             // ambiguous for the screen: queued for the fp64 draw (zfallback_kernel)
             const int slot = atomicAdd(a.fq_len, 1);
-            a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(m));
+            a.fq[slot] = make_int2(static_cast<int>(t), static_cast<int>(doc));
           }
         }
       }
     }
-    __syncthreads();
+    if constexpr (WM) __syncwarp();
+    else __syncthreads();
   }
 }
 
@@ -2157,6 +2245,17 @@ class Lda final : public Model {
     choose_screen();
     Kp32_ = CW32_ * G32_ * RS_;
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(Vpad_) * Kp32_);
+    {
+      // word-major z-step order when the fp32 rows exceed half the L2 (1B: 410 MB);
+      // BNMC_ZSTEP_WM=0/1 forces it off / on (on: the default layouts only)
+      const std::size_t rows32 = sizeof(float) * static_cast<std::size_t>(V_) * Kp32_;
+      const bool can = screen_ && !transposed_ && Ml_ > 0 && wm_layout(screen_key());
+      wm_ = can && rows32 > (64ull << 20);
+      if (const char* e = std::getenv("BNMC_ZSTEP_WM")) wm_ = can && std::string(e) != "0";
+      // theta/S rows of a document block: ~24 MB of fp32
+      wm_block_docs_ = std::max<std::int64_t>(1, (24ll << 20) / (4ll * Kp32_));
+      if (const char* e = std::getenv("BNMC_WM_BLOCK_DOCS")) wm_block_docs_ = std::max<std::int64_t>(1, std::atoll(e));
+    }
     theta_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
     nkw_.alloc(static_cast<std::size_t>(Vpad_) * Kp_);
     nmk_.alloc(std::max<std::int64_t>(Ml_ * K_, 1));
@@ -2372,6 +2471,7 @@ class Lda final : public Model {
     BNMC_CUDA(cudaGetLastError());
     data_on_device_ = true;
     after_state_change(st);
+    if (with_data) build_word_major(st);
   }
 
   // An event other streams can wait on: inside a stream capture it must be an external
@@ -2597,6 +2697,7 @@ class Lda final : public Model {
     data_on_device_ = true;
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
+    build_word_major(st);
   }
 
   std::vector<StateBuf> state_buffers() override {
@@ -2652,6 +2753,7 @@ class Lda final : public Model {
     }
     BNMC_CUDA(cudaGetLastError());
     BNMC_CUDA(cudaStreamSynchronize(st));
+    build_word_major(st);
     prior_init(seed, st);
   }
 
@@ -2773,28 +2875,112 @@ class Lda final : public Model {
     else if (G32_ != 8 && G32_ != 4) RS_ = 4;
   }
 
-  template <int G, int CW, int R, bool TFR>
+  template <int G, int CW, int R, bool TFR, bool WM>
   void zscreen_launch(const LdaArgs& a, cudaStream_t st) {
-    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(n_units_, 1 << 24));
-    const std::size_t sm = sizeof(float) * G * (CW * R + 4);
-    zscreen_kernel<G, CW, R, TFR><<<g, kZThreads, sm, st>>>(a, out.iter);
+    const unsigned g = static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(a.n_units, 1 << 24)));
+    const std::size_t sm = sizeof(float) * G * (CW * R + 4) * (WM ? kZThreads / 32 : 1);
+    if (WM && sm > 48 * 1024)
+      BNMC_CUDA(cudaFuncSetAttribute(zscreen_kernel<G, CW, R, TFR, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)));
+    // word-major: one resident wave (warps stride over the units in order, so the units
+    // in flight stay within one document block and its theta/S rows stay in L2)
+    unsigned gw = g;
+    if constexpr (WM) {
+      int per_sm = 1, sms = 148, dev = 0;
+      BNMC_CUDA(cudaGetDevice(&dev));
+      BNMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      BNMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zscreen_kernel<G, CW, R, TFR, WM>, kZThreads, sm));
+      gw = static_cast<unsigned>(std::max<std::int64_t>(
+          1, std::min<std::int64_t>((a.n_units + kZThreads / 32 - 1) / (kZThreads / 32),
+                                    static_cast<std::int64_t>(sms) * std::max(per_sm, 1))));
+    }
+    zscreen_kernel<G, CW, R, TFR, WM><<<gw, kZThreads, sm, st>>>(a, out.iter);
   }
 
-  template <int G, int CW, bool TFR>
+  template <int G, int CW, bool TFR, bool WM = false>
   void zscreen_rounds(const LdaArgs& a, cudaStream_t st) {
     if constexpr (G <= 8) {
       switch (RS_) {
-        case 1: zscreen_launch<G, CW, 1, TFR>(a, st); return;
-        case 2: zscreen_launch<G, CW, 2, TFR>(a, st); return;
-        case 3: zscreen_launch<G, CW, 3, TFR>(a, st); return;
-        default: zscreen_launch<G, CW, 4, TFR>(a, st); return;
+        case 1: zscreen_launch<G, CW, 1, TFR, WM>(a, st); return;
+        case 2: zscreen_launch<G, CW, 2, TFR, WM>(a, st); return;
+        case 3: zscreen_launch<G, CW, 3, TFR, WM>(a, st); return;
+        default: zscreen_launch<G, CW, 4, TFR, WM>(a, st); return;
       }
     } else if constexpr (G == 32 && CW == 8 && !TFR) {
-      if (RS_ > 4) zscreen_launch<G, CW, 8, TFR>(a, st);
-      else zscreen_launch<G, CW, 4, TFR>(a, st);
+      if (RS_ > 4) zscreen_launch<G, CW, 8, TFR, WM>(a, st);
+      else zscreen_launch<G, CW, 4, TFR, WM>(a, st);
     } else {
-      zscreen_launch<G, CW, 4, TFR>(a, st);
+      zscreen_launch<G, CW, 4, TFR, WM>(a, st);
     }
+  }
+
+  // the screen layouts choose_screen picks by default (the word-major order exists for them)
+  int screen_key() const { return G32_ * 100 + CW32_ * 10 + (tfr_ ? 1 : 0); }
+  static bool wm_layout(int key) { return key == 3280 || key == 3241 || key == 1641 || key == 841; }
+
+  // Word-major z-step order for corpora whose fp32 rows (V x Kp32) do not stay in L2:
+  // the local tokens sorted by (block of documents, word); a work unit is one word's
+  // tokens within a block (<= kChunk), so the word's row is read from HBM once per block
+  // and the block's theta/S rows (wm_block_docs_ x Kp32 fp32, ~24 MB) stay in L2.
+  void build_word_major(cudaStream_t st) {
+    n_wm_units_ = 0;
+    if (!wm_ || Nl_ == 0) return;
+    const std::int64_t nblocks = (Ml_ + wm_block_docs_ - 1) / wm_block_docs_;
+    const std::uint64_t maxkey = static_cast<std::uint64_t>(nblocks) * static_cast<std::uint64_t>(V_);
+    if (maxkey >= (1ull << 32)) {  // keys must fit 32 bits: stay document-major
+      wm_ = false;
+      return;
+    }
+    int end_bit = 1;
+    while ((1ull << end_bit) < maxkey) ++end_bit;
+    DevBuf<std::uint32_t> keys, keys_alt;
+    DevBuf<int> tok_a, tok_b, docof;
+    keys.alloc(Nl_);
+    keys_alt.alloc(Nl_);
+    tok_a.alloc(Nl_);
+    tok_b.alloc(Nl_);
+    docof.alloc(Nl_);
+    const LdaArgs a = args();
+    wm_keys_kernel<<<grid_docs(), 256, 0, st>>>(a, wm_block_docs_, keys.p, tok_a.p, docof.p);
+    BNMC_CUDA(cudaGetLastError());
+    const int which = sort_pairs_u32(keys.p, keys_alt.p, tok_a.p, tok_b.p, Nl_, end_bit, st);
+    std::uint32_t* skeys = which ? keys_alt.p : keys.p;
+    DevBuf<int>& stok = which ? tok_b : tok_a;
+    std::swap(wm_tok_.p, stok.p);
+    std::swap(wm_tok_.n, stok.n);
+    wm_doc_.alloc(Nl_);
+    wm_gather_kernel<<<148 * 8, 256, 0, st>>>(wm_tok_.p, docof.p, wm_doc_.p, Nl_);
+    // runs of (block, word) -> work units (word, i0, i1), <= kChunk tokens each
+    std::uint32_t* uniq = which ? keys.p : keys_alt.p;  // the free buffer of the pair
+    int* counts = docof.p;  // free after the gather (same stream)
+    const std::int64_t nruns = run_length_u32(skeys, Nl_, uniq, counts, st);
+    std::vector<std::uint32_t> hk(static_cast<std::size_t>(nruns));
+    std::vector<int> hc(static_cast<std::size_t>(nruns));
+    BNMC_CUDA(cudaMemcpyAsync(hk.data(), uniq, sizeof(std::uint32_t) * nruns, cudaMemcpyDeviceToHost, st));
+    BNMC_CUDA(cudaMemcpyAsync(hc.data(), counts, sizeof(int) * nruns, cudaMemcpyDeviceToHost, st));
+    BNMC_CUDA(cudaStreamSynchronize(st));
+    std::vector<std::int64_t> u;
+    u.reserve(static_cast<std::size_t>(nruns) * 3);
+    std::int64_t pos = 0;
+    for (std::int64_t r = 0; r < nruns; ++r) {
+      const std::int64_t word = hk[r] % static_cast<std::uint32_t>(V_), end = pos + hc[r];
+      for (std::int64_t i = pos; i < end; i += kChunk) {
+        u.push_back(word);
+        u.push_back(i);
+        u.push_back(std::min<std::int64_t>(i + kChunk, end));
+      }
+      pos = end;
+    }
+    require(pos == Nl_, BNMC_GPU_ERR_RUNTIME, "word-major order: token count mismatch");
+    n_wm_units_ = static_cast<std::int64_t>(u.size() / 3);
+    wm_units_.alloc(std::max<std::size_t>(u.size(), 3));
+    BNMC_CUDA(cudaMemcpyAsync(wm_units_.p, u.data(), sizeof(std::int64_t) * u.size(), cudaMemcpyHostToDevice, st));
+    if (th32_.n == 0) {
+      th32_.alloc(static_cast<std::size_t>(Ml_) * Kp32_);
+      th32_.zero(st);
+      wm_ticket_.alloc(1);
+    }
+    BNMC_CUDA(cudaStreamSynchronize(st));
   }
 
   template <int R, bool TFR>
@@ -2831,7 +3017,23 @@ class Lda final : public Model {
       launch_pdl(zfallback_kernel, dim3(148 * 8), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter), out.err);
       return;
     }
-    const int key = G32_ * 100 + CW32_ * 10 + (tfr_ ? 1 : 0);
+    const int key = screen_key();
+    if (wm_ && n_wm_units_ > 0) {
+      LdaArgs aw = a;
+      aw.units = wm_units_.p;
+      aw.n_units = n_wm_units_;
+      aw.wm_ticket = wm_ticket_.p;
+      th32_kernel<<<148 * 16, 256, 0, st>>>(aw);
+      BNMC_CUDA(cudaMemsetAsync(wm_ticket_.p, 0, sizeof(unsigned long long), st));
+      switch (key) {
+        case 841: zscreen_rounds<8, 4, true, true>(aw, st); break;
+        case 1641: zscreen_rounds<16, 4, true, true>(aw, st); break;
+        case 3241: zscreen_rounds<32, 4, true, true>(aw, st); break;
+        default: zscreen_rounds<32, 8, false, true>(aw, st); break;
+      }
+      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
+      return;
+    }
     switch (key) {
       case 441: zscreen_rounds<4, 4, true>(a, st); break;   // (G*CW < 32: experiments only)
       case 481: zscreen_rounds<4, 8, true>(a, st); break;
@@ -2937,6 +3139,9 @@ class Lda final : public Model {
     a.screen_margin = screen_margin_;
     a.fq = fq_.p;
     a.fq_len = fq_len_.p;
+    a.wm_tok = wm_tok_.p;
+    a.wm_doc = wm_doc_.p;
+    a.th32 = th32_.p;
     return a;
   }
 
@@ -2968,6 +3173,13 @@ class Lda final : public Model {
   int nbw_ = 1, col_stripes_ = kColStripes;
   float screen_margin_ = kScreenMargin;
   bool fq_reset_ = false;  // phi_colsum2 of this sweep zeroes the fallback queue
+  // word-major z-step order (build_word_major)
+  bool wm_ = false;
+  std::int64_t wm_block_docs_ = 1, n_wm_units_ = 0;
+  DevBuf<int> wm_tok_, wm_doc_;
+  DevBuf<std::int64_t> wm_units_;
+  DevBuf<float> th32_;
+  DevBuf<unsigned long long> wm_ticket_;
 
   // cudaLaunchKernelEx with programmatic stream serialization (PDL): the kernel's
   // launch overlaps the predecessor's tail; it calls pdl_wait() before its inputs.

@@ -433,6 +433,35 @@ def test_lda_doc_running_sums_equal_the_scan(g, monkeypatch, K):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("K,V,block_docs", [(1000, 5000, 3), (300, 20000, 7), (150, 3000, 1), (1000, 100000, 0)],
+                         ids=["k1000", "k300", "k150", "k1000-v1e5-default"])
+def test_lda_word_major_zstep_equals_document_major(g, monkeypatch, K, V, block_docs):
+    """The word-major z-step order (tokens sorted by (document block, word), the word's
+    row resident, theta/S rows streamed) draws bitwise the document-major z: same
+    products, sums and decisions (sampler.cpp:222-265); 3 sweeps, ragged and empty docs."""
+    rng = np.random.default_rng(K + V)
+    lens = rng.integers(0, 400, 40)
+    lens[3] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    w = rng.integers(0, V, int(off[-1])).astype(np.int64)
+    hyper = {"K": K, "V": V, "M": len(lens), "N": [int(x) for x in lens]}
+    got = {}
+    for wm in ("0", "1"):
+        monkeypatch.setenv("BNMC_ZSTEP_WM", wm)
+        if block_docs:
+            monkeypatch.setenv("BNMC_WM_BLOCK_DOCS", str(block_docs))
+        e = g.Engine("lda", hyper, g.RunConfig(seed=17))
+        s = e.allocate()
+        s["w"] = w
+        e.prior_init(s, 17)
+        ljs = [e.sweep(s, it) for it in range(3)]
+        got[wm] = (ljs, s["z"].copy(), s["phi"].copy(), s["theta"].copy(), e.lda_counts()[0].copy())
+        e.close()
+    assert got["0"][0] == got["1"][0]
+    for a, b in zip(got["0"][1:], got["1"][1:]):
+        assert np.array_equal(a, b)
+
+
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
