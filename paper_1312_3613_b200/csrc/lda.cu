@@ -919,9 +919,14 @@ __global__ void wm_gather_kernel(const int* tok, const int* docof, int* doc, std
 //    warp handles token j of the warp's 32-token batch, then the values are
 //    shuffled to the group that draws that token;
 //  * FMA in the screen (explicit __fmaf_rn: --fmad=false only governs contraction).
-// Error budget: every screen partial sum is within (8 + R + log2 G + 4) * 2^-24 *
-// total of the exact cumulative weight (non-negative terms, fma chains); with
-// G <= 32, R <= 8 that is < 2^-19 * total, 8x below the 2^-16 margin.
+// Error budget (u = 2^-24, T = the exact total; non-negative terms, so every rounding
+// is bounded relative to T): each fp32 product carries 2u from its rounded operands;
+// a compared running sum (prev / acc) passes through CW (the lane's round), R (its
+// run), log2 G (the group scan), 1 (lo) and CW (the owner's re-scan) roundings:
+// <= (2 CW + R + log2 G + 3) u T; uf = u01 * total: <= (CW + R + log2 G + 4) u T. The
+// decision equals the fp64 one when the margin exceeds their sum, (3 CW + 2 R +
+// 2 log2 G + 7) u: 49 u for G = 32, CW = 8, R = 4 and at most 57 u (R = 8). The
+// grouped kernel uses 2^-17 = 128 u (>= 2.2x that), the transposed one 2^-16.
 
 template <int CW>
 struct FChunk {
@@ -1323,12 +1328,24 @@ __global__ void __launch_bounds__(kZThreads, TFR ? 3 : 1) zscreen_t_kernel(LdaAr
 // [l*c, (l+1)*c), c = ceil(K/32); warp scan of the lane sums, the owner rescans
 // its chunk (the reference's candidate order and u = next_unit * total rule,
 // dist.cpp:202-215).  Tokens whose product weights underflow take the sequential
-// log-space draw.
-__global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
+// log-space draw.  The products (theta/S) * g are formed in candidate order by the
+// whole warp (coalesced row loads) into the warp's shared-memory slice, one pad
+// double per 32 (lane-contiguous reads then hit distinct banks); the sums read them
+// in the lane-contiguous order (the same additions as reading the rows directly,
+// which cost 32 L1 wavefronts per load: ncu, 1B, L1TEX 98 %, 166 ms).
+constexpr int kFallbackThreads = 128;
+
+__host__ __device__ constexpr int fallback_stride(int K) { return K + (K >> 5) + 1; }
+
+// kStage = false (K <= 128: <= 4 candidates per lane): the lanes read the rows directly.
+template <bool kStage>
+__global__ void __launch_bounds__(kFallbackThreads) zfallback_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
+  extern __shared__ double fprod[];
   pdl_wait();
   pdl_trigger();
   const std::int64_t iter = *iter_p;
   const int lane = threadIdx.x & 31;
+  double* prod = fprod + (threadIdx.x >> 5) * fallback_stride(a.K);
   const int n = *a.fq_len;
   const int c = (a.K + 31) / 32;
   const int k0 = min(a.K, lane * c), k1 = min(a.K, k0 + c);
@@ -1341,8 +1358,14 @@ __global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::in
     Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                     static_cast<std::uint64_t>(iter)));
     const double u01 = rng.next_unit();
+    auto term = [&](int k) { return kStage ? prod[k + (k >> 5)] : (thg[k] / a.S[k]) * row[k]; };
+    if constexpr (kStage) {
+      __syncwarp();  // the previous token's reads of prod are done
+      for (int k = lane; k < a.K; k += 32) prod[k + (k >> 5)] = (thg[k] / a.S[k]) * row[k];
+      __syncwarp();
+    }
     double own = 0.0;
-    for (int k = k0; k < k1; ++k) own += (thg[k] / a.S[k]) * row[k];
+    for (int k = k0; k < k1; ++k) own += term(k);
     double inc = own;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1360,7 +1383,7 @@ __global__ void __launch_bounds__(256) zfallback_kernel(LdaArgs a, const std::in
         double acc = start;
         cand = k1 - 1;
         for (int k = k0; k < k1; ++k) {
-          acc += (thg[k] / a.S[k]) * row[k];
+          acc += term(k);
           if (u < acc) {
             cand = k;
             break;
@@ -2239,6 +2262,12 @@ class Lda final : public Model {
     }
     phiT_.alloc(static_cast<std::size_t>(Vpad_) * Kp_);
     if (exact_) logphiT_.alloc(static_cast<std::size_t>(V_) * Kp_);
+    // K <= 128 (transposed screen, a few thousand queued tokens): the r01 grid, 9472 warps
+    fb_blocks_ = K_ <= 128 ? 148 * 16 : 148 * 12;
+    if (const char* e = std::getenv("BNMC_FB_BLOCKS")) fb_blocks_ = std::max(1, std::atoi(e));
+    if (fallback_smem() > 48 * 1024)
+      BNMC_CUDA(cudaFuncSetAttribute(zfallback_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(fallback_smem())));
     // fp32-screened z-step (product weights only); BNMC_ZSTEP_SCREEN=0 disables it.
     const char* sc = std::getenv("BNMC_ZSTEP_SCREEN");
     screen_ = !exact_ && !(sc && std::string(sc) == "0");
@@ -2338,6 +2367,9 @@ class Lda final : public Model {
     // or registers (BNMC_ZSTEP_THETA=regs: 128 registers; measured 20 % slower on NIPS).
     const char* tr = std::getenv("BNMC_ZSTEP_THETA");
     theta_regs_ = tr && std::string(tr) == "regs";
+    // grouped screen (K > 128): 2^-17, >= 2.2x its error budget (above zscreen_kernel);
+    // 1B: the fp64 queue 1.2 % -> 0.6 % of the tokens, sweep 424 -> 390 ms
+    if (!transposed_) screen_margin_ = kScreenMargin * 0.5f;
     if (const char* e = std::getenv("BNMC_SCREEN_MARGIN")) screen_margin_ = static_cast<float>(std::atof(e));
     if (const char* e = std::getenv("BNMC_PDL")) pdl_ = std::string(e) != "0";
     configure_kernels();
@@ -2793,6 +2825,8 @@ class Lda final : public Model {
 
   std::size_t zstep_smem() const { return sizeof(double) * 2 * Kp_; }
 
+  std::size_t fallback_smem() const { return sizeof(double) * (kFallbackThreads / 32) * fallback_stride(K_); }
+
   template <int G, int R, bool E>
   void zstep_attr() {
     const int sm = static_cast<int>(zstep_smem());
@@ -3014,7 +3048,8 @@ class Lda final : public Model {
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
-      launch_pdl(zfallback_kernel, dim3(148 * 8), dim3(256), 0, st, a, static_cast<const std::int64_t*>(out.iter), out.err);
+      launch_pdl(zfallback_kernel<false>, dim3(fb_blocks_), dim3(kFallbackThreads), 0, st, a,
+                 static_cast<const std::int64_t*>(out.iter), out.err);
       return;
     }
     const int key = screen_key();
@@ -3029,9 +3064,12 @@ class Lda final : public Model {
         case 841: zscreen_rounds<8, 4, true, true>(aw, st); break;
         case 1641: zscreen_rounds<16, 4, true, true>(aw, st); break;
         case 3241: zscreen_rounds<32, 4, true, true>(aw, st); break;
-        default: zscreen_rounds<32, 8, false, true>(aw, st); break;
+        default:
+          if (wm_tfr_) zscreen_rounds<32, 8, true, true>(aw, st);
+          else zscreen_rounds<32, 8, false, true>(aw, st);
+          break;
       }
-      zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
+      zfallback_kernel<true><<<fb_blocks_, kFallbackThreads, fallback_smem(), st>>>(a, out.iter, out.err);
       return;
     }
     switch (key) {
@@ -3046,7 +3084,7 @@ class Lda final : public Model {
       case 3240: zscreen_rounds<32, 4, false>(a, st); break;
       default: zscreen_rounds<32, 8, false>(a, st); break;
     }
-    zfallback_kernel<<<148 * 8, 256, 0, st>>>(a, out.iter, out.err);
+    zfallback_kernel<true><<<fb_blocks_, kFallbackThreads, fallback_smem(), st>>>(a, out.iter, out.err);
   }
 
   void launch_zstep(const LdaArgs& a, cudaStream_t st) {
@@ -3173,8 +3211,9 @@ class Lda final : public Model {
   int nbw_ = 1, col_stripes_ = kColStripes;
   float screen_margin_ = kScreenMargin;
   bool fq_reset_ = false;  // phi_colsum2 of this sweep zeroes the fallback queue
+  int fb_blocks_ = 148 * 12;  // zfallback_kernel grid
   // word-major z-step order (build_word_major)
-  bool wm_ = false;
+  bool wm_ = false, wm_tfr_ = !(std::getenv("BNMC_WM_TFR") && std::string(std::getenv("BNMC_WM_TFR")) == "0");
   std::int64_t wm_block_docs_ = 1, n_wm_units_ = 0;
   DevBuf<int> wm_tok_, wm_doc_;
   DevBuf<std::int64_t> wm_units_;
