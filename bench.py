@@ -17,9 +17,11 @@ Prints ONE JSON line (rank 0).  Fields beyond the base contract:
                HBM fraction is small and `binding` names the unit that bounds the kernel
                (ncu: the L1TEX data pipe); `l2` relates the operand bytes the kernel
                actually streams to the L2 -> SM read bandwidth measured in this run.
-  roofline_1b  (default NIPS run, N=1) a short pass over the 1B-token config, where the
-               z-step IS HBM-bound (410 MB of screen rows, no word reuse): its DRAM
-               fraction with its own clocks
+  roofline_1b  (default NIPS run, N=1) a short pass over the 1B-token config (410 MB of
+               screen rows): the z-step runs in the word-major order (tokens sorted by
+               document block x word, theta/S rows L2-resident per block), so like NIPS
+               it reports its compulsory DRAM fraction, the binding unit and the L2
+               operand fraction, with its own clocks
   cpu_baseline the compiled reference (oracle/_ref) timed on one host core on half of
                the same corpus (identical documents)
   e2e          the same metric through the public API with HOST buffers: every step
@@ -359,6 +361,21 @@ def lda_zstep_bytes(docs, V, K, L):
     return compulsory, operand
 
 
+def lda_wm_bytes(docs, V, K, L):
+    """Compulsory DRAM bytes per z-step launch in the word-major order (K > 128 corpora
+    whose fp32 rows exceed the L2, lda.cu build_word_major): per token its sorted index,
+    document and z (12 B); theta/S fp32 rows read once (4 Kp32 per document, the blocks'
+    rows then stay in L2); the doc-topic counts read and written (8 K per document); each
+    word's fp32 row once per document block (the words of a ~24 MB block of theta/S rows).
+    The operand stream (a theta/S row per token) is served by L2."""
+    N = docs * L
+    kp32 = -(-K // 32) * 32
+    block_docs = max(1, (24 << 20) // (4 * kp32))
+    nblocks = -(-docs // block_docs)
+    words_per_block = min(V, block_docs * L)
+    return 12 * N + 4 * kp32 * docs + 8 * K * docs + 4 * kp32 * words_per_block * nblocks
+
+
 def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
     nccl_id = None
     if world > 1:
@@ -394,9 +411,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         dominant = "zstep"
         compulsory, operand = lda_zstep_bytes(e - b, V, K, L)
         if args.workload == "1b":
-            # 410 MB of rows, no word reuse within documents: every token's row is
-            # algorithmically a DRAM read (roofline_1b in the NIPS run)
-            compulsory = operand
+            # word-major order: theta/S rows of a document block stay in L2
+            compulsory = lda_wm_bytes(e - b, V, K, L)
         extra["weights"] = "product theta*phi (fp64; fp32 screen + fp64 fallback, z bit-exact)"
     elif model == "gmm":
         N, K = wl["points"], wl["topics"]
@@ -464,7 +480,10 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
                     "traffic": prof.get("dram_bytes"), "algorithmic_bytes_per_launch": compulsory,
                     "kernel_ms": round(dom_ms, 5), "share_of_sweep": round(dom_ms / sum(phases.values()), 3)}
         if model == "lda" and args.workload == "1b":
-            roofline["algorithmic_bytes_note"] = "the fp32 screen row of every token (4 Kp32 + 16 B per token)"
+            roofline["algorithmic_bytes_note"] = (
+                "compulsory DRAM bytes of the word-major z-step (sorted token index, document and z per "
+                "token; theta/S rows once; doc-topic counts; each word's row once per document block); "
+                "the theta/S operand rows stream from L2")
             if prof.get("dram_bytes"):
                 roofline["dram_frac"] = round(prof["dram_bytes"] / (dom_ms / 1e3) / 1e9 / peak, 4)
         elif model == "lda":
@@ -475,7 +494,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             roofline["algorithmic_bytes_note"] = (
                 "x row + y per data row, read once per step (a read-only stream; the copy peak counts "
                 "read + write traffic, so a pure read stream can reach slightly above it)")
-        if model == "lda" and args.workload != "1b":
+        if model == "lda":
             if prof.get("l1tex_pct") is not None:
                 roofline["binding"] = {"unit": "l1tex data pipe", "pct_of_peak": prof.get("l1tex_pct"),
                                        "lts_pct_of_peak": prof.get("lts_pct"),
@@ -610,22 +629,33 @@ def roofline_1b(args, g, torch, stream, flush, gpu_index):
         zms = phases["zstep"]
         N = docs * L
         peak, peak_src = measured_peak_hbm()
-        compulsory, operand = lda_zstep_bytes(docs, V, K, L)
-        # no word reuse within documents or blocks of documents in this corpus (SURVEY 8d,
-        # DESIGN 3): the algorithmic DRAM bytes are the operand bytes, 4 Kp32 + 16 per token
-        ach = operand / (zms / 1e3) / 1e9
+        _, operand = lda_zstep_bytes(docs, V, K, L)
+        compulsory = lda_wm_bytes(docs, V, K, L)
+        ach = compulsory / (zms / 1e3) / 1e9
         prof = ncu_profile("1b:zstep") or {}
         dram = prof.get("dram_bytes")
         out = {"bound": "hbm", "kernel": "zstep", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-               "frac": round(ach / peak, 4), "peak_source": peak_src, "algorithmic_bytes_per_launch": operand,
+               "frac": round(ach / peak, 4), "peak_source": peak_src, "algorithmic_bytes_per_launch": compulsory,
+               "algorithmic_bytes_note": (
+                   "compulsory DRAM bytes of the word-major z-step (tokens sorted by document block x word: "
+                   "12 B per token, theta/S rows once, doc-topic counts, each word's row once per block); "
+                   "the per-token operand rows (theta/S, 4 Kp32 B) are served by L2"),
                "traffic": dram, "kernel_ms": round(zms, 3), "sweep_ms": round(ms, 3),
                "sites_per_s": N / (ms / 1e3), "phases_ms": {k: round(v, 3) for k, v in phases.items()},
                "clocks": clocks, "setup_s": round(setup, 2),
                "config": {"workload": "lda-1b", "docs": docs, "vocab": V, "topics": K, "doc_len": L, "tokens": N}}
         if dram:
             out["dram_frac"] = round(dram / (zms / 1e3) / 1e9 / peak, 4)
-            out["dram_note"] = ("ncu DRAM bytes per launch (profiles/) over this run's kernel time: the "
-                                "operand rows come ~85 % from DRAM, the rest from L2 hits")
+        if prof.get("l1tex_pct") is not None:
+            out["binding"] = {"unit": "l1tex data pipe", "pct_of_peak": prof.get("l1tex_pct"),
+                              "lts_pct_of_peak": prof.get("lts_pct"), "source": prof.get("source")}
+        try:
+            l2_bw = g.read_bandwidth(24 << 20, 200)
+            ach_l2 = operand / (zms / 1e3) / 1e9
+            out["l2"] = {"achieved": round(ach_l2, 1), "peak": round(l2_bw, 1), "unit": "GB/s",
+                         "frac": round(ach_l2 / l2_bw, 4), "operand_bytes_per_launch": operand}
+        except Exception as ex:  # reported, never fatal
+            out["l2"] = {"error": str(ex)}
         return out
     except Exception as ex:  # reported, never fatal for the NIPS line
         return {"error": str(ex)}
