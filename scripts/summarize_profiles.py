@@ -70,6 +70,15 @@ def to_bytes(v, unit):
     return float(v) * f if f else None
 
 
+def to_us(v, unit):
+    f = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+         "second": 1e6, "s": 1e6}.get(unit)
+    try:
+        return round(float(v) * f, 2) if f else None
+    except (TypeError, ValueError):
+        return None
+
+
 def full(rep, dst, key, raw=None, src=None, source_name=None):
     if raw is None:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -100,8 +109,9 @@ def full(rep, dst, key, raw=None, src=None, source_name=None):
             traffic.append({"dram_bytes": rb + wb,
                             "l1tex_pct": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
                             "lts_pct": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                            "issue_pct": pct("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
                             "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
-                            "kernel_us_ncu": pct("gpu__time_duration.sum"),
+                            "kernel_us_ncu": to_us(m.get("gpu__time_duration.sum"), un.get("gpu__time_duration.sum")),
                             "source": os.path.relpath(dst, ROOT)})
             out.append(f"  dram read+write bytes per launch: {rb + wb:.4g}")
     # SASS opcode mix (instructions executed)
