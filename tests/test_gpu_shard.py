@@ -158,6 +158,35 @@ def test_sharded_equals_unsharded_on_a_large_corpus(g, restatement, W, exact):
     sh.close()
 
 
+@pytest.mark.parametrize("K", [300, 1000])
+def test_sharded_word_major_equals_unsharded_document_major(g, restatement, monkeypatch, K):
+    """Word-major z-step order on W = 2 shards (each rank sorts its own tokens by
+    (document block, word)) against one document-major context: z, theta, phi bitwise
+    over 3 sweeps (a Zipf corpus, so frequent words span several kChunk units)."""
+    V, seed, W = 3000, 9, 2
+    off, w, phi, theta, z = _nips_like(restatement, M=120, V=V, K=K, L=500, seed=seed)
+    hyper = {"K": K, "V": V, "M": len(off) - 1, "N": np.diff(off).tolist()}
+    monkeypatch.setenv("BNMC_ZSTEP_WM", "0")
+    one = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+    s1 = one.allocate()
+    s1["w"], s1["z"], s1["phi"], s1["theta"] = w, z, phi, theta
+    monkeypatch.setenv("BNMC_ZSTEP_WM", "1")
+    monkeypatch.setenv("BNMC_WM_BLOCK_DOCS", "7")
+    sh = ShardedLda(g, K, V, off, w, seed, W)
+    sh.set_state(z, phi, theta)
+    for it in range(3):
+        lj1 = one.sweep(s1, it)
+        ljs = sh.sweep(it)
+        zg, thg = sh.gather()
+        assert np.array_equal(zg, s1["z"]), f"sweep {it}: {(zg != s1['z']).sum()} z mismatches"
+        assert np.array_equal(thg, s1["theta"])
+        for r in range(W):
+            assert np.array_equal(sh.st[r]["phi"], s1["phi"])
+            assert abs(ljs[r] - lj1) <= RTOL_LJ * abs(lj1)
+    one.close()
+    sh.close()
+
+
 def test_sharded_speculation_with_an_edit_on_one_rank(g, restatement):
     """Bound-store sweeps speculate collectively: a caller edit of z on ONE rank's shard
     must make every rank redo the sweep from the edited state (the vote is an all-reduce
