@@ -462,6 +462,26 @@ def test_lda_word_major_zstep_equals_document_major(g, monkeypatch, K, V, block_
         assert np.array_equal(a, b)
 
 
+def test_lda_1b_word_major_equals_document_major_at_full_size(g, monkeypatch):
+    """The 1B config itself (1e6 documents x 1000 tokens, K=1000, V=1e5; device generator +
+    prior_init): two sweeps in the word-major order and in the document-major order give
+    the same log-joints (bitwise) and the same topic-word counts."""
+    K, V, M, L, seed = 1000, 100000, 1000000, 1000, 2024
+    hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
+    got = {}
+    for wm in ("1", "0"):
+        monkeypatch.setenv("BNMC_ZSTEP_WM", wm)
+        e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
+        e.lda_generate(seed)
+        lj, _ = e.run_device(0, 2)
+        nkw, _ = e.lda_counts()
+        got[wm] = (lj, nkw.sum(axis=1).copy(), nkw[:, :2000].copy())
+        e.close()
+    assert int(got["1"][1].sum()) == M * L
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
