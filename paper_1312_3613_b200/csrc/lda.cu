@@ -1361,7 +1361,25 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_kernel(LdaArgs a, 
     auto term = [&](int k) { return kStage ? prod[k + (k >> 5)] : (thg[k] / a.S[k]) * row[k]; };
     if constexpr (kStage) {
       __syncwarp();  // the previous token's reads of prod are done
-      for (int k = lane; k < a.K; k += 32) prod[k + (k >> 5)] = (thg[k] / a.S[k]) * row[k];
+      // 8 candidates per lane in flight (24 loads) before the divisions and stores: the
+      // loop one load round trip at a time took ~60 us per token at 1B
+      for (int kb = lane; kb < a.K; kb += 32 * 8) {
+        double th[8], sv[8], rw[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kb + 32 * j;
+          if (k < a.K) {
+            th[j] = __ldg(thg + k);
+            sv[j] = __ldg(a.S + k);
+            rw[j] = __ldg(row + k);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kb + 32 * j;
+          if (k < a.K) prod[k + (k >> 5)] = (th[j] / sv[j]) * rw[j];
+        }
+      }
       __syncwarp();
     }
     double own = 0.0;
