@@ -2293,11 +2293,13 @@ class Lda final : public Model {
     Kp32_ = CW32_ * G32_ * RS_;
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(Vpad_) * Kp32_);
     {
-      // word-major z-step order when the fp32 rows exceed half the L2 (1B: 410 MB);
+      // word-major z-step order when the fp32 rows exceed a quarter of the L2 (measured,
+      // scripts/wm_probe.py: faster at 37 MB of rows and above (K = 300 / V = 3e4: 6.1 ->
+      // 4.8 ms; 1B: 410 MB), slower at <= 20 MB (K = 1000 / V = 5000: 2.2 -> 3.0 ms));
       // BNMC_ZSTEP_WM=0/1 forces it off / on (on: the default layouts only)
       const std::size_t rows32 = sizeof(float) * static_cast<std::size_t>(V_) * Kp32_;
       const bool can = screen_ && !transposed_ && Ml_ > 0 && wm_layout(screen_key());
-      wm_ = can && rows32 > (64ull << 20);
+      wm_ = can && rows32 > (32ull << 20);
       if (const char* e = std::getenv("BNMC_ZSTEP_WM")) wm_ = can && std::string(e) != "0";
       // theta/S rows of a document block: ~24 MB of fp32
       wm_block_docs_ = std::max<std::int64_t>(1, (24ll << 20) / (4ll * Kp32_));
