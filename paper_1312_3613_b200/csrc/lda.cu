@@ -1106,20 +1106,25 @@ __global__ void __launch_bounds__(kZThreads) zscreen_kernel(LdaArgs a, const std
             const float4 y = *reinterpret_cast<const float4*>(thf + gl * KLP + CW * rr + j);
             tv[j] = y.x, tv[j + 1] = y.y, tv[j + 2] = y.z, tv[j + 3] = y.w;
           }
-          float acc = lo, prev = lo;
-          int j = -1;
+          // the chunk's running sums (the same fma chain), then the crossing candidate by
+          // counting the sums <= uf (they never decrease) and an unrolled select
+          float nx[CW];
+          float run_c = lo;
 #pragma unroll
           for (int jj = 0; jj < CW; ++jj) {
-            const float nx = __fmaf_rn(tv[jj], p.v[jj], acc);
-            if (j < 0) {
-              if (uf < nx) {
-                j = jj;
-                prev = acc;
-              }
-              acc = nx;
-            }
+            run_c = __fmaf_rn(tv[jj], p.v[jj], run_c);
+            nx[jj] = run_c;
           }
-          if (j >= 0 && kl0 + j < a.K && uf - prev >= mg && acc - uf >= mg) k = kl0 + j;
+          int j = 0;
+#pragma unroll
+          for (int jj = 0; jj < CW; ++jj) j += uf >= nx[jj] ? 1 : 0;
+          if (j < CW) {
+            float acc = nx[0], prev = lo;
+#pragma unroll
+            for (int jj = 1; jj < CW; ++jj)
+              if (j == jj) acc = nx[jj], prev = nx[jj - 1];
+            if (kl0 + j < a.K && uf - prev >= mg && acc - uf >= mg) k = kl0 + j;
+          }
         }
         const bool decided = ((__ballot_sync(0xffffffffu, k >= 0) >> gshift) & gbits) != 0;
         if (valid) {
