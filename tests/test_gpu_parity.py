@@ -395,16 +395,18 @@ def test_lda_prior_init_long_rows(g, restatement, monkeypatch, V, K):
     assert np.array_equal(got["0"][2], z)
 
 
-def test_lda_generate_long_rows(g, monkeypatch):
-    """lda_generate's true-phi rows (concentration 0.05, gen.cpp:26-31) through the
-    segmented walk: the corpus and the prior state equal the thread-per-row draw's."""
+@pytest.mark.parametrize("phi_conc", [0.05, 2.0], ids=["boost", "no-boost"])
+def test_lda_generate_long_rows(g, monkeypatch, phi_conc):
+    """lda_generate's true-phi rows (concentration 0.05 as gen.cpp:26-31, and 2.0: gammas
+    without the shape < 1 boost, 3 counters per attempt) through the segmented walk: the
+    corpus and the prior state equal the thread-per-row draw's."""
     K, V, M, L, seed = 6, 100000, 16, 64, 5
     hyper = {"K": K, "V": V, "M": M, "N": [L] * M}
     got = {}
     for serial in ("1", "0"):
         monkeypatch.setenv("BNMC_PRIOR_SERIAL", serial)
         e = g.Engine("lda", hyper, g.RunConfig(seed=seed))
-        e.lda_generate(seed)
+        e.lda_generate(seed, phi_conc=phi_conc)
         s = e.allocate()
         e.download(s)
         got[serial] = (e.lda_counts()[0].copy(), s["phi"].copy(), s["z"].copy())
