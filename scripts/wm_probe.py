@@ -19,6 +19,11 @@ SHAPES = [  # K, V, docs, doc_len
     (1000, 5000, 5000, 1000),
     (150, 12419, 1500, 1267),
     (400, 12419, 1500, 1267),
+    (100, 200000, 50000, 400),
+    (100, 80000, 50000, 400),
+    (100, 40000, 50000, 400),
+    (100, 12419, 1500, 1267),
+    (50, 100000, 50000, 400),
 ]
 if len(sys.argv) > 1:
     SHAPES = SHAPES[int(sys.argv[1]):]
