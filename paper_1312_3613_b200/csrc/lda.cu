@@ -121,6 +121,7 @@ struct LdaArgs {
   const int* wm_tok;
   const int* wm_doc;
   float* th32;
+  double* thS;                    // word-major: theta/S in fp64 [Ml][K] (the fallback's operand)
   unsigned long long* wm_ticket;  // next unit to claim (zeroed before each word-major launch)
 };
 
@@ -873,13 +874,17 @@ __device__ int draw_topic_logspace(const double* lth, const double* row, int K, 
 // Word-major z-step operand: theta/S of every local document in fp32, in the phiT32
 // column order (the value the document-major z-step forms per unit in shared memory).
 // Padding columns stay 0 (zeroed at allocation).
+// Also theta/S in fp64 for the fallback draw (one division per cell per sweep instead of
+// one per cell per queued token: the divisions were half the fallback's instructions).
 __global__ void th32_kernel(LdaArgs a) {
   const std::int64_t n = a.Ml * a.K;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const std::int64_t m = i / a.K;
     const int k = static_cast<int>(i - m * a.K);
-    a.th32[m * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(a.theta[i] / a.S[k]);
+    const double q = a.theta[i] / a.S[k];
+    a.th32[m * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(q);
+    a.thS[i] = q;  // the same quotient the fallback would form per token
   }
 }
 
@@ -1374,15 +1379,15 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_kernel(LdaArgs a, 
         for (int j = 0; j < 8; ++j) {
           const int k = kb + 32 * j;
           if (k < a.K) {
-            th[j] = __ldg(thg + k);
-            sv[j] = __ldg(a.S + k);
+            th[j] = __ldg((a.thS ? a.thS + m * a.K : thg) + k);
+            sv[j] = a.thS ? 1.0 : __ldg(a.S + k);
             rw[j] = __ldg(row + k);
           }
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int k = kb + 32 * j;
-          if (k < a.K) prod[k + (k >> 5)] = (th[j] / sv[j]) * rw[j];
+          if (k < a.K) prod[k + (k >> 5)] = (a.thS ? th[j] : th[j] / sv[j]) * rw[j];
         }
       }
       __syncwarp();
@@ -3037,6 +3042,7 @@ class Lda final : public Model {
     if (th32_.n == 0) {
       th32_.alloc(static_cast<std::size_t>(Ml_) * Kp32_);
       th32_.zero(st);
+      thS_.alloc(static_cast<std::size_t>(Ml_) * K_);
       wm_ticket_.alloc(1);
     }
     BNMC_CUDA(cudaStreamSynchronize(st));
@@ -3205,6 +3211,7 @@ class Lda final : public Model {
     a.wm_tok = wm_tok_.p;
     a.wm_doc = wm_doc_.p;
     a.th32 = th32_.p;
+    a.thS = wm_ && n_wm_units_ > 0 ? thS_.p : nullptr;
     return a;
   }
 
@@ -3243,6 +3250,7 @@ class Lda final : public Model {
   DevBuf<int> wm_tok_, wm_doc_;
   DevBuf<std::int64_t> wm_units_;
   DevBuf<float> th32_;
+  DevBuf<double> thS_;
   DevBuf<unsigned long long> wm_ticket_;
 
   // cudaLaunchKernelEx with programmatic stream serialization (PDL): the kernel's
