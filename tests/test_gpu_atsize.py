@@ -7,6 +7,8 @@ the LIVE compiled reference (oracle/_ref, the unmodified sampler) on the same in
   LDA    the 1B shape K=1000, V=1e5 on an 8 x 10k-token slice, 1 sweep,
          and the device prior_init of that slice                          (batch.cpp:45-83)
   MH     regression.bn on gen_regression(1e5, 64), 10 steps               (sampler.cpp:284-340)
+  HMM    hmm.bn on 1e5 random flips, S = 4 and 16, 5 sweeps (the chunked s-scan vs the
+         reference's sequential scan)                                      (sampler.cpp:259-264)
 
 Contract: z / counts / accept decisions bit-exact on every sweep (0
 mismatches); phi, theta, pi <= 1e-12 relative; GMM mu, sigma2 <= 1e-10; log-joint <= 1e-10.
@@ -199,4 +201,30 @@ def test_lda_long_chain_posterior_vs_reference(g):
             thetas.append(s["theta"].copy())
     assert rel(np.mean(phis, axis=0), ref["phi"][n // 2:].mean(axis=0)) < 1e-10
     assert rel(np.mean(thetas, axis=0), ref["theta"][n // 2:].mean(axis=0)) < 1e-10
+    e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# HMM: the chunked s-scan (composed chunk maps) against the reference's sequential scan
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("S", [4, 16])
+def test_hmm_1e5_5_sweeps(g, S):
+    N, seed, n = 100000, 77, 5
+    flips = np.random.default_rng(seed).integers(0, 2, N).astype(np.int64)
+    ref = run_chain({"model": "hmm", "hyper": {"N": N, "S": S}, "method": "gibbs", "seed": seed, "threads": 1,
+                     "observed": ["flips"], "init": "prior", "sweeps": n, "record": ["s", "T", "bias"]},
+                    data={"flips": flips})
+    e = g.Engine("hmm", {"N": N, "S": S}, g.RunConfig(seed=seed))
+    st = e.allocate()
+    st["flips"] = flips
+    e.prior_init(st, seed)                 # the chunked prior chain against the reference's
+    assert np.array_equal(st["s"], ref["s_init"])
+    assert rel(st["T"], ref["T_init"]) < RTOL_PARAM and rel(st["bias"], ref["bias_init"]) < RTOL_PARAM
+    st["s"], st["T"], st["bias"] = ref["s_init"], ref["T_init"], ref["bias_init"]
+    for it in range(n):
+        lj = e.sweep(st, it)
+        mism = int((st["s"] != ref["s"][it]).sum())
+        assert mism == 0, f"sweep {it}: {mism} s mismatches of {N}"
+        assert rel(st["T"], ref["T"][it]) < RTOL_PARAM and rel(st["bias"], ref["bias"][it]) < RTOL_PARAM
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
     e.close()
