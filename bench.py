@@ -401,7 +401,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         docs = config["docs"]
         V, K, L = wl["vocab"], wl["topics"], wl["doc_len"]
         hyper = {"K": K, "V": V, "M": docs, "N": [L] * docs}
-        cfg = g.RunConfig(seed=args.seed, device=local_rank)
+        exact = args.weights == "exact"
+        cfg = g.RunConfig(seed=args.seed, device=local_rank, exact_weights=exact)
         eng = g.Engine("lda", hyper, cfg, rank=rank, world_size=world, nccl_id=nccl_id,
                        stream=stream.cuda_stream)
         sites_total = docs * L
@@ -418,12 +419,18 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         # conj_pool, colsum_rows, z-step screen, z-step fallback, wterm<FINAL>
         # (sharded: + finalize after the log-joint all-reduce; NCCL's own kernels not counted)
         per_sweep_kernels = 5 + (1 if world > 1 else 0)
+        if exact:  # + phi normalisation and S = 1; one fp64 log-space z kernel (no screen)
+            per_sweep_kernels += 1
         dominant = "zstep"
         compulsory, operand = lda_zstep_bytes(e - b, V, K, L)
         if args.workload == "1b":
             # word-major order: theta/S rows of a document block stay in L2
             compulsory = lda_wm_bytes(e - b, V, K, L)
-        extra["weights"] = "product theta*phi (fp64; fp32 screen + fp64 fallback, z bit-exact)"
+        extra["weights"] = ("log-space exp(log theta + log phi - max): the reference's arithmetic "
+                            "(draw_from_log_weights, dist.cpp:202-215), fp64, no screen" if exact else
+                            "product theta*phi (fp64; fp32 screen + fp64 fallback, z bit-exact)")
+        if exact:
+            config = dict(config, weights="log-space (BNMC_GPU_EXACT_WEIGHTS)")
     elif model == "gmm":
         N, K = wl["points"], wl["topics"]
         hyper = {"N": N, "K": K}
@@ -557,7 +564,8 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
             # the same loop with the store left pageable (pin_host=False): a fresh engine on
             # the same stream, the store's state as the pinned loop left it
             eng.close()
-            eng = g.Engine(model, hyper, g.RunConfig(seed=args.seed, device=local_rank, pin_host=False),
+            eng = g.Engine(model, hyper, g.RunConfig(seed=args.seed, device=local_rank, pin_host=False,
+                                                     exact_weights=args.weights == "exact" and model == "lda"),
                            stream=stream.cuda_stream)
             sp, up2, down2, it = e2e_loop(eng, store, it)
             e2e_pageable = {"value": sites_total / sp, "unit": UNIT, "ms_per_step": sp * 1e3,
@@ -576,9 +584,9 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
            "roofline": roofline, "phases_ms": {k: round(v, 5) for k, v in phases.items()},
            "e2e": e2e, "e2e_pageable": e2e_pageable, "gpu_launches": per_sweep_kernels * args.steps,
            "clocks": clocks, "wall_s_timed": wall, "setup_s": setup_s, "last_log_joint": lj_last}
-    if rank == 0 and world == 1 and model == "lda" and host_corpus:
+    if rank == 0 and world == 1 and model == "lda" and host_corpus and args.weights == "product":
         out["e2e_reference_engine"] = e2e_reference_engine(args, config, store["w"])
-    if rank == 0 and world == 1 and args.workload == "nips" and not args.no_1b:
+    if rank == 0 and world == 1 and args.workload == "nips" and not args.no_1b and args.weights == "product":
         out["roofline_1b"] = roofline_1b(args, g, torch, stream, flush, gpu_index)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
@@ -824,6 +832,8 @@ def main():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-1b", action="store_true", help="skip the 1B-token roofline pass of the NIPS run")
+    ap.add_argument("--weights", default="product", choices=["product", "exact"],
+                    help="LDA z-step arithmetic: product form (default) or the reference's log-space form")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)

@@ -575,7 +575,11 @@ __global__ void phi_norm_kernel(LdaArgs a) {
     for (int v = v0; v < v1; ++v) {
       const std::size_t c = static_cast<std::size_t>(v) * a.Kp + k;
       const double x = a.phiT[c] / S;
-      if (NORMALISE) a.phiT[c] = x;
+      if (NORMALISE) {
+        a.phiT[c] = x;
+        // (exact mode: the fp32 screen then reads phi itself, with S = 1)
+        if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(x);
+      }
       const double lx = x > 0.0 ? log(x) : -INFINITY;
       if (a.logphiT) a.logphiT[c] = lx;
       lp += (a.beta - 1.0) * lx;
@@ -1458,6 +1462,82 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_kernel(LdaArgs a, 
   }
 }
 
+// The log-space draw (draw_from_log_weights, dist.cpp:202-215) for the tokens the fp32
+// screen could not decide in the exact-weights mode: w_k = log theta_k + log phi_k (the
+// logphiT table), mx = max, exp(w_k - mx) summed in the lane-contiguous order of
+// zfallback_kernel, u = next_unit * total, the owner rescans. The screen's decisions are
+// the real-number ones (margin >> the ~1e-14 relative error of the fp64 log-space sums),
+// so screened tokens get the log-space draw's topic too.
+__global__ void __launch_bounds__(kFallbackThreads) zfallback_log_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
+  extern __shared__ double fw_s[];
+  pdl_wait();
+  pdl_trigger();
+  const std::int64_t iter = *iter_p;
+  const int lane = threadIdx.x & 31;
+  double* fw = fw_s + (threadIdx.x >> 5) * fallback_stride(a.K);
+  const int n = *a.fq_len;
+  const int c = (a.K + 31) / 32;
+  const int k0 = min(a.K, lane * c), k1 = min(a.K, k0 + c);
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const int2 q = a.fq[i];
+    const std::int64_t t = q.x, m = q.y;
+    const int wv = a.w[t];
+    const double* thg = a.theta + m * a.K;
+    const double* lrow = a.logphiT + static_cast<std::size_t>(wv) * a.Kp;
+    Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
+                    static_cast<std::uint64_t>(iter)));
+    const double u01 = rng.next_unit();
+    __syncwarp();
+    double lmx = -INFINITY;
+    for (int k = lane; k < a.K; k += 32) {
+      const double x = thg[k];
+      const double w = (x > 0.0 ? log(x) : -INFINITY) + lrow[k];
+      fw[k + (k >> 5)] = w;
+      lmx = fmax(lmx, w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmx = fmax(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
+    __syncwarp();
+    int pick = -1;
+    if (isfinite(lmx)) {
+      double own = 0.0;
+      for (int k = k0; k < k1; ++k) own += exp(fw[k + (k >> 5)] - lmx);
+      double inc = own;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+      }
+      double start = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) start = 0.0;
+      const double total = __shfl_sync(0xffffffffu, inc, 31);
+      const double u = u01 * total;
+      int cand = (lane == 31 && !(u < inc)) ? a.K - 1 : -1;  // past-the-end: K - 1
+      if (start <= u && u < inc && k0 < k1) {
+        double acc = start;
+        cand = k1 - 1;
+        for (int k = k0; k < k1; ++k) {
+          acc += exp(fw[k + (k >> 5)] - lmx);
+          if (u < acc) {
+            cand = k;
+            break;
+          }
+        }
+      }
+      pick = __reduce_max_sync(0xffffffffu, cand);
+    }
+    if (lane == 0) {
+      if (pick < 0) {
+        atomicOr(err, kErrDomain);
+      } else {
+        a.z[t] = pick;
+        atomicAdd(&a.nkw[static_cast<std::size_t>(wv) * a.Kp + pick], 1);
+        atomicAdd(&a.nmk[m * a.K + pick], 1);
+      }
+    }
+  }
+}
+
 // One CTA per work unit (a chunk of <= kChunk tokens of one document).
 template <int G, int R, bool EXACT, bool TR>
 __global__ void __launch_bounds__(kZThreads) zstep_kernel(LdaArgs a, const std::int64_t* iter_p, int* err) {
@@ -2294,11 +2374,17 @@ class Lda final : public Model {
     fb_blocks_ = K_ <= 128 ? 148 * 16 : 148 * 12;
     if (const char* e = std::getenv("BNMC_FB_BLOCKS")) fb_blocks_ = std::max(1, std::atoi(e));
     if (fallback_smem() > 48 * 1024)
+    {
       BNMC_CUDA(cudaFuncSetAttribute(zfallback_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(fallback_smem())));
-    // fp32-screened z-step (product weights only); BNMC_ZSTEP_SCREEN=0 disables it.
+      BNMC_CUDA(cudaFuncSetAttribute(zfallback_log_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(fallback_smem())));
+    }
+    // fp32-screened z-step; BNMC_ZSTEP_SCREEN=0 disables it.
     const char* sc = std::getenv("BNMC_ZSTEP_SCREEN");
-    screen_ = !exact_ && !(sc && std::string(sc) == "0");
+    // (exact-weights mode too: the screen decides the real-number topic; its undecided
+    // tokens take the log-space fallback, zfallback_log_kernel)
+    screen_ = !(sc && std::string(sc) == "0");
     choose_screen();
     Kp32_ = CW32_ * G32_ * RS_;
     if (screen_) phiT32_.alloc(static_cast<std::size_t>(Vpad_) * Kp32_);
@@ -2857,6 +2943,18 @@ class Lda final : public Model {
 
   std::size_t fallback_smem() const { return sizeof(double) * (kFallbackThreads / 32) * fallback_stride(K_); }
 
+  // The fp64 redraw of the screen's undecided tokens: the log-space draw in the exact-
+  // weights mode, else the product form (staged through shared memory for K > 128).
+  void launch_fallback(const LdaArgs& a, cudaStream_t st) {
+    const std::int64_t* it = out.iter;
+    if (exact_)
+      launch_pdl(zfallback_log_kernel, dim3(fb_blocks_), dim3(kFallbackThreads), fallback_smem(), st, a, it, out.err);
+    else if (K_ <= 128)
+      launch_pdl(zfallback_kernel<false>, dim3(fb_blocks_), dim3(kFallbackThreads), 0, st, a, it, out.err);
+    else
+      launch_pdl(zfallback_kernel<true>, dim3(fb_blocks_), dim3(kFallbackThreads), fallback_smem(), st, a, it, out.err);
+  }
+
   template <int G, int R, bool E>
   void zstep_attr() {
     const int sm = static_cast<int>(zstep_smem());
@@ -3079,8 +3177,7 @@ class Lda final : public Model {
     if (transposed_) {
       if (tfr_) zscreen_t_rounds<true>(a, st);
       else zscreen_t_rounds<false>(a, st);
-      launch_pdl(zfallback_kernel<false>, dim3(fb_blocks_), dim3(kFallbackThreads), 0, st, a,
-                 static_cast<const std::int64_t*>(out.iter), out.err);
+      launch_fallback(a, st);
       return;
     }
     const int key = screen_key();
@@ -3100,7 +3197,7 @@ class Lda final : public Model {
           else zscreen_rounds<32, 8, false, true>(aw, st);
           break;
       }
-      zfallback_kernel<true><<<fb_blocks_, kFallbackThreads, fallback_smem(), st>>>(a, out.iter, out.err);
+      launch_fallback(a, st);
       return;
     }
     switch (key) {
@@ -3115,7 +3212,7 @@ class Lda final : public Model {
       case 3240: zscreen_rounds<32, 4, false>(a, st); break;
       default: zscreen_rounds<32, 8, false>(a, st); break;
     }
-    zfallback_kernel<true><<<fb_blocks_, kFallbackThreads, fallback_smem(), st>>>(a, out.iter, out.err);
+    launch_fallback(a, st);
   }
 
   void launch_zstep(const LdaArgs& a, cudaStream_t st) {
@@ -3126,11 +3223,9 @@ class Lda final : public Model {
     dispatch_zstep([&](auto gg, auto r, auto e) {
       constexpr int GG = decltype(gg)::value, RR = decltype(r)::value;
       constexpr bool EE = decltype(e)::value;
-      if constexpr (!EE) {
-        if (screen_) {
-          launch_zscreen(a, st);
-          return;
-        }
+      if (screen_) {
+        launch_zscreen(a, st);
+        return;
       }
       if (theta_regs_)
         zstep_kernel<GG, RR, EE, true><<<g, kZThreads, sm, st>>>(a, it, const_cast<int*>(err));

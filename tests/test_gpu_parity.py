@@ -484,6 +484,34 @@ def test_lda_1b_word_major_equals_document_major_at_full_size(g, monkeypatch):
         assert np.array_equal(np.asarray(a), np.asarray(b))
 
 
+@pytest.mark.parametrize("K,V,margin", [(100, 6000, None), (100, 6000, "1.0"), (300, 8000, None), (300, 8000, "1.0")],
+                         ids=["k100", "k100-all-fallback", "k300", "k300-all-fallback"])
+def test_lda_exact_weights_screen_equals_unscreened(g, monkeypatch, K, V, margin):
+    """Exact-weights (log-space) mode: the fp32 screen + log-space fallback draws the
+    topics of the unscreened log-space z-step (draw_from_log_weights, dist.cpp:202-215)
+    over 3 sweeps; margin 1.0 sends every token through zfallback_log_kernel."""
+    rng = np.random.default_rng(K)
+    lens = rng.integers(50, 700, 300)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    w = rng.integers(0, V, int(off[-1])).astype(np.int64)
+    hyper = {"K": K, "V": V, "M": len(lens), "N": [int(x) for x in lens]}
+    got = {}
+    for screen in ("0", "1"):
+        monkeypatch.setenv("BNMC_ZSTEP_SCREEN", screen)
+        if margin and screen == "1":
+            monkeypatch.setenv("BNMC_SCREEN_MARGIN", margin)
+        e = g.Engine("lda", hyper, g.RunConfig(seed=23, exact_weights=True))
+        s = e.allocate()
+        s["w"] = w
+        e.prior_init(s, 23)
+        ljs = [e.sweep(s, it) for it in range(3)]
+        got[screen] = (ljs, s["z"].copy(), s["phi"].copy(), s["theta"].copy())
+        e.close()
+    assert np.array_equal(got["0"][1], got["1"][1])
+    assert np.array_equal(got["0"][2], got["1"][2]) and np.array_equal(got["0"][3], got["1"][3])
+    assert got["0"][0] == got["1"][0]
+
+
 # ----------------------------------------------------------------------------------------
 # GMM and MH
 # ----------------------------------------------------------------------------------------
