@@ -564,6 +564,9 @@ __global__ void fill_kernel(double* p, int n, double v) {
 }
 
 // phi = g / S[k]; accumulates (beta-1)*log(phi) and phi per topic for the log-joint.
+// NORMALISE (the exact-mode sweep, a checkpoint restore): phi written back in place; its
+// colpart2 pieces are not read afterwards (the sweep's phi prior term comes from
+// phi_colsum2, a restore recomputes them), so only the log phi table takes logs.
 template <bool NORMALISE>
 __global__ void phi_norm_kernel(LdaArgs a) {
   const int b = blockIdx.x;
@@ -580,11 +583,13 @@ __global__ void phi_norm_kernel(LdaArgs a) {
         // (exact mode: the fp32 screen then reads phi itself, with S = 1)
         if (a.phiT32) a.phiT32[static_cast<std::size_t>(v) * a.Kp32 + phys32(k, a.R32, a.G32, a.CW32)] = static_cast<float>(x);
       }
+      if (NORMALISE && !a.logphiT) continue;
       const double lx = x > 0.0 ? log(x) : -INFINITY;
       if (a.logphiT) a.logphiT[c] = lx;
       lp += (a.beta - 1.0) * lx;
       sx += x;
     }
+    if (NORMALISE) continue;
     double* o = a.colpart2 + (static_cast<std::size_t>(b) * a.K + k) * 2;
     o[0] = lp;
     o[1] = sx;
@@ -1464,7 +1469,7 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_kernel(LdaArgs a, 
 
 // The log-space draw (draw_from_log_weights, dist.cpp:202-215) for the tokens the fp32
 // screen could not decide in the exact-weights mode: w_k = log theta_k + log phi_k (the
-// logphiT table), mx = max, exp(w_k - mx) summed in the lane-contiguous order of
+// values the logphiT table would hold), mx = max, exp(w_k - mx) summed in the lane-contiguous order of
 // zfallback_kernel, u = next_unit * total, the owner rescans. The screen's decisions are
 // the real-number ones (margin >> the ~1e-14 relative error of the fp64 log-space sums),
 // so screened tokens get the log-space draw's topic too.
@@ -1483,15 +1488,15 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_log_kernel(LdaArgs
     const std::int64_t t = q.x, m = q.y;
     const int wv = a.w[t];
     const double* thg = a.theta + m * a.K;
-    const double* lrow = a.logphiT + static_cast<std::size_t>(wv) * a.Kp;
+    const double* prow = a.phiT + static_cast<std::size_t>(wv) * a.Kp;  // phi (normalised, S = 1)
     Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                     static_cast<std::uint64_t>(iter)));
     const double u01 = rng.next_unit();
     __syncwarp();
     double lmx = -INFINITY;
     for (int k = lane; k < a.K; k += 32) {
-      const double x = thg[k];
-      const double w = (x > 0.0 ? log(x) : -INFINITY) + lrow[k];
+      const double x = thg[k], p = prow[k];
+      const double w = (x > 0.0 ? log(x) : -INFINITY) + (p > 0.0 ? log(p) : -INFINITY);  // = log theta + logphiT
       fw[k + (k >> 5)] = w;
       lmx = fmax(lmx, w);
     }
@@ -3260,7 +3265,9 @@ class Lda final : public Model {
     a.R32 = RS_;
     a.CW32 = CW32_;
     a.col_stripes = col_stripes_;
-    a.logphiT = exact_ ? logphiT_.p : nullptr;
+    // the log phi table feeds the unscreened log-space z-step only (the screened mode's
+    // fallback takes the logs of its few tokens' rows itself)
+    a.logphiT = exact_ && !screen_ ? logphiT_.p : nullptr;
     a.theta = theta_.p;
     a.nkw = nkw_.p;
     a.colpart2 = colpart2_.p;
