@@ -3,18 +3,21 @@
 // One reference sweep (Engine::sweep, proj/src/sampler.cpp:390-405; plan order
 // phi, theta, z per tests/golden/describe_lda.txt) becomes, per GPU, one CUDA graph:
 //
-//   [allreduce nkw]      NCCL int32 sum of the topic-word counts (world > 1 only)
+//   [reduce-scatter nkw] the topic-word counts by vocabulary slices (world > 1 only)
 //   phi_pool_kernel      phi AND theta blocks: every cell's Gamma(prior + count) draw
 //                        (batch.cpp:38-41 streams, dist.cpp:136-155 Marsaglia-Tsang) by
 //                        a persistent warp pool; consumes the counts (zeroes them for
-//                        this sweep's z-step)
+//                        this sweep's z-step); sharded: this rank's phi rows, then
+//                        [all-gather] of the drawn rows
 //   phi_colsum2_kernel   phi column sums S[k] and the phi factor of the log-joint;
 //                        theta rows: normalise, theta factor (extra y-blocks)
 //   zscreen_t_kernel     z block (sampler.cpp:222-265, draw_from_log_weights
 //   / zscreen_kernel     dist.cpp:202-215): fp32 screen of the product-form draw, new z,
 //                        the NEXT sweep's counts (integer atomics); ambiguous tokens
-//                        queued for
-//   zfallback_kernel     the fp64 product-form draw (one warp per queued token)
+//                        queued for; K > 128 with > 32 MB of rows: the word-major
+//                        order (th32_kernel + zscreen_kernel<.., WM>, build_word_major)
+//   zfallback_kernel     the fp64 product-form draw (one warp per queued token;
+//   / zfallback_log_k.   the log-space draw in the exact-weights mode)
 //   wterm_kernel<FINAL>  w- and z-factors of the log-joint from the counts, the fixed-
 //                        order final sum (eval.cpp:393-422); sharded: this rank's
 //                        pieces -> [allreduce 3 doubles] -> finalize_kernel
