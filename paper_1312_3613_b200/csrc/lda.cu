@@ -2694,7 +2694,9 @@ class Lda final : public Model {
     LdaArgs a = args();
     // this sweep's phi block leaves g (unnormalised) + logS: the w-factor takes
     // log g - log S (the exact mode normalises phiT in place, S = 1: the phi/S path)
-    a.logg_valid = (!observe_phi_ && !exact_) ? 1 : 0;
+    // (exact mode: phiT is normalised in place below and log S zeroed, so the w-factor
+    // takes the same compacted n log phi path)
+    a.logg_valid = !observe_phi_ ? 1 : 0;
     const bool timed = marks != nullptr;  // phase timing: everything on one stream
     mark(st, "begin");
     // warp-pool conjugate block: phi and theta cells in one balanced kernel, then the
@@ -2738,6 +2740,7 @@ class Lda final : public Model {
       // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
       phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
       fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
+      fill_kernel<<<1, 256, 0, st>>>(logS_.p, K_, 0.0);
       mark(st, "phi_norm");
     }
     if (!timed) {  // phi, theta final: overlapped downloads may start (external event nodes)
