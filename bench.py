@@ -419,8 +419,7 @@ def _run_ours(args, rank, world, local_rank, g, torch, dist, wl, stream):
         # conj_pool, colsum_rows, z-step screen, z-step fallback, wterm<FINAL>
         # (sharded: + finalize after the log-joint all-reduce; NCCL's own kernels not counted)
         per_sweep_kernels = 5 + (1 if world > 1 else 0)
-        if exact:  # + phi normalisation, S = 1, log S = 0 (the fallback is the log-space one)
-            per_sweep_kernels += 3
+        # exact: the same kernels; the fallback is the log-space one (zfallback_log_kernel)
         dominant = "zstep"
         compulsory, operand = lda_zstep_bytes(e - b, V, K, L)
         if args.workload == "1b":

@@ -1491,14 +1491,14 @@ __global__ void __launch_bounds__(kFallbackThreads) zfallback_log_kernel(LdaArgs
     const std::int64_t t = q.x, m = q.y;
     const int wv = a.w[t];
     const double* thg = a.theta + m * a.K;
-    const double* prow = a.phiT + static_cast<std::size_t>(wv) * a.Kp;  // phi (normalised, S = 1)
+    const double* prow = a.phiT + static_cast<std::size_t>(wv) * a.Kp;  // g (phi = g / S)
     Stream rng(fold(fold(a.zkey_prefix, static_cast<std::uint64_t>(a.tok_base + t)),
                     static_cast<std::uint64_t>(iter)));
     const double u01 = rng.next_unit();
     __syncwarp();
     double lmx = -INFINITY;
     for (int k = lane; k < a.K; k += 32) {
-      const double x = thg[k], p = prow[k];
+      const double x = thg[k], p = prow[k] / a.S[k];  // phi exactly as phi_norm_kernel forms it
       const double w = (x > 0.0 ? log(x) : -INFINITY) + (p > 0.0 ? log(p) : -INFINITY);  // = log theta + logphiT
       fw[k + (k >> 5)] = w;
       lmx = fmax(lmx, w);
@@ -2736,8 +2736,10 @@ class Lda final : public Model {
       fq_reset_ = true;
       mark(st, "colsum_rows");
     }
-    if (!observe_phi_ && exact_) {
-      // log-space weights read log phi: normalise in place, then phi = phiT (S = 1).
+    if (!observe_phi_ && exact_ && !screen_) {
+      // the unscreened log-space z-step reads log phi: normalise in place, then phi =
+      // phiT (S = 1). (Screened, phiT keeps g as in the product mode: the screen reads
+      // g and theta/S, the log-space fallback forms phi = g / S itself.)
       phi_norm_kernel<true><<<nb_phi_, phi_threads_, 0, st>>>(a);
       fill_kernel<<<1, 256, 0, st>>>(S_.p, K_, 1.0);
       fill_kernel<<<1, 256, 0, st>>>(logS_.p, K_, 0.0);
