@@ -4,7 +4,7 @@ the LIVE compiled reference (oracle/_ref, the unmodified sampler) on the same in
   GMM    gen_gmm(1e5, {-5,-1,1,5}, {1,0.1,2,1}) + prior_init, 100 sweeps   (sampler.cpp:114-130,222-265)
   LDA    NIPS gen_lda(1500, 12419, 100, 1267) + prior_init, 3 sweeps,
          product-form (default) and log-space (EXACT_WEIGHTS) modes       (sampler.cpp:52-265)
-  LDA    the 1B shape K=1000, V=1e5 on an 8 x 10k-token slice, 1 sweep,
+  LDA    the 1B shape K=1000, V=1e5 on an 8 x 10k-token slice, 1 sweep (both weight modes),
          and the device prior_init of that slice                          (batch.cpp:45-83)
   MH     regression.bn on gen_regression(1e5, 64), 10 steps               (sampler.cpp:284-340)
   HMM    hmm.bn on 1e5 random flips, S = 4 and 16, 5 sweeps (the chunked s-scan vs the
@@ -124,12 +124,21 @@ def test_lda_nips_3_sweeps(g, nips_ref, exact):
 # ----------------------------------------------------------------------------------------
 # LDA at the 1B shape (K = 1000, V = 1e5): an 8-document x 10k-token slice, one sweep
 # ----------------------------------------------------------------------------------------
-def test_lda_k1000_v1e5_slice(g):
+@pytest.fixture(scope="module")
+def k1000_ref():
     M, V, K, L, seed = 8, 100000, 1000, 10000, 7
-    ref = run_chain({"model": "lda", "hyper": {"K": K, "V": V, "M": M, "N": [L] * M}, "method": "gibbs",
-                     "seed": seed, "threads": THREADS, "gen": ["lda", [M, V, K, L, seed]], "observed": ["w"],
-                     "init": "prior", "sweeps": 1, "record": ["z", "phi", "theta"]}, timeout=1800)
-    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed))
+    return run_chain({"model": "lda", "hyper": {"K": K, "V": V, "M": M, "N": [L] * M}, "method": "gibbs",
+                      "seed": seed, "threads": THREADS, "gen": ["lda", [M, V, K, L, seed]], "observed": ["w"],
+                      "init": "prior", "sweeps": 1, "record": ["z", "phi", "theta"]}, timeout=1800)
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["product-form", "log-space"])
+def test_lda_k1000_v1e5_slice(g, k1000_ref, exact):
+    """(word-major z-step order: > 32 MB of fp32 rows; log-space: the screen + the
+    log-space fallback)"""
+    M, V, K, L, seed = 8, 100000, 1000, 10000, 7
+    ref = k1000_ref
+    e = g.Engine("lda", {"K": K, "V": V, "M": M, "N": [L] * M}, g.RunConfig(seed=seed, exact_weights=exact))
     s = e.allocate()
     s["w"] = ref["w"]
     e.prior_init(s, seed)
