@@ -9,6 +9,8 @@ the LIVE compiled reference (oracle/_ref, the unmodified sampler) on the same in
   MH     regression.bn on gen_regression(1e5, 64), 10 steps               (sampler.cpp:284-340)
   HMM    hmm.bn on 1e5 random flips, S = 4 and 16, 5 sweeps (the chunked s-scan vs the
          reference's sequential scan)                                      (sampler.cpp:259-264)
+  catmix catmix.bn on 1e5 categorical points, K = 8, V = 200, 5 sweeps
+  NB     naivebayes.bn on 2e4 rows x 32 features, 5 sweeps
 
 Contract: z / counts / accept decisions bit-exact on every sweep (0
 mismatches); phi, theta, pi <= 1e-12 relative; GMM mu, sigma2 <= 1e-10; log-joint <= 1e-10.
@@ -235,5 +237,48 @@ def test_hmm_1e5_5_sweeps(g, S):
         mism = int((st["s"] != ref["s"][it]).sum())
         assert mism == 0, f"sweep {it}: {mism} s mismatches of {N}"
         assert rel(st["T"], ref["T"][it]) < RTOL_PARAM and rel(st["bias"], ref["bias"][it]) < RTOL_PARAM
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+    e.close()
+
+
+# ----------------------------------------------------------------------------------------
+# catmix and naive Bayes at size: parallel prior_init, the per-block log-joint partials
+# ----------------------------------------------------------------------------------------
+def test_catmix_1e5_5_sweeps(g):
+    N, K, V, seed, n = 100000, 8, 200, 91, 5
+    x = np.random.default_rng(seed).integers(0, V, N).astype(np.int64)
+    ref = run_chain({"model": "catmix", "hyper": {"N": N, "K": K, "V": V}, "method": "gibbs", "seed": seed,
+                     "threads": 1, "observed": ["x"], "init": "prior", "sweeps": n,
+                     "record": ["z", "theta", "phi"]}, data={"x": x})
+    e = g.Engine("catmix", {"N": N, "K": K, "V": V}, g.RunConfig(seed=seed))
+    st = e.allocate()
+    st["x"] = x
+    e.prior_init(st, seed)
+    assert np.array_equal(st["z"], ref["z_init"])
+    assert rel(st["theta"], ref["theta_init"]) < RTOL_PARAM and rel(st["phi"], ref["phi_init"]) < RTOL_PARAM
+    for it in range(n):
+        lj = e.sweep(st, it)
+        assert np.array_equal(st["z"], ref["z"][it]), it
+        assert rel(st["theta"], ref["theta"][it]) < RTOL_PARAM and rel(st["phi"], ref["phi"][it]) < RTOL_PARAM
+        assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
+    e.close()
+
+
+def test_naivebayes_2e4x32_5_sweeps(g):
+    N, K, seed, n = 20000, 32, 93, 5
+    rs = np.random.default_rng(seed)
+    c = rs.integers(0, 2, N).astype(np.int64)
+    f = rs.integers(0, 2, N * K).astype(np.int64)
+    ref = run_chain({"model": "naivebayes", "hyper": {"N": N, "K": K}, "method": "gibbs", "seed": seed,
+                     "threads": 1, "observed": ["c", "f"], "init": "prior", "sweeps": n,
+                     "record": ["pC", "pF"]}, data={"c": c, "f": f})
+    e = g.Engine("naivebayes", {"N": N, "K": K}, g.RunConfig(seed=seed))
+    st = e.allocate()
+    st["c"], st["f"] = c, f
+    e.prior_init(st, seed)
+    assert rel(st["pC"], ref["pC_init"]) < RTOL_PARAM and rel(st["pF"], ref["pF_init"]) < RTOL_PARAM
+    for it in range(n):
+        lj = e.sweep(st, it)
+        assert rel(st["pC"], ref["pC"][it]) < RTOL_PARAM and rel(st["pF"], ref["pF"][it]) < RTOL_PARAM
         assert _lj_ok(lj, ref["lj"][it]), (it, lj, ref["lj"][it])
     e.close()
